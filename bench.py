@@ -1,0 +1,415 @@
+#!/usr/bin/env python3
+"""Benchmark of the gear-plan sweep (headline) and the stage step.
+
+Headline workload (BASELINE.json configs[1]): Sentiment-140-shaped 4-stage
+cascade (BERT tiny/mini/small/base stand-ins m0..m3, cost ratios 1:4:16:64),
+1M synthetic validation samples with the reference make_validation
+semantics, 100-level threshold grids per model -> the full cascade x
+threshold product, C = 1,040,604 configs.  One step = one full sweep
+(histogram + prefix tables + every config's accuracy / mean_cost /
+forward_frac) with inputs resident in HBM.  Metric: config-evals/s.
+
+`e2e`: the same sweep through the public API from HOST buffers: pinned
+H2D of the certainty / correct matrices, sweep, exact Pareto front, D2H of
+the front (config index, accuracy, mean_cost, forward_frac) every step.
+
+Multi-GPU (torchrun): weak scaling — every rank sweeps its own tenant's
+validation set (per-GPU work fixed) and the ranks all-gather their Pareto
+fronts over NCCL each step (distributed.gather_fronts).
+
+--impl reference: the reference algorithm's CPU implementation (the oracle
+port of _evaluate_numba, oracle/oracle_eval.c, all host threads) on a
+bounded config sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_REC = 1_000_000
+N_MODELS = 4
+LEVELS = 100
+COST_RATIOS = (1.0, 4.0, 16.0, 64.0)
+METRIC = "gear-plan config-evals/sec"
+WORKLOAD = ("cfg2: Sentiment-140-shaped 4-stage cascade, 1M synthetic samples, binary scores, "
+            "100-level grids, full cascade x threshold product")
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def workload(seed: int = 0):
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.cascades import grid_values
+    profiles = synth.make_profiles(n_models=N_MODELS, cost_ratios=COST_RATIOS)
+    cert, corr = synth.validation_matrices(N_MODELS, N_REC, 0.8, seed)
+    grids = [np.array(grid_values(cert[:, j], LEVELS)) for j in range(N_MODELS)]
+    return profiles, cert, corr, grids, profiles.cost1()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 7
+                          for k in range(4) if "Active" in s[3 + k] and "Not" not in s[3 + k]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def init_dist():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    import torch
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------- ours -----
+def run_ours(args, world, rank, local):
+    import torch
+
+    from oracle import oracle
+    from paper_2406_14424_b200 import distributed as gdist
+    from paper_2406_14424_b200.gridsweep import GridSweep, pareto_counts
+
+    profiles, cert, corr, grids, cost1 = workload(seed=rank)  # one tenant per rank
+    sw = GridSweep(cert, corr, grids, cost1, build=False)
+    C = sw.n_configs
+    L = sw.max_len
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = None
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        nonlocal out
+        sw.build()
+        out = sw.evaluate(out=out)
+
+    # warm-up
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+
+    # timed: per-step CUDA events on the launching stream, L2 flushed between steps
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier(world)
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            sw.build()
+            ev[i][1].record(stream)
+            out = sw.evaluate(out=out)
+            ev[i][2].record(stream)
+        barrier(world)
+    build_ms = [a.elapsed_time(b) for a, b, _ in ev]
+    eval_ms = [b.elapsed_time(c) for _, b, c in ev]
+    step_ms = sum(build_ms) / args.steps + sum(eval_ms) / args.steps
+    step_ms = max_over_ranks(step_ms, world)
+    value = world * C / (step_ms * 1e-3)
+
+    # correctness spot-check of the timed outputs (rank 0, sampled configs)
+    check = None
+    if rank == 0:
+        rng = np.random.default_rng(1)
+        pick = np.sort(rng.choice(C, size=64, replace=False))
+        sm, thr, ns = oracle.grid_configs(grids)
+        want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1,
+                                       n_threads=os.cpu_count() or 1)
+        got_acc = out.accuracy.cpu().numpy()[pick]
+        got_cost = out.mean_cost.cpu().numpy()[pick]
+        check = bool(np.array_equal(got_acc, want[0]) and np.array_equal(got_cost, want[1]))
+
+    # ---- e2e through the public API from host buffers (+ front all-gather)
+    pin_cert = torch.from_numpy(cert).pin_memory()
+    pin_corr = torch.from_numpy(corr).pin_memory()
+    dcert = torch.empty_like(pin_cert, device=dev)
+    dcorr = torch.empty_like(pin_corr, device=dev)
+    sw_e2e = GridSweep(dcert, dcorr, grids, cost1, build=False)
+    e2e_out = None
+    h2d = pin_cert.numel() * 8 + pin_corr.numel()
+    d2h_total = 0
+
+    def e2e_step():
+        nonlocal e2e_out, d2h_total
+        dcert.copy_(pin_cert, non_blocking=True)
+        dcorr.copy_(pin_corr, non_blocking=True)
+        sw_e2e.build()
+        e2e_out = sw_e2e.evaluate(n_correct=True, out=e2e_out)
+        idx = pareto_counts(e2e_out.n_correct, e2e_out.mean_cost, N_REC)
+        front = gdist.gather_fronts(idx, e2e_out, world) if world > 1 else None
+        host = [idx.cpu(), e2e_out.accuracy[idx].cpu(), e2e_out.mean_cost[idx].cpu(),
+                e2e_out.forward_frac[idx].cpu()]
+        d2h_total = sum(t.numel() * t.element_size() for t in host)
+        if front is not None:
+            d2h_total += front.numel() * front.element_size()
+        return host
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier(world)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        flush.zero_()  # same L2 state as the device-timed loop
+        e2e_step()
+    t1.record(stream)
+    barrier(world)
+    e2e_ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
+    # subtract the flush (timed separately) so e2e counts only the sweep path
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        flush.zero_()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    flush_ms = f0.elapsed_time(f1) / args.steps
+    e2e_ms = max(e2e_ms - flush_ms, 1e-6)
+
+    # ---- stage step (config 3 shape: 1M x 1000-class f32 logits, entropy)
+    stage = stage_bench(args, dev, flush) if (rank == 0 and not args.skip_stage) else None
+
+    # ---- roofline for the dominant kernel phase
+    pk = peaks()
+    b_in = N_REC * N_MODELS * 9
+    b_out = C * (16 + 8 * L)
+    build_avg = sum(build_ms) / args.steps
+    eval_avg = sum(eval_ms) / args.steps
+    if eval_avg >= build_avg:
+        dom, dom_bytes, dom_ms = "grid_eval_kernel (epilogue: acc, cost, frac per config)", b_out, eval_avg
+    else:
+        dom, dom_bytes, dom_ms = "grid build (hist + prefix scans)", b_in, build_avg
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    step_gbs = (b_in + b_out) / (step_ms * 1e-3) / 1e9
+
+    cpu = cpu_baseline(cert, corr, grids, cost1, args) if (rank == 0 and not args.no_cpu) else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "config-evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference make_validation semantics, default_rng(rank))",
+            "config": {"workload": WORKLOAD, "n_records": N_REC, "n_models": N_MODELS,
+                       "grid_levels": LEVELS, "n_configs_per_gpu": C,
+                       "cost_ratios": list(COST_RATIOS), "l2": "flushed (512 MB write) "
+                       "between timed steps", "parallelism": f"weak: 1 tenant sweep per GPU, "
+                       f"NCCL all-gather of Pareto fronts in e2e ({world} ranks)"},
+            "breakdown_ms": {"build": build_avg, "eval": eval_avg},
+            "e2e": {"value": world * C / (e2e_ms * 1e-3), "unit": "config-evals/s",
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h_total,
+                    "path": "GridSweep from pinned host matrices -> build -> eval -> "
+                            "pareto_counts -> D2H front"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
+                         "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                         "traffic": None, "algorithmic_bytes": dom_bytes,
+                         "peak_source": pk["source"],
+                         "step": {"bytes": b_in + b_out, "achieved": step_gbs,
+                                  "frac": step_gbs / pk["hbm_gbs"]}},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps * (2 + (N_MODELS - 1)),
+            "parity_spot_check": check,
+        }
+        if stage is not None:
+            line["stage_step"] = stage
+        print(json.dumps(line), flush=True)
+
+
+def stage_bench(args, dev, flush):
+    """Config-3 shape stage step: 1M rows x 1000-class f32 logits (4 GB),
+    entropy certainty, per-row thresholds, compaction of deferred rows."""
+    import torch
+
+    from paper_2406_14424_b200.stage import stage_step
+    n, c = N_REC, 1000
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    x = torch.randn((n, c), generator=g, device=dev, dtype=torch.float32)
+    thr = torch.full((n,), 0.05, dtype=torch.float64, device=dev)
+    out = {}
+    pk = peaks()
+    for kind in ("entropy", "margin"):
+        for _ in range(max(args.warmup, 1)):
+            r = stage_step(x, thr, kind=kind)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(max(args.steps, 3)):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            r = stage_step(x, thr, kind=kind)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        ms = float(np.median(times))
+        d = int(r.deferred_idx.numel())
+        bytes_ = n * c * 4 + n * (8 + 1 + 8) + d * 8
+        gbs = bytes_ / (ms * 1e-3) / 1e9
+        out[kind] = {"samples_per_s": n / (ms * 1e-3), "ms": ms, "deferred": d,
+                     "algorithmic_bytes": bytes_, "achieved_gbs": gbs,
+                     "frac": gbs / pk["hbm_gbs"],
+                     "note": "includes host sync for the deferred count (API call)"}
+    out["workload"] = "cfg3 shape: 1M x 1000-class f32 logits, per-row thr, stable compaction"
+    return out
+
+
+def cpu_baseline(cert, corr, grids, cost1, args):
+    """Oracle port of _evaluate_numba on a bounded config sample, all threads."""
+    from oracle import oracle
+    threads = os.cpu_count() or 1
+    sm, thr, ns = oracle.grid_configs(grids)
+    rng = np.random.default_rng(2)
+    n = max(threads * 2, 32)
+    pick = np.sort(rng.choice(sm.shape[0], size=n, replace=False))
+    oracle.evaluate_encoded(cert, corr, sm[pick[:threads]], thr[pick[:threads]],
+                            ns[pick[:threads]], cost1, n_threads=threads)  # warm
+    t = time.perf_counter()
+    oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1, n_threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": "config-evals/s", "cores": threads, "kind": "port",
+            "sample": f"{n} configs sampled uniformly from the {sm.shape[0]} of cfg2, all 1M "
+                      f"records each ({dt:.1f} s)"}
+
+
+# ---------------------------------------------------------- reference -----
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import oracle
+    _, cert, corr, grids, cost1 = workload(seed=0)
+    threads = os.cpu_count() or 1
+    sm, thr, ns = oracle.grid_configs(grids)
+    rng = np.random.default_rng(3)
+    per_step = max(threads, 16)
+    for _ in range(args.warmup):
+        p = rng.choice(sm.shape[0], size=per_step, replace=False)
+        oracle.evaluate_encoded(cert, corr, sm[p], thr[p], ns[p], cost1, n_threads=threads)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        p = rng.choice(sm.shape[0], size=per_step, replace=False)
+        oracle.evaluate_encoded(cert, corr, sm[p], thr[p], ns[p], cost1, n_threads=threads)
+    dt = time.perf_counter() - t
+    value = args.steps * per_step / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "config-evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_records": N_REC, "n_models": N_MODELS,
+                   "grid_levels": LEVELS},
+        "cpu_baseline": {"value": value, "unit": "config-evals/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{per_step} random configs per step x all 1M records "
+                                   f"(oracle/oracle_eval.c restating kernels._evaluate_numba)"},
+        "e2e": {"value": value, "unit": "config-evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--skip-stage", action="store_true", help="skip the stage-step leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")),
+                      int(os.environ.get("RANK", "0")))
+        return
+    world, rank, local = init_dist()
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

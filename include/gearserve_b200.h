@@ -1,0 +1,187 @@
+/*
+ * gearserve_b200.h — C ABI of the B200-native CascadeServe hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * passed as void*.  No torch types cross this boundary.  Functions return
+ * GS_OK (0) or a negative GS_E* code; gs_strerror() names it.  The library
+ * keeps no global mutable state: scratch memory is caller-owned workspace
+ * whose size is queried first, so every call is re-entrant per stream.
+ *
+ * The reference (gearserve, pure Python) has no native code; each entry
+ * point below replaces one Python function of the reference, cited by
+ * file:line under /root/reference/pkg/src/gearserve/.
+ */
+#ifndef GEARSERVE_B200_H
+#define GEARSERVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_OK 0
+#define GS_EINVAL (-1)       /* malformed argument -> Python ValueError      */
+#define GS_ECUDA (-2)        /* CUDA runtime error -> Python RuntimeError    */
+#define GS_EWORKSPACE (-3)   /* workspace smaller than the queried size      */
+#define GS_EUNSUPPORTED (-4) /* shape outside the kernel's supported range   */
+
+#define GS_MAX_MODELS 8      /* grid path: models per validation set        */
+#define GS_MAX_STAGES 16     /* list path: stages per encoded cascade        */
+
+/* certainty kinds for gs_certainty / gs_stage_step */
+#define GS_CERT_MARGIN 0      /* Eq. 5: top1 - top2 (singleton: the score)   */
+#define GS_CERT_MAX_SOFTMAX 1 /* extension: max_i softmax(x)_i              */
+#define GS_CERT_ENTROPY 2     /* extension: 1 - H(softmax(x)) / ln(n_cls)    */
+
+/* score dtypes */
+#define GS_F32 0
+#define GS_F64 1
+#define GS_BF16 2
+
+int gs_version(void);
+const char* gs_strerror(int code);
+/* last CUDA error string seen by this thread (for GS_ECUDA) */
+const char* gs_last_cuda_error(void);
+
+/* ------------------------------------------------------------------------
+ * List path: drop-in for kernels.evaluate_encoded (src/kernels.py:93-108),
+ * same arithmetic as _evaluate_numba (src/kernels.py:39-62).
+ *   certainty    [n_rec, n_models] f64 row-major
+ *   correct      [n_rec, n_models] u8
+ *   stage_model  [n_casc, max_len] i32, -1 padded
+ *   thresholds   [n_casc, max_len] f64 (last stage unused)
+ *   n_stages     [n_casc] i32
+ *   cost1        [n_models] f64
+ * outputs: accuracy [n_casc] f64, mean_cost [n_casc] f64,
+ *          forward_frac [n_casc, max_len] f64 (padding columns = 0)
+ * ---------------------------------------------------------------------- */
+int gs_eval_encoded_workspace(int64_t n_rec, int32_t n_models, int64_t n_casc,
+                              int32_t max_len, size_t* bytes);
+int gs_eval_encoded(const double* certainty, const uint8_t* correct,
+                    int64_t n_rec, int32_t n_models,
+                    const int32_t* stage_model, const double* thresholds,
+                    const int32_t* n_stages, int64_t n_casc, int32_t max_len,
+                    const double* cost1, double* accuracy, double* mean_cost,
+                    double* forward_frac, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Grid path: the full cascade x per-stage-threshold product over per-model
+ * threshold grids (cascades.ThresholdGrid, src/cascades.py:132-163), scored
+ * with the same outputs as evaluate_encoded on the enumerated cascades.
+ *
+ * Model columns are taken in the given order (the caller passes them cheap
+ * to expensive, the order sample_cascades uses, src/cascades.py:181-182).
+ * Enumeration: every non-empty model subset ("structure"), by size, then
+ * lexicographically (itertools.combinations order); inside a structure the
+ * threshold index tuple (k_1..k_{K-1}) is lexicographic, k_1 slowest.
+ *   grids     concatenated per-model grids on the DEVICE, f64, each strictly
+ *             increasing (grid_len[j] values for model j)
+ *   grid_len  HOST array [n_models]
+ * gs_grid_info reports the config count and the workspace the table needs.
+ * gs_grid_build fills the workspace (histogram + prefix tables); it must run
+ * before gs_grid_eval / gs_grid_pareto on the same workspace.
+ * ---------------------------------------------------------------------- */
+typedef struct gs_grid_info {
+  int64_t n_configs;      /* total configs of the enumeration            */
+  int64_t n_cells;        /* prefix-table cells                          */
+  int32_t n_structures;   /* 2^n_models - 1                              */
+  int32_t words_per_cell; /* packed u64 words per cell                   */
+  int32_t field_bits;     /* bits per packed count field                 */
+  int32_t max_len;        /* = n_models (forward_frac row width)         */
+  size_t workspace_bytes; /* for gs_grid_build / eval / pareto           */
+} gs_grid_info;
+
+int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
+                 gs_grid_info* info);
+int gs_grid_build(const double* certainty, const uint8_t* correct,
+                  int64_t n_rec, int32_t n_models, const double* grids,
+                  const int32_t* grid_len, void* workspace,
+                  size_t workspace_bytes, void* stream);
+/* Score configs [config_begin, config_begin + config_count).  Any output
+ * pointer may be NULL to skip it.  n_correct receives the integer correct
+ * count (accuracy * n_rec) used by the exact Pareto reduction. */
+int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
+                 const double* cost1, int64_t config_begin,
+                 int64_t config_count, double* accuracy, double* mean_cost,
+                 double* forward_frac, uint32_t* n_correct,
+                 const void* workspace, size_t workspace_bytes, void* stream);
+/* Decode config indices into the encoded-cascade form of
+ * cascades.encode_cascades (src/cascades.py:66-79): stage_model (-1 pad),
+ * thresholds (grid values, 0 pad), n_stages.  max_len = n_models. */
+int gs_grid_decode(int32_t n_models, const int32_t* grid_len,
+                   const double* grids, const int64_t* config_idx,
+                   int64_t count, int32_t* stage_model, double* thresholds,
+                   int32_t* n_stages, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Pareto front, semantics of cascades.pareto_filter (src/cascades.py:116-129):
+ * keep items no other item dominates (acc >=, cost <=, one strict); exact
+ * ties survive; output in input order.
+ *
+ * gs_pareto_counts: accuracy given as integer correct counts in [0, n_rec]
+ * (division by the same n_rec is monotone, so this is exact).  O(n + n_rec).
+ * Writes keep[n] (optional) and the kept indices (ascending, + base_index)
+ * to kept_idx with their count to *n_kept (device int64).
+ * gs_pareto_generic: float accuracies, O(n^2) tiled; for small lists.
+ * ---------------------------------------------------------------------- */
+int gs_pareto_counts_workspace(int64_t n, int64_t n_rec, size_t* bytes);
+int gs_pareto_counts(const uint32_t* n_correct, const double* cost, int64_t n,
+                     int64_t n_rec, int64_t base_index, uint8_t* keep,
+                     int64_t* kept_idx, int64_t* n_kept, void* workspace,
+                     size_t workspace_bytes, void* stream);
+int gs_pareto_generic(const double* accuracy, const double* cost, int64_t n,
+                      uint8_t* keep, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Certainty of score rows: cascades.certainty (src/cascades.py:20-28) for
+ * GS_CERT_MARGIN, bit-exact (top two found in the source dtype, subtracted
+ * in f64; a row of length 1 returns its score).  row_len (optional, device
+ * i32 [n_rows]) gives ragged row lengths <= n_cls (0 -> GS_EINVAL).
+ * ---------------------------------------------------------------------- */
+int gs_certainty(const void* scores, int32_t dtype, int64_t n_rows,
+                 int32_t n_cls, int64_t row_stride, const int32_t* row_len,
+                 int32_t kind, double* cert_out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Online stage step (EngineState.finish_batch gate, src/engine.py:355-383):
+ * certainty of each row's logits -> gate (last || cert >= thr, inclusive)
+ * -> stable compaction of deferred rows in batch order -> optional gather of
+ * the deferred rows' payload into the next stage's contiguous buffer.
+ *   thr       [n_rows] f64 per-row threshold (rows may carry different gears)
+ *   is_last   [n_rows] u8 (NULL = none last)
+ *   cert_out  [n_rows] f64 (optional), stop_out [n_rows] u8 (optional)
+ *   deferred_idx [n_rows] i64 capacity; *n_deferred (device i64)
+ *   near_idx  rows with |cert - thr| <= near_eps (non-last), ascending,
+ *             *n_near (device i64); NULL to skip
+ *   payload / next_payload: row-major, payload_row_bytes each (NULL to skip)
+ * ---------------------------------------------------------------------- */
+int gs_stage_step_workspace(int64_t n_rows, size_t* bytes);
+int gs_stage_step(const void* scores, int32_t dtype, int64_t n_rows,
+                  int32_t n_cls, int64_t row_stride, int32_t kind,
+                  const double* thr, const uint8_t* is_last, double* cert_out,
+                  uint8_t* stop_out, int64_t* deferred_idx,
+                  int64_t* n_deferred, double near_eps, int64_t* near_idx,
+                  int64_t* n_near, const void* payload,
+                  int64_t payload_row_bytes, void* next_payload,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Gate over precomputed certainty matrices (the engine's CompiledPlan.cert /
+ * corr, src/engine.py:217): item i looks up cert[row[i], model[i]].  Writes
+ * stop[i], correct[i] (= corr[row, model] for stopped items, else 0) and the
+ * deferred item positions in batch order. */
+int gs_stage_gate(const double* certainty, const uint8_t* correct,
+                  int64_t n_rec, int32_t n_models, const int64_t* row,
+                  const int32_t* model, const double* thr,
+                  const uint8_t* is_last, int64_t n_items, uint8_t* stop_out,
+                  uint8_t* correct_out, int64_t* deferred_idx,
+                  int64_t* n_deferred, double near_eps, int64_t* near_idx,
+                  int64_t* n_near, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEARSERVE_B200_H */

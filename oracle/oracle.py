@@ -1,0 +1,296 @@
+"""CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Restatements of the reference (gearserve, /root/reference/pkg/src/gearserve)
+for the hot path, used as the checker by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference arm.  Nothing in the product
+package imports this module.
+
+Pinned: tests/test_oracle.py checks every function here against golden
+vectors captured from the reference itself (tests/golden/make_golden.py,
+run where /root/reference is importable) — see DESIGN.md "Oracle".
+
+Functions and the reference lines they restate:
+  evaluate_encoded      kernels._evaluate_numba        kernels.py:39-62   (C, oracle_eval.c)
+  grid_configs          enumeration of the grid product (documented in gridsweep.py)
+  certainty             cascades.certainty              cascades.py:20-28
+  margin_rows           cascades.certainty over a matrix (f64 after promotion)
+  max_softmax_rows / entropy_rows   extension definitions (no reference; unpinned)
+  pareto_keep           cascades.pareto_filter          cascades.py:116-129
+  choose_weighted       engine.choose_weighted          engine.py:238-245
+  finish_batch          EngineState.finish_batch        engine.py:355-383
+  stage_step            gate + stable compaction of finish_batch on score rows
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+BUILD = HERE / "_build"
+LIB = BUILD / "liboracle.so"
+
+
+def build(force: bool = False) -> Path:
+    """gcc the C restatement (OpenMP, no FP contraction)."""
+    src = HERE / "oracle_eval.c"
+    if not force and LIB.exists() and LIB.stat().st_mtime >= src.stat().st_mtime:
+        return LIB
+    BUILD.mkdir(exist_ok=True)
+    tmp = LIB.with_suffix(".so.tmp")
+    subprocess.run(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
+                    str(src), "-o", str(tmp)], check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(str(LIB))
+        P = ctypes.c_void_p
+        lib.oracle_evaluate_encoded.argtypes = [P, P, ctypes.c_int64, ctypes.c_int32, P, P, P,
+                                                ctypes.c_int64, ctypes.c_int32, P, P, P, P,
+                                                ctypes.c_int32]
+        lib.oracle_evaluate_encoded.restype = None
+        lib.oracle_grid_n_configs.argtypes = [ctypes.c_int32, P]
+        lib.oracle_grid_n_configs.restype = ctypes.c_int64
+        lib.oracle_grid_configs.argtypes = [ctypes.c_int32, P, P, ctypes.c_int64,
+                                            ctypes.c_int64, P, P, P]
+        lib.oracle_grid_configs.restype = ctypes.c_int
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ------------------------------------------------------------ the walk ----
+def evaluate_encoded(certainty, correct, stage_model, thresholds, n_stages, cost1,
+                     n_threads: int = 1):
+    """(accuracy, mean_cost, forward_frac) exactly as _evaluate_numba."""
+    cert = np.ascontiguousarray(certainty, dtype=np.float64)
+    corr = np.ascontiguousarray(correct, dtype=np.uint8)
+    sm = np.ascontiguousarray(stage_model, dtype=np.int32)
+    thr = np.ascontiguousarray(thresholds, dtype=np.float64)
+    ns = np.ascontiguousarray(n_stages, dtype=np.int32)
+    c1 = np.ascontiguousarray(cost1, dtype=np.float64)
+    n_casc, L = sm.shape
+    acc = np.zeros(n_casc)
+    cost = np.zeros(n_casc)
+    frac = np.zeros((n_casc, L))
+    if n_casc:
+        _load().oracle_evaluate_encoded(_p(cert), _p(corr), cert.shape[0], cert.shape[1],
+                                        _p(sm), _p(thr), _p(ns), n_casc, L, _p(c1), _p(acc),
+                                        _p(cost), _p(frac), int(n_threads))
+    return acc, cost, frac
+
+
+def walk_python(certainty, correct, stage_model, thresholds, n_stages, cost1):
+    """Pure-Python restatement (small cases only) — pins the C port."""
+    n_rec = certainty.shape[0]
+    n_casc, L = stage_model.shape
+    acc = np.zeros(n_casc)
+    cost = np.zeros(n_casc)
+    frac = np.zeros((n_casc, L))
+    for c in range(n_casc):
+        ns = int(n_stages[c])
+        n_correct = 0
+        for r in range(n_rec):
+            for s in range(ns):
+                m = int(stage_model[c, s])
+                frac[c, s] += 1.0
+                if s == ns - 1 or certainty[r, m] >= thresholds[c, s]:
+                    n_correct += int(correct[r, m])
+                    break
+        for s in range(ns):
+            f = frac[c, s] / n_rec
+            frac[c, s] = f
+            cost[c] += f * cost1[int(stage_model[c, s])]
+        acc[c] = n_correct / n_rec
+    return acc, cost, frac
+
+
+def grid_n_configs(grid_len) -> int:
+    gl = np.ascontiguousarray(grid_len, dtype=np.int32)
+    return int(_load().oracle_grid_n_configs(len(gl), _p(gl)))
+
+
+def grid_configs(grids, begin: int = 0, count: int | None = None):
+    """Encoded cascades (stage_model, thresholds, n_stages) of the grid
+    product configs [begin, begin+count)."""
+    gl = np.ascontiguousarray([len(g) for g in grids], dtype=np.int32)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(g, np.float64) for g in grids]))
+    total = grid_n_configs(gl)
+    if count is None:
+        count = total - begin
+    M = len(grids)
+    sm = np.empty((count, M), dtype=np.int32)
+    thr = np.empty((count, M), dtype=np.float64)
+    ns = np.empty(count, dtype=np.int32)
+    if count:
+        _load().oracle_grid_configs(M, _p(gl), _p(flat), begin, count, _p(sm), _p(thr), _p(ns))
+    return sm, thr, ns
+
+
+# ------------------------------------------------------------ certainty ---
+def certainty(scores) -> float:
+    """cascades.certainty: top minus second of the sorted scores; a single
+    score is returned as is; empty raises ValueError."""
+    if len(scores) == 0:
+        raise ValueError("certainty of empty scores")
+    if len(scores) == 1:
+        return float(scores[0])
+    top, second = sorted(scores, reverse=True)[:2]
+    return float(top - second)
+
+
+def margin_rows(scores: np.ndarray, row_len=None) -> np.ndarray:
+    """Eq. 5 per row on the values promoted to f64 (vectorised)."""
+    x = np.asarray(scores).astype(np.float64)
+    n, c = x.shape
+    if row_len is not None:
+        row_len = np.asarray(row_len)
+        x = x.copy()
+        x[np.arange(c)[None, :] >= row_len[:, None]] = -np.inf
+    else:
+        row_len = np.full(n, c)
+    if c == 1:
+        return x[:, 0].copy()
+    part = -np.partition(-x, 1, axis=1)[:, :2]
+    out = part[:, 0] - part[:, 1]
+    single = row_len == 1
+    out[single] = x[single, 0]
+    return out
+
+
+def max_softmax_rows(scores: np.ndarray) -> np.ndarray:
+    """Extension: max softmax probability = 1 / sum exp(x - max), f64."""
+    x = np.asarray(scores).astype(np.float64)
+    m = x.max(axis=1, keepdims=True)
+    return 1.0 / np.exp(x - m).sum(axis=1)
+
+
+def entropy_rows(scores: np.ndarray) -> np.ndarray:
+    """Extension: 1 - H(softmax(x)) / ln(n_cls), f64 (1.0 for n_cls == 1)."""
+    x = np.asarray(scores).astype(np.float64)
+    n_cls = x.shape[1]
+    if n_cls == 1:
+        return np.ones(x.shape[0])
+    d = x - x.max(axis=1, keepdims=True)
+    e = np.exp(d)
+    s = e.sum(axis=1)
+    t = (e * d).sum(axis=1)
+    H = np.log(s) - t / s
+    return 1.0 - H / np.log(n_cls)
+
+
+CERT_ORACLES = {"margin": margin_rows, "max_softmax": max_softmax_rows,
+                "entropy": entropy_rows}
+
+
+# ---------------------------------------------------------------- pareto --
+def pareto_keep(acc, cost) -> np.ndarray:
+    """Boolean keep mask with pareto_filter's exact semantics (O(n log n)):
+    keep e iff acc_e is the max of its cost group and exceeds the best
+    accuracy over strictly cheaper groups."""
+    acc = np.asarray(acc, dtype=np.float64)
+    cost = np.asarray(cost, dtype=np.float64)
+    n = acc.size
+    if n == 0:
+        return np.zeros(0, dtype=bool)
+    order = np.lexsort((-acc, cost))
+    keep = np.zeros(n, dtype=bool)
+    best_cheaper = -np.inf
+    i = 0
+    while i < n:
+        j = i
+        c = cost[order[i]]
+        while j < n and cost[order[j]] == c:
+            j += 1
+        group = order[i:j]
+        gmax = acc[group].max()
+        if gmax > best_cheaper:
+            keep[group[acc[group] == gmax]] = True
+        best_cheaper = max(best_cheaper, gmax)
+        i = j
+    return keep
+
+
+def pareto_keep_quadratic(acc, cost) -> np.ndarray:
+    """Literal O(n^2) restatement of pareto_filter (small n)."""
+    n = len(acc)
+    keep = np.ones(n, dtype=bool)
+    for i in range(n):
+        for j in range(n):
+            if (acc[j] >= acc[i] and cost[j] <= cost[i]
+                    and (acc[j] > acc[i] or cost[j] < cost[i])):
+                keep[i] = False
+                break
+    return keep
+
+
+# ------------------------------------------------------------ stage step --
+def choose_weighted(cum_weights: np.ndarray, rng: np.random.Generator) -> int:
+    """engine.choose_weighted: one rng.random() scaled by the total, or
+    rng.integers(len) when every weight is zero."""
+    total = cum_weights[-1]
+    if total <= 0.0:
+        return int(rng.integers(len(cum_weights)))
+    x = rng.random() * total
+    return int(np.searchsorted(cum_weights, x, side="right").clip(0, len(cum_weights) - 1))
+
+
+def stage_step(cert: np.ndarray, thr: np.ndarray, is_last=None, near_eps: float = 1e-6,
+               payload: np.ndarray | None = None):
+    """finish_batch's gate on a batch: stop mask, deferred rows in batch
+    order, rows within near_eps of their threshold (non-last), gathered
+    payload."""
+    cert = np.asarray(cert, dtype=np.float64)
+    thr = np.broadcast_to(np.asarray(thr, dtype=np.float64), cert.shape)
+    last = np.zeros(cert.shape, dtype=bool) if is_last is None else np.asarray(is_last, bool)
+    stop = last | (cert >= thr)
+    deferred = np.flatnonzero(~stop)
+    near = np.flatnonzero(~last & (np.abs(cert - thr) <= near_eps))
+    nxt = None if payload is None else payload[deferred]
+    return stop, deferred, near, nxt
+
+
+def finish_batch(items, gears, cert, corr, rng, now):
+    """EngineState.finish_batch restated on plain data.
+
+    items: list of dicts {request_id, row, stage, gear, arrival_us}
+    gears: list of dicts {stage_model: [..], thresholds: [.., None],
+           replica_idx: [array per stage], cum_weights: [array per stage]}
+    Returns (completed, forwarded): completed = [(request_id, correct,
+    stages_executed, latency)], forwarded = [(item position, replica)] in
+    batch order; rng is advanced exactly as the reference advances it.
+    """
+    completed, forwarded = [], []
+    for pos, it in enumerate(items):
+        g = gears[it["gear"]]
+        m = g["stage_model"][it["stage"]]
+        thr = g["thresholds"][it["stage"]]
+        last = it["stage"] == len(g["stage_model"]) - 1
+        if last or cert[it["row"], m] >= thr:
+            completed.append((it["request_id"], bool(corr[it["row"], m]), it["stage"] + 1,
+                              now - it["arrival_us"]))
+        else:
+            nxt = it["stage"] + 1
+            p = choose_weighted(g["cum_weights"][nxt], rng)
+            forwarded.append((pos, int(g["replica_idx"][nxt][p])))
+    return completed, forwarded

@@ -1,0 +1,562 @@
+// gs_stage.cu — online cascade stage step.
+//
+// Reference: EngineState.finish_batch (/root/reference/pkg/src/gearserve/
+// engine.py:355-383): item i stops when its stage is the cascade's last or
+// cert[row, m] >= thr (inclusive, :366-367); otherwise it is forwarded and
+// appended, in batch order, to a next-stage queue (:377-382).  Certainty is
+// Eq. 5, top score minus second score, a singleton returning the score
+// itself (cascades.certainty, src/cascades.py:20-28).
+//
+// B200 mapping.  One pass over the stage's score rows:
+//   * wide rows (n_cls >= 32): one warp per row, 128-bit vector loads,
+//     per-lane top-2 / max / exp-sums, warp-shuffle reductions;
+//   * narrow rows (binary heads etc.): one thread per row;
+//   * gate, then order-preserving compaction of the deferred rows with a
+//     single-pass decoupled look-back scan (ballot + popc inside the block),
+//     so deferred indices land in batch order without a second kernel;
+//   * the deferred rows' payload is gathered into the next stage's
+//     contiguous batch buffer by the same CTA.
+// Margin certainty is bit-exact: the top two are found in the source dtype
+// (exact) and subtracted in f64, like the reference on the same values
+// promoted to f64.  Max-softmax / entropy are extensions (no reference
+// oracle): exp in f32 (expf, <= 2 ulp), sums in f64.
+#include <algorithm>
+
+#include "gs_common.cuh"
+
+namespace gs {
+namespace {
+
+struct bf16_t {
+  uint16_t v;
+};
+
+__device__ __forceinline__ float to_float(float x) { return x; }
+__device__ __forceinline__ double to_float(double x) { return x; }
+__device__ __forceinline__ float to_float(bf16_t x) {
+  return __uint_as_float((uint32_t)x.v << 16);
+}
+
+template <typename T>
+struct Compute {
+  using type = float;
+};
+template <>
+struct Compute<double> {
+  using type = double;
+};
+
+template <typename C>
+__device__ __forceinline__ C neg_inf();
+template <>
+__device__ __forceinline__ float neg_inf<float>() {
+  return __int_as_float(0xff800000);
+}
+template <>
+__device__ __forceinline__ double neg_inf<double>() {
+  return __longlong_as_double(0xfff0000000000000ll);
+}
+
+template <typename C>
+__device__ __forceinline__ void push_top2(C x, C& m1, C& m2) {
+  if (x > m1) {
+    m2 = m1;
+    m1 = x;
+  } else if (x > m2) {
+    m2 = x;
+  }
+}
+
+template <typename C>
+__device__ __forceinline__ void merge_top2(C& m1, C& m2, C o1, C o2) {
+  const C hi = m1 > o1 ? m1 : o1;
+  const C lo = m1 > o1 ? o1 : m1;
+  const C s = m2 > o2 ? m2 : o2;
+  m1 = hi;
+  m2 = lo > s ? lo : s;
+}
+
+__device__ __forceinline__ double exp_term(float d) { return (double)expf(d); }
+__device__ __forceinline__ double exp_term(double d) { return exp(d); }
+
+// 16-byte vector of T
+template <typename T>
+struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+
+template <typename T, typename F>
+__device__ __forceinline__ void warp_for_each(const T* row, int n, bool vec_ok, F&& f) {
+  const int lane = (int)lane_id();
+  if (vec_ok) {
+    constexpr int V = Vec16<T>::N;
+    const int nv = n / V;
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    int i = lane;
+    // two 16-byte loads in flight per lane per iteration
+    for (; i + 32 < nv; i += 64) {
+      uint4 r0 = __ldg(rv + i);
+      uint4 r1 = __ldg(rv + i + 32);
+      const T* t0 = reinterpret_cast<const T*>(&r0);
+      const T* t1 = reinterpret_cast<const T*>(&r1);
+#pragma unroll
+      for (int u = 0; u < V; ++u) f(t0[u]);
+#pragma unroll
+      for (int u = 0; u < V; ++u) f(t1[u]);
+    }
+    for (; i < nv; i += 32) {
+      uint4 r0 = __ldg(rv + i);
+      const T* t0 = reinterpret_cast<const T*>(&r0);
+#pragma unroll
+      for (int u = 0; u < V; ++u) f(t0[u]);
+    }
+    for (int j = nv * V + lane; j < n; j += 32) f(row[j]);
+  } else {
+    for (int j = lane; j < n; j += 32) f(row[j]);
+  }
+}
+
+// Certainty of one row, computed by a full warp; result valid in all lanes.
+template <typename T, int KIND>
+__device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok) {
+  using C = typename Compute<T>::type;
+  if (n == 1) {
+    const double x0 = (double)to_float(row[0]);
+    return KIND == GS_CERT_MARGIN ? x0 : 1.0;
+  }
+  if (KIND == GS_CERT_MARGIN) {
+    C m1 = neg_inf<C>(), m2 = neg_inf<C>();
+    warp_for_each<T>(row, n, vec_ok, [&](T x) { push_top2<C>((C)to_float(x), m1, m2); });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const C o1 = __shfl_xor_sync(0xffffffffu, m1, o);
+      const C o2 = __shfl_xor_sync(0xffffffffu, m2, o);
+      merge_top2<C>(m1, m2, o1, o2);
+    }
+    return (double)m1 - (double)m2;
+  } else {
+    C m = neg_inf<C>();
+    warp_for_each<T>(row, n, vec_ok, [&](T x) {
+      const C v = (C)to_float(x);
+      m = v > m ? v : m;
+    });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const C y = __shfl_xor_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
+    }
+    double s = 0.0, t = 0.0;
+    warp_for_each<T>(row, n, vec_ok, [&](T x) {
+      const C d = (C)to_float(x) - m;
+      const double e = exp_term(d);
+      s += e;
+      if (KIND == GS_CERT_ENTROPY) t += e * (double)d;
+    });
+    s = warp_sum(s);
+    if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / s;
+    t = warp_sum(t);
+    const double H = log(s) - t / s;
+    return 1.0 - H / log((double)n);
+  }
+}
+
+// Certainty of one row computed by one thread.
+template <typename T, int KIND>
+__device__ __forceinline__ double thread_row_cert(const T* row, int n) {
+  using C = typename Compute<T>::type;
+  if (n == 1) {
+    const double x0 = (double)to_float(row[0]);
+    return KIND == GS_CERT_MARGIN ? x0 : 1.0;
+  }
+  if (KIND == GS_CERT_MARGIN) {
+    C m1 = neg_inf<C>(), m2 = neg_inf<C>();
+    for (int j = 0; j < n; ++j) push_top2<C>((C)to_float(row[j]), m1, m2);
+    return (double)m1 - (double)m2;
+  } else {
+    C m = neg_inf<C>();
+    for (int j = 0; j < n; ++j) {
+      const C v = (C)to_float(row[j]);
+      m = v > m ? v : m;
+    }
+    double s = 0.0, t = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const C d = (C)to_float(row[j]) - m;
+      const double e = exp_term(d);
+      s += e;
+      if (KIND == GS_CERT_ENTROPY) t += e * (double)d;
+    }
+    if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / s;
+    const double H = log(s) - t / s;
+    return 1.0 - H / log((double)n);
+  }
+}
+
+// --------------------------------------------------------- gs_certainty --
+template <typename T, int KIND, bool WIDE>
+__global__ void __launch_bounds__(256) certainty_kernel(const T* scores, int64_t n_rows, int n_cls,
+                                                        int64_t stride, const int32_t* row_len,
+                                                        bool vec_ok, double* out) {
+  if (WIDE) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw) {
+      const int n = row_len ? row_len[r] : n_cls;
+      const double c = warp_row_cert<T, KIND>(scores + r * stride, n, vec_ok && n == n_cls);
+      if (lane_id() == 0) out[r] = c;
+    }
+  } else {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      const int n = row_len ? row_len[r] : n_cls;
+      out[r] = thread_row_cert<T, KIND>(scores + r * stride, n);
+    }
+  }
+}
+
+// --------------------------------------------------------- stage step ----
+struct StepArgs {
+  const void* scores;
+  int64_t n_rows;
+  int32_t n_cls;
+  int64_t stride;
+  int32_t vec_ok;
+  const double* thr;
+  const uint8_t* is_last;
+  double* cert_out;
+  uint8_t* stop_out;
+  int64_t* deferred_idx;
+  int64_t* n_deferred;
+  double near_eps;
+  int64_t* near_idx;
+  int64_t* n_near;
+  const uint8_t* payload;
+  int64_t payload_bytes;
+  uint8_t* next_payload;
+  uint64_t* states;
+  unsigned long long* counter;
+  int64_t n_tiles;
+  int32_t rows_per_tile;
+};
+
+constexpr int kStepThreads = 256;
+constexpr int kWideRowsPerWarp = 8;
+constexpr int kWideTile = (kStepThreads / 32) * kWideRowsPerWarp;  // 64 rows
+
+__device__ __forceinline__ void copy_payload_row(const uint8_t* src, uint8_t* dst, int64_t bytes,
+                                                 bool vec) {
+  const int lane = (int)lane_id();
+  if (vec) {
+    const int64_t nv = bytes / 16;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int64_t j = lane; j < nv; j += 32) d[j] = __ldg(s + j);
+  } else {
+    for (int64_t j = lane; j < bytes; j += 32) dst[j] = src[j];
+  }
+}
+
+// Gate + compaction + payload gather for one tile; `cert` is this thread's
+// row certainty (thread t owns row base + t when t < rows).
+__device__ __forceinline__ void gate_tile(const StepArgs& a, int64_t tile, int64_t base, int rows,
+                                          double cert, int64_t* s_rows, uint32_t* s_warp,
+                                          uint64_t* s_misc) {
+  const int t = threadIdx.x;
+  const int64_t r = base + t;
+  bool defer = false, near = false;
+  if (t < rows) {
+    const bool last = a.is_last ? a.is_last[r] != 0 : false;
+    const double th = a.thr[r];
+    const bool stop = last || cert >= th;
+    defer = !stop;
+    near = !last && fabs(cert - th) <= a.near_eps;
+    if (a.cert_out) a.cert_out[r] = cert;
+    if (a.stop_out) a.stop_out[r] = stop ? 1 : 0;
+  }
+  const PairScan ps = block_pair_scan(defer, near && a.near_idx != nullptr, a.states, tile, s_warp, s_misc);
+  if (defer) a.deferred_idx[ps.a_off] = r;
+  if (near && a.near_idx) a.near_idx[ps.b_off] = r;
+  if (tile == a.n_tiles - 1 && t == 0) {
+    *a.n_deferred = (int64_t)ps.a_total;
+    if (a.n_near) *a.n_near = a.near_idx ? (int64_t)ps.b_total : 0;
+  }
+  if (a.payload && a.next_payload && a.payload_bytes > 0) {
+    const uint32_t tile_count = __syncthreads_count(defer);
+    const uint64_t tile_base = ps.a_total - tile_count;
+    if (defer) s_rows[ps.a_off - tile_base] = r;
+    __syncthreads();
+    const bool vec = aligned16(a.payload) && aligned16(a.next_payload) && (a.payload_bytes % 16 == 0);
+    for (uint32_t j = threadIdx.x >> 5; j < tile_count; j += blockDim.x >> 5) {
+      const int64_t src_row = s_rows[j];
+      copy_payload_row(a.payload + src_row * a.payload_bytes,
+                       a.next_payload + (int64_t)(tile_base + j) * a.payload_bytes,
+                       a.payload_bytes, vec);
+    }
+  }
+}
+
+template <typename T, int KIND, bool WIDE>
+__global__ void __launch_bounds__(kStepThreads) stage_step_kernel(const __grid_constant__ StepArgs a) {
+  __shared__ uint32_t s_warp[64];
+  __shared__ uint64_t s_misc[4];
+  __shared__ int64_t s_tile;
+  __shared__ double s_cert[kStepThreads];
+  __shared__ int64_t s_rows[kStepThreads];
+  const int64_t tile = next_tile_id(a.counter, &s_tile);
+  const int64_t base = tile * a.rows_per_tile;
+  const int rows = (int)min((int64_t)a.rows_per_tile, a.n_rows - base);
+  const T* scores = static_cast<const T*>(a.scores);
+  double cert = 0.0;
+  if (WIDE) {
+    const int warp = threadIdx.x >> 5;
+    for (int k = 0; k < kWideRowsPerWarp; ++k) {
+      const int lr = warp * kWideRowsPerWarp + k;
+      if (lr < rows) {
+        const double c = warp_row_cert<T, KIND>(scores + (base + lr) * a.stride, a.n_cls, a.vec_ok);
+        if (lane_id() == 0) s_cert[lr] = c;
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < rows) cert = s_cert[threadIdx.x];
+  } else {
+    if ((int)threadIdx.x < rows)
+      cert = thread_row_cert<T, KIND>(scores + (base + threadIdx.x) * a.stride, a.n_cls);
+  }
+  gate_tile(a, tile, base, rows, cert, s_rows, s_warp, s_misc);
+}
+
+// ------------------------------------------------------------- gate -------
+struct GateArgs {
+  const double* cert;
+  const uint8_t* corr;
+  int64_t n_rec;
+  int32_t n_models;
+  const int64_t* row;
+  const int32_t* model;
+  const double* thr;
+  const uint8_t* is_last;
+  int64_t n_items;
+  uint8_t* stop_out;
+  uint8_t* correct_out;
+  int64_t* deferred_idx;
+  int64_t* n_deferred;
+  double near_eps;
+  int64_t* near_idx;
+  int64_t* n_near;
+  uint64_t* states;
+  unsigned long long* counter;
+  int64_t n_tiles;
+};
+
+__global__ void __launch_bounds__(256) stage_gate_kernel(const __grid_constant__ GateArgs a) {
+  __shared__ uint32_t s_warp[64];
+  __shared__ uint64_t s_misc[4];
+  __shared__ int64_t s_tile;
+  const int64_t tile = next_tile_id(a.counter, &s_tile);
+  const int64_t i = tile * blockDim.x + threadIdx.x;
+  bool defer = false, near = false;
+  if (i < a.n_items) {
+    const int64_t r = a.row[i];
+    const int m = a.model[i];
+    const bool ok = r >= 0 && r < a.n_rec && m >= 0 && m < a.n_models;
+    const double c = ok ? a.cert[r * a.n_models + m] : 0.0;
+    const bool last = a.is_last ? a.is_last[i] != 0 : false;
+    const double th = a.thr[i];
+    const bool stop = last || c >= th;
+    defer = !stop;
+    near = !last && fabs(c - th) <= a.near_eps;
+    if (a.stop_out) a.stop_out[i] = stop ? 1 : 0;
+    if (a.correct_out) a.correct_out[i] = (stop && ok) ? a.corr[r * a.n_models + m] : 0;
+  }
+  const PairScan ps = block_pair_scan(defer, near && a.near_idx != nullptr, a.states, tile, s_warp, s_misc);
+  if (defer) a.deferred_idx[ps.a_off] = i;
+  if (near && a.near_idx) a.near_idx[ps.b_off] = i;
+  if (tile == a.n_tiles - 1 && threadIdx.x == 0) {
+    *a.n_deferred = (int64_t)ps.a_total;
+    if (a.n_near) *a.n_near = a.near_idx ? (int64_t)ps.b_total : 0;
+  }
+}
+
+size_t step_ws_bytes(int64_t n_rows) {
+  const int64_t tiles = (n_rows + kWideTile - 1) / kWideTile;
+  return round_up((size_t)(tiles + 1) * 8, 256) + 256;
+}
+
+template <typename T, int KIND>
+cudaError_t launch_certainty(const void* scores, int64_t n_rows, int n_cls, int64_t stride,
+                             const int32_t* row_len, double* out, cudaStream_t st) {
+  const T* s = static_cast<const T*>(scores);
+  const bool vec_ok = aligned16(scores) && ((stride * (int64_t)sizeof(T)) % 16 == 0);
+  if (n_cls >= 32) {
+    int64_t blocks = (n_rows * 32 + 255) / 256;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
+    certainty_kernel<T, KIND, true><<<(unsigned)blocks, 256, 0, st>>>(s, n_rows, n_cls, stride, row_len,
+                                                                      vec_ok, out);
+  } else {
+    int64_t blocks = (n_rows + 255) / 256;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
+    certainty_kernel<T, KIND, false><<<(unsigned)blocks, 256, 0, st>>>(s, n_rows, n_cls, stride, row_len,
+                                                                       vec_ok, out);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch_certainty(int kind, const void* scores, int64_t n_rows, int n_cls, int64_t stride,
+                               const int32_t* row_len, double* out, cudaStream_t st) {
+  switch (kind) {
+    case GS_CERT_MARGIN: return launch_certainty<T, GS_CERT_MARGIN>(scores, n_rows, n_cls, stride, row_len, out, st);
+    case GS_CERT_MAX_SOFTMAX: return launch_certainty<T, GS_CERT_MAX_SOFTMAX>(scores, n_rows, n_cls, stride, row_len, out, st);
+    default: return launch_certainty<T, GS_CERT_ENTROPY>(scores, n_rows, n_cls, stride, row_len, out, st);
+  }
+}
+
+template <typename T, int KIND>
+cudaError_t launch_step(StepArgs a, cudaStream_t st) {
+  const bool wide = a.n_cls >= 32;
+  a.rows_per_tile = wide ? kWideTile : kStepThreads;
+  a.n_tiles = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
+  a.vec_ok = aligned16(a.scores) && ((a.stride * (int64_t)sizeof(T)) % 16 == 0);
+  if (a.n_tiles > 0x7fffffff) return cudaErrorInvalidValue;
+  if (wide)
+    stage_step_kernel<T, KIND, true><<<(unsigned)a.n_tiles, kStepThreads, 0, st>>>(a);
+  else
+    stage_step_kernel<T, KIND, false><<<(unsigned)a.n_tiles, kStepThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t dispatch_step(int kind, const StepArgs& a, cudaStream_t st) {
+  switch (kind) {
+    case GS_CERT_MARGIN: return launch_step<T, GS_CERT_MARGIN>(a, st);
+    case GS_CERT_MAX_SOFTMAX: return launch_step<T, GS_CERT_MAX_SOFTMAX>(a, st);
+    default: return launch_step<T, GS_CERT_ENTROPY>(a, st);
+  }
+}
+
+}  // namespace
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" int gs_certainty(const void* scores, int32_t dtype, int64_t n_rows, int32_t n_cls,
+                            int64_t row_stride, const int32_t* row_len, int32_t kind,
+                            double* cert_out, void* stream) {
+  GS_REQUIRE(n_rows >= 0 && n_cls >= 1 && row_stride >= n_cls);
+  GS_REQUIRE(kind >= GS_CERT_MARGIN && kind <= GS_CERT_ENTROPY);
+  if (n_rows == 0) return GS_OK;
+  GS_REQUIRE(scores && cert_out);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  switch (dtype) {
+    case GS_F32: e = dispatch_certainty<float>(kind, scores, n_rows, n_cls, row_stride, row_len, cert_out, st); break;
+    case GS_F64: e = dispatch_certainty<double>(kind, scores, n_rows, n_cls, row_stride, row_len, cert_out, st); break;
+    case GS_BF16: e = dispatch_certainty<bf16_t>(kind, scores, n_rows, n_cls, row_stride, row_len, cert_out, st); break;
+    default: return GS_EINVAL;
+  }
+  GS_CUDA_TRY(e);
+  return GS_OK;
+}
+
+extern "C" int gs_stage_step_workspace(int64_t n_rows, size_t* bytes) {
+  GS_REQUIRE(bytes && n_rows >= 0);
+  *bytes = step_ws_bytes(n_rows);
+  return GS_OK;
+}
+
+extern "C" int gs_stage_step(const void* scores, int32_t dtype, int64_t n_rows, int32_t n_cls,
+                             int64_t row_stride, int32_t kind, const double* thr,
+                             const uint8_t* is_last, double* cert_out, uint8_t* stop_out,
+                             int64_t* deferred_idx, int64_t* n_deferred, double near_eps,
+                             int64_t* near_idx, int64_t* n_near, const void* payload,
+                             int64_t payload_row_bytes, void* next_payload, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  GS_REQUIRE(n_rows >= 0 && n_cls >= 1 && row_stride >= n_cls && n_deferred);
+  GS_REQUIRE(kind >= GS_CERT_MARGIN && kind <= GS_CERT_ENTROPY);
+  GS_REQUIRE(payload_row_bytes >= 0);
+  if (n_rows >= ((int64_t)1 << 31) - 1) return GS_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_rows == 0) {
+    GS_CUDA_TRY(cudaMemsetAsync(n_deferred, 0, 8, st));
+    if (n_near) GS_CUDA_TRY(cudaMemsetAsync(n_near, 0, 8, st));
+    return GS_OK;
+  }
+  GS_REQUIRE(scores && thr && deferred_idx);
+  const size_t need = step_ws_bytes(n_rows);
+  if (!workspace || workspace_bytes < need) return GS_EWORKSPACE;
+  GS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, st));
+  StepArgs a{};
+  a.scores = scores;
+  a.n_rows = n_rows;
+  a.n_cls = n_cls;
+  a.stride = row_stride;
+  a.thr = thr;
+  a.is_last = is_last;
+  a.cert_out = cert_out;
+  a.stop_out = stop_out;
+  a.deferred_idx = deferred_idx;
+  a.n_deferred = n_deferred;
+  a.near_eps = near_eps;
+  a.near_idx = near_idx;
+  a.n_near = n_near;
+  a.payload = static_cast<const uint8_t*>(payload);
+  a.payload_bytes = payload_row_bytes;
+  a.next_payload = static_cast<uint8_t*>(next_payload);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  a.counter = reinterpret_cast<unsigned long long*>(ws);
+  a.states = reinterpret_cast<uint64_t*>(ws + 256);
+  cudaError_t e;
+  switch (dtype) {
+    case GS_F32: e = dispatch_step<float>(kind, a, st); break;
+    case GS_F64: e = dispatch_step<double>(kind, a, st); break;
+    case GS_BF16: e = dispatch_step<bf16_t>(kind, a, st); break;
+    default: return GS_EINVAL;
+  }
+  GS_CUDA_TRY(e);
+  return GS_OK;
+}
+
+extern "C" int gs_stage_gate(const double* certainty, const uint8_t* correct, int64_t n_rec,
+                             int32_t n_models, const int64_t* row, const int32_t* model,
+                             const double* thr, const uint8_t* is_last, int64_t n_items,
+                             uint8_t* stop_out, uint8_t* correct_out, int64_t* deferred_idx,
+                             int64_t* n_deferred, double near_eps, int64_t* near_idx,
+                             int64_t* n_near, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  GS_REQUIRE(n_items >= 0 && n_rec >= 0 && n_models >= 1 && n_deferred);
+  if (n_items >= ((int64_t)1 << 31) - 1) return GS_EUNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_items == 0) {
+    GS_CUDA_TRY(cudaMemsetAsync(n_deferred, 0, 8, st));
+    if (n_near) GS_CUDA_TRY(cudaMemsetAsync(n_near, 0, 8, st));
+    return GS_OK;
+  }
+  GS_REQUIRE(certainty && correct && row && model && thr && deferred_idx);
+  const size_t need = step_ws_bytes(n_items);
+  if (!workspace || workspace_bytes < need) return GS_EWORKSPACE;
+  GS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, st));
+  GateArgs a{};
+  a.cert = certainty;
+  a.corr = correct;
+  a.n_rec = n_rec;
+  a.n_models = n_models;
+  a.row = row;
+  a.model = model;
+  a.thr = thr;
+  a.is_last = is_last;
+  a.n_items = n_items;
+  a.stop_out = stop_out;
+  a.correct_out = correct_out;
+  a.deferred_idx = deferred_idx;
+  a.n_deferred = n_deferred;
+  a.near_eps = near_eps;
+  a.near_idx = near_idx;
+  a.n_near = n_near;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  a.counter = reinterpret_cast<unsigned long long*>(ws);
+  a.states = reinterpret_cast<uint64_t*>(ws + 256);
+  a.n_tiles = (n_items + 255) / 256;
+  stage_gate_kernel<<<(unsigned)a.n_tiles, 256, 0, st>>>(a);
+  GS_LAUNCH_CHECK();
+  return GS_OK;
+}

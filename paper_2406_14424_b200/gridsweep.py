@@ -1,0 +1,193 @@
+"""Full-grid gear-plan sweep over a validation set resident in HBM.
+
+Scores every (cascade structure x per-stage threshold) config of the grid
+product — the search space planner SP1 samples from
+(/root/reference/pkg/src/gearserve/planner.py:365-390 via
+cascades.sample_cascades, src/cascades.py:166-193) — with the reference's
+per-config outputs (accuracy, mean_cost, forward_frac; src/kernels.py:39-62)
+and the reference's Pareto semantics (src/cascades.py:116-129).
+
+Config enumeration (identical in the kernels, here, and in oracle/):
+structures are the non-empty model subsets in column order (columns are the
+cost order), by size then lexicographically (itertools.combinations); a
+structure (m_1..m_K) owns prod_{s<K} |grid[m_s]| configs whose threshold
+indices (k_1..k_{K-1}) are lexicographic with k_1 slowest.  Config c decodes
+to the encoded cascade stage_model = (m_1..m_K, -1 pad),
+thresholds = (grid[m_1][k_1], ..., grid[m_{K-1}][k_{K-1}], 0 pad).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .types import Cascade
+
+
+def structures(n_models: int, grid_len: Sequence[int]) -> list[tuple[tuple[int, ...], int, int]]:
+    """[(models, first_config, n_configs)] in enumeration order."""
+    out = []
+    off = 0
+    for k in range(1, n_models + 1):
+        for combo in itertools.combinations(range(n_models), k):
+            n = 1
+            for m in combo[:-1]:
+                n *= int(grid_len[m])
+            out.append((combo, off, n))
+            off += n
+    return out
+
+
+def n_configs(grid_len: Sequence[int]) -> int:
+    return sum(n for _, _, n in structures(len(grid_len), grid_len))
+
+
+@dataclass
+class SweepResult:
+    accuracy: torch.Tensor | None
+    mean_cost: torch.Tensor | None
+    forward_frac: torch.Tensor | None
+    n_correct: torch.Tensor | None
+    config_begin: int
+
+
+class GridSweep:
+    """Histogram + prefix tables for one validation set and one grid,
+    built once (gs_grid_build); configs are then scored in ranges
+    (gs_grid_eval) and reduced to a Pareto front (gs_pareto_counts)."""
+
+    def __init__(self, certainty, correct, grids: Sequence, cost1, *, build: bool = True):
+        dev = _lib.device()
+        self.cert = _lib.to_device(certainty, torch.float64)
+        self.corr = _lib.to_device(correct, torch.uint8)
+        if self.cert.ndim != 2 or tuple(self.corr.shape) != tuple(self.cert.shape):
+            raise ValueError("certainty and correct must both be [n_records, n_models]")
+        self.n_rec, self.n_models = int(self.cert.shape[0]), int(self.cert.shape[1])
+        if len(grids) != self.n_models:
+            raise ValueError(f"need {self.n_models} grids, got {len(grids)}")
+        host_grids = []
+        for j, g in enumerate(grids):
+            g = np.asarray(g.cpu() if isinstance(g, torch.Tensor) else g, dtype=np.float64)
+            if g.ndim != 1 or g.size == 0:
+                raise ValueError(f"grid {j} must be a non-empty 1-D array")
+            if np.any(np.diff(g) <= 0):
+                raise ValueError(f"grid {j} is not strictly increasing")
+            host_grids.append(g)
+        self.grids_host = host_grids
+        self.grid_len = [int(g.size) for g in host_grids]
+        self._glen = _lib.int32_array(self.grid_len)
+        self.grids = _lib.to_device(np.concatenate(host_grids), torch.float64)
+        self.cost1 = _lib.to_device(np.asarray(cost1, dtype=np.float64), torch.float64)
+        if self.cost1.numel() != self.n_models:
+            raise ValueError("cost1 must have one entry per model")
+        info = _lib.gs_grid_info()
+        lib = _lib.load()
+        _lib.check(lib.gs_grid_plan(self.n_rec, self.n_models, self._glen, ctypes.byref(info)),
+                   "grid plan")
+        self.info = info
+        self.n_configs = int(info.n_configs)
+        self.max_len = int(info.max_len)
+        self.table = torch.empty(int(info.workspace_bytes), dtype=torch.uint8, device=dev)
+        self._built = False
+        if build:
+            self.build()
+
+    # -- table -------------------------------------------------------------
+    def build(self) -> None:
+        lib = _lib.load()
+        rc = lib.gs_grid_build(self.cert.data_ptr(), self.corr.data_ptr(), self.n_rec,
+                               self.n_models, self.grids.data_ptr(), self._glen,
+                               self.table.data_ptr(), self.table.numel(), _lib.stream_ptr())
+        _lib.check(rc, "grid build")
+        self._built = True
+
+    # -- scoring -----------------------------------------------------------
+    def evaluate(self, begin: int = 0, count: int | None = None, *, accuracy: bool = True,
+                 mean_cost: bool = True, forward_frac: bool = True,
+                 n_correct: bool = False, out: SweepResult | None = None) -> SweepResult:
+        if not self._built:
+            raise RuntimeError("GridSweep.build() has not run")
+        if count is None:
+            count = self.n_configs - begin
+        if begin < 0 or count < 0 or begin + count > self.n_configs:
+            raise ValueError("config range outside the enumeration")
+        dev = self.cert.device
+        if out is None:
+            f64 = dict(dtype=torch.float64, device=dev)
+            out = SweepResult(
+                torch.empty(count, **f64) if accuracy else None,
+                torch.empty(count, **f64) if mean_cost else None,
+                torch.empty((count, self.max_len), **f64) if forward_frac else None,
+                torch.empty(count, dtype=torch.int32, device=dev) if n_correct else None,
+                begin)
+        out.config_begin = begin
+        lib = _lib.load()
+        rc = lib.gs_grid_eval(self.n_rec, self.n_models, self._glen, self.cost1.data_ptr(),
+                              begin, count, _lib.ptr(out.accuracy), _lib.ptr(out.mean_cost),
+                              _lib.ptr(out.forward_frac), _lib.ptr(out.n_correct),
+                              self.table.data_ptr(), self.table.numel(), _lib.stream_ptr())
+        _lib.check(rc, "grid eval")
+        return out
+
+    def pareto(self, begin: int = 0, count: int | None = None,
+               res: SweepResult | None = None) -> tuple[torch.Tensor, SweepResult]:
+        """Config indices (ascending) of the Pareto front of [begin, begin+count),
+        plus the scored range."""
+        if res is None:
+            res = self.evaluate(begin, count, accuracy=True, mean_cost=True,
+                                forward_frac=True, n_correct=True)
+        idx = pareto_counts(res.n_correct, res.mean_cost, self.n_rec, base_index=res.config_begin)
+        return idx, res
+
+    # -- decoding ----------------------------------------------------------
+    def decode(self, config_idx) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+        idx = _lib.to_device(config_idx, torch.int64)
+        n = int(idx.numel())
+        dev = self.cert.device
+        sm = torch.empty((n, self.n_models), dtype=torch.int32, device=dev)
+        thr = torch.empty((n, self.n_models), dtype=torch.float64, device=dev)
+        ns = torch.empty(n, dtype=torch.int32, device=dev)
+        if n:
+            if int(idx.min()) < 0 or int(idx.max()) >= self.n_configs:
+                raise IndexError("config index outside the enumeration")
+            lib = _lib.load()
+            rc = lib.gs_grid_decode(self.n_models, self._glen, self.grids.data_ptr(),
+                                    idx.data_ptr(), n, sm.data_ptr(), thr.data_ptr(),
+                                    ns.data_ptr(), _lib.stream_ptr())
+            _lib.check(rc, "grid decode")
+        return sm, thr, ns
+
+    def cascades(self, config_idx, model_ids: Sequence[str]) -> list[Cascade]:
+        sm, thr, ns = (t.cpu().numpy() for t in self.decode(config_idx))
+        out = []
+        for i in range(sm.shape[0]):
+            k = int(ns[i])
+            out.append(Cascade(stages=tuple(model_ids[int(m)] for m in sm[i, :k]),
+                               thresholds=tuple(float(x) for x in thr[i, :k - 1])))
+        return out
+
+
+def pareto_counts(n_correct: torch.Tensor, mean_cost: torch.Tensor, n_rec: int,
+                  base_index: int = 0, keep: torch.Tensor | None = None) -> torch.Tensor:
+    """Indices (+base_index, ascending) of the exact Pareto front of points
+    given as integer correct counts and f64 costs (gs_pareto_counts)."""
+    lib = _lib.load()
+    n = int(n_correct.numel())
+    dev = _lib.device()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.gs_pareto_counts_workspace(n, n_rec, ctypes.byref(nbytes)), "pareto")
+    ws = _lib.workspace(nbytes.value)
+    kept = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    n_kept = torch.zeros(1, dtype=torch.int64, device=dev)
+    rc = lib.gs_pareto_counts(n_correct.data_ptr() if n else None,
+                              mean_cost.data_ptr() if n else None, n, n_rec, base_index,
+                              _lib.ptr(keep), kept.data_ptr(), n_kept.data_ptr(),
+                              ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "pareto")
+    return kept[: int(n_kept.item())]

@@ -1,0 +1,143 @@
+"""Online cascade stage step on the device.
+
+Reference: EngineState.finish_batch (/root/reference/pkg/src/gearserve/
+engine.py:355-383) — per item, in batch order: stop if the stage is the
+gear's last or cert[row, m] >= thr (inclusive), else forward to the next
+stage's queue — with certainty per cascades.certainty (src/cascades.py:20-28).
+
+stage_step(): certainty of each row's scores (margin = Eq. 5, bit-exact;
+max_softmax / entropy are extensions), the gate, order-preserving
+compaction of the deferred rows, rows whose certainty is within near_eps of
+their threshold listed, and the deferred rows' payload gathered contiguously
+into the next stage's batch buffer — one kernel (csrc/gs_stage.cu).
+
+stage_gate(): the same gate over the engine's precomputed certainty
+matrices (CompiledPlan.cert/corr, src/engine.py:217), per item
+(row, model, threshold, is_last), returning stop / correct / deferred order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+NEAR_EPS = 1e-6
+
+
+@dataclass
+class StageStepResult:
+    cert: torch.Tensor            # f64 [n]
+    stop: torch.Tensor            # u8 [n]
+    deferred_idx: torch.Tensor    # i64 [n_deferred], batch order
+    near_idx: torch.Tensor        # i64 [n_near], ascending
+    next_payload: torch.Tensor | None  # [n_deferred, ...] gathered payload rows
+
+
+def _thr_tensor(thr, n: int, dev) -> torch.Tensor:
+    if isinstance(thr, (int, float)):
+        return torch.full((n,), float(thr), dtype=torch.float64, device=dev)
+    t = _lib.to_device(thr, torch.float64)
+    if t.numel() != n:
+        raise ValueError("thr must be a scalar or one threshold per row")
+    return t
+
+
+def stage_step(scores: torch.Tensor, thr, is_last=None, *, kind: str = "margin",
+               payload: torch.Tensor | None = None, near_eps: float = NEAR_EPS,
+               list_near: bool = True) -> StageStepResult:
+    """Gate one stage's batch.  scores: CUDA [n, n_cls] f32/f64/bf16 (row
+    stride may exceed n_cls); thr: scalar or [n] f64; is_last: None or [n]
+    bool/u8; payload: optional CUDA tensor with leading dim n."""
+    if kind not in _lib.CERT_KINDS:
+        raise ValueError(f"unknown certainty kind {kind!r}")
+    dev = _lib.device()
+    if scores.device.type != "cuda":
+        scores = _lib.to_device(scores, scores.dtype)
+    if scores.dtype not in _lib.DTYPES:
+        raise ValueError(f"unsupported score dtype {scores.dtype}")
+    if scores.ndim != 2 or scores.stride(1) != 1:
+        raise ValueError("scores must be a row-major [n_rows, n_cls] matrix")
+    n, c = int(scores.shape[0]), int(scores.shape[1])
+    if c == 0:
+        raise ValueError("certainty of empty scores")
+    th = _thr_tensor(thr, n, dev)
+    last = None
+    if is_last is not None:
+        last = _lib.to_device(is_last, torch.uint8) if not isinstance(is_last, torch.Tensor) \
+            else is_last.to(dev, torch.uint8).contiguous()
+        if last.numel() != n:
+            raise ValueError("is_last must have one flag per row")
+    cert = torch.empty(n, dtype=torch.float64, device=dev)
+    stop = torch.empty(n, dtype=torch.uint8, device=dev)
+    deferred = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    near = torch.empty(max(n, 1), dtype=torch.int64, device=dev) if list_near else None
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    nxt = None
+    row_bytes = 0
+    if payload is not None:
+        if payload.shape[0] != n or not payload.is_contiguous() or payload.device.type != "cuda":
+            raise ValueError("payload must be a contiguous CUDA tensor with one row per score row")
+        row_bytes = payload[0].numel() * payload.element_size() if n else 0
+        nxt = torch.empty_like(payload)
+    lib = _lib.load()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.gs_stage_step_workspace(n, ctypes.byref(nbytes)), "stage_step")
+    ws = _lib.workspace(nbytes.value)
+    rc = lib.gs_stage_step(
+        scores.data_ptr() if n else None, _lib.DTYPES[scores.dtype], n, c, int(scores.stride(0)),
+        _lib.CERT_KINDS[kind], th.data_ptr() if n else None, _lib.ptr(last),
+        cert.data_ptr(), stop.data_ptr(), deferred.data_ptr(), counts.data_ptr(),
+        float(near_eps), _lib.ptr(near), counts.data_ptr() + 8 if list_near else None,
+        _lib.ptr(payload), row_bytes, _lib.ptr(nxt), ws.data_ptr(), ws.numel(),
+        _lib.stream_ptr())
+    _lib.check(rc, "stage_step")
+    nd, nn = (int(x) for x in counts.tolist())
+    return StageStepResult(cert=cert, stop=stop, deferred_idx=deferred[:nd],
+                           near_idx=near[:nn] if list_near else deferred[:0],
+                           next_payload=None if nxt is None else nxt[:nd])
+
+
+@dataclass
+class GateResult:
+    stop: torch.Tensor           # u8 [n_items]
+    correct: torch.Tensor        # u8 [n_items] (0 for forwarded items)
+    deferred_idx: torch.Tensor   # i64 item positions, batch order
+    near_idx: torch.Tensor       # i64 item positions within near_eps
+
+
+def stage_gate(cert: torch.Tensor, corr: torch.Tensor, row, model, thr, is_last=None, *,
+               near_eps: float = NEAR_EPS) -> GateResult:
+    """Gate items against precomputed certainty/correct matrices."""
+    dev = _lib.device()
+    rows = _lib.to_device(row, torch.int64)
+    models = _lib.to_device(model, torch.int32)
+    n = int(rows.numel())
+    th = _thr_tensor(thr, n, dev)
+    last = None if is_last is None else _lib.to_device(
+        np.asarray(is_last, dtype=np.uint8) if not isinstance(is_last, torch.Tensor) else is_last,
+        torch.uint8)
+    stop = torch.empty(n, dtype=torch.uint8, device=dev)
+    correct = torch.empty(n, dtype=torch.uint8, device=dev)
+    deferred = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    near = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.gs_stage_step_workspace(n, ctypes.byref(nbytes)), "stage_gate")
+    ws = _lib.workspace(nbytes.value)
+    rc = lib.gs_stage_gate(cert.data_ptr(), corr.data_ptr(), int(cert.shape[0]),
+                           int(cert.shape[1]), rows.data_ptr() if n else None,
+                           models.data_ptr() if n else None, th.data_ptr() if n else None,
+                           _lib.ptr(last), n, stop.data_ptr(), correct.data_ptr(),
+                           deferred.data_ptr(), counts.data_ptr(), float(near_eps),
+                           near.data_ptr(), counts.data_ptr() + 8, ws.data_ptr(), ws.numel(),
+                           _lib.stream_ptr())
+    _lib.check(rc, "stage_gate")
+    nd, nn = (int(x) for x in counts.tolist())
+    return GateResult(stop=stop, correct=correct, deferred_idx=deferred[:nd],
+                      near_idx=near[:nn])

@@ -1,0 +1,138 @@
+"""Synthetic workloads for the hot path, vectorised.
+
+make_profiles / make_validation_arrays restate gearserve.synth
+(/root/reference/pkg/src/gearserve/synth.py:29-111) without building Python
+record objects: the same numpy Generator draws in the same order, so the
+certainty / correct matrices equal the reference's bit for bit
+(tests/golden/synth.npz pins this), at 1M-sample scale in a fraction of a
+second.  Tier semantics: tier 0 is easy (every model confident and
+correct); tier t > 0 is answered correctly only by models with index >= t,
+and a wrong model is unconfident; scores are (0.5 + c/2, 0.5 - c/2).
+
+imagenet_logits builds the 1000-class config-3 workload on the device
+(there is no reference generator for it).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .types import ModelProfile, ProfileSet, ValidationArrays
+
+DEFAULT_COST_RATIOS = (1.0, 4.0, 16.0)
+DEFAULT_BATCHES = (1, 2, 4, 8)
+
+
+def make_profiles(n_models: int = 3, cost_ratios=DEFAULT_COST_RATIOS,
+                  base_runtime_us: int = 2_000, base_memory_bytes: int = 2_000_000_000,
+                  memory_ratios=None, batches=DEFAULT_BATCHES,
+                  batching_exponent: float = 0.7) -> ProfileSet:
+    """Models m0..m{k-1}, cheapest first (reference synth.py:33-62)."""
+    if n_models < 1:
+        raise ValueError(f"n_models must be >= 1, got {n_models}")
+    if len(cost_ratios) != n_models:
+        raise ValueError(f"need {n_models} cost ratios, got {len(cost_ratios)}")
+    if any(r <= 0 for r in cost_ratios):
+        raise ValueError("cost ratios must be positive")
+    if list(cost_ratios) != sorted(cost_ratios):
+        raise ValueError("cost ratios must be non-decreasing")
+    if not (0 < batching_exponent <= 1):
+        raise ValueError("batching exponent must be in (0, 1]")
+    memory_ratios = memory_ratios if memory_ratios is not None else cost_ratios
+    if len(memory_ratios) != n_models:
+        raise ValueError(f"need {n_models} memory ratios, got {len(memory_ratios)}")
+    models = []
+    for j in range(n_models):
+        r1 = base_runtime_us * cost_ratios[j]
+        table = {b: int(round(r1 * b ** batching_exponent)) for b in sorted(batches)}
+        models.append(ModelProfile(model_id=f"m{j}",
+                                   memory_bytes=int(round(base_memory_bytes * memory_ratios[j])),
+                                   runtime_table=table))
+    return ProfileSet(models)
+
+
+def tier_pattern(n_samples: int, easy_fraction: float, n_tiers: int) -> np.ndarray:
+    """Bresenham-spread difficulty tiers (reference synth.py:65-75)."""
+    tiers = np.zeros(n_samples, dtype=np.int64)
+    if easy_fraction >= 1.0:
+        return tiers
+    i = np.arange(n_samples, dtype=np.int64)
+    hard = np.flatnonzero(((i + 1) * easy_fraction).astype(np.int64)
+                          == (i * easy_fraction).astype(np.int64))
+    tiers[hard] = 1 + np.arange(hard.size) % max(1, n_tiers)
+    return tiers
+
+
+def validation_matrices(n_models: int, n_samples: int, easy_fraction: float = 0.8,
+                        seed: int = 0, confident_range=(0.6, 0.95), unsure_range=(0.0, 0.3),
+                        shuffle: bool = False, return_scores: bool = False):
+    """(certainty [n, M] f64, correct [n, M] u8[, scores [M][n, 2] f64]) with the
+    reference make_validation semantics and RNG stream."""
+    if not 0.0 <= easy_fraction <= 1.0:
+        raise ValueError(f"easy_fraction must be in [0, 1], got {easy_fraction}")
+    if n_samples < 1:
+        raise ValueError(f"n_samples must be >= 1, got {n_samples}")
+    if not confident_range[0] > unsure_range[1]:
+        raise ValueError("confident range must sit strictly above unsure range")
+    tiers = tier_pattern(n_samples, easy_fraction, max(1, n_models - 1))
+    rng = np.random.default_rng(seed)
+    if shuffle:
+        tiers = rng.permutation(tiers)
+    correct = tiers[:, None] <= np.arange(n_models)[None, :]
+    lo = np.where(correct, confident_range[0], unsure_range[0])
+    hi = np.where(correct, confident_range[1], unsure_range[1])
+    c = rng.uniform(lo, hi)                      # C order = (sample, model) loop order
+    top = 0.5 + c / 2
+    second = 0.5 - c / 2
+    cert = top - second                          # cascades.certainty on the 2-score tuple
+    out = (np.ascontiguousarray(cert), correct.astype(np.uint8))
+    if return_scores:
+        out = out + (np.stack([top, second], axis=-1).transpose(1, 0, 2),)
+    return out
+
+
+def make_validation_arrays(profiles: ProfileSet, n_samples: int = 500,
+                           easy_fraction: float = 0.8, seed: int = 0,
+                           confident_range=(0.6, 0.95), unsure_range=(0.0, 0.3),
+                           shuffle: bool = False) -> ValidationArrays:
+    """Columnar make_validation (reference synth.py:78-111)."""
+    cert, corr = validation_matrices(len(profiles), n_samples, easy_fraction, seed,
+                                     confident_range, unsure_range, shuffle)
+    return ValidationArrays(profiles.model_ids, certainty=cert, correct=corr)
+
+
+def binary_logit_arrays(profiles: ProfileSet, n_samples: int, easy_fraction: float = 0.8,
+                        seed: int = 0, dtype=np.float32) -> ValidationArrays:
+    """Config-2 shape: per-model binary score heads [n, 2] in `dtype`
+    (reference semantics; certainty is then the margin of the stored
+    values, computed on the device)."""
+    _, corr, scores = validation_matrices(len(profiles), n_samples, easy_fraction, seed,
+                                          return_scores=True)
+    return ValidationArrays(profiles.model_ids,
+                            scores={m: np.ascontiguousarray(scores[j].astype(dtype))
+                                    for j, m in enumerate(profiles.model_ids)},
+                            correct=corr)
+
+
+def imagenet_logits(n_samples: int, n_cls: int = 1000, n_models: int = 3, seed: int = 0,
+                    dtype: torch.dtype = torch.float32, device=None):
+    """Config-3 shape on the device: per model [n, n_cls] logits ~ N(0, 1)
+    with the label's logit boosted on rows the model gets right; a model of
+    index j is right on tiers <= j (same tier scheme as make_validation)."""
+    device = device or torch.device("cuda")
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    tiers = torch.from_numpy(tier_pattern(n_samples, 0.8, max(1, n_models - 1))).to(device)
+    labels = torch.randint(0, n_cls, (n_samples,), generator=g, device=device)
+    rows = torch.arange(n_samples, device=device)
+    out, correct = [], []
+    for j in range(n_models):
+        x = torch.randn((n_samples, n_cls), generator=g, device=device, dtype=torch.float32)
+        right = tiers <= j
+        boost = torch.where(right, 4.0 + 2.0 * torch.rand(n_samples, generator=g, device=device),
+                            torch.zeros(n_samples, device=device))
+        x[rows, labels] += boost
+        out.append(x.to(dtype))
+        correct.append(right.to(torch.uint8))
+    return out, torch.stack(correct, dim=1), labels

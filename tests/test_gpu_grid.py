@@ -1,0 +1,123 @@
+"""Grid path (gs_grid_build/eval/decode + gs_pareto_counts) vs the reference
+golden (config 1) and the oracle walk over the enumerated configs."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _sweep(cert, corr, grids, cost1):
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    sw = GridSweep(cert, corr, grids, cost1)
+    res = sw.evaluate(n_correct=True)
+    return sw, [t.cpu().numpy() for t in (res.accuracy, res.mean_cost, res.forward_frac,
+                                          res.n_correct)]
+
+
+def test_config1_full_grid_bitwise():
+    from paper_2406_14424_b200 import synth
+    g = golden("config1.npz")
+    cert, corr = synth.validation_matrices(3, 10_000, 0.8, 0)
+    grids = [g["grid0"], g["grid1"], g["grid2"]]
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, g["cost1"])
+    assert sw.n_configs == 10_303
+    assert np.array_equal(acc, g["acc"])
+    assert np.array_equal(cost, g["cost"])
+    assert np.array_equal(frac, g["frac"])
+    assert np.array_equal(nc / 10_000, g["acc"])
+
+
+def _random_case(rng, n_rec, n_models, levels, ties=False):
+    if ties:
+        cert = np.round(rng.random((n_rec, n_models)), 1)
+    else:
+        cert = rng.random((n_rec, n_models))
+    corr = (rng.random((n_rec, n_models)) < 0.6).astype(np.uint8)
+    grids = []
+    for j in range(n_models):
+        q = np.quantile(cert[:, j], np.arange(1, levels) / levels)
+        grids.append(np.array(sorted({0.0} | {float(x) for x in q})))
+    cost1 = rng.uniform(100, 5000, n_models)
+    return cert, corr, grids, cost1
+
+
+@pytest.mark.parametrize("n_rec,n_models,levels,ties", [
+    (1, 1, 2, False), (7, 2, 3, False), (500, 3, 10, True), (3000, 4, 12, False),
+    (2000, 5, 6, True), (900, 6, 4, False), (300, 8, 3, True), (65_537, 2, 50, False)])
+def test_random_grids_vs_oracle(n_rec, n_models, levels, ties):
+    rng = np.random.default_rng(n_rec + 31 * n_models)
+    cert, corr, grids, cost1 = _random_case(rng, n_rec, n_models, levels, ties)
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, cost1)
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
+    assert np.array_equal(acc, want[0])
+    assert np.array_equal(cost, want[1])
+    assert np.array_equal(frac, want[2])
+    # decode reproduces the enumeration
+    dsm, dthr, dns = (t.cpu().numpy() for t in sw.decode(np.arange(sw.n_configs)))
+    assert np.array_equal(dsm, sm) and np.array_equal(dthr, thr) and np.array_equal(dns, ns)
+    # exact Pareto front vs the restated pareto_filter
+    idx, _ = sw.pareto()
+    keep = oracle.pareto_keep(want[0], want[1])
+    assert np.array_equal(idx.cpu().numpy(), np.flatnonzero(keep))
+
+
+def test_config_ranges_equal_full_sweep():
+    rng = np.random.default_rng(9)
+    cert, corr, grids, cost1 = _random_case(rng, 4000, 4, 9)
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    sw = GridSweep(cert, corr, grids, cost1)
+    full = sw.evaluate()
+    for begin, count in ((0, 1), (3, 100), (sw.n_configs - 7, 7), (123, 4567)):
+        part = sw.evaluate(begin, count)
+        assert np.array_equal(part.accuracy.cpu().numpy(),
+                              full.accuracy[begin:begin + count].cpu().numpy())
+        assert np.array_equal(part.forward_frac.cpu().numpy(),
+                              full.forward_frac[begin:begin + count].cpu().numpy())
+
+
+def test_negative_singleton_certainty_bins_below_zero():
+    """Singleton scores can be negative (cascades.certainty returns the score):
+    such records sit below grid value 0 and forward at every threshold."""
+    cert = np.array([[-0.5, 0.2], [0.3, 0.9], [0.0, 0.1]])
+    corr = np.array([[1, 0], [0, 1], [1, 1]], dtype=np.uint8)
+    grids = [np.array([0.0, 0.3]), np.array([0.0, 0.5])]
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, np.array([1.0, 10.0]))
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, np.array([1.0, 10.0]))
+    assert np.array_equal(acc, want[0]) and np.array_equal(frac, want[2])
+
+
+def test_config2_shape_sampled_configs():
+    """Config 2 at full size (1M records, 4 models, 100-level grids): a fixed
+    sample of configs from every structure matches the oracle walk exactly,
+    and the front is a fixed point of the Pareto filter."""
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.cascades import grid_values
+    from paper_2406_14424_b200.gridsweep import GridSweep, pareto_counts, structures
+    cert, corr = synth.validation_matrices(4, 1_000_000, 0.8, 0)
+    grids = [np.array(grid_values(cert[:, j], 100)) for j in range(4)]
+    cost1 = np.array([2000.0, 8000.0, 32000.0, 128000.0])
+    sw = GridSweep(cert, corr, grids, cost1)
+    assert sw.n_configs == sum(n for _, _, n in structures(4, [len(x) for x in grids]))
+    res = sw.evaluate(n_correct=True)
+    rng = np.random.default_rng(0)
+    pick = []
+    for _, b, n in structures(4, sw.grid_len):
+        pick.extend(sorted(set(rng.integers(b, b + n, size=min(n, 40)).tolist())))
+    pick = np.array(pick)
+    sm, thr, ns = oracle.grid_configs(grids)  # full enumeration, 1M rows
+    want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1,
+                                   n_threads=8)
+    assert np.array_equal(res.accuracy.cpu().numpy()[pick], want[0])
+    assert np.array_equal(res.mean_cost.cpu().numpy()[pick], want[1])
+    assert np.array_equal(res.forward_frac.cpu().numpy()[pick], want[2])
+    idx, _ = sw.pareto(res=res)
+    again = pareto_counts(res.n_correct[idx], res.mean_cost[idx], sw.n_rec)
+    assert np.array_equal(idx[again].cpu().numpy(), idx.cpu().numpy())
+    keep = oracle.pareto_keep(res.accuracy.cpu().numpy(), res.mean_cost.cpu().numpy())
+    assert np.array_equal(idx.cpu().numpy(), np.flatnonzero(keep))

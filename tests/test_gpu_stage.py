@@ -1,0 +1,120 @@
+"""Online stage step (gs_certainty / gs_stage_step / gs_stage_gate) vs the
+reference golden certainties and the oracle gate.
+
+Tolerances: margin certainty is bit-exact (the reference computes it on the
+same values promoted to f64).  max_softmax / entropy are extensions with no
+reference; against the f64 numpy oracle they must agree within 5e-7
+absolute (f32 expf, f64 sums), and every row whose gate decision differs
+from the oracle's must be in the kernel's near-threshold list (1e-6)."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_inputs as gi
+from conftest import golden
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+CERT_TOL = 5e-7
+
+
+def test_margin_matches_reference_tuples_and_logits():
+    from paper_2406_14424_b200 import cascades
+    g = golden("certainty.npz")
+    rows, lens = gi.certainty_tuples()
+    got = cascades.certainty_rows(rows, row_len=lens).cpu().numpy()
+    assert np.array_equal(got, g["tuples"])
+    logits = gi.logits_f32(seed=3, n=256, n_cls=1000)
+    got = cascades.certainty_rows(logits).cpu().numpy()
+    assert np.array_equal(got, g["logits"])
+    assert cascades.certainty((0.9, 0.1)) == pytest.approx(0.8)
+    assert cascades.certainty((0.7,)) == 0.7
+    with pytest.raises(ValueError):
+        cascades.certainty(())
+
+
+@pytest.mark.parametrize("n_cls", [1, 2, 3, 31, 32, 33, 100, 1000, 1003])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float64])
+def test_certainty_kinds(n_cls, dtype):
+    from paper_2406_14424_b200 import cascades
+    x = torch.from_numpy(gi.logits_f32(seed=n_cls, n=777, n_cls=n_cls)).to(dtype)
+    ref_in = x.to(torch.float64).numpy()
+    for kind in ("margin", "max_softmax", "entropy"):
+        got = cascades.certainty_rows(x.cuda(), kind=kind).cpu().numpy()
+        want = oracle.CERT_ORACLES[kind](ref_in)
+        if kind == "margin":
+            assert np.array_equal(got, want)
+        else:
+            assert np.max(np.abs(got - want)) <= CERT_TOL
+
+
+@pytest.mark.parametrize("n_rows,n_cls,kind,dtype,payload_bytes", [
+    (1, 2, "margin", torch.float32, 0), (1000, 2, "margin", torch.float32, 64),
+    (100_003, 2, "margin", torch.float64, 0), (4096, 1000, "margin", torch.float32, 16),
+    (3000, 1000, "max_softmax", torch.float32, 0), (3000, 1000, "entropy", torch.bfloat16, 0),
+    (777, 33, "entropy", torch.float32, 12), (300_000, 10, "max_softmax", torch.float32, 32)])
+def test_stage_step_vs_oracle(n_rows, n_cls, kind, dtype, payload_bytes):
+    from paper_2406_14424_b200.stage import stage_step
+    rng = np.random.default_rng(n_rows + n_cls)
+    x = torch.from_numpy(gi.logits_f32(seed=n_rows % 97, n=n_rows, n_cls=n_cls)).to(dtype)
+    cert_ref = oracle.CERT_ORACLES[kind](x.to(torch.float64).numpy())
+    # thresholds around the certainty distribution, some exactly equal
+    thr = np.quantile(cert_ref, rng.random(n_rows))
+    eq = rng.random(n_rows) < 0.05
+    thr[eq] = cert_ref[eq]
+    last = rng.random(n_rows) < 0.1
+    payload = None
+    if payload_bytes:
+        payload = torch.from_numpy(rng.integers(0, 255, size=(n_rows, payload_bytes),
+                                                dtype=np.uint8)).cuda()
+    res = stage_step(x.cuda(), thr, last, kind=kind, payload=payload)
+    cert = res.cert.cpu().numpy()
+    if kind == "margin":
+        assert np.array_equal(cert, cert_ref)
+    else:
+        assert np.max(np.abs(cert - cert_ref)) <= CERT_TOL
+    stop, deferred, near, nxt = oracle.stage_step(cert, thr, last,
+                                                  payload=None if payload is None
+                                                  else payload.cpu().numpy())
+    # the kernel's own decisions, order and lists are exact w.r.t. its certainty
+    assert np.array_equal(res.stop.cpu().numpy().astype(bool), stop)
+    assert np.array_equal(res.deferred_idx.cpu().numpy(), deferred)
+    assert np.array_equal(res.near_idx.cpu().numpy(), near)
+    if payload is not None:
+        assert np.array_equal(res.next_payload.cpu().numpy(), nxt)
+    # against the f64 oracle certainty: disagreements only inside the near list
+    stop_ref, _, _, _ = oracle.stage_step(cert_ref, thr, last)
+    diff = np.flatnonzero(stop_ref != stop)
+    assert np.all(np.isin(diff, near))
+
+
+def test_stage_step_empty_and_all_last():
+    from paper_2406_14424_b200.stage import stage_step
+    res = stage_step(torch.zeros((0, 4), device="cuda"), 0.5)
+    assert res.deferred_idx.numel() == 0
+    x = torch.randn(5000, 8, device="cuda")
+    res = stage_step(x, 10.0, np.ones(5000, dtype=bool))
+    assert res.deferred_idx.numel() == 0 and bool(res.stop.all())
+    res = stage_step(x, 1e9)
+    assert np.array_equal(res.deferred_idx.cpu().numpy(), np.arange(5000))
+
+
+def test_stage_gate_vs_oracle():
+    from paper_2406_14424_b200.stage import stage_gate
+    rng = np.random.default_rng(2)
+    n_rec, M, n = 5000, 4, 200_000
+    cert = np.round(rng.random((n_rec, M)), 2)
+    corr = (rng.random((n_rec, M)) < 0.6).astype(np.uint8)
+    rows = rng.integers(0, n_rec, n)
+    models = rng.integers(0, M, n).astype(np.int32)
+    thr = np.round(rng.random(n), 2)
+    last = rng.random(n) < 0.2
+    res = stage_gate(torch.from_numpy(cert).cuda(), torch.from_numpy(corr).cuda(), rows, models,
+                     thr, last)
+    c = cert[rows, models]
+    stop, deferred, near, _ = oracle.stage_step(c, thr, last)
+    assert np.array_equal(res.stop.cpu().numpy().astype(bool), stop)
+    assert np.array_equal(res.deferred_idx.cpu().numpy(), deferred)
+    assert np.array_equal(res.near_idx.cpu().numpy(), near)
+    assert np.array_equal(res.correct.cpu().numpy(), np.where(stop, corr[rows, models], 0))
