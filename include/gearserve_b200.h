@@ -81,17 +81,17 @@ int gs_eval_encoded(const double* certainty, const uint8_t* correct,
  *             increasing (grid_len[j] values for model j)
  *   grid_len  HOST array [n_models]
  * gs_grid_info reports the config count and the workspace the table needs.
+ * Counts are accumulated exactly in f32 lanes, so n_rec < 2^24.
  * gs_grid_build fills the workspace (histogram + prefix tables); it must run
  * before gs_grid_eval / gs_grid_pareto on the same workspace.
  * ---------------------------------------------------------------------- */
 typedef struct gs_grid_info {
   int64_t n_configs;      /* total configs of the enumeration            */
-  int64_t n_cells;        /* prefix-table cells                          */
+  int64_t n_cells;        /* main prefix-table cells (dims 0..M-2)       */
+  int64_t side_cells;     /* side table cells (dims 0..M-4), 0 if M < 4  */
   int32_t n_structures;   /* 2^n_models - 1                              */
-  int32_t words_per_cell; /* packed u64 words per cell                   */
-  int32_t field_bits;     /* bits per packed count field                 */
   int32_t max_len;        /* = n_models (forward_frac row width)         */
-  size_t workspace_bytes; /* for gs_grid_build / eval / pareto           */
+  size_t workspace_bytes; /* for gs_grid_build / eval                    */
 } gs_grid_info;
 
 int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid_len,

@@ -38,9 +38,8 @@ DTYPES = {torch.float32: GS_F32, torch.float64: GS_F64, torch.bfloat16: GS_BF16}
 
 
 class gs_grid_info(ctypes.Structure):
-    _fields_ = [("n_configs", c_int64), ("n_cells", c_int64), ("n_structures", c_int32),
-                ("words_per_cell", c_int32), ("field_bits", c_int32), ("max_len", c_int32),
-                ("workspace_bytes", c_size_t)]
+    _fields_ = [("n_configs", c_int64), ("n_cells", c_int64), ("side_cells", c_int64),
+                ("n_structures", c_int32), ("max_len", c_int32), ("workspace_bytes", c_size_t)]
 
 
 # symbol -> argtypes (all return c_int unless listed in _RESTYPES)
@@ -162,3 +161,9 @@ def to_numpy(t: torch.Tensor) -> np.ndarray:
 
 __all__ = [name for name in globals() if not name.startswith("_")]
 _ = (c_uint8, c_uint32)
+
+
+def row_stride(t: torch.Tensor) -> int:
+    """Row pitch (elements) of a 2-D row-major matrix; size-1 leading dims
+    may carry any stride (numpy broadcasting views), so use the width."""
+    return int(t.stride(0)) if t.shape[0] > 1 else int(t.shape[1])

@@ -60,7 +60,7 @@ def certainty_rows(scores, row_len=None, kind: str = "margin") -> torch.Tensor:
         if int(rl.max()) > c:
             raise ValueError("row length exceeds the score matrix width")
     lib = _lib.load()
-    rc = lib.gs_certainty(s.data_ptr(), _lib.DTYPES[s.dtype], n, c, int(s.stride(0)),
+    rc = lib.gs_certainty(s.data_ptr(), _lib.DTYPES[s.dtype], n, c, _lib.row_stride(s),
                           _lib.ptr(rl), _lib.CERT_KINDS[kind], out.data_ptr(),
                           _lib.stream_ptr())
     _lib.check(rc, "certainty")

@@ -3,30 +3,39 @@
 // Reference semantics: every config is an encoded cascade scored exactly as
 // _evaluate_numba scores it (/root/reference/pkg/src/gearserve/kernels.py:
 // 39-62); thresholds come from per-model grids (cascades.ThresholdGrid,
-// src/cascades.py:132-163), structures are model subsets ordered cheap to
+// src/cascades.py:132-163); structures are model subsets walked cheap to
 // expensive like sample_cascades builds them (src/cascades.py:181-185).
 //
-// Algorithm (dominance counting instead of walking every record through
-// every config).  With grid G_j of model j, let b_j(r) = #{g in G_j :
-// g <= cert[r, j]}.  For threshold index k, cert >= G_j[k]  <=>  b_j > k, so
-// a record is forwarded past stage s iff b_{m_s}(r) <= k_s.  Models are in
-// cost order and a subset is walked in that order, so the last model M-1 is
-// never a forwarding stage: one (M-1)-dimensional table indexed by
-// (b_0 .. b_{M-2}) answers every structure.  Each cell holds M+1 integer
-// channels — the record count and the correct count of each model — packed
-// into u64 words (fields of ceil(log2(n_rec+1)) bits; every prefix sum is
-// <= n_rec, so packed words add without carries).  After an inclusive
-// prefix sum along every dimension, P[pos] counts records whose bins are
-// dominated by pos; a dimension left at its maximum index means "any".
-//   reach(stage t+1) = P_cnt[pos with k_0..k_t set]
-//   correct         = sum_t (P_c[m_t] before setting k_t - after) + P_c[m_K] at the end
-// which is exactly the per-record walk's count.  The f64 epilogue then
-// follows the reference's order (frac = count / n, mean += frac * cost1,
-// acc = correct / n) with non-contracted multiply/add.
+// Algorithm: dominance counting instead of walking every record through
+// every config.  With grid G_j of model j let b_j(r) = #{g in G_j : g <=
+// cert[r, j]}.  cert >= G_j[k] <=> b_j > k, so record r is forwarded past a
+// stage of model j with threshold index k iff b_j(r) <= k.  Models are in
+// cost order and subsets are walked in that order, so model M-1 never
+// forwards: one (M-1)-dimensional table over (b_0 .. b_{M-2}) answers every
+// structure.  After an inclusive prefix sum along every dimension, a cell
+// counts the records whose bins it dominates; a dimension at its maximum
+// index g_j means "any".  With pos holding the thresholds of the stages
+// walked so far:
+//   reach(stage t+1) = cnt[pos after setting k_t]
+//   correct          = sum_t (c_{m_t}[pos before k_t] - c_{m_t}[pos after])
+//                      + c_{m_K}[final pos]
+// which is the per-record walk's count, exactly.
 //
-// Kernels: hist (one pass over the records, vector loads, warp-aggregated
-// u64 atomics), scan along each table dimension (L2-resident), epilogue
-// (one thread per config, coalesced output rows).
+// Table layout (HBM / L2): the main table F holds, per cell, one 16-byte
+// vector of four counts {cnt, c_{M-1}, c_{M-2}, c_{M-3}}.  A correct count
+// c_j is only ever read at positions whose dimensions > j are at "any", so
+// models j <= M-4 live in a smaller side table S over dims 0..M-4 (for the
+// 4-model cascade: one row of 101 cells, privatised in shared memory).
+// The histogram adds each record with ONE red.global.add.v4.f32 (integer
+// counts are exact in f32 below 2^24), so the histogram costs one L2 vector
+// atomic per record.  The prefix sums convert to u32.
+//
+// Kernels: grid_hist (one pass over the records, vector loads, binary search
+// in shared-memory grids), rowscan (contiguous last dim, warp-shuffle scan),
+// colscan (strided dims: [len x 32]-cell tiles staged in shared memory with
+// cp.async, one round trip per 128 rows), grid_eval (R consecutive configs per thread; everything that
+// depends only on the leading thresholds is computed once per "row" of
+// configs; f64 epilogue in the reference's order, no FMA contraction).
 #include <algorithm>
 
 #include "gs_common.cuh"
@@ -35,49 +44,52 @@ namespace gs {
 namespace {
 
 constexpr int kMaxM = GS_MAX_MODELS;
-constexpr int kMaxW = 5;  // ceil((8 + 1) / 2)
+constexpr int64_t kMaxExactF32 = 1ll << 24;
+constexpr int kHistThreads = 512;
+constexpr size_t kSidePrivMax = 16 * 1024;
 
 struct Plan {
-  int M = 0, D = 0, bits = 0, F = 0, W = 0, n_struct = 0;
+  int M = 0, D = 0, DP = 0, NVP = 0, n_struct = 0;
   int glen[kMaxM] = {};
   int64_t dims[kMaxM] = {};
-  int64_t stride[kMaxM] = {};
-  int64_t n_cells = 1;
+  int64_t strideF[kMaxM] = {};
+  int64_t strideP[kMaxM] = {};
+  int64_t cellsF = 1, cellsP = 0;
   int64_t n_configs = 0;
   int64_t struct_begin[256 + 1] = {};
   uint32_t struct_mask[256] = {};
-  size_t table_bytes = 0;
+  size_t offP = 0, bytes = 0;
 };
 
 int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   if (M < 1 || !grid_len || n_rec < 1) return GS_EINVAL;
-  if (M > kMaxM || n_rec >= (int64_t)UINT32_MAX) return GS_EUNSUPPORTED;
+  if (M > kMaxM || n_rec >= kMaxExactF32) return GS_EUNSUPPORTED;
   p->M = M;
   p->D = M - 1;
+  p->DP = M >= 4 ? M - 3 : 0;
+  p->NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
   for (int j = 0; j < M; ++j) {
-    if (grid_len[j] < 1) return GS_EINVAL;
+    if (grid_len[j] < 1 || grid_len[j] > (1 << 20)) return GS_EINVAL;
     p->glen[j] = grid_len[j];
   }
-  // packed fields
-  int bits = 1;
-  while (bits < 63 && ((int64_t)1 << bits) <= n_rec) ++bits;
-  p->bits = bits;
-  p->F = 64 / bits;
-  p->W = (M + 1 + p->F - 1) / p->F;
-  if (p->W > kMaxW) return GS_EUNSUPPORTED;
-  // table dims (b_j in [0, glen_j]) and row-major strides, last dim fastest
   double cells = 1.0;
   for (int j = 0; j < p->D; ++j) {
     p->dims[j] = (int64_t)p->glen[j] + 1;
     cells *= (double)p->dims[j];
   }
-  if (cells * p->W * 8.0 > 1.4e11) return GS_EUNSUPPORTED;  // > 140 GB of table
+  if (cells * 16.0 > 1.4e11) return GS_EUNSUPPORTED;
   int64_t s = 1;
   for (int j = p->D - 1; j >= 0; --j) {
-    p->stride[j] = s;
+    p->strideF[j] = s;
     s *= p->dims[j];
   }
-  p->n_cells = s;
+  p->cellsF = s;
+  s = 1;
+  for (int j = p->DP - 1; j >= 0; --j) {
+    p->strideP[j] = s;
+    s *= p->dims[j];
+  }
+  p->cellsP = p->DP > 0 ? s : 0;
   // structures: size ascending, then lexicographic (itertools.combinations)
   int ns = 0;
   int64_t off = 0;
@@ -110,30 +122,19 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->n_struct = ns;
   p->struct_begin[ns] = off;
   p->n_configs = off;
-  p->table_bytes = round_up((size_t)p->n_cells * p->W * sizeof(uint64_t), 256);
+  p->offP = round_up((size_t)p->cellsF * 16, 256);
+  p->bytes = p->offP + round_up((size_t)p->cellsP * p->NVP * 16, 256);
   return GS_OK;
 }
 
-// ------------------------------------------------------------------ hist --
-struct HistArgs {
-  const double* cert;
-  const uint8_t* corr;
-  int64_t n_rec;
-  const double* grids;  // concatenated
-  int32_t goff[kMaxM];
-  int32_t glen[kMaxM];
-  int64_t stride[kMaxM];
-  int64_t n_cells;
-  int32_t bits, F, W;
-  int32_t vec_ok;  // 16-byte aligned rows (M even, aligned base)
-  uint64_t* P;
-};
-
-constexpr int kHistThreads = 256;
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
 
 __device__ __forceinline__ int upper_count(const double* g, int n, double x) {
-  // #{g[i] <= x} for strictly increasing g
-  int lo = 0, hi = n;
+  int lo = 0, hi = n;  // #{g[i] <= x}, g strictly increasing
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (g[mid] <= x)
@@ -144,162 +145,252 @@ __device__ __forceinline__ int upper_count(const double* g, int n, double x) {
   return lo;
 }
 
+// ------------------------------------------------------------------ hist --
+struct HistArgs {
+  const double* cert;
+  const uint8_t* corr;
+  int64_t n_rec;
+  const double* grids;
+  int32_t goff[kMaxM];
+  int32_t glen[kMaxM];
+  int64_t strideF[kMaxM];
+  int64_t strideP[kMaxM];
+  int64_t cellsP;
+  int32_t grid_doubles;  // grids of models 0..D-1 staged in smem
+  int32_t vec_ok;
+  int32_t priv;          // side table privatised in shared memory
+  float* F;
+  float* P;
+};
+
 template <int M>
-__global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(HistArgs a) {
-  extern __shared__ __align__(16) double s_grid[];
+__global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
   constexpr int D = M - 1;
-  int total = 0;
-#pragma unroll
-  for (int j = 0; j < D; ++j) total = max(total, a.goff[j] + a.glen[j]);
-  for (int i = threadIdx.x; i < total; i += blockDim.x) s_grid[i] = a.grids[i];
+  constexpr int DP = M >= 4 ? M - 3 : 0;
+  constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  extern __shared__ __align__(16) double s_grid[];
+  float* s_side = reinterpret_cast<float*>(s_grid + a.grid_doubles);
+  for (int i = threadIdx.x; i < a.grid_doubles; i += blockDim.x) s_grid[i] = a.grids[i];
+  if (DP > 0 && a.priv)
+    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) s_side[i] = 0.f;
   __syncthreads();
 
-  const int64_t stride_r = (int64_t)gridDim.x * blockDim.x;
-  const int64_t n_iter = (a.n_rec + stride_r - 1) / stride_r;
-  for (int64_t it = 0; it < n_iter; ++it) {
-    const int64_t r = it * stride_r + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = r < a.n_rec;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n_rec; r += step) {
     double x[M];
     uint32_t k[M];
-    if (valid) {
-      const double* row = a.cert + r * M;
-      if constexpr (M % 2 == 0) {
-        if (a.vec_ok) {
+    const double* row = a.cert + r * M;
+    if (M % 2 == 0 && a.vec_ok) {
 #pragma unroll
-          for (int j = 0; j < M; j += 2) {
-            double2 v = __ldg(reinterpret_cast<const double2*>(row + j));
-            x[j] = v.x;
-            x[j + 1] = v.y;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < M; ++j) x[j] = __ldg(row + j);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < M; ++j) x[j] = __ldg(row + j);
+      for (int j = 0; j < (M / 2) * 2; j += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(row) + j / 2);
+        x[j] = v.x;
+        x[j + 1] = v.y;
       }
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) x[j] = __ldg(row + j);
+    }
+    if (M == 4 && a.vec_ok) {
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a.corr) + r);
+#pragma unroll
+      for (int j = 0; j < M; ++j) k[j] = (w >> (8 * j)) & 0xffu;
+    } else {
 #pragma unroll
       for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j);
     }
-    int64_t cell = 0;
-    uint64_t w[kMaxW];
+    int64_t cellF = 0, cellP = 0;
+    int off = 0;
 #pragma unroll
-    for (int q = 0; q < kMaxW; ++q) w[q] = 0;
-    if (valid) {
+    for (int j = 0; j < D; ++j) {
+      const int b = upper_count(s_grid + off, a.glen[j], x[j]);
+      off += a.glen[j];
+      cellF += (int64_t)b * a.strideF[j];
+      if (j < DP) cellP += (int64_t)b * a.strideP[j];
+    }
+    // main table: {cnt, c_{M-1}, c_{M-2}, c_{M-3}}
+    float v[4] = {1.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        const int b = upper_count(s_grid + a.goff[j], a.glen[j], x[j]);
-        cell += (int64_t)b * a.stride[j];
-      }
-      w[0] = 1ull;  // channel 0: record count
+    for (int i = 0; i < 3; ++i)
+      if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i] ? 1.f : 0.f;
+    red_add_v4(a.F + cellF * 4, v[0], v[1], v[2], v[3]);
+    // side table: c_j for j <= M-4 at (b_0..b_{M-4})
+    if constexpr (DP > 0) {
 #pragma unroll
-      for (int j = 0; j < M; ++j) {
-        const int ch = 1 + j;
-        const int q = ch / a.F;
-        const int sh = (ch % a.F) * a.bits;
-        w[q] += (uint64_t)(k[j] != 0) << sh;
+      for (int j = 0; j < DP; ++j) {
+        if (!k[j]) continue;
+        const int64_t e = (cellP * NVP + j / 4) * 4 + (j % 4);
+        if (a.priv)
+          atomicAdd(s_side + e, 1.f);
+        else
+          atomicAdd(a.P + e, 1.f);
       }
     }
-    // warp aggregation of duplicate cells (heavy ties, tiny tables)
-    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-    const uint64_t key = valid ? (uint64_t)cell : ~0ull;
-    const uint32_t peers = __match_any_sync(0xffffffffu, key);
-    const bool dup = __any_sync(0xffffffffu, valid && __popc(peers) > 1);
-    bool leader = valid;
-    if (dup) {
-      const int lane = (int)lane_id();
-      leader = valid && (__ffs(peers) - 1) == lane;
-#pragma unroll
-      for (int q = 0; q < kMaxW; ++q) {
-        if (q >= a.W) break;
-        uint64_t s = 0;
-        for (int src = 0; src < 32; ++src) {
-          const uint64_t v = __shfl_sync(0xffffffffu, w[q], src);
-          if (((peers >> src) & 1u) && ((vmask >> src) & 1u)) s += v;
-        }
-        w[q] = s;
-      }
-    }
-    if (leader) {
-#pragma unroll
-      for (int q = 0; q < kMaxW; ++q) {
-        if (q >= a.W) break;
-        if (w[q]) atomicAdd(reinterpret_cast<unsigned long long*>(a.P + (int64_t)q * a.n_cells + cell),
-                            (unsigned long long)w[q]);
-      }
+  }
+  if (DP > 0 && a.priv) {
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) {
+      const float c = s_side[i];
+      if (c != 0.f) atomicAdd(a.P + i, c);
     }
   }
 }
 
 // ----------------------------------------------------------------- scans --
-// Inclusive prefix along a dimension whose stride is 1: one warp per row.
-__global__ void scan_rows_kernel(uint64_t* P, int64_t n_cells, int64_t len, int64_t n_rows, int W) {
-  const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ uint4 to_u4(float4 f) {
+  return make_uint4(__float2uint_rn(f.x), __float2uint_rn(f.y), __float2uint_rn(f.z),
+                    __float2uint_rn(f.w));
+}
+__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) {
+  return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ uint4 shfl_up4(uint4 v, int o) {
+  return make_uint4(__shfl_up_sync(0xffffffffu, v.x, o), __shfl_up_sync(0xffffffffu, v.y, o),
+                    __shfl_up_sync(0xffffffffu, v.z, o), __shfl_up_sync(0xffffffffu, v.w, o));
+}
+__device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
+  return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                    __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+
+// Inclusive prefix along the contiguous last dimension: one warp per row of
+// `len` uint4 cells, four consecutive cells per lane, warp-shuffle scan, one
+// load round trip per 128 cells.  from_f32 converts the f32 histogram.
+__global__ void __launch_bounds__(256) rowscan_kernel(uint4* T, int64_t n_rows, int len, int from_f32) {
   const int lane = (int)lane_id();
-  const int64_t total = n_rows * W;
-  for (int64_t wr = warp_global; wr < total; wr += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int q = (int)(wr / n_rows);
-    const int64_t row = wr - (int64_t)q * n_rows;
-    uint64_t* p = P + (int64_t)q * n_cells + row * len;
-    uint64_t carry = 0;
-    for (int64_t base = 0; base < len; base += 32) {
-      const int64_t t = base + lane;
-      uint64_t v = t < len ? p[t] : 0;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
+    uint4* row = T + r * len;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (int base = 0; base < len; base += 128) {
+      uint4 e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        e[u] = c < len ? row[c] : make_uint4(0, 0, 0, 0);
+        if (from_f32) e[u] = to_u4(*reinterpret_cast<float4*>(&e[u]));
+      }
+      uint4 tot = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        tot = add4(tot, e[u]);
+        e[u] = tot;
+      }
+      uint4 incl = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
+        const uint4 y = shfl_up4(incl, o);
+        if (lane >= o) incl = add4(incl, y);
       }
-      v += carry;
-      if (t < len) p[t] = v;
-      carry = __shfl_sync(0xffffffffu, v, 31);
+      const uint4 excl = add4(carry, make_uint4(incl.x - tot.x, incl.y - tot.y, incl.z - tot.z,
+                                                incl.w - tot.w));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        if (c < len) row[c] = add4(e[u], excl);
+      }
+      carry = add4(carry, shfl4(incl, 31));
     }
   }
 }
 
-// Inclusive prefix along a dimension with stride `inner` > 1: one thread per
-// (outer, inner) column, coalesced across threads, 8 loads in flight.
-__global__ void scan_cols_kernel(uint64_t* P, int64_t n_cells, int64_t outer, int64_t len,
-                                 int64_t inner, int W) {
-  const int64_t n_cols = outer * inner;
-  const int64_t total = n_cols * W;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(t / n_cols);
-    const int64_t col = t - (int64_t)q * n_cols;
-    const int64_t o = col / inner;
-    const int64_t i = col - o * inner;
-    uint64_t* p = P + (int64_t)q * n_cells + o * len * inner + i;
-    uint64_t acc = 0;
-    int64_t k = 0;
-    for (; k + 8 <= len; k += 8) {
-      uint64_t v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = p[(k + u) * inner];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc += v[u];
-        p[(k + u) * inner] = acc;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+constexpr int kColTile = 32;    // consecutive inner cells per CTA
+constexpr int kColChunk = 128;  // rows of the scanned dimension per smem pass
+
+// Inclusive prefix along a strided dimension of a table of uint4 cells viewed
+// as [outer][len][inner].  A CTA owns kColTile consecutive inner cells of one
+// outer index: it stages the [len x kColTile] tile in shared memory with
+// cp.async (one round trip per 128 rows), scans each (cell, lane) column in
+// shared memory, and writes the tile back coalesced.
+__global__ void __launch_bounds__(256) colscan_kernel(uint4* T, int64_t outer, int64_t len,
+                                                      int64_t inner, int from_f32) {
+  extern __shared__ __align__(16) uint4 s[];  // [kColChunk][kColTile]
+  const int64_t tiles_per_outer = (inner + kColTile - 1) / kColTile;
+  const int64_t n_tiles = outer * tiles_per_outer;
+  const int t = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t o = tile / tiles_per_outer;
+    const int64_t i0 = (tile - o * tiles_per_outer) * kColTile;
+    const int w = (int)min((int64_t)kColTile, inner - i0);
+    uint4* base = T + o * len * inner + i0;
+    // scanning threads: (cell c, lane q) = (t / 4, t % 4) for t < 4 * w
+    uint32_t carry = 0;
+    for (int64_t r0 = 0; r0 < len; r0 += kColChunk) {
+      const int rows = (int)min((int64_t)kColChunk, len - r0);
+      for (int e = t; e < rows * w; e += blockDim.x) {
+        const int rr = e / w, cc = e - (e / w) * w;
+        cp_async16(s + rr * kColTile + cc, base + (r0 + rr) * inner + cc);
       }
-    }
-    for (; k < len; ++k) {
-      acc += p[k * inner];
-      p[k * inner] = acc;
+      cp_async_wait_all();
+      __syncthreads();
+      if (t < 4 * w) {
+        uint32_t* col = reinterpret_cast<uint32_t*>(s) + (t >> 2) * 4 + (t & 3);
+        uint32_t acc = carry;
+        int r = 0;
+        for (; r + 4 <= rows; r += 4) {
+          uint32_t v0 = col[(r + 0) * kColTile * 4], v1 = col[(r + 1) * kColTile * 4];
+          uint32_t v2 = col[(r + 2) * kColTile * 4], v3 = col[(r + 3) * kColTile * 4];
+          if (from_f32) {
+            v0 = __float2uint_rn(__uint_as_float(v0));
+            v1 = __float2uint_rn(__uint_as_float(v1));
+            v2 = __float2uint_rn(__uint_as_float(v2));
+            v3 = __float2uint_rn(__uint_as_float(v3));
+          }
+          acc += v0;
+          col[(r + 0) * kColTile * 4] = acc;
+          acc += v1;
+          col[(r + 1) * kColTile * 4] = acc;
+          acc += v2;
+          col[(r + 2) * kColTile * 4] = acc;
+          acc += v3;
+          col[(r + 3) * kColTile * 4] = acc;
+        }
+        for (; r < rows; ++r) {
+          uint32_t v = col[r * kColTile * 4];
+          if (from_f32) v = __float2uint_rn(__uint_as_float(v));
+          acc += v;
+          col[r * kColTile * 4] = acc;
+        }
+        carry = acc;
+      }
+      __syncthreads();
+      for (int e = t; e < rows * w; e += blockDim.x) {
+        const int rr = e / w, cc = e - (e / w) * w;
+        base[(r0 + rr) * inner + cc] = s[rr * kColTile + cc];
+      }
+      __syncthreads();
     }
   }
 }
 
 // -------------------------------------------------------------- epilogue --
+// Configs are processed in "rows": the configs of one structure that share
+// every threshold except the last forwarding stage's (consecutive in the
+// enumeration).  One warp owns a row: the row-shared part of the walk (cells
+// of the leading stages, their forward fractions and the partial mean cost)
+// is computed once per warp from broadcast loads, then each lane finishes
+// configs kl = lane, lane+32, ... with one 16-byte cell load, two f64
+// divisions and coalesced stores.
 struct EvalGridArgs {
-  int32_t M, W, bits, F, n_struct;
+  int32_t M, n_struct, NVP, DP;
   int32_t glen[kMaxM];
-  int64_t stride[kMaxM];
-  int64_t n_rec, n_cells;
+  int64_t strideF[kMaxM];
+  int64_t strideP[kMaxM];
+  int64_t n_rec, cellsF, cellsP;
   int64_t cfg_begin, cfg_count;
+  int64_t row_lo, row_hi;
   int64_t struct_begin[256 + 1];
+  int64_t row_begin[256 + 1];
   uint32_t struct_mask[256];
-  const uint64_t* P;
+  const uint4* F;
+  const uint4* P;
   const double* cost1;
   double* acc;
   double* cost;
@@ -307,106 +398,152 @@ struct EvalGridArgs {
   uint32_t* n_correct;
 };
 
-__device__ __forceinline__ uint32_t field(const uint64_t* w, int ch, int F, int bits) {
-  const uint64_t mask = (bits >= 64) ? ~0ull : ((1ull << bits) - 1);
-  return (uint32_t)((w[ch / F] >> ((ch % F) * bits)) & mask);
+__device__ __forceinline__ uint32_t lane4(const uint4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
-__device__ __forceinline__ int find_struct(const EvalGridArgs& a, int64_t c) {
-  int lo = 0, hi = a.n_struct - 1;  // last s with struct_begin[s] <= c
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.struct_begin[mid] <= c)
-      lo = mid;
-    else
-      hi = mid - 1;
+// correct count of model m at the current position
+template <int M>
+__device__ __forceinline__ uint32_t chan(const uint4& vF, const uint4* vP, int m) {
+  if (m >= M - 3) return lane4(vF, 1 + (M - 1 - m));
+  return lane4(vP[m / 4], m % 4);
+}
+
+template <int M>
+__device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, const double* fr,
+                                             int K, double frK, double mean, uint32_t correct,
+                                             double n) {
+  if (a.frac) {
+    double o[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) o[t] = t < K - 1 ? fr[t] : (t == K - 1 ? frK : 0.0);
+    double* row = a.frac + i * M;
+    if constexpr (M % 2 == 0) {
+#pragma unroll
+      for (int t = 0; t < M; t += 2) reinterpret_cast<double2*>(row)[t / 2] = make_double2(o[t], o[t + 1]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < M; ++t) row[t] = o[t];
+    }
   }
-  return lo;
+  if (a.cost) a.cost[i] = mean;
+  if (a.acc) a.acc[i] = ddiv((double)correct, n);
+  if (a.n_correct) a.n_correct[i] = correct;
 }
 
 template <int M>
 __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ EvalGridArgs a) {
-  const int W = a.W;
+  constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  constexpr int NVPX = NVP > 0 ? NVP : 1;
+  const int lane = (int)lane_id();
   const double n = (double)a.n_rec;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.cfg_count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = a.cfg_begin + i;
-    const int s = find_struct(a, c);
+  const double one = ddiv(n, n);  // first-stage fraction, as the reference computes it
+  const uint4 totF = __ldg(a.F + a.cellsF - 1);
+  uint4 totP[NVPX];
+#pragma unroll
+  for (int v = 0; v < NVPX; ++v)
+    totP[v] = NVP > 0 ? __ldg(a.P + (a.cellsP - 1) * NVP + v) : make_uint4(0, 0, 0, 0);
+
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t rg = a.row_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+       rg < a.row_hi; rg += nw) {
+    int s = 0;
+    {
+      int lo = 0, hi = a.n_struct - 1;  // last s with row_begin[s] <= rg
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.row_begin[mid] <= rg)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      s = lo;
+    }
     const uint32_t mask = a.struct_mask[s];
     int K = 0;
-    int mdl[M];
+    uint32_t mdl = 0;  // stage models, 4 bits each, stage 0 lowest
 #pragma unroll
-    for (int j = 0; j < M; ++j) {
+    for (int j = 0; j < M; ++j)
       if ((mask >> j) & 1u) {
-        mdl[K] = j;
+        mdl |= (uint32_t)j << (4 * K);
         ++K;
       }
-    }
-    // decode threshold indices, last forwarding stage fastest
-    int64_t local = c - a.struct_begin[s];
-    int kidx[M];
-#pragma unroll
-    for (int t = M - 2; t >= 0; --t) {
-      if (t < K - 1) {
-        const int g = a.glen[mdl[t]];
-        if (local < 0x7fffffffLL) {
-          const int l32 = (int)local;
-          kidx[t] = l32 % g;
-          local = l32 / g;
-        } else {
-          kidx[t] = (int)(local % g);
-          local /= g;
-        }
-      }
-    }
-    // dominance-count walk
-    int64_t cell = a.n_cells - 1;  // every dimension at "any"
-    uint64_t wv[kMaxW];
-#pragma unroll
-    for (int q = 0; q < kMaxW; ++q)
-      if (q < W) wv[q] = __ldg(a.P + (int64_t)q * a.n_cells + cell);
-    uint32_t reach[M];
-    reach[0] = (uint32_t)a.n_rec;
-    int64_t correct = 0;
-#pragma unroll
-    for (int t = 0; t < M - 1; ++t) {
-      if (t < K - 1) {
-        const int m = mdl[t];
-        const int64_t before = field(wv, 1 + m, a.F, a.bits);
-        cell -= (int64_t)(a.glen[m] - kidx[t]) * a.stride[m];
-#pragma unroll
-        for (int q = 0; q < kMaxW; ++q)
-          if (q < W) wv[q] = __ldg(a.P + (int64_t)q * a.n_cells + cell);
-        reach[t + 1] = field(wv, 0, a.F, a.bits);
-        correct += before - (int64_t)field(wv, 1 + m, a.F, a.bits);
-      }
-    }
-    correct += field(wv, 1 + mdl[K - 1], a.F, a.bits);
-    // f64 epilogue in the reference's order (src/kernels.py:57-61)
-    double mean = 0.0;
+    const int64_t row = rg - a.row_begin[s];
+    const int64_t s_begin = a.struct_begin[s];
+    const int mK = (mdl >> (4 * (K - 1))) & 15u;
     double fr[M];
 #pragma unroll
-    for (int t = 0; t < M; ++t) {
-      fr[t] = 0.0;
-      if (t < K) {
-        fr[t] = ddiv((double)reach[t], n);
-        mean = dadd(mean, dmul(fr[t], __ldg(a.cost1 + mdl[t])));
+    for (int t = 0; t < M; ++t) fr[t] = 0.0;
+    if (K == 1) {
+      const int64_t i = s_begin - a.cfg_begin;
+      if (lane == 0 && i >= 0 && i < a.cfg_count) {
+        const double mean = dadd(0.0, dmul(one, __ldg(a.cost1 + mK)));
+        store_config<M>(a, i, fr, 1, one, mean, chan<M>(totF, totP, mK), n);
+      }
+      continue;
+    }
+    const int mL = (mdl >> (4 * (K - 2))) & 15u;
+    const int gL = a.glen[mL];
+    // leading thresholds k_0 .. k_{K-3} from the row index
+    int kk[M];
+    int64_t rem = row;
+#pragma unroll
+    for (int t = M - 1; t >= 0; --t) {
+      kk[t] = 0;
+      if (t <= K - 3) {
+        const int g = a.glen[(mdl >> (4 * t)) & 15u];
+        kk[t] = (int)(rem % g);
+        rem /= g;
       }
     }
-    if (a.frac) {
-      double* row = a.frac + i * M;
-      if constexpr (M % 2 == 0) {
+    int64_t cF = a.cellsF - 1, cP = a.cellsP - 1;
+    uint4 vF = totF;
+    uint4 vP[NVPX];
 #pragma unroll
-        for (int t = 0; t < M; t += 2)
-          reinterpret_cast<double2*>(row)[t / 2] = make_double2(fr[t], fr[t + 1]);
-      } else {
+    for (int v = 0; v < NVPX; ++v) vP[v] = totP[v];
+    uint32_t cp = 0;
+    fr[0] = one;
+    double mp = dadd(0.0, dmul(one, __ldg(a.cost1 + (mdl & 15u))));
 #pragma unroll
-        for (int t = 0; t < M; ++t) row[t] = fr[t];
+    for (int t = 0; t < M - 2; ++t) {
+      if (t <= K - 3) {
+        const int m = (mdl >> (4 * t)) & 15u;
+        const uint32_t A = chan<M>(vF, vP, m);
+        const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
+        cF -= dk * a.strideF[m];
+        vF = __ldg(a.F + cF);
+        if (NVP > 0 && m < a.DP) {
+          cP -= dk * a.strideP[m];
+#pragma unroll
+          for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
+        }
+        cp += A - chan<M>(vF, vP, m);
+        fr[t + 1] = ddiv((double)vF.x, n);
+        mp = dadd(mp, dmul(fr[t + 1], __ldg(a.cost1 + ((mdl >> (4 * (t + 1))) & 15u))));
       }
     }
-    if (a.cost) a.cost[i] = mean;
-    if (a.acc) a.acc[i] = ddiv((double)correct, n);
-    if (a.n_correct) a.n_correct[i] = (uint32_t)correct;
+    const uint32_t a_last = chan<M>(vF, vP, mL);
+    const double costK = __ldg(a.cost1 + mK);
+    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
+    const int64_t c_row = s_begin + row * gL - a.cfg_begin;
+    for (int kl = lane; kl < gL; kl += 32) {
+      const int64_t i = c_row + kl;
+      if (i < 0 || i >= a.cfg_count) continue;
+      const int64_t dk = (int64_t)(gL - kl);
+      const uint4 wF = __ldg(a.F + cF - dk * a.strideF[mL]);
+      uint4 wP[NVPX];
+#pragma unroll
+      for (int v = 0; v < NVPX; ++v) wP[v] = make_uint4(0, 0, 0, 0);
+      if (needP) {
+        const int64_t q = cP - (mL < a.DP ? dk * a.strideP[mL] : 0);
+#pragma unroll
+        for (int v = 0; v < NVPX; ++v) wP[v] = __ldg(a.P + q * NVP + v);
+      }
+      const uint32_t correct = cp + a_last - chan<M>(wF, wP, mL) + chan<M>(wF, wP, mK);
+      const double frK = ddiv((double)wF.x, n);
+      const double mean = dadd(mp, dmul(frK, costK));
+      store_config<M>(a, i, fr, K, frK, mean, correct, n);
+    }
   }
 }
 
@@ -457,25 +594,76 @@ __global__ void grid_decode_kernel(const __grid_constant__ DecodeArgs a) {
   }
 }
 
+// configs per row of structure s (the last forwarding stage's grid size)
+int64_t row_len(const Plan& p, int s) {
+  const uint32_t mask = p.struct_mask[s];
+  int prev = -1, last = -1;
+  for (int j = 0; j < p.M; ++j)
+    if ((mask >> j) & 1u) {
+      prev = last;
+      last = j;
+    }
+  return prev < 0 ? 1 : p.glen[prev];
+}
+
+int64_t global_row(const Plan& p, const int64_t* row_begin, int64_t c) {
+  int s = 0;
+  while (s + 1 < p.n_struct && p.struct_begin[s + 1] <= c) ++s;
+  return row_begin[s] + (c - p.struct_begin[s]) / row_len(p, s);
+}
+
 template <int M>
 cudaError_t launch_hist(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
   auto k = grid_hist_kernel<M>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 8));
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
   k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
   return cudaGetLastError();
 }
 
 template <int M>
 cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
-  int64_t blocks = (a.cfg_count + 255) / 256;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
+  const int64_t rows = a.row_hi - a.row_lo;
+  int64_t blocks = (rows * 32 + 255) / 256;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
   grid_eval_kernel<M><<<(unsigned)blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+// Inclusive prefix over every dimension of a table of uint4 elements
+// (`vec` elements per cell), starting from the f32 histogram.
+cudaError_t prefix_table(uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
+                         cudaStream_t st) {
+  if (ndim == 0) {  // a single cell: convert in place
+    rowscan_kernel<<<1, 32, 0, st>>>(T, 1, 1, 1);
+    return cudaGetLastError();
+  }
+  int64_t inner = vec;
+  bool converted = false;
+  for (int d = ndim - 1; d >= 0; --d) {
+    const int64_t len = dims[d];
+    const int64_t outer = cells * vec / (len * inner);
+    if (inner == 1) {
+      int64_t blocks = (outer * 32 + 255) / 256;
+      blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
+      rowscan_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, outer, (int)len, converted ? 0 : 1);
+    } else {
+      const size_t smem = (size_t)kColChunk * kColTile * sizeof(uint4);
+      cudaError_t e = cudaFuncSetAttribute(colscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      const int64_t tiles = outer * ((inner + kColTile - 1) / kColTile);
+      const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 8));
+      colscan_kernel<<<(unsigned)blocks, 256, smem, st>>>(T, outer, len, inner, converted ? 0 : 1);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    converted = true;
+    inner *= len;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -490,12 +678,11 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
   int rc = make_plan(n_rec, n_models, grid_len, &p);
   if (rc != GS_OK) return rc;
   info->n_configs = p.n_configs;
-  info->n_cells = p.n_cells;
+  info->n_cells = p.cellsF;
+  info->side_cells = p.cellsP;
   info->n_structures = p.n_struct;
-  info->words_per_cell = p.W;
-  info->field_bits = p.bits;
   info->max_len = p.M;
-  info->workspace_bytes = p.table_bytes;
+  info->workspace_bytes = p.bytes;
   return GS_OK;
 }
 
@@ -506,10 +693,12 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   int rc = make_plan(n_rec, n_models, grid_len, &p);
   if (rc != GS_OK) return rc;
   GS_REQUIRE(certainty && correct && grids);
-  if (!workspace || workspace_bytes < p.table_bytes) return GS_EWORKSPACE;
+  if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  uint64_t* P = static_cast<uint64_t*>(workspace);
-  GS_CUDA_TRY(cudaMemsetAsync(P, 0, (size_t)p.n_cells * p.W * sizeof(uint64_t), st));
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  GS_CUDA_TRY(cudaMemsetAsync(ws, 0, p.bytes, st));
+  float* F = reinterpret_cast<float*>(ws);
+  float* P = reinterpret_cast<float*>(ws + p.offP);
 
   HistArgs h{};
   h.cert = certainty;
@@ -522,15 +711,16 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
     h.glen[j] = p.glen[j];
     off += p.glen[j];
   }
-  for (int j = 0; j < p.D; ++j) h.stride[j] = p.stride[j];
-  h.n_cells = p.n_cells;
-  h.bits = p.bits;
-  h.F = p.F;
-  h.W = p.W;
-  h.vec_ok = aligned16(certainty) && (n_models % 2 == 0);
+  for (int j = 0; j < p.D; ++j) h.strideF[j] = p.strideF[j];
+  for (int j = 0; j < p.DP; ++j) h.strideP[j] = p.strideP[j];
+  h.cellsP = p.cellsP;
+  h.grid_doubles = p.D > 0 ? h.goff[p.D - 1] + h.glen[p.D - 1] : 0;
+  h.vec_ok = aligned16(certainty) && ((reinterpret_cast<uintptr_t>(correct) & 3u) == 0);
+  const size_t side_bytes = (size_t)p.cellsP * p.NVP * 16;
+  h.priv = p.DP > 0 && side_bytes <= kSidePrivMax;
+  h.F = F;
   h.P = P;
-  // shared memory holds the grids of the forwarding models 0..M-2
-  const size_t smem = (size_t)std::max(1, p.D > 0 ? h.goff[p.D - 1] + h.glen[p.D - 1] : 1) * sizeof(double);
+  const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (h.priv ? side_bytes : 0) + 16;
   if (smem > 200 * 1024) return GS_EUNSUPPORTED;
   cudaError_t e = cudaSuccess;
   switch (n_models) {
@@ -545,25 +735,9 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
     default: return GS_EUNSUPPORTED;
   }
   GS_CUDA_TRY(e);
-
-  // inclusive prefix along every dimension
-  for (int d = p.D - 1; d >= 0; --d) {
-    const int64_t len = p.dims[d];
-    const int64_t inner = p.stride[d];
-    const int64_t outer = p.n_cells / (len * inner);
-    if (inner == 1) {
-      const int64_t warps = outer * p.W;
-      int64_t blocks = (warps * 32 + 255) / 256;
-      blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
-      scan_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(P, p.n_cells, len, outer, p.W);
-    } else {
-      const int64_t cols = outer * inner * p.W;
-      int64_t blocks = (cols + 255) / 256;
-      blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
-      scan_cols_kernel<<<(unsigned)blocks, 256, 0, st>>>(P, p.n_cells, outer, len, inner, p.W);
-    }
-    GS_LAUNCH_CHECK();
-  }
+  GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(F), p.D, p.dims, p.cellsF, 1, st));
+  if (p.DP > 0)
+    GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), p.DP, p.dims, p.cellsP, p.NVP, st));
   return GS_OK;
 }
 
@@ -578,23 +752,38 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
   GS_REQUIRE(cost1 && config_begin >= 0 && config_count >= 0 &&
              config_begin + config_count <= p.n_configs);
   if (config_count == 0) return GS_OK;
-  if (!workspace || workspace_bytes < p.table_bytes) return GS_EWORKSPACE;
-  if (forward_frac && n_models % 2 == 0 && !aligned16(forward_frac)) return GS_EINVAL;
+  if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
+  // vector stores need 16-byte aligned outputs
+  if ((accuracy && !aligned16(accuracy)) || (mean_cost && !aligned16(mean_cost)) ||
+      (n_correct && !aligned16(n_correct)) || (forward_frac && !aligned16(forward_frac)))
+    return GS_EINVAL;
   EvalGridArgs a{};
   a.M = p.M;
-  a.W = p.W;
-  a.bits = p.bits;
-  a.F = p.F;
   a.n_struct = p.n_struct;
+  a.NVP = p.NVP;
+  a.DP = p.DP;
   for (int j = 0; j < p.M; ++j) a.glen[j] = p.glen[j];
-  for (int j = 0; j < p.D; ++j) a.stride[j] = p.stride[j];
+  for (int j = 0; j < p.D; ++j) a.strideF[j] = p.strideF[j];
+  for (int j = 0; j < p.DP; ++j) a.strideP[j] = p.strideP[j];
   a.n_rec = n_rec;
-  a.n_cells = p.n_cells;
+  a.cellsF = p.cellsF;
+  a.cellsP = p.cellsP;
   a.cfg_begin = config_begin;
   a.cfg_count = config_count;
   for (int s = 0; s <= p.n_struct; ++s) a.struct_begin[s] = p.struct_begin[s];
   for (int s = 0; s < p.n_struct; ++s) a.struct_mask[s] = p.struct_mask[s];
-  a.P = static_cast<const uint64_t*>(workspace);
+  // rows: configs sharing all thresholds but the last forwarding stage's
+  int64_t rows = 0;
+  for (int s = 0; s < p.n_struct; ++s) {
+    a.row_begin[s] = rows;
+    rows += (p.struct_begin[s + 1] - p.struct_begin[s]) / row_len(p, s);
+  }
+  a.row_begin[p.n_struct] = rows;
+  a.row_lo = global_row(p, a.row_begin, config_begin);
+  a.row_hi = global_row(p, a.row_begin, config_begin + config_count - 1) + 1;
+  const uint8_t* ws = static_cast<const uint8_t*>(workspace);
+  a.F = reinterpret_cast<const uint4*>(ws);
+  a.P = reinterpret_cast<const uint4*>(ws + p.offP);
   a.cost1 = cost1;
   a.acc = accuracy;
   a.cost = mean_cost;

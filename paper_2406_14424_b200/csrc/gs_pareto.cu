@@ -32,13 +32,31 @@ __device__ __forceinline__ uint64_t cost_key(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Many configs share a correct count (thresholds that change no decision),
+// so the per-bucket atomicMin is aggregated first: lanes with the same count
+// take their group minimum, and the group leader only issues the atomic when
+// it would lower the bucket (a stale read can only be too high, never too
+// low, so skipping on it is safe).
 __global__ void bucket_min_kernel(const uint32_t* n_correct, const double* cost, int64_t n,
                                   int64_t n_rec, unsigned long long* mincost) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t a = n_correct[i];
-    if ((int64_t)a > n_rec) a = (uint32_t)n_rec;
-    atomicMin(mincost + a, (unsigned long long)cost_key(cost[i]));
+  const int lane = (int)lane_id();
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += step) {
+    const int64_t i = base + lane;
+    const bool valid = i < n;
+    uint32_t a = valid ? n_correct[i] : 0xffffffffu;
+    if (valid && (int64_t)a > n_rec) a = (uint32_t)n_rec;
+    unsigned long long key = valid ? cost_key(cost[i]) : ~0ull;
+    const uint32_t peers = __match_any_sync(0xffffffffu, a);
+    unsigned long long m = key;
+    for (int src = 0; src < 32; ++src) {
+      const unsigned long long v = __shfl_sync(0xffffffffu, key, src);
+      if ((peers >> src) & 1u) m = min(m, v);
+    }
+    if (valid && (__ffs(peers) - 1) == lane) {
+      volatile unsigned long long* slot = mincost + a;
+      if (m < *slot) atomicMin(mincost + a, m);
+    }
   }
 }
 

@@ -89,7 +89,7 @@ def stage_step(scores: torch.Tensor, thr, is_last=None, *, kind: str = "margin",
     _lib.check(lib.gs_stage_step_workspace(n, ctypes.byref(nbytes)), "stage_step")
     ws = _lib.workspace(nbytes.value)
     rc = lib.gs_stage_step(
-        scores.data_ptr() if n else None, _lib.DTYPES[scores.dtype], n, c, int(scores.stride(0)),
+        scores.data_ptr() if n else None, _lib.DTYPES[scores.dtype], n, c, _lib.row_stride(scores),
         _lib.CERT_KINDS[kind], th.data_ptr() if n else None, _lib.ptr(last),
         cert.data_ptr(), stop.data_ptr(), deferred.data_ptr(), counts.data_ptr(),
         float(near_eps), _lib.ptr(near), counts.data_ptr() + 8 if list_near else None,

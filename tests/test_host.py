@@ -58,8 +58,9 @@ def test_grid_plan_matches_enumeration(glen):
     assert info.n_configs == gridsweep.n_configs(glen) == oracle.grid_n_configs(glen)
     assert info.n_structures == 2 ** len(glen) - 1
     assert info.n_cells == int(np.prod([g + 1 for g in glen[:-1]]))
-    assert info.field_bits == 14  # 10_000 < 2^14
-    assert info.words_per_cell == -(-(len(glen) + 1) // (64 // 14))
+    side = int(np.prod([g + 1 for g in glen[:len(glen) - 3]])) if len(glen) >= 4 else 0
+    assert info.side_cells == side
+    assert info.workspace_bytes >= 16 * (info.n_cells + side)
 
 
 def test_config2_size():
@@ -74,6 +75,7 @@ def test_grid_plan_rejects_bad_input():
     assert lib.gs_grid_plan(0, 2, _lib.int32_array([3, 3]), ctypes.byref(info)) == -1
     assert lib.gs_grid_plan(10, 2, _lib.int32_array([0, 3]), ctypes.byref(info)) == -1
     assert lib.gs_grid_plan(10, 9, _lib.int32_array([2] * 9), ctypes.byref(info)) == -4
+    assert lib.gs_grid_plan(1 << 24, 2, _lib.int32_array([3, 3]), ctypes.byref(info)) == -4
 
 
 def test_structures_order_matches_oracle_enumeration():
