@@ -80,11 +80,15 @@ int gs_eval_encoded(const double* certainty, const uint8_t* correct,
  *   grids     concatenated per-model grids on the DEVICE, f64, each strictly
  *             increasing (grid_len[j] values for model j)
  *   grid_len  HOST array [n_models]
- * gs_grid_info reports the config count and the workspace the table needs.
- * Counts are accumulated exactly in f32 lanes, so n_rec < 2^24.
- * gs_grid_build fills the workspace (histogram + prefix tables); it must run
- * before gs_grid_eval / gs_grid_pareto on the same workspace.
+ * gs_grid_info reports the config count and the workspace the tables need
+ * (n_rec < 2^24).  gs_grid_build fills the prefix tables; it must run
+ * before gs_grid_eval on the same workspace.  The workspace's histogram
+ * region must be zero when gs_grid_build starts and is left zero when it
+ * returns; pass GS_GRID_WORKSPACE_DIRTY on the first build of a fresh (or
+ * reused-for-something-else) workspace to have it zeroed first.
  * ---------------------------------------------------------------------- */
+#define GS_GRID_WORKSPACE_DIRTY 1
+
 typedef struct gs_grid_info {
   int64_t n_configs;      /* total configs of the enumeration            */
   int64_t n_cells;        /* main prefix-table cells (dims 0..M-2)       */
@@ -99,7 +103,7 @@ int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
 int gs_grid_build(const double* certainty, const uint8_t* correct,
                   int64_t n_rec, int32_t n_models, const double* grids,
                   const int32_t* grid_len, void* workspace,
-                  size_t workspace_bytes, void* stream);
+                  size_t workspace_bytes, int32_t flags, void* stream);
 /* Score configs [config_begin, config_begin + config_count).  Any output
  * pointer may be NULL to skip it.  n_correct receives the integer correct
  * count (accuracy * n_rec) used by the exact Pareto reduction. */

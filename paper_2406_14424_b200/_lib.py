@@ -53,7 +53,7 @@ _SIGNATURES = {
                         c_size_t, c_void_p],
     "gs_grid_plan": [c_int64, c_int32, POINTER(c_int32), POINTER(gs_grid_info)],
     "gs_grid_build": [c_void_p, c_void_p, c_int64, c_int32, c_void_p, POINTER(c_int32),
-                      c_void_p, c_size_t, c_void_p],
+                      c_void_p, c_size_t, c_int32, c_void_p],
     "gs_grid_eval": [c_int64, c_int32, POINTER(c_int32), c_void_p, c_int64, c_int64, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "gs_grid_decode": [c_int32, POINTER(c_int32), c_void_p, c_void_p, c_int64, c_void_p,

@@ -16,6 +16,7 @@
 // are merged across record splits with u32 atomics (exact, order-free); a
 // finalize kernel does the f64 epilogue in the reference's order.
 #include <algorithm>
+#include <atomic>
 
 #include "gs_common.cuh"
 
@@ -200,8 +201,12 @@ __global__ void eval_finalize_kernel(const uint32_t* counts, const int32_t* stag
 template <int MAXL>
 cudaError_t launch_eval(const EvalArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   auto k = eval_list_kernel<MAXL>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static std::atomic<int> smem_set{0};
+  if ((int)smem > smem_set.load()) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set.store((int)smem);
+  }
   k<<<grid, kEvalThreads, smem, st>>>(a);
   return cudaGetLastError();
 }

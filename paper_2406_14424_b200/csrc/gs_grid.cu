@@ -21,22 +21,27 @@
 //                      + c_{m_K}[final pos]
 // which is the per-record walk's count, exactly.
 //
-// Table layout (HBM / L2): the main table F holds, per cell, one 16-byte
-// vector of four counts {cnt, c_{M-1}, c_{M-2}, c_{M-3}}.  A correct count
-// c_j is only ever read at positions whose dimensions > j are at "any", so
-// models j <= M-4 live in a smaller side table S over dims 0..M-4 (for the
-// 4-model cascade: one row of 101 cells, privatised in shared memory).
-// The histogram adds each record with ONE red.global.add.v4.f32 (integer
-// counts are exact in f32 below 2^24), so the histogram costs one L2 vector
-// atomic per record.  The prefix sums convert to u32.
+// Table layout.  A correct count c_j is only ever read at positions whose
+// dimensions > j are at "any", so:
+//   main table F over dims 0..M-2, channels {cnt, c_{M-1}, c_{M-2}};
+//   side table S over dims 0..M-3, channels {c_0 .. c_{M-3}}.
+// Channels are packed as fields of B = bitlen(n_rec) bits into u64 words
+// (three per word while n_rec < 2^21).  Every count — histogram or prefix —
+// is <= n_rec < 2^B, so packed words add without carries: the histogram is
+// one 64-bit L2 atomic per record per table, and the prefix sums add whole
+// words.  (Random-scatter L2 atomic throughput bounds the histogram, so
+// packing three counts into one op matters more than anything else there.)
+// Histogram and prefix live in separate buffers: the first scan pass reads
+// the histogram, writes the prefix and re-zeroes the histogram, so no
+// memset runs per build (the caller zeroes the workspace once).
 //
-// Kernels: grid_hist (one pass over the records, vector loads, binary search
-// in shared-memory grids), rowscan (contiguous last dim, warp-shuffle scan),
-// colscan (strided dims: [len x 32]-cell tiles staged in shared memory with
-// cp.async, one round trip per 128 rows), grid_eval (R consecutive configs per thread; everything that
-// depends only on the leading thresholds is computed once per "row" of
-// configs; f64 epilogue in the reference's order, no FMA contraction).
+// Kernels: grid_hist (one pass over the records), rowscan (contiguous last
+// dim, warp-shuffle scan), colscan (strided dims: [128 x 32]-element tiles in
+// shared memory, two-level scan), grid_eval (one warp per "row" of configs
+// sharing every threshold but the last forwarding one; f64 epilogue in the
+// reference's order with non-contracted multiply/add).
 #include <algorithm>
+#include <atomic>
 
 #include "gs_common.cuh"
 
@@ -44,40 +49,49 @@ namespace gs {
 namespace {
 
 constexpr int kMaxM = GS_MAX_MODELS;
-constexpr int64_t kMaxExactF32 = 1ll << 24;
+constexpr int64_t kMaxRec = 1ll << 24;
 constexpr int kHistThreads = 512;
-constexpr size_t kSidePrivMax = 16 * 1024;
+constexpr size_t kSidePrivMax = 32 * 1024;
+constexpr int kMaxWF = 2;  // words per main-table cell
+constexpr int kMaxWS = 3;  // words per side-table cell
 
 struct Plan {
-  int M = 0, D = 0, DP = 0, NVP = 0, n_struct = 0;
+  int M = 0, D = 0, DS = 0, n_struct = 0;
+  int B = 0, F = 0, WF = 0, WS = 0;
   int glen[kMaxM] = {};
   int64_t dims[kMaxM] = {};
   int64_t strideF[kMaxM] = {};
-  int64_t strideP[kMaxM] = {};
-  int64_t cellsF = 1, cellsP = 0;
+  int64_t strideS[kMaxM] = {};
+  int64_t cellsF = 1, cellsS = 0;
   int64_t n_configs = 0;
   int64_t struct_begin[256 + 1] = {};
   uint32_t struct_mask[256] = {};
-  size_t offP = 0, bytes = 0;
+  size_t offHF = 0, offF = 0, offHS = 0, offS = 0, bytes = 0;
 };
 
 int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   if (M < 1 || !grid_len || n_rec < 1) return GS_EINVAL;
-  if (M > kMaxM || n_rec >= kMaxExactF32) return GS_EUNSUPPORTED;
+  if (M > kMaxM || n_rec >= kMaxRec) return GS_EUNSUPPORTED;
   p->M = M;
   p->D = M - 1;
-  p->DP = M >= 4 ? M - 3 : 0;
-  p->NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  p->DS = M >= 3 ? M - 2 : 0;
   for (int j = 0; j < M; ++j) {
     if (grid_len[j] < 1 || grid_len[j] > (1 << 20)) return GS_EINVAL;
     p->glen[j] = grid_len[j];
   }
+  int B = 1;
+  while (((int64_t)1 << B) <= n_rec) ++B;
+  p->B = B;
+  p->F = 64 / B;
+  p->WF = (3 + p->F - 1) / p->F;
+  p->WS = p->DS > 0 ? (M - 2 + p->F - 1) / p->F : 0;
+  if (p->WF > kMaxWF || p->WS > kMaxWS) return GS_EUNSUPPORTED;
   double cells = 1.0;
   for (int j = 0; j < p->D; ++j) {
     p->dims[j] = (int64_t)p->glen[j] + 1;
     cells *= (double)p->dims[j];
   }
-  if (cells * 16.0 > 1.4e11) return GS_EUNSUPPORTED;
+  if (cells * 16.0 * p->WF > 1.4e11) return GS_EUNSUPPORTED;
   int64_t s = 1;
   for (int j = p->D - 1; j >= 0; --j) {
     p->strideF[j] = s;
@@ -85,11 +99,11 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   }
   p->cellsF = s;
   s = 1;
-  for (int j = p->DP - 1; j >= 0; --j) {
-    p->strideP[j] = s;
+  for (int j = p->DS - 1; j >= 0; --j) {
+    p->strideS[j] = s;
     s *= p->dims[j];
   }
-  p->cellsP = p->DP > 0 ? s : 0;
+  p->cellsS = p->DS > 0 ? s : 0;
   // structures: size ascending, then lexicographic (itertools.combinations)
   int ns = 0;
   int64_t off = 0;
@@ -122,61 +136,69 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->n_struct = ns;
   p->struct_begin[ns] = off;
   p->n_configs = off;
-  p->offP = round_up((size_t)p->cellsF * 16, 256);
-  p->bytes = p->offP + round_up((size_t)p->cellsP * p->NVP * 16, 256);
+  const size_t bF = round_up((size_t)p->cellsF * p->WF * 8, 256);
+  const size_t bS = round_up((size_t)p->cellsS * p->WS * 8, 256);
+  p->offHF = 0;
+  p->offF = bF;
+  p->offHS = 2 * bF;
+  p->offS = 2 * bF + bS;
+  p->bytes = 2 * bF + 2 * bS;
   return GS_OK;
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
+// #{g[i] <= x} for strictly increasing g (n >= 1).  Branch-free: the trip
+// count depends on n only, so a warp never diverges in the search.
+__device__ __forceinline__ int upper_count(const double* g, int n, double x) {
+  int base = 0, len = n;
+  while (len > 1) {
+    const int half = len >> 1;
+    base = (g[base + half - 1] <= x) ? base + half : base;
+    len -= half;
+  }
+  return base + (g[base] <= x ? 1 : 0);
 }
 
-__device__ __forceinline__ int upper_count(const double* g, int n, double x) {
-  int lo = 0, hi = n;  // #{g[i] <= x}, g strictly increasing
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (g[mid] <= x)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size,
+// so later calls (e.g. inside a CUDA-graph capture) issue no attribute calls.
+template <typename Kernel>
+cudaError_t ensure_smem(Kernel k, std::atomic<int>& done, size_t bytes) {
+  if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.store((int)bytes, std::memory_order_release);
+  return e;
 }
 
 // ------------------------------------------------------------------ hist --
 struct HistArgs {
   const double* cert;
   const uint8_t* corr;
-  int64_t n_rec;
+  int32_t n_rec;
   const double* grids;
-  int32_t goff[kMaxM];
   int32_t glen[kMaxM];
   int64_t strideF[kMaxM];
-  int64_t strideP[kMaxM];
-  int64_t cellsP;
-  int32_t grid_doubles;  // grids of models 0..D-1 staged in smem
+  int64_t strideS[kMaxM];
+  int64_t cellsS;
+  int32_t B, F, WF, WS;
+  int32_t grid_doubles;  // grids of models 0..M-2 staged in smem
   int32_t vec_ok;
   int32_t priv;          // side table privatised in shared memory
-  float* F;
-  float* P;
+  unsigned long long* HF;
+  unsigned long long* HS;
 };
 
-template <int M>
+template <int M, typename Cell>
 __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
   constexpr int D = M - 1;
-  constexpr int DP = M >= 4 ? M - 3 : 0;
-  constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  constexpr int DS = M >= 3 ? M - 2 : 0;
   extern __shared__ __align__(16) double s_grid[];
-  float* s_side = reinterpret_cast<float*>(s_grid + a.grid_doubles);
+  unsigned long long* s_side = reinterpret_cast<unsigned long long*>(s_grid + a.grid_doubles);
   for (int i = threadIdx.x; i < a.grid_doubles; i += blockDim.x) s_grid[i] = a.grids[i];
-  if (DP > 0 && a.priv)
-    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) s_side[i] = 0.f;
+  if (DS > 0 && a.priv)
+    for (int64_t i = threadIdx.x; i < a.cellsS * a.WS; i += blockDim.x) s_side[i] = 0ull;
   __syncthreads();
 
-  const int64_t step = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n_rec; r += step) {
+  const int step = gridDim.x * blockDim.x;  // n_rec < 2^24, M <= 8: 32-bit offsets
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.n_rec; r += step) {
     double x[M];
     uint32_t k[M];
     const double* row = a.cert + r * M;
@@ -197,174 +219,173 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
       for (int j = 0; j < M; ++j) k[j] = (w >> (8 * j)) & 0xffu;
     } else {
 #pragma unroll
-      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j);
+      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j) != 0;
     }
-    int64_t cellF = 0, cellP = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) k[j] = k[j] != 0;
+    Cell cellF = 0, cellS = 0;
     int off = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       const int b = upper_count(s_grid + off, a.glen[j], x[j]);
       off += a.glen[j];
-      cellF += (int64_t)b * a.strideF[j];
-      if (j < DP) cellP += (int64_t)b * a.strideP[j];
+      cellF += (Cell)b * (Cell)a.strideF[j];
+      if (j < DS) cellS += (Cell)b * (Cell)a.strideS[j];
     }
-    // main table: {cnt, c_{M-1}, c_{M-2}, c_{M-3}}
-    float v[4] = {1.f, 0.f, 0.f, 0.f};
+    // main table: fields {cnt, c_{M-1}, c_{M-2}}
+    unsigned long long wf[kMaxWF] = {0ull, 0ull};
+    {
+      const uint32_t f[3] = {1u, k[M - 1], M >= 2 ? k[M >= 2 ? M - 2 : 0] : 0u};
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
-      if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i] ? 1.f : 0.f;
-    red_add_v4(a.F + cellF * 4, v[0], v[1], v[2], v[3]);
-    // side table: c_j for j <= M-4 at (b_0..b_{M-4})
-    if constexpr (DP > 0) {
+      for (int c = 0; c < 3; ++c) wf[c / a.F] += (unsigned long long)f[c] << ((c % a.F) * a.B);
+    }
 #pragma unroll
-      for (int j = 0; j < DP; ++j) {
-        if (!k[j]) continue;
-        const int64_t e = (cellP * NVP + j / 4) * 4 + (j % 4);
+    for (int w = 0; w < kMaxWF; ++w)
+      if (w < a.WF && wf[w]) atomicAdd(a.HF + (Cell)cellF * a.WF + w, wf[w]);
+    // side table: fields {c_0 .. c_{M-3}}
+    if constexpr (DS > 0) {
+      unsigned long long ws[kMaxWS] = {0ull, 0ull, 0ull};
+#pragma unroll
+      for (int j = 0; j < DS; ++j) ws[j / a.F] += (unsigned long long)k[j] << ((j % a.F) * a.B);
+#pragma unroll
+      for (int w = 0; w < kMaxWS; ++w) {
+        if (w >= a.WS || !ws[w]) continue;
         if (a.priv)
-          atomicAdd(s_side + e, 1.f);
+          atomicAdd(s_side + (Cell)cellS * a.WS + w, ws[w]);
         else
-          atomicAdd(a.P + e, 1.f);
+          atomicAdd(a.HS + (Cell)cellS * a.WS + w, ws[w]);
       }
     }
   }
-  if (DP > 0 && a.priv) {
+  if (DS > 0 && a.priv) {
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) {
-      const float c = s_side[i];
-      if (c != 0.f) atomicAdd(a.P + i, c);
+    for (int64_t i = threadIdx.x; i < a.cellsS * a.WS; i += blockDim.x) {
+      const unsigned long long c = s_side[i];
+      if (c) atomicAdd(a.HS + i, c);
     }
   }
 }
 
 // ----------------------------------------------------------------- scans --
-__device__ __forceinline__ uint4 to_u4(float4 f) {
-  return make_uint4(__float2uint_rn(f.x), __float2uint_rn(f.y), __float2uint_rn(f.z),
-                    __float2uint_rn(f.w));
-}
-__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) {
-  return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
-}
-__device__ __forceinline__ uint4 shfl_up4(uint4 v, int o) {
-  return make_uint4(__shfl_up_sync(0xffffffffu, v.x, o), __shfl_up_sync(0xffffffffu, v.y, o),
-                    __shfl_up_sync(0xffffffffu, v.z, o), __shfl_up_sync(0xffffffffu, v.w, o));
-}
-__device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
-  return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
-                    __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
-}
-
-// Inclusive prefix along the contiguous last dimension: one warp per row of
-// `len` uint4 cells, four consecutive cells per lane, warp-shuffle scan, one
-// load round trip per 128 cells.  from_f32 converts the f32 histogram.
-__global__ void __launch_bounds__(256) rowscan_kernel(uint4* T, int64_t n_rows, int len, int from_f32) {
+// Inclusive prefix along the contiguous last dimension (rows of `len` u64
+// words): one warp per row, four consecutive words per lane, warp-shuffle
+// scan.  When src != dst the source (the histogram) is zeroed after reading.
+__global__ void __launch_bounds__(256) rowscan_kernel(unsigned long long* src,
+                                                      unsigned long long* dst, int64_t n_rows,
+                                                      int len) {
   const int lane = (int)lane_id();
+  const bool zero = src != dst;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
-    uint4* row = T + r * len;
-    uint4 carry = make_uint4(0, 0, 0, 0);
+    unsigned long long* in = src + r * len;
+    unsigned long long* out = dst + r * len;
+    unsigned long long carry = 0;
     for (int base = 0; base < len; base += 128) {
-      uint4 e[4];
+      unsigned long long e[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = base + lane * 4 + u;
-        e[u] = c < len ? row[c] : make_uint4(0, 0, 0, 0);
-        if (from_f32) e[u] = to_u4(*reinterpret_cast<float4*>(&e[u]));
+        e[u] = c < len ? in[c] : 0ull;
       }
-      uint4 tot = make_uint4(0, 0, 0, 0);
+      if (zero) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = base + lane * 4 + u;
+          if (c < len) in[c] = 0ull;
+        }
+      }
+      unsigned long long tot = 0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        tot = add4(tot, e[u]);
+        tot += e[u];
         e[u] = tot;
       }
-      uint4 incl = tot;
+      unsigned long long incl = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint4 y = shfl_up4(incl, o);
-        if (lane >= o) incl = add4(incl, y);
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      const uint4 excl = add4(carry, make_uint4(incl.x - tot.x, incl.y - tot.y, incl.z - tot.z,
-                                                incl.w - tot.w));
+      const unsigned long long excl = carry + incl - tot;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = base + lane * 4 + u;
-        if (c < len) row[c] = add4(e[u], excl);
+        if (c < len) out[c] = e[u] + excl;
       }
-      carry = add4(carry, shfl4(incl, 31));
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
-
-constexpr int kColTile = 32;    // consecutive inner cells per CTA
+constexpr int kColTile = 32;    // consecutive inner elements per CTA
 constexpr int kColChunk = 128;  // rows of the scanned dimension per smem pass
+constexpr int kColSeg = 16;     // rows per scanning thread (8 segments x 32 columns)
 
-// Inclusive prefix along a strided dimension of a table of uint4 cells viewed
-// as [outer][len][inner].  A CTA owns kColTile consecutive inner cells of one
-// outer index: it stages the [len x kColTile] tile in shared memory with
-// cp.async (one round trip per 128 rows), scans each (cell, lane) column in
-// shared memory, and writes the tile back coalesced.
-__global__ void __launch_bounds__(256) colscan_kernel(uint4* T, int64_t outer, int64_t len,
-                                                      int64_t inner, int from_f32) {
-  extern __shared__ __align__(16) uint4 s[];  // [kColChunk][kColTile]
+// Inclusive prefix along a strided dimension of a u64 table viewed as
+// [outer][len][inner].  A CTA owns kColTile consecutive inner elements of one
+// outer index: it loads a [128 x 32] tile (16 independent loads per thread,
+// one round trip), scans it in shared memory (each thread a 16-row segment
+// of one column, then segment offsets), and writes it back coalesced.
+__global__ void __launch_bounds__(256) colscan_kernel(unsigned long long* src,
+                                                      unsigned long long* dst, int64_t outer,
+                                                      int64_t len, int64_t inner) {
+  __shared__ unsigned long long s[kColChunk][kColTile + 1];
+  __shared__ unsigned long long s_seg[kColChunk / kColSeg][kColTile];
+  const bool zero = src != dst;
   const int64_t tiles_per_outer = (inner + kColTile - 1) / kColTile;
   const int64_t n_tiles = outer * tiles_per_outer;
   const int t = threadIdx.x;
+  const int col = t & (kColTile - 1);
+  const int seg = t >> 5;  // 0..7
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t o = tile / tiles_per_outer;
     const int64_t i0 = (tile - o * tiles_per_outer) * kColTile;
     const int w = (int)min((int64_t)kColTile, inner - i0);
-    uint4* base = T + o * len * inner + i0;
-    // scanning threads: (cell c, lane q) = (t / 4, t % 4) for t < 4 * w
-    uint32_t carry = 0;
+    unsigned long long* in = src + o * len * inner + i0;
+    unsigned long long* out = dst + o * len * inner + i0;
+    unsigned long long carry = 0;  // per column, kept by segment-7 threads' view via smem
     for (int64_t r0 = 0; r0 < len; r0 += kColChunk) {
       const int rows = (int)min((int64_t)kColChunk, len - r0);
-      for (int e = t; e < rows * w; e += blockDim.x) {
-        const int rr = e / w, cc = e - (e / w) * w;
-        cp_async16(s + rr * kColTile + cc, base + (r0 + rr) * inner + cc);
+      // load: thread (seg, col) loads rows seg, seg+8, ... of column col
+      unsigned long long v[kColChunk / 8];
+#pragma unroll
+      for (int u = 0; u < kColChunk / 8; ++u) {
+        const int rr = seg + 8 * u;
+        v[u] = (rr < rows && col < w) ? in[(r0 + rr) * inner + col] : 0ull;
       }
-      cp_async_wait_all();
-      __syncthreads();
-      if (t < 4 * w) {
-        uint32_t* col = reinterpret_cast<uint32_t*>(s) + (t >> 2) * 4 + (t & 3);
-        uint32_t acc = carry;
-        int r = 0;
-        for (; r + 4 <= rows; r += 4) {
-          uint32_t v0 = col[(r + 0) * kColTile * 4], v1 = col[(r + 1) * kColTile * 4];
-          uint32_t v2 = col[(r + 2) * kColTile * 4], v3 = col[(r + 3) * kColTile * 4];
-          if (from_f32) {
-            v0 = __float2uint_rn(__uint_as_float(v0));
-            v1 = __float2uint_rn(__uint_as_float(v1));
-            v2 = __float2uint_rn(__uint_as_float(v2));
-            v3 = __float2uint_rn(__uint_as_float(v3));
-          }
-          acc += v0;
-          col[(r + 0) * kColTile * 4] = acc;
-          acc += v1;
-          col[(r + 1) * kColTile * 4] = acc;
-          acc += v2;
-          col[(r + 2) * kColTile * 4] = acc;
-          acc += v3;
-          col[(r + 3) * kColTile * 4] = acc;
+      if (zero) {
+#pragma unroll
+        for (int u = 0; u < kColChunk / 8; ++u) {
+          const int rr = seg + 8 * u;
+          if (rr < rows && col < w) in[(r0 + rr) * inner + col] = 0ull;
         }
-        for (; r < rows; ++r) {
-          uint32_t v = col[r * kColTile * 4];
-          if (from_f32) v = __float2uint_rn(__uint_as_float(v));
-          acc += v;
-          col[r * kColTile * 4] = acc;
-        }
-        carry = acc;
       }
+#pragma unroll
+      for (int u = 0; u < kColChunk / 8; ++u) s[seg + 8 * u][col] = v[u];
       __syncthreads();
-      for (int e = t; e < rows * w; e += blockDim.x) {
-        const int rr = e / w, cc = e - (e / w) * w;
-        base[(r0 + rr) * inner + cc] = s[rr * kColTile + cc];
+      // segment scan: thread (seg, col) scans rows [seg*16, seg*16+16)
+      unsigned long long acc = 0;
+#pragma unroll
+      for (int q = 0; q < kColSeg; ++q) {
+        acc += s[seg * kColSeg + q][col];
+        s[seg * kColSeg + q][col] = acc;
       }
+      s_seg[seg][col] = acc;
+      __syncthreads();
+      unsigned long long total = carry;
+#pragma unroll
+      for (int q = 0; q < kColChunk / kColSeg; ++q) total += s_seg[q][col];
+#pragma unroll
+      for (int u = 0; u < kColChunk / 8; ++u) {
+        const int rr = seg + 8 * u;
+        if (rr < rows && col < w) {
+          // rows of segment rr/16 get that segment's offset
+          unsigned long long base = carry;
+          for (int q = 0; q < rr / kColSeg; ++q) base += s_seg[q][col];
+          out[(r0 + rr) * inner + col] = s[rr][col] + base;
+        }
+      }
+      carry = total;
       __syncthreads();
     }
   }
@@ -376,21 +397,21 @@ __global__ void __launch_bounds__(256) colscan_kernel(uint4* T, int64_t outer, i
 // enumeration).  One warp owns a row: the row-shared part of the walk (cells
 // of the leading stages, their forward fractions and the partial mean cost)
 // is computed once per warp from broadcast loads, then each lane finishes
-// configs kl = lane, lane+32, ... with one 16-byte cell load, two f64
-// divisions and coalesced stores.
+// configs kl = lane, lane+32, ... (four loads in flight) with one cell load,
+// two f64 divisions and coalesced stores.
 struct EvalGridArgs {
-  int32_t M, n_struct, NVP, DP;
+  int32_t M, n_struct, B, F, WF, WS, DS;
   int32_t glen[kMaxM];
   int64_t strideF[kMaxM];
-  int64_t strideP[kMaxM];
-  int64_t n_rec, cellsF, cellsP;
+  int64_t strideS[kMaxM];
+  int64_t n_rec, cellsF, cellsS;
   int64_t cfg_begin, cfg_count;
   int64_t row_lo, row_hi;
   int64_t struct_begin[256 + 1];
   int64_t row_begin[256 + 1];
   uint32_t struct_mask[256];
-  const uint4* F;
-  const uint4* P;
+  const unsigned long long* Ft;
+  const unsigned long long* St;
   const double* cost1;
   double* acc;
   double* cost;
@@ -398,15 +419,43 @@ struct EvalGridArgs {
   uint32_t* n_correct;
 };
 
-__device__ __forceinline__ uint32_t lane4(const uint4& v, int c) {
-  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+struct CellF {
+  unsigned long long w[kMaxWF];
+};
+struct CellS {
+  unsigned long long w[kMaxWS];
+};
+
+// field c of a packed cell (word chosen with selects, never a dynamic
+// register-array index, so cells stay in registers)
+template <int W>
+__device__ __forceinline__ uint32_t fieldw(const unsigned long long (&w)[W], int c, int F, int B) {
+  const int q = c / F;
+  unsigned long long word = w[0];
+#pragma unroll
+  for (int i = 1; i < W; ++i) word = q == i ? w[i] : word;
+  return (uint32_t)((word >> ((c - q * F) * B)) & ((1ull << B) - 1));
+}
+
+__device__ __forceinline__ CellF loadF(const EvalGridArgs& a, int64_t cell) {
+  CellF v;
+#pragma unroll
+  for (int q = 0; q < kMaxWF; ++q) v.w[q] = q < a.WF ? __ldg(a.Ft + cell * a.WF + q) : 0ull;
+  return v;
+}
+__device__ __forceinline__ CellS loadS(const EvalGridArgs& a, int64_t cell) {
+  CellS v;
+#pragma unroll
+  for (int q = 0; q < kMaxWS; ++q) v.w[q] = q < a.WS ? __ldg(a.St + cell * a.WS + q) : 0ull;
+  return v;
 }
 
 // correct count of model m at the current position
 template <int M>
-__device__ __forceinline__ uint32_t chan(const uint4& vF, const uint4* vP, int m) {
-  if (m >= M - 3) return lane4(vF, 1 + (M - 1 - m));
-  return lane4(vP[m / 4], m % 4);
+__device__ __forceinline__ uint32_t chan(const EvalGridArgs& a, const CellF& f, const CellS& s, int m) {
+  if (m == M - 1) return fieldw(f.w, 1, a.F, a.B);
+  if (m == M - 2) return fieldw(f.w, 2, a.F, a.B);
+  return fieldw(s.w, m, a.F, a.B);
 }
 
 template <int M>
@@ -433,21 +482,19 @@ __device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, c
 
 template <int M>
 __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ EvalGridArgs a) {
-  constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
-  constexpr int NVPX = NVP > 0 ? NVP : 1;
   const int lane = (int)lane_id();
   const double n = (double)a.n_rec;
   const double one = ddiv(n, n);  // first-stage fraction, as the reference computes it
-  const uint4 totF = __ldg(a.F + a.cellsF - 1);
-  uint4 totP[NVPX];
+  const CellF totF = loadF(a, a.cellsF - 1);
+  CellS totS;
 #pragma unroll
-  for (int v = 0; v < NVPX; ++v)
-    totP[v] = NVP > 0 ? __ldg(a.P + (a.cellsP - 1) * NVP + v) : make_uint4(0, 0, 0, 0);
+  for (int q = 0; q < kMaxWS; ++q) totS.w[q] = 0ull;
+  if (a.DS > 0) totS = loadS(a, a.cellsS - 1);
 
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t rg = a.row_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
        rg < a.row_hi; rg += nw) {
-    int s = 0;
+    int s;
     {
       int lo = 0, hi = a.n_struct - 1;  // last s with row_begin[s] <= rg
       while (lo < hi) {
@@ -478,7 +525,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       const int64_t i = s_begin - a.cfg_begin;
       if (lane == 0 && i >= 0 && i < a.cfg_count) {
         const double mean = dadd(0.0, dmul(one, __ldg(a.cost1 + mK)));
-        store_config<M>(a, i, fr, 1, one, mean, chan<M>(totF, totP, mK), n);
+        store_config<M>(a, i, fr, 1, one, mean, chan<M>(a, totF, totS, mK), n);
       }
       continue;
     }
@@ -492,15 +539,19 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       kk[t] = 0;
       if (t <= K - 3) {
         const int g = a.glen[(mdl >> (4 * t)) & 15u];
-        kk[t] = (int)(rem % g);
-        rem /= g;
+        if (rem < 0x7fffffffLL) {  // 32-bit division in the common case
+          const int r32 = (int)rem;
+          kk[t] = r32 % g;
+          rem = r32 / g;
+        } else {
+          kk[t] = (int)(rem % g);
+          rem /= g;
+        }
       }
     }
-    int64_t cF = a.cellsF - 1, cP = a.cellsP - 1;
-    uint4 vF = totF;
-    uint4 vP[NVPX];
-#pragma unroll
-    for (int v = 0; v < NVPX; ++v) vP[v] = totP[v];
+    int64_t cF = a.cellsF - 1, cS = a.cellsS - 1;
+    CellF vF = totF;
+    CellS vS = totS;
     uint32_t cp = 0;
     fr[0] = one;
     double mp = dadd(0.0, dmul(one, __ldg(a.cost1 + (mdl & 15u))));
@@ -508,41 +559,57 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
     for (int t = 0; t < M - 2; ++t) {
       if (t <= K - 3) {
         const int m = (mdl >> (4 * t)) & 15u;
-        const uint32_t A = chan<M>(vF, vP, m);
+        const uint32_t A = chan<M>(a, vF, vS, m);
         const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
         cF -= dk * a.strideF[m];
-        vF = __ldg(a.F + cF);
-        if (NVP > 0 && m < a.DP) {
-          cP -= dk * a.strideP[m];
-#pragma unroll
-          for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
+        vF = loadF(a, cF);
+        if (m < a.DS) {
+          cS -= dk * a.strideS[m];
+          vS = loadS(a, cS);
         }
-        cp += A - chan<M>(vF, vP, m);
-        fr[t + 1] = ddiv((double)vF.x, n);
+        cp += A - chan<M>(a, vF, vS, m);
+        fr[t + 1] = ddiv((double)fieldw(vF.w, 0, a.F, a.B), n);
         mp = dadd(mp, dmul(fr[t + 1], __ldg(a.cost1 + ((mdl >> (4 * (t + 1))) & 15u))));
       }
     }
-    const uint32_t a_last = chan<M>(vF, vP, mL);
+    const uint32_t a_last = chan<M>(a, vF, vS, mL);
     const double costK = __ldg(a.cost1 + mK);
-    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
+    const bool needS = mL < a.DS || mK < a.DS;
     const int64_t c_row = s_begin + row * gL - a.cfg_begin;
-    for (int kl = lane; kl < gL; kl += 32) {
-      const int64_t i = c_row + kl;
-      if (i < 0 || i >= a.cfg_count) continue;
-      const int64_t dk = (int64_t)(gL - kl);
-      const uint4 wF = __ldg(a.F + cF - dk * a.strideF[mL]);
-      uint4 wP[NVPX];
+    // cell of threshold index kl = base cell + kl * stride (kl = gL is "any")
+    const int64_t sFL = a.strideF[mL];
+    const int64_t rowF = cF - (int64_t)gL * sFL;
+    const int64_t sSL = mL < a.DS ? a.strideS[mL] : 0;
+    const int64_t rowS = cS - (int64_t)gL * sSL;
+    constexpr int U = 4;  // configs per lane per pass, loads issued together
+    for (int base = 0; base < gL; base += 32 * U) {
+      CellF wF[U];
+      CellS wS[U];
 #pragma unroll
-      for (int v = 0; v < NVPX; ++v) wP[v] = make_uint4(0, 0, 0, 0);
-      if (needP) {
-        const int64_t q = cP - (mL < a.DP ? dk * a.strideP[mL] : 0);
+      for (int u = 0; u < U; ++u) {
+        const int kl = base + lane + 32 * u;
 #pragma unroll
-        for (int v = 0; v < NVPX; ++v) wP[v] = __ldg(a.P + q * NVP + v);
+        for (int q = 0; q < kMaxWF; ++q) wF[u].w[q] = 0ull;
+#pragma unroll
+        for (int q = 0; q < kMaxWS; ++q) wS[u].w[q] = 0ull;
+        if (kl < gL) {
+          wF[u] = loadF(a, rowF + (int64_t)kl * sFL);
+          if (needS) wS[u] = loadS(a, rowS + (int64_t)kl * sSL);
+        }
       }
-      const uint32_t correct = cp + a_last - chan<M>(wF, wP, mL) + chan<M>(wF, wP, mK);
-      const double frK = ddiv((double)wF.x, n);
-      const double mean = dadd(mp, dmul(frK, costK));
-      store_config<M>(a, i, fr, K, frK, mean, correct, n);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kl = base + lane + 32 * u;
+        const int64_t i = c_row + kl;
+        if (kl >= gL || i < 0 || i >= a.cfg_count) continue;
+        CellS sv;
+#pragma unroll
+        for (int q = 0; q < kMaxWS; ++q) sv.w[q] = needS ? wS[u].w[q] : vS.w[q];
+        const uint32_t correct = cp + a_last - chan<M>(a, wF[u], sv, mL) + chan<M>(a, wF[u], sv, mK);
+        const double frK = ddiv((double)fieldw(wF[u].w, 0, a.F, a.B), n);
+        const double mean = dadd(mp, dmul(frK, costK));
+        store_config<M>(a, i, fr, K, frK, mean, correct, n);
+      }
     }
   }
 }
@@ -612,15 +679,24 @@ int64_t global_row(const Plan& p, const int64_t* row_begin, int64_t c) {
   return row_begin[s] + (c - p.struct_begin[s]) / row_len(p, s);
 }
 
-template <int M>
-cudaError_t launch_hist(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
-  auto k = grid_hist_kernel<M>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int M, typename Cell>
+cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
+  auto k = grid_hist_kernel<M, Cell>;
+  static std::atomic<int> smem_set{0};
+  cudaError_t e = ensure_smem(k, smem_set, smem);
   if (e != cudaSuccess) return e;
   int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
   k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
   return cudaGetLastError();
+}
+
+// 32-bit cell arithmetic whenever every table index fits
+template <int M>
+cudaError_t launch_hist(const HistArgs& h, int64_t n_rec, size_t smem, int64_t max_index,
+                        cudaStream_t st) {
+  return max_index < ((int64_t)1 << 32) ? launch_hist_t<M, uint32_t>(h, n_rec, smem, st)
+                                        : launch_hist_t<M, int64_t>(h, n_rec, smem, st);
 }
 
 template <int M>
@@ -632,35 +708,36 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Inclusive prefix over every dimension of a table of uint4 elements
-// (`vec` elements per cell), starting from the f32 histogram.
-cudaError_t prefix_table(uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
-                         cudaStream_t st) {
-  if (ndim == 0) {  // a single cell: convert in place
-    rowscan_kernel<<<1, 32, 0, st>>>(T, 1, 1, 1);
-    return cudaGetLastError();
-  }
+// Inclusive prefix over every dimension of a u64 table with `vec` words per
+// cell.  The first pass reads the histogram `H` (and re-zeroes it), writes
+// `T`; later passes run in place on `T`.
+cudaError_t prefix_table(unsigned long long* H, unsigned long long* T, int ndim,
+                         const int64_t* dims, int64_t cells, int vec, cudaStream_t st) {
   int64_t inner = vec;
-  bool converted = false;
+  unsigned long long* src = H;
+  if (ndim == 0) {  // one cell of `vec` words: copy-and-zero as a 1 x vec "scan"
+    for (int q = 0; q < vec; ++q) {
+      rowscan_kernel<<<1, 32, 0, st>>>(H + q, T + q, 1, 1);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   for (int d = ndim - 1; d >= 0; --d) {
     const int64_t len = dims[d];
     const int64_t outer = cells * vec / (len * inner);
     if (inner == 1) {
       int64_t blocks = (outer * 32 + 255) / 256;
       blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
-      rowscan_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, outer, (int)len, converted ? 0 : 1);
+      rowscan_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, T, outer, (int)len);
     } else {
-      const size_t smem = (size_t)kColChunk * kColTile * sizeof(uint4);
-      cudaError_t e = cudaFuncSetAttribute(colscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
       const int64_t tiles = outer * ((inner + kColTile - 1) / kColTile);
       const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 8));
-      colscan_kernel<<<(unsigned)blocks, 256, smem, st>>>(T, outer, len, inner, converted ? 0 : 1);
+      colscan_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, T, outer, len, inner);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    converted = true;
+    src = T;
     inner *= len;
   }
   return cudaSuccess;
@@ -679,7 +756,7 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
   if (rc != GS_OK) return rc;
   info->n_configs = p.n_configs;
   info->n_cells = p.cellsF;
-  info->side_cells = p.cellsP;
+  info->side_cells = p.cellsS;
   info->n_structures = p.n_struct;
   info->max_len = p.M;
   info->workspace_bytes = p.bytes;
@@ -688,7 +765,8 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
 
 extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, int64_t n_rec,
                              int32_t n_models, const double* grids, const int32_t* grid_len,
-                             void* workspace, size_t workspace_bytes, void* stream) {
+                             void* workspace, size_t workspace_bytes, int32_t flags,
+                             void* stream) {
   Plan p;
   int rc = make_plan(n_rec, n_models, grid_len, &p);
   if (rc != GS_OK) return rc;
@@ -696,48 +774,57 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  GS_CUDA_TRY(cudaMemsetAsync(ws, 0, p.bytes, st));
-  float* F = reinterpret_cast<float*>(ws);
-  float* P = reinterpret_cast<float*>(ws + p.offP);
+  auto* HF = reinterpret_cast<unsigned long long*>(ws + p.offHF);
+  auto* Ft = reinterpret_cast<unsigned long long*>(ws + p.offF);
+  auto* HS = reinterpret_cast<unsigned long long*>(ws + p.offHS);
+  auto* St = reinterpret_cast<unsigned long long*>(ws + p.offS);
+  if (flags & GS_GRID_WORKSPACE_DIRTY) {
+    GS_CUDA_TRY(cudaMemsetAsync(HF, 0, (size_t)p.cellsF * p.WF * 8, st));
+    if (p.cellsS) GS_CUDA_TRY(cudaMemsetAsync(HS, 0, (size_t)p.cellsS * p.WS * 8, st));
+  }
 
   HistArgs h{};
   h.cert = certainty;
   h.corr = correct;
-  h.n_rec = n_rec;
+  h.n_rec = (int32_t)n_rec;
   h.grids = grids;
   int off = 0;
   for (int j = 0; j < n_models; ++j) {
-    h.goff[j] = off;
     h.glen[j] = p.glen[j];
-    off += p.glen[j];
+    if (j < p.D) off += p.glen[j];
   }
   for (int j = 0; j < p.D; ++j) h.strideF[j] = p.strideF[j];
-  for (int j = 0; j < p.DP; ++j) h.strideP[j] = p.strideP[j];
-  h.cellsP = p.cellsP;
-  h.grid_doubles = p.D > 0 ? h.goff[p.D - 1] + h.glen[p.D - 1] : 0;
+  for (int j = 0; j < p.DS; ++j) h.strideS[j] = p.strideS[j];
+  h.cellsS = p.cellsS;
+  h.B = p.B;
+  h.F = p.F;
+  h.WF = p.WF;
+  h.WS = p.WS;
+  h.grid_doubles = off;
   h.vec_ok = aligned16(certainty) && ((reinterpret_cast<uintptr_t>(correct) & 3u) == 0);
-  const size_t side_bytes = (size_t)p.cellsP * p.NVP * 16;
-  h.priv = p.DP > 0 && side_bytes <= kSidePrivMax;
-  h.F = F;
-  h.P = P;
-  const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (h.priv ? side_bytes : 0) + 16;
+  const size_t side_bytes = (size_t)p.cellsS * p.WS * 8;
+  h.priv = p.DS > 0 && side_bytes <= kSidePrivMax;
+  h.HF = HF;
+  h.HS = HS;
+  const size_t smem = round_up((size_t)h.grid_doubles * sizeof(double), 16) +
+                      (h.priv ? side_bytes : 0) + 16;
   if (smem > 200 * 1024) return GS_EUNSUPPORTED;
+  const int64_t imax = std::max<int64_t>(p.cellsF * p.WF, p.cellsS * p.WS);
   cudaError_t e = cudaSuccess;
   switch (n_models) {
-    case 1: e = launch_hist<1>(h, n_rec, smem, st); break;
-    case 2: e = launch_hist<2>(h, n_rec, smem, st); break;
-    case 3: e = launch_hist<3>(h, n_rec, smem, st); break;
-    case 4: e = launch_hist<4>(h, n_rec, smem, st); break;
-    case 5: e = launch_hist<5>(h, n_rec, smem, st); break;
-    case 6: e = launch_hist<6>(h, n_rec, smem, st); break;
-    case 7: e = launch_hist<7>(h, n_rec, smem, st); break;
-    case 8: e = launch_hist<8>(h, n_rec, smem, st); break;
+    case 1: e = launch_hist<1>(h, n_rec, smem, imax, st); break;
+    case 2: e = launch_hist<2>(h, n_rec, smem, imax, st); break;
+    case 3: e = launch_hist<3>(h, n_rec, smem, imax, st); break;
+    case 4: e = launch_hist<4>(h, n_rec, smem, imax, st); break;
+    case 5: e = launch_hist<5>(h, n_rec, smem, imax, st); break;
+    case 6: e = launch_hist<6>(h, n_rec, smem, imax, st); break;
+    case 7: e = launch_hist<7>(h, n_rec, smem, imax, st); break;
+    case 8: e = launch_hist<8>(h, n_rec, smem, imax, st); break;
     default: return GS_EUNSUPPORTED;
   }
   GS_CUDA_TRY(e);
-  GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(F), p.D, p.dims, p.cellsF, 1, st));
-  if (p.DP > 0)
-    GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), p.DP, p.dims, p.cellsP, p.NVP, st));
+  GS_CUDA_TRY(prefix_table(HF, Ft, p.D, p.dims, p.cellsF, p.WF, st));
+  if (p.DS > 0) GS_CUDA_TRY(prefix_table(HS, St, p.DS, p.dims, p.cellsS, p.WS, st));
   return GS_OK;
 }
 
@@ -753,21 +840,21 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
              config_begin + config_count <= p.n_configs);
   if (config_count == 0) return GS_OK;
   if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
-  // vector stores need 16-byte aligned outputs
-  if ((accuracy && !aligned16(accuracy)) || (mean_cost && !aligned16(mean_cost)) ||
-      (n_correct && !aligned16(n_correct)) || (forward_frac && !aligned16(forward_frac)))
-    return GS_EINVAL;
+  if (forward_frac && n_models % 2 == 0 && !aligned16(forward_frac)) return GS_EINVAL;
   EvalGridArgs a{};
   a.M = p.M;
   a.n_struct = p.n_struct;
-  a.NVP = p.NVP;
-  a.DP = p.DP;
+  a.B = p.B;
+  a.F = p.F;
+  a.WF = p.WF;
+  a.WS = p.WS;
+  a.DS = p.DS;
   for (int j = 0; j < p.M; ++j) a.glen[j] = p.glen[j];
   for (int j = 0; j < p.D; ++j) a.strideF[j] = p.strideF[j];
-  for (int j = 0; j < p.DP; ++j) a.strideP[j] = p.strideP[j];
+  for (int j = 0; j < p.DS; ++j) a.strideS[j] = p.strideS[j];
   a.n_rec = n_rec;
   a.cellsF = p.cellsF;
-  a.cellsP = p.cellsP;
+  a.cellsS = p.cellsS;
   a.cfg_begin = config_begin;
   a.cfg_count = config_count;
   for (int s = 0; s <= p.n_struct; ++s) a.struct_begin[s] = p.struct_begin[s];
@@ -782,8 +869,8 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
   a.row_lo = global_row(p, a.row_begin, config_begin);
   a.row_hi = global_row(p, a.row_begin, config_begin + config_count - 1) + 1;
   const uint8_t* ws = static_cast<const uint8_t*>(workspace);
-  a.F = reinterpret_cast<const uint4*>(ws);
-  a.P = reinterpret_cast<const uint4*>(ws + p.offP);
+  a.Ft = reinterpret_cast<const unsigned long long*>(ws + p.offF);
+  a.St = reinterpret_cast<const unsigned long long*>(ws + p.offS);
   a.cost1 = cost1;
   a.acc = accuracy;
   a.cost = mean_cost;

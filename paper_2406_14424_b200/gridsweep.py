@@ -29,6 +29,8 @@ import torch
 from . import _lib
 from .types import Cascade
 
+GS_GRID_WORKSPACE_DIRTY = 1
+
 
 def structures(n_models: int, grid_len: Sequence[int]) -> list[tuple[tuple[int, ...], int, int]]:
     """[(models, first_config, n_configs)] in enumeration order."""
@@ -93,17 +95,22 @@ class GridSweep:
         self.info = info
         self.n_configs = int(info.n_configs)
         self.max_len = int(info.max_len)
-        self.table = torch.empty(int(info.workspace_bytes), dtype=torch.uint8, device=dev)
+        # zeroed once: each build leaves its histogram region zero again
+        self.table = torch.zeros(int(info.workspace_bytes), dtype=torch.uint8, device=dev)
         self._built = False
+        self._clean = True
         if build:
             self.build()
 
     # -- table -------------------------------------------------------------
     def build(self) -> None:
         lib = _lib.load()
+        flags = 0 if self._clean else GS_GRID_WORKSPACE_DIRTY
         rc = lib.gs_grid_build(self.cert.data_ptr(), self.corr.data_ptr(), self.n_rec,
                                self.n_models, self.grids.data_ptr(), self._glen,
-                               self.table.data_ptr(), self.table.numel(), _lib.stream_ptr())
+                               self.table.data_ptr(), self.table.numel(), flags,
+                               _lib.stream_ptr())
+        self._clean = rc == _lib.GS_OK
         _lib.check(rc, "grid build")
         self._built = True
 
@@ -134,6 +141,26 @@ class GridSweep:
                               self.table.data_ptr(), self.table.numel(), _lib.stream_ptr())
         _lib.check(rc, "grid eval")
         return out
+
+    def capture(self, out: SweepResult, build: bool = True,
+                evaluate: bool = True) -> torch.cuda.CUDAGraph:
+        """CUDA graph of one sweep step (table build and/or scoring every
+        config into `out`), so a step is one graph launch instead of a
+        Python-driven sequence of kernel launches."""
+        def body():
+            if build:
+                self.build()
+            if evaluate:
+                self.evaluate(out=out)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            body()  # first call does one-time kernel attribute setup outside capture
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            body()
+        return graph
 
     def pareto(self, begin: int = 0, count: int | None = None,
                res: SweepResult | None = None) -> tuple[torch.Tensor, SweepResult]:
