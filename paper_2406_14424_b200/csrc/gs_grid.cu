@@ -67,7 +67,14 @@ struct Plan {
   int64_t struct_begin[256 + 1] = {};
   uint32_t struct_mask[256] = {};
   size_t offHF = 0, offF = 0, offHS = 0, offS = 0, bytes = 0;
+  // bucketed build: records grouped by b_0, one CTA per b_0 slab
+  bool bucket = false;
+  int64_t d0 = 0, slab_cells = 0, side_slab = 0, cap = 0;
+  size_t offBk = 0, offCur = 0;
 };
+
+constexpr size_t kSlabSmemMax = 160 * 1024;
+constexpr double kBucketBytesMax = 4.0e9;
 
 int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   if (M < 1 || !grid_len || n_rec < 1) return GS_EINVAL;
@@ -79,10 +86,9 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
     if (grid_len[j] < 1 || grid_len[j] > (1 << 20)) return GS_EINVAL;
     p->glen[j] = grid_len[j];
   }
-  int B = 1;
-  while (((int64_t)1 << B) <= n_rec) ++B;
-  p->B = B;
-  p->F = 64 / B;
+  // field width: 21 bits (three fields per word) while every count fits
+  p->B = n_rec < ((int64_t)1 << 21) ? 21 : 32;
+  p->F = 64 / p->B;
   p->WF = (3 + p->F - 1) / p->F;
   p->WS = p->DS > 0 ? (M - 2 + p->F - 1) / p->F : 0;
   if (p->WF > kMaxWF || p->WS > kMaxWS) return GS_EUNSUPPORTED;
@@ -138,11 +144,31 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->n_configs = off;
   const size_t bF = round_up((size_t)p->cellsF * p->WF * 8, 256);
   const size_t bS = round_up((size_t)p->cellsS * p->WS * 8, 256);
-  p->offHF = 0;
-  p->offF = bF;
-  p->offHS = 2 * bF;
-  p->offS = 2 * bF + bS;
-  p->bytes = 2 * bF + 2 * bS;
+  // bucketed build when a b_0 slab (dims 1..M-2, at most two of them) and its
+  // side-table row fit in shared memory
+  if (p->D >= 2 && p->D <= 3) {
+    p->d0 = p->dims[0];
+    p->slab_cells = p->cellsF / p->d0;
+    p->side_slab = p->DS > 0 ? p->cellsS / p->d0 : 0;
+    p->cap = n_rec;
+    const size_t smem = (size_t)(p->slab_cells * p->WF + p->side_slab * p->WS) * 8;
+    p->bucket = smem <= kSlabSmemMax && p->slab_cells < (1 << 24) &&
+                (double)p->d0 * (double)p->cap * 4.0 <= kBucketBytesMax;
+  }
+  if (p->bucket) {
+    p->offF = 0;
+    p->offS = bF;
+    p->offBk = bF + bS;
+    p->offCur = p->offBk + round_up((size_t)p->d0 * p->cap * 4, 256);
+    p->bytes = p->offCur + round_up((size_t)p->d0 * 4, 256);
+    p->offHF = p->offHS = 0;  // unused
+  } else {
+    p->offHF = 0;
+    p->offF = bF;
+    p->offHS = 2 * bF;
+    p->offS = 2 * bF + bS;
+    p->bytes = 2 * bF + 2 * bS;
+  }
   return GS_OK;
 }
 
@@ -186,8 +212,9 @@ struct HistArgs {
   unsigned long long* HS;
 };
 
-template <int M, typename Cell>
+template <int M, int PB, typename Cell>
 __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
+  constexpr int PF = 64 / PB;  // packed fields per word
   constexpr int D = M - 1;
   constexpr int DS = M >= 3 ? M - 2 : 0;
   extern __shared__ __align__(16) double s_grid[];
@@ -237,7 +264,7 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     {
       const uint32_t f[3] = {1u, k[M - 1], M >= 2 ? k[M >= 2 ? M - 2 : 0] : 0u};
 #pragma unroll
-      for (int c = 0; c < 3; ++c) wf[c / a.F] += (unsigned long long)f[c] << ((c % a.F) * a.B);
+      for (int c = 0; c < 3; ++c) wf[c / PF] += (unsigned long long)f[c] << ((c % PF) * PB);
     }
 #pragma unroll
     for (int w = 0; w < kMaxWF; ++w)
@@ -246,7 +273,7 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     if constexpr (DS > 0) {
       unsigned long long ws[kMaxWS] = {0ull, 0ull, 0ull};
 #pragma unroll
-      for (int j = 0; j < DS; ++j) ws[j / a.F] += (unsigned long long)k[j] << ((j % a.F) * a.B);
+      for (int j = 0; j < DS; ++j) ws[j / PF] += (unsigned long long)k[j] << ((j % PF) * PB);
 #pragma unroll
       for (int w = 0; w < kMaxWS; ++w) {
         if (w >= a.WS || !ws[w]) continue;
@@ -263,6 +290,214 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
       const unsigned long long c = s_side[i];
       if (c) atomicAdd(a.HS + i, c);
     }
+  }
+}
+
+// ------------------------------------------------------- bucketed build --
+// Pass 1 (bucket_scatter): bin every record and append a 32-bit payload
+// (cell inside its b_0 slab | correct bits << 24) to bucket b_0.  A CTA ranks
+// its chunk per bucket with shared-memory counters and reserves each
+// bucket's range with ONE global atomic per (chunk, bucket); order inside a
+// bucket is irrelevant (counts are order-free).
+// Pass 2 (slab_hist): one CTA per b_0 slab accumulates the slab's main-table
+// cells and side-table row with shared-memory atomics, takes the prefix over
+// the slab's own dimensions in shared memory and writes both out.  The only
+// remaining global pass is the prefix along b_0 (colscan).
+struct BucketArgs {
+  const double* cert;
+  const uint8_t* corr;
+  int32_t n_rec;
+  const double* grids;
+  int32_t glen[kMaxM];
+  int64_t strideF[kMaxM];
+  int32_t d0;
+  int64_t cap;
+  int32_t grid_doubles;
+  int32_t vec_ok;
+  uint32_t* buckets;
+  uint32_t* cursor;
+};
+
+constexpr int kScatterThreads = 512;
+constexpr int kScatterR = 4;  // records per thread per chunk
+
+template <int M>
+__global__ void __launch_bounds__(kScatterThreads) bucket_scatter_kernel(const __grid_constant__ BucketArgs a) {
+  constexpr int D = M - 1;
+  extern __shared__ __align__(16) double s_grid[];
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_grid + a.grid_doubles);
+  uint32_t* s_base = s_cnt + a.d0;
+  for (int i = threadIdx.x; i < a.grid_doubles; i += blockDim.x) s_grid[i] = a.grids[i];
+  for (int i = threadIdx.x; i < a.d0; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int chunk = blockDim.x * kScatterR;
+  for (int c0 = blockIdx.x * chunk; c0 < a.n_rec; c0 += gridDim.x * chunk) {
+    uint32_t pay[kScatterR], rank[kScatterR];
+    int b0[kScatterR];
+#pragma unroll
+    for (int u = 0; u < kScatterR; ++u) {
+      const int r = c0 + u * blockDim.x + threadIdx.x;
+      b0[u] = -1;
+      if (r >= a.n_rec) continue;
+      double x[M];
+      uint32_t k[M];
+      const double* row = a.cert + r * M;
+      if (M % 2 == 0 && a.vec_ok) {
+#pragma unroll
+        for (int j = 0; j < (M / 2) * 2; j += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(row) + j / 2);
+          x[j] = v.x;
+          x[j + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < M; ++j) x[j] = __ldg(row + j);
+      }
+      if (M == 4 && a.vec_ok) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a.corr) + r);
+#pragma unroll
+        for (int j = 0; j < M; ++j) k[j] = ((w >> (8 * j)) & 0xffu) != 0;
+      } else {
+#pragma unroll
+        for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j) != 0;
+      }
+      uint32_t cell = 0, bits = 0;
+      int off = 0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const int b = upper_count(s_grid + off, a.glen[j], x[j]);
+        off += a.glen[j];
+        if (j == 0)
+          b0[u] = b;
+        else
+          cell += (uint32_t)b * (uint32_t)a.strideF[j];
+      }
+#pragma unroll
+      for (int j = 0; j < M; ++j) bits |= k[j] << j;
+      pay[u] = cell | (bits << 24);
+      rank[u] = atomicAdd(s_cnt + b0[u], 1u);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < a.d0; t += blockDim.x) {
+      const uint32_t c = s_cnt[t];
+      if (c) {
+        s_base[t] = atomicAdd(a.cursor + t, c);
+        s_cnt[t] = 0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kScatterR; ++u)
+      if (b0[u] >= 0) a.buckets[(int64_t)b0[u] * a.cap + s_base[b0[u]] + rank[u]] = pay[u];
+    __syncthreads();
+  }
+}
+
+struct SlabArgs {
+  int32_t d0, rows, cols;       // slab = [rows][cols] cells (rows = 1 for a 1-D slab)
+  int32_t side_cells, side_div;  // side row cells; slab cell / side_div = side cell
+  int64_t cap;
+  const uint32_t* buckets;
+  uint32_t* cursor;
+  unsigned long long* Ft;
+  unsigned long long* St;
+};
+
+// inclusive prefix of `len` u64 elements (stride `step`) by one warp
+__device__ __forceinline__ void warp_scan_line(unsigned long long* p, int len, int step) {
+  const int lane = (int)lane_id();
+  unsigned long long carry = 0;
+  for (int base = 0; base < len; base += 128) {
+    unsigned long long e[4], tot = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = base + lane * 4 + u;
+      e[u] = c < len ? p[c * step] : 0ull;
+      tot += e[u];
+      e[u] = tot;
+    }
+    unsigned long long incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned long long excl = carry + incl - tot;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = base + lane * 4 + u;
+      if (c < len) p[c * step] = e[u] + excl;
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+template <int M, int PB>
+__global__ void __launch_bounds__(1024) slab_hist_kernel(const __grid_constant__ SlabArgs a) {
+  constexpr int PF = 64 / PB;
+  constexpr int WF = (3 + PF - 1) / PF;
+  constexpr int DS = M >= 3 ? M - 2 : 0;
+  constexpr int WS = DS > 0 ? (DS + PF - 1) / PF : 0;
+  extern __shared__ __align__(16) unsigned long long s_slab[];
+  const int slab_words = a.rows * a.cols * WF;
+  unsigned long long* s_side = s_slab + slab_words;
+  const int side_words = a.side_cells * WS;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int b0 = blockIdx.x; b0 < a.d0; b0 += gridDim.x) {
+    for (int i = threadIdx.x; i < slab_words + side_words; i += blockDim.x) s_slab[i] = 0ull;
+    __syncthreads();
+    const uint32_t n = a.cursor[b0];
+    const uint32_t* src = a.buckets + (int64_t)b0 * a.cap;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t p = __ldg(src + i);
+      const uint32_t cell = p & 0xffffffu, bits = p >> 24;
+      unsigned long long wf[WF];
+#pragma unroll
+      for (int w = 0; w < WF; ++w) wf[w] = 0ull;
+      const uint32_t f[3] = {1u, (bits >> (M - 1)) & 1u, M >= 2 ? (bits >> (M >= 2 ? M - 2 : 0)) & 1u : 0u};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wf[c / PF] += (unsigned long long)f[c] << ((c % PF) * PB);
+#pragma unroll
+      for (int w = 0; w < WF; ++w)
+        if (wf[w]) atomicAdd(s_slab + cell * WF + w, wf[w]);
+      if constexpr (DS > 0) {
+        unsigned long long ws[WS > 0 ? WS : 1];
+#pragma unroll
+        for (int w = 0; w < WS; ++w) ws[w] = 0ull;
+#pragma unroll
+        for (int j = 0; j < DS; ++j) ws[j / PF] += (unsigned long long)((bits >> j) & 1u) << ((j % PF) * PB);
+        const uint32_t sc = cell / (uint32_t)a.side_div;
+#pragma unroll
+        for (int w = 0; w < WS; ++w)
+          if (ws[w]) atomicAdd(s_side + sc * WS + w, ws[w]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) a.cursor[b0] = 0;  // leave the cursors zero for the next build
+    // prefix along cols (each row, each word), then along rows (each col, each word)
+    for (int t = warp; t < a.rows * WF; t += nwarps)
+      warp_scan_line(s_slab + (t / WF) * a.cols * WF + (t % WF), a.cols, WF);
+    __syncthreads();
+    if (a.rows > 1) {
+      for (int t = threadIdx.x; t < a.cols * WF; t += blockDim.x) {
+        unsigned long long acc = 0;
+        unsigned long long* p = s_slab + t;
+        for (int r = 0; r < a.rows; ++r) {
+          acc += p[(int64_t)r * a.cols * WF];
+          p[(int64_t)r * a.cols * WF] = acc;
+        }
+      }
+    }
+    if (DS > 0 && a.side_cells > 1)
+      for (int t = warp; t < WS; t += nwarps) warp_scan_line(s_side + t, a.side_cells, WS);
+    __syncthreads();
+    unsigned long long* dF = a.Ft + (int64_t)b0 * slab_words;
+    for (int i = threadIdx.x; i < slab_words; i += blockDim.x) dF[i] = s_slab[i];
+    if (DS > 0) {
+      unsigned long long* dS = a.St + (int64_t)b0 * side_words;
+      for (int i = threadIdx.x; i < side_words; i += blockDim.x) dS[i] = s_side[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -451,11 +686,12 @@ __device__ __forceinline__ CellS loadS(const EvalGridArgs& a, int64_t cell) {
 }
 
 // correct count of model m at the current position
-template <int M>
+template <int M, int PB>
 __device__ __forceinline__ uint32_t chan(const EvalGridArgs& a, const CellF& f, const CellS& s, int m) {
-  if (m == M - 1) return fieldw(f.w, 1, a.F, a.B);
-  if (m == M - 2) return fieldw(f.w, 2, a.F, a.B);
-  return fieldw(s.w, m, a.F, a.B);
+  constexpr int PF = 64 / PB;
+  if (m == M - 1) return fieldw(f.w, 1, PF, PB);
+  if (m == M - 2) return fieldw(f.w, 2, PF, PB);
+  return fieldw(s.w, m, PF, PB);
 }
 
 template <int M>
@@ -480,8 +716,9 @@ __device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, c
   if (a.n_correct) a.n_correct[i] = correct;
 }
 
-template <int M>
+template <int M, int PB>
 __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ EvalGridArgs a) {
+  constexpr int PF = 64 / PB;
   const int lane = (int)lane_id();
   const double n = (double)a.n_rec;
   const double one = ddiv(n, n);  // first-stage fraction, as the reference computes it
@@ -525,7 +762,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       const int64_t i = s_begin - a.cfg_begin;
       if (lane == 0 && i >= 0 && i < a.cfg_count) {
         const double mean = dadd(0.0, dmul(one, __ldg(a.cost1 + mK)));
-        store_config<M>(a, i, fr, 1, one, mean, chan<M>(a, totF, totS, mK), n);
+        store_config<M>(a, i, fr, 1, one, mean, chan<M, PB>(a, totF, totS, mK), n);
       }
       continue;
     }
@@ -559,7 +796,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
     for (int t = 0; t < M - 2; ++t) {
       if (t <= K - 3) {
         const int m = (mdl >> (4 * t)) & 15u;
-        const uint32_t A = chan<M>(a, vF, vS, m);
+        const uint32_t A = chan<M, PB>(a, vF, vS, m);
         const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
         cF -= dk * a.strideF[m];
         vF = loadF(a, cF);
@@ -567,12 +804,12 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
           cS -= dk * a.strideS[m];
           vS = loadS(a, cS);
         }
-        cp += A - chan<M>(a, vF, vS, m);
-        fr[t + 1] = ddiv((double)fieldw(vF.w, 0, a.F, a.B), n);
+        cp += A - chan<M, PB>(a, vF, vS, m);
+        fr[t + 1] = ddiv((double)fieldw(vF.w, 0, PF, PB), n);
         mp = dadd(mp, dmul(fr[t + 1], __ldg(a.cost1 + ((mdl >> (4 * (t + 1))) & 15u))));
       }
     }
-    const uint32_t a_last = chan<M>(a, vF, vS, mL);
+    const uint32_t a_last = chan<M, PB>(a, vF, vS, mL);
     const double costK = __ldg(a.cost1 + mK);
     const bool needS = mL < a.DS || mK < a.DS;
     const int64_t c_row = s_begin + row * gL - a.cfg_begin;
@@ -605,8 +842,8 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
         CellS sv;
 #pragma unroll
         for (int q = 0; q < kMaxWS; ++q) sv.w[q] = needS ? wS[u].w[q] : vS.w[q];
-        const uint32_t correct = cp + a_last - chan<M>(a, wF[u], sv, mL) + chan<M>(a, wF[u], sv, mK);
-        const double frK = ddiv((double)fieldw(wF[u].w, 0, a.F, a.B), n);
+        const uint32_t correct = cp + a_last - chan<M, PB>(a, wF[u], sv, mL) + chan<M, PB>(a, wF[u], sv, mK);
+        const double frK = ddiv((double)fieldw(wF[u].w, 0, PF, PB), n);
         const double mean = dadd(mp, dmul(frK, costK));
         store_config<M>(a, i, fr, K, frK, mean, correct, n);
       }
@@ -679,9 +916,9 @@ int64_t global_row(const Plan& p, const int64_t* row_begin, int64_t c) {
   return row_begin[s] + (c - p.struct_begin[s]) / row_len(p, s);
 }
 
-template <int M, typename Cell>
+template <int M, int PB, typename Cell>
 cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
-  auto k = grid_hist_kernel<M, Cell>;
+  auto k = grid_hist_kernel<M, PB, Cell>;
   static std::atomic<int> smem_set{0};
   cudaError_t e = ensure_smem(k, smem_set, smem);
   if (e != cudaSuccess) return e;
@@ -691,12 +928,16 @@ cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStr
   return cudaGetLastError();
 }
 
-// 32-bit cell arithmetic whenever every table index fits
+// compile-time field width; 32-bit cell arithmetic whenever every index fits
 template <int M>
 cudaError_t launch_hist(const HistArgs& h, int64_t n_rec, size_t smem, int64_t max_index,
                         cudaStream_t st) {
-  return max_index < ((int64_t)1 << 32) ? launch_hist_t<M, uint32_t>(h, n_rec, smem, st)
-                                        : launch_hist_t<M, int64_t>(h, n_rec, smem, st);
+  const bool narrow = max_index < ((int64_t)1 << 32);
+  if (h.B == 21)
+    return narrow ? launch_hist_t<M, 21, uint32_t>(h, n_rec, smem, st)
+                  : launch_hist_t<M, 21, int64_t>(h, n_rec, smem, st);
+  return narrow ? launch_hist_t<M, 32, uint32_t>(h, n_rec, smem, st)
+                : launch_hist_t<M, 32, int64_t>(h, n_rec, smem, st);
 }
 
 template <int M>
@@ -704,7 +945,10 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
   const int64_t rows = a.row_hi - a.row_lo;
   int64_t blocks = (rows * 32 + 255) / 256;
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
-  grid_eval_kernel<M><<<(unsigned)blocks, 256, 0, st>>>(a);
+  if (a.B == 21)
+    grid_eval_kernel<M, 21><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else
+    grid_eval_kernel<M, 32><<<(unsigned)blocks, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -743,6 +987,89 @@ cudaError_t prefix_table(unsigned long long* H, unsigned long long* T, int ndim,
   return cudaSuccess;
 }
 
+template <int M, int PB>
+cudaError_t bucket_build_t(const Plan& p, const double* cert, const uint8_t* corr,
+                           const double* grids, uint8_t* ws, int flags, cudaStream_t st) {
+  auto* Ft = reinterpret_cast<unsigned long long*>(ws + p.offF);
+  auto* St = reinterpret_cast<unsigned long long*>(ws + p.offS);
+  auto* bk = reinterpret_cast<uint32_t*>(ws + p.offBk);
+  auto* cur = reinterpret_cast<uint32_t*>(ws + p.offCur);
+  cudaError_t e;
+  if (flags & GS_GRID_WORKSPACE_DIRTY) {
+    e = cudaMemsetAsync(cur, 0, (size_t)p.d0 * 4, st);
+    if (e != cudaSuccess) return e;
+  }
+  BucketArgs b{};
+  b.cert = cert;
+  b.corr = corr;
+  b.n_rec = (int32_t)p.cap;
+  b.grids = grids;
+  int gd = 0;
+  for (int j = 0; j < p.M; ++j) {
+    b.glen[j] = p.glen[j];
+    if (j < p.D) gd += p.glen[j];
+  }
+  for (int j = 0; j < p.D; ++j) b.strideF[j] = p.strideF[j];
+  b.d0 = (int32_t)p.d0;
+  b.cap = p.cap;
+  b.grid_doubles = gd;
+  b.vec_ok = aligned16(cert) && ((reinterpret_cast<uintptr_t>(corr) & 3u) == 0);
+  b.buckets = bk;
+  b.cursor = cur;
+  const size_t smem1 = round_up((size_t)gd * 8, 16) + (size_t)p.d0 * 8;
+  static std::atomic<int> smem1_set{0};
+  e = ensure_smem(bucket_scatter_kernel<M>, smem1_set, smem1);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (p.cap + kScatterThreads * kScatterR - 1) / (kScatterThreads * kScatterR);
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 2));
+  bucket_scatter_kernel<M><<<(unsigned)blocks, kScatterThreads, smem1, st>>>(b);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  SlabArgs s{};
+  s.d0 = (int32_t)p.d0;
+  s.rows = p.D == 3 ? (int32_t)p.dims[1] : 1;
+  s.cols = (int32_t)p.dims[p.D - 1];
+  s.side_cells = (int32_t)std::max<int64_t>(p.side_slab, 1);
+  int64_t div = 1;
+  for (int j = p.DS; j < p.D; ++j) div *= p.dims[j];
+  s.side_div = (int32_t)div;
+  s.cap = p.cap;
+  s.buckets = bk;
+  s.cursor = cur;
+  s.Ft = Ft;
+  s.St = St;
+  const size_t smem2 = (size_t)(p.slab_cells * p.WF + p.side_slab * p.WS) * 8 + 16;
+  static std::atomic<int> smem2_set{0};
+  e = ensure_smem(slab_hist_kernel<M, PB>, smem2_set, smem2);
+  if (e != cudaSuccess) return e;
+  slab_hist_kernel<M, PB><<<(unsigned)p.d0, 1024, smem2, st>>>(s);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // prefix along b_0
+  const int64_t innerF = p.slab_cells * p.WF;
+  int64_t nb = std::max<int64_t>(1, std::min<int64_t>((innerF + kColTile - 1) / kColTile, (int64_t)sm_count() * 8));
+  colscan_kernel<<<(unsigned)nb, 256, 0, st>>>(Ft, Ft, 1, p.d0, innerF);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (p.DS > 0) {
+    const int64_t innerS = p.side_slab * p.WS;
+    nb = std::max<int64_t>(1, std::min<int64_t>((innerS + kColTile - 1) / kColTile, (int64_t)sm_count() * 8));
+    colscan_kernel<<<(unsigned)nb, 256, 0, st>>>(St, St, 1, p.d0, innerS);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+cudaError_t bucket_build(const Plan& p, const double* cert, const uint8_t* corr,
+                         const double* grids, uint8_t* ws, int flags, cudaStream_t st) {
+  if (p.M == 3)
+    return p.B == 21 ? bucket_build_t<3, 21>(p, cert, corr, grids, ws, flags, st)
+                     : bucket_build_t<3, 32>(p, cert, corr, grids, ws, flags, st);
+  return p.B == 21 ? bucket_build_t<4, 21>(p, cert, corr, grids, ws, flags, st)
+                   : bucket_build_t<4, 32>(p, cert, corr, grids, ws, flags, st);
+}
+
 }  // namespace
 }  // namespace gs
 
@@ -778,6 +1105,10 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   auto* Ft = reinterpret_cast<unsigned long long*>(ws + p.offF);
   auto* HS = reinterpret_cast<unsigned long long*>(ws + p.offHS);
   auto* St = reinterpret_cast<unsigned long long*>(ws + p.offS);
+  if (p.bucket) {
+    GS_CUDA_TRY(bucket_build(p, certainty, correct, grids, ws, flags, st));
+    return GS_OK;
+  }
   if (flags & GS_GRID_WORKSPACE_DIRTY) {
     GS_CUDA_TRY(cudaMemsetAsync(HF, 0, (size_t)p.cellsF * p.WF * 8, st));
     if (p.cellsS) GS_CUDA_TRY(cudaMemsetAsync(HS, 0, (size_t)p.cellsS * p.WS * 8, st));
