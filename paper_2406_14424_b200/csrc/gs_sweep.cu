@@ -1,0 +1,913 @@
+// gs_grid.cu — grid path: the full cascade x per-stage-threshold product.
+//
+// Reference semantics: every config is an encoded cascade scored exactly as
+// _evaluate_numba scores it (/root/reference/pkg/src/gearserve/kernels.py:
+// 39-62); thresholds come from per-model grids (cascades.ThresholdGrid,
+// src/cascades.py:132-163); structures are model subsets walked cheap to
+// expensive like sample_cascades builds them (src/cascades.py:181-185).
+//
+// Algorithm: dominance counting instead of walking every record through
+// every config.  With grid G_j of model j let b_j(r) = #{g in G_j : g <=
+// cert[r, j]}.  cert >= G_j[k] <=> b_j > k, so record r is forwarded past a
+// stage of model j with threshold index k iff b_j(r) <= k.  Models are in
+// cost order and subsets are walked in that order, so model M-1 never
+// forwards: one (M-1)-dimensional table over (b_0 .. b_{M-2}) answers every
+// structure.  After an inclusive prefix sum along every dimension, a cell
+// counts the records whose bins it dominates; a dimension at its maximum
+// index g_j means "any".  With pos holding the thresholds of the stages
+// walked so far:
+//   reach(stage t+1) = cnt[pos after setting k_t]
+//   correct          = sum_t (c_{m_t}[pos before k_t] - c_{m_t}[pos after])
+//                      + c_{m_K}[final pos]
+// which is the per-record walk's count, exactly.
+//
+// Table layout (HBM / L2): the main table F holds, per cell, one 16-byte
+// vector of four counts {cnt, c_{M-1}, c_{M-2}, c_{M-3}}.  A correct count
+// c_j is only ever read at positions whose dimensions > j are at "any", so
+// models j <= M-4 live in a smaller side table S over dims 0..M-4 (for the
+// 4-model cascade: one row of 101 cells, privatised in shared memory).
+// The histogram adds each record with ONE red.global.add.v4.f32 (integer
+// counts are exact in f32 below 2^24), so the histogram costs one L2 vector
+// atomic per record.  The prefix sums convert to u32.
+//
+// Histogram and prefix tables are separate buffers: the first scan pass
+// reads the f32 histogram, writes the u32 prefix and re-zeroes the histogram,
+// so no memset runs per build (the caller zeroes the workspace once).
+//
+// Kernels: grid_hist (one pass over the records, vector loads, binary search
+// in shared-memory grids), rowscan (contiguous last dim, warp-shuffle scan),
+// colscan (strided dims: [len x 32]-cell tiles staged in shared memory with
+// cp.async, one round trip per 128 rows), grid_eval (R consecutive configs per thread; everything that
+// depends only on the leading thresholds is computed once per "row" of
+// configs; f64 epilogue in the reference's order, no FMA contraction).
+#include <algorithm>
+#include <atomic>
+
+#include "gs_common.cuh"
+
+namespace gs {
+namespace {
+
+constexpr int kMaxM = GS_MAX_MODELS;
+constexpr int64_t kMaxExactF32 = 1ll << 24;
+constexpr int kHistThreads = 512;
+constexpr size_t kSidePrivMax = 16 * 1024;
+
+struct Plan {
+  int M = 0, D = 0, DP = 0, NVP = 0, n_struct = 0;
+  int glen[kMaxM] = {};
+  int64_t dims[kMaxM] = {};
+  int64_t strideF[kMaxM] = {};
+  int64_t strideP[kMaxM] = {};
+  int64_t cellsF = 1, cellsP = 0;
+  int64_t n_configs = 0;
+  int64_t struct_begin[256 + 1] = {};
+  uint32_t struct_mask[256] = {};
+  size_t offHF = 0, offF = 0, offHP = 0, offP = 0, bytes = 0;
+};
+
+int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
+  if (M < 1 || !grid_len || n_rec < 1) return GS_EINVAL;
+  if (M > kMaxM || n_rec >= kMaxExactF32) return GS_EUNSUPPORTED;
+  p->M = M;
+  p->D = M - 1;
+  p->DP = M >= 4 ? M - 3 : 0;
+  p->NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  for (int j = 0; j < M; ++j) {
+    if (grid_len[j] < 1 || grid_len[j] > (1 << 20)) return GS_EINVAL;
+    p->glen[j] = grid_len[j];
+  }
+  double cells = 1.0;
+  for (int j = 0; j < p->D; ++j) {
+    p->dims[j] = (int64_t)p->glen[j] + 1;
+    cells *= (double)p->dims[j];
+  }
+  if (cells * 16.0 > 1.4e11) return GS_EUNSUPPORTED;
+  int64_t s = 1;
+  for (int j = p->D - 1; j >= 0; --j) {
+    p->strideF[j] = s;
+    s *= p->dims[j];
+  }
+  p->cellsF = s;
+  s = 1;
+  for (int j = p->DP - 1; j >= 0; --j) {
+    p->strideP[j] = s;
+    s *= p->dims[j];
+  }
+  p->cellsP = p->DP > 0 ? s : 0;
+  // structures: size ascending, then lexicographic (itertools.combinations)
+  int ns = 0;
+  int64_t off = 0;
+  double total = 0.0;
+  for (int K = 1; K <= M; ++K) {
+    int idx[kMaxM];
+    for (int i = 0; i < K; ++i) idx[i] = i;
+    while (true) {
+      uint32_t mask = 0;
+      double cnt = 1.0;
+      int64_t icnt = 1;
+      for (int i = 0; i < K; ++i) mask |= 1u << idx[i];
+      for (int i = 0; i + 1 < K; ++i) {
+        cnt *= p->glen[idx[i]];
+        icnt *= p->glen[idx[i]];
+      }
+      p->struct_mask[ns] = mask;
+      p->struct_begin[ns] = off;
+      off += icnt;
+      total += cnt;
+      ++ns;
+      int i = K - 1;
+      while (i >= 0 && idx[i] == M - K + i) --i;
+      if (i < 0) break;
+      ++idx[i];
+      for (int q = i + 1; q < K; ++q) idx[q] = idx[q - 1] + 1;
+    }
+  }
+  if (total > 9.0e18) return GS_EUNSUPPORTED;
+  p->n_struct = ns;
+  p->struct_begin[ns] = off;
+  p->n_configs = off;
+  const size_t bF = round_up((size_t)p->cellsF * 16, 256);
+  const size_t bP = round_up((size_t)p->cellsP * p->NVP * 16, 256);
+  p->offHF = 0;
+  p->offF = bF;
+  p->offHP = 2 * bF;
+  p->offP = 2 * bF + bP;
+  p->bytes = 2 * bF + 2 * bP;
+  return GS_OK;
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+// #{g[i] <= x} for strictly increasing g (n >= 1).  Branch-free: the trip
+// count depends on n only, so a warp never diverges in the search.
+__device__ __forceinline__ int upper_count(const double* g, int n, double x) {
+  int base = 0, len = n;
+  while (len > 1) {
+    const int half = len >> 1;
+    base = (g[base + half - 1] <= x) ? base + half : base;
+    len -= half;
+  }
+  return base + (g[base] <= x ? 1 : 0);
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size,
+// so later calls (e.g. inside a CUDA-graph capture) issue no attribute calls.
+template <typename Kernel>
+cudaError_t ensure_smem(Kernel k, std::atomic<int>& done, size_t bytes) {
+  if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.store((int)bytes, std::memory_order_release);
+  return e;
+}
+
+// ------------------------------------------------------------------ hist --
+struct HistArgs {
+  const double* cert;
+  const uint8_t* corr;
+  int64_t n_rec;
+  const double* grids;
+  int32_t goff[kMaxM];
+  int32_t glen[kMaxM];
+  int64_t strideF[kMaxM];
+  int64_t strideP[kMaxM];
+  int64_t cellsP;
+  int32_t grid_doubles;  // grids of models 0..D-1 staged in smem
+  int32_t vec_ok;
+  int32_t priv;          // side table privatised in shared memory
+  float* F;
+  float* P;
+};
+
+template <int M, typename Cell>
+__global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
+  constexpr int D = M - 1;
+  constexpr int DP = M >= 4 ? M - 3 : 0;
+  constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  extern __shared__ __align__(16) double s_grid[];
+  float* s_side = reinterpret_cast<float*>(s_grid + a.grid_doubles);
+  for (int i = threadIdx.x; i < a.grid_doubles; i += blockDim.x) s_grid[i] = a.grids[i];
+  if (DP > 0 && a.priv)
+    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) s_side[i] = 0.f;
+  __syncthreads();
+
+  // n_rec < 2^24 and M <= 8, so record offsets fit 32 bits
+  const int n_rec = (int)a.n_rec;
+  const int step = gridDim.x * blockDim.x;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rec; r += step) {
+    double x[M];
+    uint32_t k[M];
+    const double* row = a.cert + r * M;
+    if (M % 2 == 0 && a.vec_ok) {
+#pragma unroll
+      for (int j = 0; j < (M / 2) * 2; j += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(row) + j / 2);
+        x[j] = v.x;
+        x[j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) x[j] = __ldg(row + j);
+    }
+    if (M == 4 && a.vec_ok) {
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a.corr) + r);
+#pragma unroll
+      for (int j = 0; j < M; ++j) k[j] = (w >> (8 * j)) & 0xffu;
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j);
+    }
+    Cell cellF = 0, cellP = 0;
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int b = upper_count(s_grid + off, a.glen[j], x[j]);
+      off += a.glen[j];
+      cellF += (Cell)b * (Cell)a.strideF[j];
+      if (j < DP) cellP += (Cell)b * (Cell)a.strideP[j];
+    }
+    // main table: {cnt, c_{M-1}, c_{M-2}, c_{M-3}}
+    float v[4] = {1.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i] ? 1.f : 0.f;
+    red_add_v4(a.F + cellF * 4, v[0], v[1], v[2], v[3]);
+    // side table: c_j for j <= M-4 at (b_0..b_{M-4})
+    if constexpr (DP > 0) {
+#pragma unroll
+      for (int j = 0; j < DP; ++j) {
+        if (!k[j]) continue;
+        const Cell e = (cellP * NVP + j / 4) * 4 + (j % 4);
+        if (a.priv)
+          atomicAdd(s_side + e, 1.f);
+        else
+          atomicAdd(a.P + e, 1.f);
+      }
+    }
+  }
+  if (DP > 0 && a.priv) {
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) {
+      const float c = s_side[i];
+      if (c != 0.f) atomicAdd(a.P + i, c);
+    }
+  }
+}
+
+// ----------------------------------------------------------------- scans --
+__device__ __forceinline__ uint4 to_u4(float4 f) {
+  return make_uint4(__float2uint_rn(f.x), __float2uint_rn(f.y), __float2uint_rn(f.z),
+                    __float2uint_rn(f.w));
+}
+__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) {
+  return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ uint4 shfl_up4(uint4 v, int o) {
+  return make_uint4(__shfl_up_sync(0xffffffffu, v.x, o), __shfl_up_sync(0xffffffffu, v.y, o),
+                    __shfl_up_sync(0xffffffffu, v.z, o), __shfl_up_sync(0xffffffffu, v.w, o));
+}
+__device__ __forceinline__ uint4 shfl4(uint4 v, int src) {
+  return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                    __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+
+// Inclusive prefix along the contiguous last dimension: one warp per row of
+// `len` uint4 cells, four consecutive cells per lane, warp-shuffle scan, one
+// load round trip per 128 cells.  from_f32 converts the f32 histogram.
+__global__ void __launch_bounds__(256) rowscan_kernel(uint4* src, uint4* T, int64_t n_rows, int len,
+                                                      int from_f32) {
+  const int lane = (int)lane_id();
+  const bool zero = src != T;  // first pass: read the histogram and re-zero it
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
+    uint4* in = src + r * len;
+    uint4* row = T + r * len;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (int base = 0; base < len; base += 128) {
+      uint4 e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        e[u] = c < len ? in[c] : make_uint4(0, 0, 0, 0);
+        if (from_f32) e[u] = to_u4(*reinterpret_cast<float4*>(&e[u]));
+      }
+      if (zero) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = base + lane * 4 + u;
+          if (c < len) in[c] = make_uint4(0, 0, 0, 0);
+        }
+      }
+      uint4 tot = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        tot = add4(tot, e[u]);
+        e[u] = tot;
+      }
+      uint4 incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint4 y = shfl_up4(incl, o);
+        if (lane >= o) incl = add4(incl, y);
+      }
+      const uint4 excl = add4(carry, make_uint4(incl.x - tot.x, incl.y - tot.y, incl.z - tot.z,
+                                                incl.w - tot.w));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        if (c < len) row[c] = add4(e[u], excl);
+      }
+      carry = add4(carry, shfl4(incl, 31));
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+constexpr int kColTile = 32;    // consecutive inner cells per CTA
+constexpr int kColChunk = 128;  // rows of the scanned dimension per smem pass
+
+// Inclusive prefix along a strided dimension of a table of uint4 cells viewed
+// as [outer][len][inner].  A CTA owns kColTile consecutive inner cells of one
+// outer index: it stages the [len x kColTile] tile in shared memory with
+// cp.async (one round trip per 128 rows), scans each (cell, lane) column in
+// shared memory, and writes the tile back coalesced.
+__global__ void __launch_bounds__(256) colscan_kernel(uint4* src, uint4* T, int64_t outer, int64_t len,
+                                                      int64_t inner, int from_f32) {
+  extern __shared__ __align__(16) uint4 s[];  // [kColChunk][kColTile]
+  const int64_t tiles_per_outer = (inner + kColTile - 1) / kColTile;
+  const int64_t n_tiles = outer * tiles_per_outer;
+  const int t = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t o = tile / tiles_per_outer;
+    const int64_t i0 = (tile - o * tiles_per_outer) * kColTile;
+    const int w = (int)min((int64_t)kColTile, inner - i0);
+    uint4* base = T + o * len * inner + i0;
+    uint4* in = src + o * len * inner + i0;
+    const bool zero = src != T;
+    // scanning threads: (cell c, lane q) = (t / 4, t % 4) for t < 4 * w
+    uint32_t carry = 0;
+    for (int64_t r0 = 0; r0 < len; r0 += kColChunk) {
+      const int rows = (int)min((int64_t)kColChunk, len - r0);
+      for (int e = t; e < rows * w; e += blockDim.x) {
+        const int rr = e / w, cc = e - (e / w) * w;
+        cp_async16(s + rr * kColTile + cc, in + (r0 + rr) * inner + cc);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      if (zero)
+        for (int e = t; e < rows * w; e += blockDim.x) {
+          const int rr = e / w, cc = e - (e / w) * w;
+          in[(r0 + rr) * inner + cc] = make_uint4(0, 0, 0, 0);
+        }
+      if (t < 4 * w) {
+        uint32_t* col = reinterpret_cast<uint32_t*>(s) + (t >> 2) * 4 + (t & 3);
+        uint32_t acc = carry;
+        int r = 0;
+        for (; r + 4 <= rows; r += 4) {
+          uint32_t v0 = col[(r + 0) * kColTile * 4], v1 = col[(r + 1) * kColTile * 4];
+          uint32_t v2 = col[(r + 2) * kColTile * 4], v3 = col[(r + 3) * kColTile * 4];
+          if (from_f32) {
+            v0 = __float2uint_rn(__uint_as_float(v0));
+            v1 = __float2uint_rn(__uint_as_float(v1));
+            v2 = __float2uint_rn(__uint_as_float(v2));
+            v3 = __float2uint_rn(__uint_as_float(v3));
+          }
+          acc += v0;
+          col[(r + 0) * kColTile * 4] = acc;
+          acc += v1;
+          col[(r + 1) * kColTile * 4] = acc;
+          acc += v2;
+          col[(r + 2) * kColTile * 4] = acc;
+          acc += v3;
+          col[(r + 3) * kColTile * 4] = acc;
+        }
+        for (; r < rows; ++r) {
+          uint32_t v = col[r * kColTile * 4];
+          if (from_f32) v = __float2uint_rn(__uint_as_float(v));
+          acc += v;
+          col[r * kColTile * 4] = acc;
+        }
+        carry = acc;
+      }
+      __syncthreads();
+      for (int e = t; e < rows * w; e += blockDim.x) {
+        const int rr = e / w, cc = e - (e / w) * w;
+        base[(r0 + rr) * inner + cc] = s[rr * kColTile + cc];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// -------------------------------------------------------------- epilogue --
+// Configs are processed in "rows": the configs of one structure that share
+// every threshold except the last forwarding stage's (consecutive in the
+// enumeration).  One warp owns a row: the row-shared part of the walk (cells
+// of the leading stages, their forward fractions and the partial mean cost)
+// is computed once per warp from broadcast loads, then each lane finishes
+// configs kl = lane, lane+32, ... with one 16-byte cell load, two f64
+// divisions and coalesced stores.
+struct EvalGridArgs {
+  int32_t M, n_struct, NVP, DP;
+  int32_t glen[kMaxM];
+  int64_t strideF[kMaxM];
+  int64_t strideP[kMaxM];
+  int64_t n_rec, cellsF, cellsP;
+  int64_t cfg_begin, cfg_count;
+  int64_t row_lo, row_hi;
+  int64_t struct_begin[256 + 1];
+  int64_t row_begin[256 + 1];
+  uint32_t struct_mask[256];
+  const uint4* F;
+  const uint4* P;
+  const double* cost1;
+  double* acc;
+  double* cost;
+  double* frac;
+  uint32_t* n_correct;
+};
+
+__device__ __forceinline__ uint32_t lane4(const uint4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+
+// correct count of model m at the current position
+template <int M>
+__device__ __forceinline__ uint32_t chan(const uint4& vF, const uint4* vP, int m) {
+  if (m >= M - 3) return lane4(vF, 1 + (M - 1 - m));
+  return lane4(vP[m / 4], m % 4);
+}
+
+template <int M>
+__device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, const double* fr,
+                                             int K, double frK, double mean, uint32_t correct,
+                                             double n) {
+  if (a.frac) {
+    double o[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) o[t] = t < K - 1 ? fr[t] : (t == K - 1 ? frK : 0.0);
+    double* row = a.frac + i * M;
+    if constexpr (M % 2 == 0) {
+#pragma unroll
+      for (int t = 0; t < M; t += 2) reinterpret_cast<double2*>(row)[t / 2] = make_double2(o[t], o[t + 1]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < M; ++t) row[t] = o[t];
+    }
+  }
+  if (a.cost) a.cost[i] = mean;
+  if (a.acc) a.acc[i] = ddiv((double)correct, n);
+  if (a.n_correct) a.n_correct[i] = correct;
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ EvalGridArgs a) {
+  constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
+  constexpr int NVPX = NVP > 0 ? NVP : 1;
+  const int lane = (int)lane_id();
+  const double n = (double)a.n_rec;
+  const double one = ddiv(n, n);  // first-stage fraction, as the reference computes it
+  const uint4 totF = __ldg(a.F + a.cellsF - 1);
+  uint4 totP[NVPX];
+#pragma unroll
+  for (int v = 0; v < NVPX; ++v)
+    totP[v] = NVP > 0 ? __ldg(a.P + (a.cellsP - 1) * NVP + v) : make_uint4(0, 0, 0, 0);
+
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t rg = a.row_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+       rg < a.row_hi; rg += nw) {
+    int s = 0;
+    {
+      int lo = 0, hi = a.n_struct - 1;  // last s with row_begin[s] <= rg
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.row_begin[mid] <= rg)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      s = lo;
+    }
+    const uint32_t mask = a.struct_mask[s];
+    int K = 0;
+    uint32_t mdl = 0;  // stage models, 4 bits each, stage 0 lowest
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+      if ((mask >> j) & 1u) {
+        mdl |= (uint32_t)j << (4 * K);
+        ++K;
+      }
+    const int64_t row = rg - a.row_begin[s];
+    const int64_t s_begin = a.struct_begin[s];
+    const int mK = (mdl >> (4 * (K - 1))) & 15u;
+    double fr[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) fr[t] = 0.0;
+    if (K == 1) {
+      const int64_t i = s_begin - a.cfg_begin;
+      if (lane == 0 && i >= 0 && i < a.cfg_count) {
+        const double mean = dadd(0.0, dmul(one, __ldg(a.cost1 + mK)));
+        store_config<M>(a, i, fr, 1, one, mean, chan<M>(totF, totP, mK), n);
+      }
+      continue;
+    }
+    const int mL = (mdl >> (4 * (K - 2))) & 15u;
+    const int gL = a.glen[mL];
+    // leading thresholds k_0 .. k_{K-3} from the row index
+    int kk[M];
+    int64_t rem = row;
+#pragma unroll
+    for (int t = M - 1; t >= 0; --t) {
+      kk[t] = 0;
+      if (t <= K - 3) {
+        const int g = a.glen[(mdl >> (4 * t)) & 15u];
+        if (rem < 0x7fffffffLL) {  // 32-bit division in the common case
+          const int r32 = (int)rem;
+          kk[t] = r32 % g;
+          rem = r32 / g;
+        } else {
+          kk[t] = (int)(rem % g);
+          rem /= g;
+        }
+      }
+    }
+    int64_t cF = a.cellsF - 1, cP = a.cellsP - 1;
+    uint4 vF = totF;
+    uint4 vP[NVPX];
+#pragma unroll
+    for (int v = 0; v < NVPX; ++v) vP[v] = totP[v];
+    uint32_t cp = 0;
+    fr[0] = one;
+    double mp = dadd(0.0, dmul(one, __ldg(a.cost1 + (mdl & 15u))));
+#pragma unroll
+    for (int t = 0; t < M - 2; ++t) {
+      if (t <= K - 3) {
+        const int m = (mdl >> (4 * t)) & 15u;
+        const uint32_t A = chan<M>(vF, vP, m);
+        const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
+        cF -= dk * a.strideF[m];
+        vF = __ldg(a.F + cF);
+        if (NVP > 0 && m < a.DP) {
+          cP -= dk * a.strideP[m];
+#pragma unroll
+          for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
+        }
+        cp += A - chan<M>(vF, vP, m);
+        fr[t + 1] = ddiv((double)vF.x, n);
+        mp = dadd(mp, dmul(fr[t + 1], __ldg(a.cost1 + ((mdl >> (4 * (t + 1))) & 15u))));
+      }
+    }
+    const uint32_t a_last = chan<M>(vF, vP, mL);
+    const double costK = __ldg(a.cost1 + mK);
+    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
+    const int64_t c_row = s_begin + row * gL - a.cfg_begin;
+    // cell of threshold index kl: rowF + kl * sL (kl = gL would be "any")
+    const int64_t sL = a.strideF[mL];
+    const uint4* rowF = a.F + (cF - (int64_t)gL * sL);
+    const int64_t sPL = (NVP > 0 && mL < a.DP) ? a.strideP[mL] : 0;
+    const int64_t rowP = cP - (int64_t)gL * sPL;
+    constexpr int U = 4;  // configs per lane per pass, loads issued together
+    for (int base = 0; base < gL; base += 32 * U) {
+      uint4 wF[U];
+      uint4 wP[U][NVPX];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kl = base + lane + 32 * u;
+        wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int v = 0; v < NVPX; ++v)
+          wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
+                                        : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kl = base + lane + 32 * u;
+        const int64_t i = c_row + kl;
+        if (kl >= gL || i < 0 || i >= a.cfg_count) continue;
+        const uint32_t correct =
+            cp + a_last - chan<M>(wF[u], wP[u], mL) + chan<M>(wF[u], wP[u], mK);
+        const double frK = ddiv((double)wF[u].x, n);
+        const double mean = dadd(mp, dmul(frK, costK));
+        store_config<M>(a, i, fr, K, frK, mean, correct, n);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- decode --
+struct DecodeArgs {
+  int32_t M, n_struct;
+  int32_t glen[kMaxM];
+  int32_t goff[kMaxM];
+  int64_t struct_begin[256 + 1];
+  uint32_t struct_mask[256];
+  const double* grids;
+  const int64_t* idx;
+  int64_t count;
+  int32_t* stage_model;
+  double* thr;
+  int32_t* n_stages;
+};
+
+__global__ void grid_decode_kernel(const __grid_constant__ DecodeArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = a.idx[i];
+    int lo = 0, hi = a.n_struct - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.struct_begin[mid] <= c)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const uint32_t mask = a.struct_mask[lo];
+    int mdl[kMaxM];
+    int K = 0;
+    for (int j = 0; j < a.M; ++j)
+      if ((mask >> j) & 1u) mdl[K++] = j;
+    int64_t local = c - a.struct_begin[lo];
+    int kidx[kMaxM];
+    for (int t = K - 2; t >= 0; --t) {
+      const int g = a.glen[mdl[t]];
+      kidx[t] = (int)(local % g);
+      local /= g;
+    }
+    for (int t = 0; t < a.M; ++t) {
+      a.stage_model[i * a.M + t] = t < K ? mdl[t] : -1;
+      a.thr[i * a.M + t] = (t < K - 1) ? a.grids[a.goff[mdl[t]] + kidx[t]] : 0.0;
+    }
+    a.n_stages[i] = K;
+  }
+}
+
+// configs per row of structure s (the last forwarding stage's grid size)
+int64_t row_len(const Plan& p, int s) {
+  const uint32_t mask = p.struct_mask[s];
+  int prev = -1, last = -1;
+  for (int j = 0; j < p.M; ++j)
+    if ((mask >> j) & 1u) {
+      prev = last;
+      last = j;
+    }
+  return prev < 0 ? 1 : p.glen[prev];
+}
+
+int64_t global_row(const Plan& p, const int64_t* row_begin, int64_t c) {
+  int s = 0;
+  while (s + 1 < p.n_struct && p.struct_begin[s + 1] <= c) ++s;
+  return row_begin[s] + (c - p.struct_begin[s]) / row_len(p, s);
+}
+
+template <int M, typename Cell>
+cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
+  auto k = grid_hist_kernel<M, Cell>;
+  static std::atomic<int> smem_set{0};
+  cudaError_t e = ensure_smem(k, smem_set, smem);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
+  k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
+  return cudaGetLastError();
+}
+
+// 32-bit cell arithmetic whenever every table index fits
+template <int M>
+cudaError_t launch_hist(const HistArgs& h, int64_t n_rec, size_t smem, int64_t max_index,
+                        cudaStream_t st) {
+  return max_index < ((int64_t)1 << 32) ? launch_hist_t<M, uint32_t>(h, n_rec, smem, st)
+                                        : launch_hist_t<M, int64_t>(h, n_rec, smem, st);
+}
+
+template <int M>
+cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
+  const int64_t rows = a.row_hi - a.row_lo;
+  int64_t blocks = (rows * 32 + 255) / 256;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
+  grid_eval_kernel<M><<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Inclusive prefix over every dimension of a table of uint4 elements
+// (`vec` elements per cell).  The first pass reads the f32 histogram H (and
+// re-zeroes it) and writes T; later passes run in place on T.
+cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
+                         cudaStream_t st) {
+  if (ndim == 0) {  // a single cell: convert, copy and re-zero
+    rowscan_kernel<<<1, 32, 0, st>>>(H, T, vec, 1, 1);
+    return cudaGetLastError();
+  }
+  int64_t inner = vec;
+  uint4* src = H;
+  for (int d = ndim - 1; d >= 0; --d) {
+    const int64_t len = dims[d];
+    const int64_t outer = cells * vec / (len * inner);
+    const int from_f32 = src == H ? 1 : 0;
+    if (inner == 1) {
+      int64_t blocks = (outer * 32 + 255) / 256;
+      blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
+      rowscan_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, T, outer, (int)len, from_f32);
+    } else {
+      const size_t smem = (size_t)kColChunk * kColTile * sizeof(uint4);
+      static std::atomic<int> smem_set{0};
+      cudaError_t e = ensure_smem(colscan_kernel, smem_set, smem);
+      if (e != cudaSuccess) return e;
+      const int64_t tiles = outer * ((inner + kColTile - 1) / kColTile);
+      const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 8));
+      colscan_kernel<<<(unsigned)blocks, 256, smem, st>>>(src, T, outer, len, inner, from_f32);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    src = T;
+    inner *= len;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
+                            gs_grid_info* info) {
+  if (!info) return GS_EINVAL;
+  Plan p;
+  int rc = make_plan(n_rec, n_models, grid_len, &p);
+  if (rc != GS_OK) return rc;
+  info->n_configs = p.n_configs;
+  info->n_cells = p.cellsF;
+  info->side_cells = p.cellsP;
+  info->n_structures = p.n_struct;
+  info->max_len = p.M;
+  info->workspace_bytes = p.bytes;
+  return GS_OK;
+}
+
+extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, int64_t n_rec,
+                             int32_t n_models, const double* grids, const int32_t* grid_len,
+                             void* workspace, size_t workspace_bytes, int32_t flags,
+                             void* stream) {
+  Plan p;
+  int rc = make_plan(n_rec, n_models, grid_len, &p);
+  if (rc != GS_OK) return rc;
+  GS_REQUIRE(certainty && correct && grids);
+  if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  float* F = reinterpret_cast<float*>(ws + p.offHF);
+  float* P = reinterpret_cast<float*>(ws + p.offHP);
+  if (flags & GS_GRID_WORKSPACE_DIRTY) {
+    GS_CUDA_TRY(cudaMemsetAsync(F, 0, (size_t)p.cellsF * 16, st));
+    if (p.cellsP) GS_CUDA_TRY(cudaMemsetAsync(P, 0, (size_t)p.cellsP * p.NVP * 16, st));
+  }
+
+  HistArgs h{};
+  h.cert = certainty;
+  h.corr = correct;
+  h.n_rec = n_rec;
+  h.grids = grids;
+  int off = 0;
+  for (int j = 0; j < n_models; ++j) {
+    h.goff[j] = off;
+    h.glen[j] = p.glen[j];
+    off += p.glen[j];
+  }
+  for (int j = 0; j < p.D; ++j) h.strideF[j] = p.strideF[j];
+  for (int j = 0; j < p.DP; ++j) h.strideP[j] = p.strideP[j];
+  h.cellsP = p.cellsP;
+  h.grid_doubles = p.D > 0 ? h.goff[p.D - 1] + h.glen[p.D - 1] : 0;
+  h.vec_ok = aligned16(certainty) && ((reinterpret_cast<uintptr_t>(correct) & 3u) == 0);
+  const size_t side_bytes = (size_t)p.cellsP * p.NVP * 16;
+  h.priv = p.DP > 0 && side_bytes <= kSidePrivMax;
+  h.F = F;
+  h.P = P;
+  const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (h.priv ? side_bytes : 0) + 16;
+  if (smem > 200 * 1024) return GS_EUNSUPPORTED;
+  const int64_t imax = std::max<int64_t>(p.cellsF * 4, p.cellsP * p.NVP * 4);
+  cudaError_t e = cudaSuccess;
+  switch (n_models) {
+    case 1: e = launch_hist<1>(h, n_rec, smem, imax, st); break;
+    case 2: e = launch_hist<2>(h, n_rec, smem, imax, st); break;
+    case 3: e = launch_hist<3>(h, n_rec, smem, imax, st); break;
+    case 4: e = launch_hist<4>(h, n_rec, smem, imax, st); break;
+    case 5: e = launch_hist<5>(h, n_rec, smem, imax, st); break;
+    case 6: e = launch_hist<6>(h, n_rec, smem, imax, st); break;
+    case 7: e = launch_hist<7>(h, n_rec, smem, imax, st); break;
+    case 8: e = launch_hist<8>(h, n_rec, smem, imax, st); break;
+    default: return GS_EUNSUPPORTED;
+  }
+  GS_CUDA_TRY(e);
+  GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(F), reinterpret_cast<uint4*>(ws + p.offF), p.D,
+                           p.dims, p.cellsF, 1, st));
+  if (p.DP > 0)
+    GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), reinterpret_cast<uint4*>(ws + p.offP), p.DP,
+                             p.dims, p.cellsP, p.NVP, st));
+  return GS_OK;
+}
+
+extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
+                            const double* cost1, int64_t config_begin, int64_t config_count,
+                            double* accuracy, double* mean_cost, double* forward_frac,
+                            uint32_t* n_correct, const void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  Plan p;
+  int rc = make_plan(n_rec, n_models, grid_len, &p);
+  if (rc != GS_OK) return rc;
+  GS_REQUIRE(cost1 && config_begin >= 0 && config_count >= 0 &&
+             config_begin + config_count <= p.n_configs);
+  if (config_count == 0) return GS_OK;
+  if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
+  // vector stores need 16-byte aligned outputs
+  if ((accuracy && !aligned16(accuracy)) || (mean_cost && !aligned16(mean_cost)) ||
+      (n_correct && !aligned16(n_correct)) || (forward_frac && !aligned16(forward_frac)))
+    return GS_EINVAL;
+  EvalGridArgs a{};
+  a.M = p.M;
+  a.n_struct = p.n_struct;
+  a.NVP = p.NVP;
+  a.DP = p.DP;
+  for (int j = 0; j < p.M; ++j) a.glen[j] = p.glen[j];
+  for (int j = 0; j < p.D; ++j) a.strideF[j] = p.strideF[j];
+  for (int j = 0; j < p.DP; ++j) a.strideP[j] = p.strideP[j];
+  a.n_rec = n_rec;
+  a.cellsF = p.cellsF;
+  a.cellsP = p.cellsP;
+  a.cfg_begin = config_begin;
+  a.cfg_count = config_count;
+  for (int s = 0; s <= p.n_struct; ++s) a.struct_begin[s] = p.struct_begin[s];
+  for (int s = 0; s < p.n_struct; ++s) a.struct_mask[s] = p.struct_mask[s];
+  // rows: configs sharing all thresholds but the last forwarding stage's
+  int64_t rows = 0;
+  for (int s = 0; s < p.n_struct; ++s) {
+    a.row_begin[s] = rows;
+    rows += (p.struct_begin[s + 1] - p.struct_begin[s]) / row_len(p, s);
+  }
+  a.row_begin[p.n_struct] = rows;
+  a.row_lo = global_row(p, a.row_begin, config_begin);
+  a.row_hi = global_row(p, a.row_begin, config_begin + config_count - 1) + 1;
+  const uint8_t* ws = static_cast<const uint8_t*>(workspace);
+  a.F = reinterpret_cast<const uint4*>(ws + p.offF);
+  a.P = reinterpret_cast<const uint4*>(ws + p.offP);
+  a.cost1 = cost1;
+  a.acc = accuracy;
+  a.cost = mean_cost;
+  a.frac = forward_frac;
+  a.n_correct = n_correct;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  switch (n_models) {
+    case 1: e = launch_grid_eval<1>(a, st); break;
+    case 2: e = launch_grid_eval<2>(a, st); break;
+    case 3: e = launch_grid_eval<3>(a, st); break;
+    case 4: e = launch_grid_eval<4>(a, st); break;
+    case 5: e = launch_grid_eval<5>(a, st); break;
+    case 6: e = launch_grid_eval<6>(a, st); break;
+    case 7: e = launch_grid_eval<7>(a, st); break;
+    case 8: e = launch_grid_eval<8>(a, st); break;
+    default: return GS_EUNSUPPORTED;
+  }
+  GS_CUDA_TRY(e);
+  return GS_OK;
+}
+
+extern "C" int gs_grid_decode(int32_t n_models, const int32_t* grid_len, const double* grids,
+                              const int64_t* config_idx, int64_t count, int32_t* stage_model,
+                              double* thresholds, int32_t* n_stages, void* stream) {
+  Plan p;
+  int rc = make_plan(1, n_models, grid_len, &p);
+  if (rc != GS_OK) return rc;
+  if (count == 0) return GS_OK;
+  GS_REQUIRE(count > 0 && grids && config_idx && stage_model && thresholds && n_stages);
+  DecodeArgs a{};
+  a.M = p.M;
+  a.n_struct = p.n_struct;
+  int off = 0;
+  for (int j = 0; j < p.M; ++j) {
+    a.glen[j] = p.glen[j];
+    a.goff[j] = off;
+    off += p.glen[j];
+  }
+  for (int s = 0; s <= p.n_struct; ++s) a.struct_begin[s] = p.struct_begin[s];
+  for (int s = 0; s < p.n_struct; ++s) a.struct_mask[s] = p.struct_mask[s];
+  a.grids = grids;
+  a.idx = config_idx;
+  a.count = count;
+  a.stage_model = stage_model;
+  a.thr = thresholds;
+  a.n_stages = n_stages;
+  int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)sm_count() * 16));
+  grid_decode_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  GS_LAUNCH_CHECK();
+  return GS_OK;
+}

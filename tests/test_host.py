@@ -58,9 +58,9 @@ def test_grid_plan_matches_enumeration(glen):
     assert info.n_configs == gridsweep.n_configs(glen) == oracle.grid_n_configs(glen)
     assert info.n_structures == 2 ** len(glen) - 1
     assert info.n_cells == int(np.prod([g + 1 for g in glen[:-1]]))
-    side = int(np.prod([g + 1 for g in glen[:len(glen) - 2]])) if len(glen) >= 3 else 0
+    side = int(np.prod([g + 1 for g in glen[:len(glen) - 3]])) if len(glen) >= 4 else 0
     assert info.side_cells == side
-    assert info.workspace_bytes >= 8 * (info.n_cells + side)
+    assert info.workspace_bytes >= 16 * (info.n_cells + side)
 
 
 def test_config2_size():
