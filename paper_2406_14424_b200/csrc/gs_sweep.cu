@@ -30,9 +30,15 @@
 // counts are exact in f32 below 2^24), so the histogram costs one L2 vector
 // atomic per record.  The prefix sums convert to u32.
 //
-// Histogram and prefix tables are separate buffers: the first scan pass
-// reads the f32 histogram, writes the u32 prefix and re-zeroes the histogram,
-// so no memset runs per build (the caller zeroes the workspace once).
+// Random-scatter L2 atomics bound the histogram, so the main table is first
+// accumulated with ONE 64-bit atomic add per record: four 16-bit counts per
+// cell.  A field can only carry if some cell holds >= 2^16 records; the
+// thread that moves a count off 0xFFFF raises a flag and a second, normally
+// empty, pass redoes the main table with f32 vector reductions (exact below
+// 2^24), all on the device.  Histogram and prefix tables are separate
+// buffers: the first scan pass reads the histogram, writes the u32 prefix and
+// re-zeroes the histogram, so no memset runs per build (the caller zeroes the
+// workspace once).
 //
 // Kernels: grid_hist (one pass over the records, vector loads, binary search
 // in shared-memory grids), rowscan (contiguous last dim, warp-shuffle scan),
@@ -63,7 +69,7 @@ struct Plan {
   int64_t n_configs = 0;
   int64_t struct_begin[256 + 1] = {};
   uint32_t struct_mask[256] = {};
-  size_t offHF = 0, offF = 0, offHP = 0, offP = 0, bytes = 0;
+  size_t offH16 = 0, offHF = 0, offF = 0, offHP = 0, offP = 0, offFlag = 0, bytes = 0;
 };
 
 int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
@@ -129,11 +135,14 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->n_configs = off;
   const size_t bF = round_up((size_t)p->cellsF * 16, 256);
   const size_t bP = round_up((size_t)p->cellsP * p->NVP * 16, 256);
-  p->offHF = 0;
-  p->offF = bF;
-  p->offHP = 2 * bF;
-  p->offP = 2 * bF + bP;
-  p->bytes = 2 * bF + 2 * bP;
+  const size_t b16 = round_up((size_t)p->cellsF * 8, 256);
+  p->offH16 = 0;
+  p->offHF = b16;
+  p->offF = b16 + bF;
+  p->offHP = b16 + 2 * bF;
+  p->offP = b16 + 2 * bF + bP;
+  p->offFlag = b16 + 2 * bF + 2 * bP;
+  p->bytes = p->offFlag + 256;
   return GS_OK;
 }
 
@@ -179,19 +188,28 @@ struct HistArgs {
   int32_t grid_doubles;  // grids of models 0..D-1 staged in smem
   int32_t vec_ok;
   int32_t priv;          // side table privatised in shared memory
-  float* F;
-  float* P;
+  float* F;                // f32 fallback main histogram
+  float* P;                // side histogram (f32)
+  unsigned long long* H16; // packed main histogram: 4 x 16-bit counts per cell
+  uint32_t* flag;          // set when a cell count reaches 2^16 (fallback needed)
 };
 
-template <int M, typename Cell>
+// MODE 0: main table as ONE 64-bit atomic add per record (fields {cnt,
+// c_{M-1}, c_{M-2}, c_{M-3}} of 16 bits; every other field of a cell is <= its
+// count, so no field can carry unless some cell's count passes 0xFFFF, and the
+// thread that moves a count from 0xFFFF sees it in the returned old value and
+// raises the flag).  MODE 1: exits at once unless the flag is up; then redoes
+// the main table with f32 vector reductions (exact below 2^24).
+template <int M, typename Cell, int MODE>
 __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
+  if (MODE == 1 && *reinterpret_cast<volatile uint32_t*>(a.flag) == 0) return;
   constexpr int D = M - 1;
   constexpr int DP = M >= 4 ? M - 3 : 0;
   constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
   extern __shared__ __align__(16) double s_grid[];
   float* s_side = reinterpret_cast<float*>(s_grid + a.grid_doubles);
   for (int i = threadIdx.x; i < a.grid_doubles; i += blockDim.x) s_grid[i] = a.grids[i];
-  if (DP > 0 && a.priv)
+  if (MODE == 0 && DP > 0 && a.priv)
     for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) s_side[i] = 0.f;
   __syncthreads();
 
@@ -235,7 +253,15 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
 #pragma unroll
     for (int i = 0; i < 3; ++i)
       if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i] ? 1.f : 0.f;
-    red_add_v4(a.F + cellF * 4, v[0], v[1], v[2], v[3]);
+    if (MODE == 1) {
+      red_add_v4(a.F + cellF * 4, v[0], v[1], v[2], v[3]);
+      continue;
+    }
+    const unsigned long long inc = 1ull | ((unsigned long long)(v[1] != 0.f) << 16) |
+                                   ((unsigned long long)(v[2] != 0.f) << 32) |
+                                   ((unsigned long long)(v[3] != 0.f) << 48);
+    const unsigned long long old = atomicAdd(a.H16 + cellF, inc);
+    if ((old & 0xffffull) == 0xffffull) *reinterpret_cast<volatile uint32_t*>(a.flag) = 1u;
     // side table: c_j for j <= M-4 at (b_0..b_{M-4})
     if constexpr (DP > 0) {
 #pragma unroll
@@ -249,7 +275,7 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
       }
     }
   }
-  if (DP > 0 && a.priv) {
+  if (MODE == 0 && DP > 0 && a.priv) {
     __syncthreads();
     for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) {
       const float c = s_side[i];
@@ -300,6 +326,69 @@ __global__ void __launch_bounds__(256) rowscan_kernel(uint4* src, uint4* T, int6
         for (int u = 0; u < 4; ++u) {
           const int c = base + lane * 4 + u;
           if (c < len) in[c] = make_uint4(0, 0, 0, 0);
+        }
+      }
+      uint4 tot = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        tot = add4(tot, e[u]);
+        e[u] = tot;
+      }
+      uint4 incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint4 y = shfl_up4(incl, o);
+        if (lane >= o) incl = add4(incl, y);
+      }
+      const uint4 excl = add4(carry, make_uint4(incl.x - tot.x, incl.y - tot.y, incl.z - tot.z,
+                                                incl.w - tot.w));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        if (c < len) row[c] = add4(e[u], excl);
+      }
+      carry = add4(carry, shfl4(incl, 31));
+    }
+  }
+}
+
+// First prefix pass of the main table (contiguous last dim): reads the packed
+// 16-bit histogram, or the f32 fallback histogram when the overflow flag is
+// up, re-zeroes what it read, and writes the u32 prefix.
+__global__ void __launch_bounds__(256) rowscan_first_kernel(unsigned long long* H16, uint4* HF,
+                                                            const uint32_t* flag, uint4* T,
+                                                            int64_t n_rows, int len) {
+  const int lane = (int)lane_id();
+  const bool fb = *flag != 0u;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
+    unsigned long long* in16 = H16 + r * len;
+    uint4* inF = HF + r * len;
+    uint4* row = T + r * len;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (int base = 0; base < len; base += 128) {
+      uint4 e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        e[u] = make_uint4(0, 0, 0, 0);
+        if (c < len) {
+          if (fb) {
+            uint4 f = inF[c];
+            e[u] = to_u4(*reinterpret_cast<float4*>(&f));
+          } else {
+            const unsigned long long w = in16[c];
+            e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
+                              (uint32_t)((w >> 32) & 0xffff), (uint32_t)(w >> 48));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = base + lane * 4 + u;
+        if (c < len) {
+          in16[c] = 0ull;
+          if (fb) inF[c] = make_uint4(0, 0, 0, 0);
         }
       }
       uint4 tot = make_uint4(0, 0, 0, 0);
@@ -671,12 +760,21 @@ int64_t global_row(const Plan& p, const int64_t* row_begin, int64_t c) {
 
 template <int M, typename Cell>
 cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
-  auto k = grid_hist_kernel<M, Cell>;
+  int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
+  {
+    auto k = grid_hist_kernel<M, Cell, 0>;
+    static std::atomic<int> smem_set{0};
+    cudaError_t e = ensure_smem(k, smem_set, smem);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  auto k = grid_hist_kernel<M, Cell, 1>;  // no-op unless a cell passed 0xFFFF records
   static std::atomic<int> smem_set{0};
   cudaError_t e = ensure_smem(k, smem_set, smem);
   if (e != cudaSuccess) return e;
-  int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
   k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
   return cudaGetLastError();
 }
@@ -702,14 +800,27 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
 // (`vec` elements per cell).  The first pass reads the f32 histogram H (and
 // re-zeroes it) and writes T; later passes run in place on T.
 cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
-                         cudaStream_t st) {
-  if (ndim == 0) {  // a single cell: convert, copy and re-zero
+                         cudaStream_t st, unsigned long long* H16 = nullptr,
+                         const uint32_t* flag = nullptr) {
+  if (H16) {  // main table: packed first pass along the last dim (vec == 1)
+    const int64_t len = ndim == 0 ? 1 : dims[ndim - 1];
+    const int64_t rows = cells / len;
+    int64_t blocks = (rows * 32 + 255) / 256;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
+    rowscan_first_kernel<<<(unsigned)blocks, 256, 0, st>>>(H16, H, flag, T, rows, (int)len);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || ndim <= 1) return e;
+  } else if (ndim == 0) {  // a single cell: convert, copy and re-zero
     rowscan_kernel<<<1, 32, 0, st>>>(H, T, vec, 1, 1);
     return cudaGetLastError();
   }
   int64_t inner = vec;
   uint4* src = H;
-  for (int d = ndim - 1; d >= 0; --d) {
+  if (H16) {
+    src = T;
+    inner *= dims[ndim - 1];
+  }
+  for (int d = ndim - 1 - (H16 ? 1 : 0); d >= 0; --d) {
     const int64_t len = dims[d];
     const int64_t outer = cells * vec / (len * inner);
     const int from_f32 = src == H ? 1 : 0;
@@ -767,7 +878,11 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   float* F = reinterpret_cast<float*>(ws + p.offHF);
   float* P = reinterpret_cast<float*>(ws + p.offHP);
+  auto* H16 = reinterpret_cast<unsigned long long*>(ws + p.offH16);
+  auto* flag = reinterpret_cast<uint32_t*>(ws + p.offFlag);
+  GS_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(uint32_t), st));
   if (flags & GS_GRID_WORKSPACE_DIRTY) {
+    GS_CUDA_TRY(cudaMemsetAsync(H16, 0, (size_t)p.cellsF * 8, st));
     GS_CUDA_TRY(cudaMemsetAsync(F, 0, (size_t)p.cellsF * 16, st));
     if (p.cellsP) GS_CUDA_TRY(cudaMemsetAsync(P, 0, (size_t)p.cellsP * p.NVP * 16, st));
   }
@@ -792,6 +907,8 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   h.priv = p.DP > 0 && side_bytes <= kSidePrivMax;
   h.F = F;
   h.P = P;
+  h.H16 = H16;
+  h.flag = flag;
   const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (h.priv ? side_bytes : 0) + 16;
   if (smem > 200 * 1024) return GS_EUNSUPPORTED;
   const int64_t imax = std::max<int64_t>(p.cellsF * 4, p.cellsP * p.NVP * 4);
@@ -809,7 +926,7 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   }
   GS_CUDA_TRY(e);
   GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(F), reinterpret_cast<uint4*>(ws + p.offF), p.D,
-                           p.dims, p.cellsF, 1, st));
+                           p.dims, p.cellsF, 1, st, H16, flag));
   if (p.DP > 0)
     GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), reinterpret_cast<uint4*>(ws + p.offP), p.DP,
                              p.dims, p.cellsP, p.NVP, st));

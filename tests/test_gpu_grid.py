@@ -81,6 +81,28 @@ def test_config_ranges_equal_full_sweep():
                               full.forward_frac[begin:begin + count].cpu().numpy())
 
 
+@pytest.mark.parametrize("n_models", [2, 4])
+def test_heavy_tie_cell_overflow_fallback(n_models):
+    """> 65535 records in one table cell: the packed 16-bit histogram flags
+    the overflow and the f32 fallback pass must give the exact counts."""
+    rng = np.random.default_rng(17)
+    n = 70_000
+    cert = np.full((n, n_models), 0.5)
+    cert[:5000] = np.round(rng.random((5000, n_models)), 1)  # a few other cells
+    corr = (rng.random((n, n_models)) < 0.5).astype(np.uint8)
+    grids = [np.array([0.0, 0.25, 0.5, 0.75])] * n_models
+    cost1 = np.arange(1, n_models + 1, dtype=np.float64) * 100.0
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, cost1)
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
+    assert np.array_equal(acc, want[0]) and np.array_equal(cost, want[1])
+    assert np.array_equal(frac, want[2])
+    # a second build on the same workspace (histogram re-zeroed by the first)
+    sw.build()
+    res = sw.evaluate()
+    assert np.array_equal(res.accuracy.cpu().numpy(), want[0])
+
+
 def test_negative_singleton_certainty_bins_below_zero():
     """Singleton scores can be negative (cascades.certainty returns the score):
     such records sit below grid value 0 and forward at every threshold."""
