@@ -80,7 +80,7 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->DP = M >= 4 ? M - 3 : 0;
   p->NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
   for (int j = 0; j < M; ++j) {
-    if (grid_len[j] < 1 || grid_len[j] > (1 << 20)) return GS_EINVAL;
+    if (grid_len[j] < 1 || grid_len[j] > 65535) return GS_EINVAL;
     p->glen[j] = grid_len[j];
   }
   double cells = 1.0;
@@ -189,7 +189,7 @@ struct HistArgs {
   int32_t vec_ok;
   int32_t priv;          // side table privatised in shared memory
   float* F;                // f32 fallback main histogram
-  float* P;                // side histogram (f32)
+  uint32_t* P;             // side histogram (u32 counts)
   unsigned long long* H16; // packed main histogram: 4 x 16-bit counts per cell
   uint32_t* flag;          // set when a cell count reaches 2^16 (fallback needed)
 };
@@ -200,6 +200,21 @@ struct HistArgs {
 // thread that moves a count from 0xFFFF sees it in the returned old value and
 // raises the flag).  MODE 1: exits at once unless the flag is up; then redoes
 // the main table with f32 vector reductions (exact below 2^24).
+// Bin lookup: per CTA, every forwarding model's grid is bucketed by a
+// monotone f64 map q(x) onto kLutBuckets buckets.  Grid values with q(g) <
+// q(x) are all <= x and those with q(g) > q(x) are all > x, so the exact
+// count #{g <= x} lies in [lb, ub) of x's bucket and only the grid values
+// sharing the bucket (usually none or one) are compared.  This replaces a
+// 7-step binary search of bank-conflicted 64-bit shared loads per model.
+constexpr int kLutBuckets = 2048;
+
+__device__ __forceinline__ int lut_bucket(double x, double lo, double hi, double scale) {
+  if (!(x >= lo)) return 0;  // below the grid (or NaN)
+  if (x >= hi) return kLutBuckets - 1;
+  const int q = (int)((x - lo) * scale);
+  return q > kLutBuckets - 1 ? kLutBuckets - 1 : q;
+}
+
 template <int M, typename Cell, int MODE>
 __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
   if (MODE == 1 && *reinterpret_cast<volatile uint32_t*>(a.flag) == 0) return;
@@ -207,10 +222,48 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
   constexpr int DP = M >= 4 ? M - 3 : 0;
   constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
   extern __shared__ __align__(16) double s_grid[];
-  float* s_side = reinterpret_cast<float*>(s_grid + a.grid_doubles);
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + a.grid_doubles);  // [D][buckets]: lb | ub << 16
+  uint32_t* s_side = s_lut + D * kLutBuckets;
+  __shared__ double s_lo[kMaxM], s_hi[kMaxM], s_scale[kMaxM];
   for (int i = threadIdx.x; i < a.grid_doubles; i += blockDim.x) s_grid[i] = a.grids[i];
+  for (int i = threadIdx.x; i < D * kLutBuckets; i += blockDim.x) s_lut[i] = 0u;
   if (MODE == 0 && DP > 0 && a.priv)
-    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) s_side[i] = 0.f;
+    for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) s_side[i] = 0u;
+  __syncthreads();
+  if ((int)threadIdx.x < D) {
+    const int j = threadIdx.x;
+    const double* g = s_grid + a.goff[j];
+    const int n = a.glen[j];
+    s_lo[j] = g[0];
+    s_hi[j] = g[n - 1];
+    s_scale[j] = n > 1 ? (double)kLutBuckets / (g[n - 1] - g[0]) : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < D; ++j)
+    for (int i = threadIdx.x; i < a.glen[j]; i += blockDim.x)
+      atomicAdd(s_lut + j * kLutBuckets + lut_bucket(s_grid[a.goff[j] + i], s_lo[j], s_hi[j], s_scale[j]), 1u);
+  __syncthreads();
+  {  // per model: exclusive scan of bucket counts -> (lb, ub); one warp per model
+    const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+    constexpr int per = kLutBuckets / 32;
+    for (int j = warp; j < D; j += blockDim.x >> 5) {
+      uint32_t* L = s_lut + j * kLutBuckets + lane * per;
+      uint32_t tot = 0;
+      for (int q = 0; q < per; ++q) tot += L[q];
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t run = incl - tot;
+      for (int q = 0; q < per; ++q) {
+        const uint32_t c = L[q];
+        L[q] = run | ((run + c) << 16);
+        run += c;
+      }
+    }
+  }
   __syncthreads();
 
   // n_rec < 2^24 and M <= 8, so record offsets fit 32 bits
@@ -234,52 +287,56 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     if (M == 4 && a.vec_ok) {
       const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a.corr) + r);
 #pragma unroll
-      for (int j = 0; j < M; ++j) k[j] = (w >> (8 * j)) & 0xffu;
+      for (int j = 0; j < M; ++j) k[j] = ((w >> (8 * j)) & 0xffu) != 0;
     } else {
 #pragma unroll
-      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j);
+      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j) != 0;
     }
     Cell cellF = 0, cellP = 0;
-    int off = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      const int b = upper_count(s_grid + off, a.glen[j], x[j]);
-      off += a.glen[j];
+      const uint32_t e = s_lut[j * kLutBuckets + lut_bucket(x[j], s_lo[j], s_hi[j], s_scale[j])];
+      const int lb = (int)(e & 0xffffu), ub = (int)(e >> 16);
+      const int b = lb + (ub > lb ? upper_count(s_grid + a.goff[j] + lb, ub - lb, x[j]) : 0);
       cellF += (Cell)b * (Cell)a.strideF[j];
       if (j < DP) cellP += (Cell)b * (Cell)a.strideP[j];
     }
     // main table: {cnt, c_{M-1}, c_{M-2}, c_{M-3}}
-    float v[4] = {1.f, 0.f, 0.f, 0.f};
+    uint32_t v[4] = {1u, 0u, 0u, 0u};
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-      if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i] ? 1.f : 0.f;
+      if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i];
     if (MODE == 1) {
-      red_add_v4(a.F + cellF * 4, v[0], v[1], v[2], v[3]);
+      red_add_v4(a.F + cellF * 4, 1.f, (float)v[1], (float)v[2], (float)v[3]);
       continue;
     }
-    const unsigned long long inc = 1ull | ((unsigned long long)(v[1] != 0.f) << 16) |
-                                   ((unsigned long long)(v[2] != 0.f) << 32) |
-                                   ((unsigned long long)(v[3] != 0.f) << 48);
+    const unsigned long long inc = 1ull | ((unsigned long long)v[1] << 16) |
+                                   ((unsigned long long)v[2] << 32) | ((unsigned long long)v[3] << 48);
     const unsigned long long old = atomicAdd(a.H16 + cellF, inc);
     if ((old & 0xffffull) == 0xffffull) *reinterpret_cast<volatile uint32_t*>(a.flag) = 1u;
-    // side table: c_j for j <= M-4 at (b_0..b_{M-4})
+    // side table: c_j for j <= M-4 at (b_0..b_{M-4}); integer counts,
+    // warp-aggregated when privatised in shared memory
     if constexpr (DP > 0) {
+      const uint32_t active = __activemask();
+      const int lane = (int)lane_id();
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
-        if (!k[j]) continue;
         const Cell e = (cellP * NVP + j / 4) * 4 + (j % 4);
-        if (a.priv)
-          atomicAdd(s_side + e, 1.f);
-        else
-          atomicAdd(a.P + e, 1.f);
+        if (a.priv) {
+          const uint32_t peers = __match_any_sync(active, (unsigned long long)e);
+          const uint32_t ones = __ballot_sync(active, k[j] != 0) & peers;
+          if (ones && (__ffs(peers) - 1) == lane) atomicAdd(s_side + e, (uint32_t)__popc(ones));
+        } else if (k[j]) {
+          atomicAdd(a.P + e, 1u);
+        }
       }
     }
   }
   if (MODE == 0 && DP > 0 && a.priv) {
     __syncthreads();
     for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) {
-      const float c = s_side[i];
-      if (c != 0.f) atomicAdd(a.P + i, c);
+      const uint32_t c = s_side[i];
+      if (c) atomicAdd(a.P + i, c);
     }
   }
 }
@@ -775,7 +832,7 @@ cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStr
   static std::atomic<int> smem_set{0};
   cudaError_t e = ensure_smem(k, smem_set, smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
+  k<<<(unsigned)std::min<int64_t>(blocks, sm_count()), kHistThreads, smem, st>>>(h);
   return cudaGetLastError();
 }
 
@@ -801,7 +858,7 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
 // re-zeroes it) and writes T; later passes run in place on T.
 cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
                          cudaStream_t st, unsigned long long* H16 = nullptr,
-                         const uint32_t* flag = nullptr) {
+                         const uint32_t* flag = nullptr, bool h_f32 = true) {
   if (H16) {  // main table: packed first pass along the last dim (vec == 1)
     const int64_t len = ndim == 0 ? 1 : dims[ndim - 1];
     const int64_t rows = cells / len;
@@ -811,7 +868,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || ndim <= 1) return e;
   } else if (ndim == 0) {  // a single cell: convert, copy and re-zero
-    rowscan_kernel<<<1, 32, 0, st>>>(H, T, vec, 1, 1);
+    rowscan_kernel<<<1, 32, 0, st>>>(H, T, vec, 1, h_f32 ? 1 : 0);
     return cudaGetLastError();
   }
   int64_t inner = vec;
@@ -823,7 +880,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
   for (int d = ndim - 1 - (H16 ? 1 : 0); d >= 0; --d) {
     const int64_t len = dims[d];
     const int64_t outer = cells * vec / (len * inner);
-    const int from_f32 = src == H ? 1 : 0;
+    const int from_f32 = (src == H && h_f32) ? 1 : 0;
     if (inner == 1) {
       int64_t blocks = (outer * 32 + 255) / 256;
       blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
@@ -877,7 +934,7 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   float* F = reinterpret_cast<float*>(ws + p.offHF);
-  float* P = reinterpret_cast<float*>(ws + p.offHP);
+  uint32_t* P = reinterpret_cast<uint32_t*>(ws + p.offHP);
   auto* H16 = reinterpret_cast<unsigned long long*>(ws + p.offH16);
   auto* flag = reinterpret_cast<uint32_t*>(ws + p.offFlag);
   GS_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(uint32_t), st));
@@ -909,7 +966,8 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   h.P = P;
   h.H16 = H16;
   h.flag = flag;
-  const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (h.priv ? side_bytes : 0) + 16;
+  const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (size_t)p.D * kLutBuckets * 4 +
+                      (h.priv ? side_bytes : 0) + 16;
   if (smem > 200 * 1024) return GS_EUNSUPPORTED;
   const int64_t imax = std::max<int64_t>(p.cellsF * 4, p.cellsP * p.NVP * 4);
   cudaError_t e = cudaSuccess;
@@ -929,7 +987,7 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
                            p.dims, p.cellsF, 1, st, H16, flag));
   if (p.DP > 0)
     GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), reinterpret_cast<uint4*>(ws + p.offP), p.DP,
-                             p.dims, p.cellsP, p.NVP, st));
+                             p.dims, p.cellsP, p.NVP, st, nullptr, nullptr, false));
   return GS_OK;
 }
 
