@@ -243,28 +243,38 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     for (int i = threadIdx.x; i < a.glen[j]; i += blockDim.x)
       atomicAdd(s_lut + j * kLutBuckets + lut_bucket(s_grid[a.goff[j] + i], s_lo[j], s_hi[j], s_scale[j]), 1u);
   __syncthreads();
-  {  // per model: exclusive scan of bucket counts -> (lb, ub); one warp per model
+  // per model: exclusive scan of the bucket counts -> (lb, ub), whole block
+  // (kLutBuckets / kHistThreads consecutive buckets per thread)
+  {
+    __shared__ uint32_t s_wsum[kHistThreads / 32];
+    constexpr int per = kLutBuckets / kHistThreads;
     const int warp = threadIdx.x >> 5, lane = (int)lane_id();
-    constexpr int per = kLutBuckets / 32;
-    for (int j = warp; j < D; j += blockDim.x >> 5) {
-      uint32_t* L = s_lut + j * kLutBuckets + lane * per;
-      uint32_t tot = 0;
-      for (int q = 0; q < per; ++q) tot += L[q];
+    for (int j = 0; j < D; ++j) {
+      uint32_t* L = s_lut + j * kLutBuckets + threadIdx.x * per;
+      uint32_t c[per], tot = 0;
+#pragma unroll
+      for (int q = 0; q < per; ++q) {
+        c[q] = L[q];
+        tot += c[q];
+      }
       uint32_t incl = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
       uint32_t run = incl - tot;
+      for (int w = 0; w < warp; ++w) run += s_wsum[w];
+#pragma unroll
       for (int q = 0; q < per; ++q) {
-        const uint32_t c = L[q];
-        L[q] = run | ((run + c) << 16);
-        run += c;
+        L[q] = run | ((run + c[q]) << 16);
+        run += c[q];
       }
+      __syncthreads();
     }
   }
-  __syncthreads();
 
   // n_rec < 2^24 and M <= 8, so record offsets fit 32 bits
   const int n_rec = (int)a.n_rec;
@@ -817,8 +827,9 @@ int64_t global_row(const Plan& p, const int64_t* row_begin, int64_t c) {
 
 template <int M, typename Cell>
 cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
+  // persistent grid: the bin lookup tables are built once per CTA
   int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 2));
   {
     auto k = grid_hist_kernel<M, Cell, 0>;
     static std::atomic<int> smem_set{0};
