@@ -279,6 +279,9 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
   // n_rec < 2^24 and M <= 8, so record offsets fit 32 bits
   const int n_rec = (int)a.n_rec;
   const int step = gridDim.x * blockDim.x;
+  // the overflow test on each atomic's old value is made one iteration late,
+  // so the loop never waits for an atomic's round trip
+  unsigned long long prev_old = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rec; r += step) {
     double x[M];
     uint32_t k[M];
@@ -322,26 +325,22 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     }
     const unsigned long long inc = 1ull | ((unsigned long long)v[1] << 16) |
                                    ((unsigned long long)v[2] << 32) | ((unsigned long long)v[3] << 48);
-    const unsigned long long old = atomicAdd(a.H16 + cellF, inc);
-    if ((old & 0xffffull) == 0xffffull) *reinterpret_cast<volatile uint32_t*>(a.flag) = 1u;
-    // side table: c_j for j <= M-4 at (b_0..b_{M-4}); integer counts,
-    // warp-aggregated when privatised in shared memory
+    if ((prev_old & 0xffffull) == 0xffffull) *reinterpret_cast<volatile uint32_t*>(a.flag) = 1u;
+    prev_old = atomicAdd(a.H16 + cellF, inc);
+    // side table: c_j for j <= M-4 at (b_0..b_{M-4}); integer counts
     if constexpr (DP > 0) {
-      const uint32_t active = __activemask();
-      const int lane = (int)lane_id();
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
         const Cell e = (cellP * NVP + j / 4) * 4 + (j % 4);
         if (a.priv) {
-          const uint32_t peers = __match_any_sync(active, (unsigned long long)e);
-          const uint32_t ones = __ballot_sync(active, k[j] != 0) & peers;
-          if (ones && (__ffs(peers) - 1) == lane) atomicAdd(s_side + e, (uint32_t)__popc(ones));
+          if (k[j]) atomicAdd(s_side + e, 1u);
         } else if (k[j]) {
           atomicAdd(a.P + e, 1u);
         }
       }
     }
   }
+  if (MODE == 0 && (prev_old & 0xffffull) == 0xffffull) *reinterpret_cast<volatile uint32_t*>(a.flag) = 1u;
   if (MODE == 0 && DP > 0 && a.priv) {
     __syncthreads();
     for (int64_t i = threadIdx.x; i < a.cellsP * NVP * 4; i += blockDim.x) {
@@ -829,7 +828,7 @@ template <int M, typename Cell>
 cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStream_t st) {
   // persistent grid: the bin lookup tables are built once per CTA
   int64_t blocks = (n_rec + kHistThreads - 1) / kHistThreads;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 2));
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
   {
     auto k = grid_hist_kernel<M, Cell, 0>;
     static std::atomic<int> smem_set{0};
