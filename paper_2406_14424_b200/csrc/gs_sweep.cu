@@ -58,6 +58,7 @@ constexpr int kMaxM = GS_MAX_MODELS;
 constexpr int64_t kMaxExactF32 = 1ll << 24;
 constexpr int kHistThreads = 512;
 constexpr size_t kSidePrivMax = 16 * 1024;
+constexpr size_t kSlabSmemMax = 200 * 1024;
 
 struct Plan {
   int M = 0, D = 0, DP = 0, NVP = 0, n_struct = 0;
@@ -481,6 +482,104 @@ __global__ void __launch_bounds__(256) rowscan_first_kernel(unsigned long long* 
   }
 }
 
+// First prefix pass of the main table when its last two dims form a slab
+// that fits in shared memory: one CTA per slab reads the packed histogram
+// (or the f32 fallback), row-scans it in registers (a warp per row), writes
+// the expanded u32 counts into a shared-memory slab, column-scans there and
+// stores the slab once — one global read and one write for two dimensions.
+__global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H16, uint4* HF,
+                                                          const uint32_t* flag, uint4* T,
+                                                          int64_t n_slabs, int rows, int cols) {
+  extern __shared__ __align__(16) uint4 s_slab[];
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const bool fb = *flag != 0u;
+  const int n = rows * cols;
+  for (int64_t slab = blockIdx.x; slab < n_slabs; slab += gridDim.x) {
+    const int64_t base = slab * (int64_t)n;
+    for (int r = warp; r < rows; r += nwarps) {
+      unsigned long long* in16 = H16 + base + (int64_t)r * cols;
+      uint4* inF = HF + base + (int64_t)r * cols;
+      uint4* out = s_slab + r * cols;
+      uint4 carry = make_uint4(0, 0, 0, 0);
+      for (int c0 = 0; c0 < cols; c0 += 128) {
+        uint4 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane * 4 + u;
+          e[u] = make_uint4(0, 0, 0, 0);
+          if (c < cols) {
+            if (fb) {
+              uint4 f = inF[c];
+              e[u] = to_u4(*reinterpret_cast<float4*>(&f));
+            } else {
+              const unsigned long long w = in16[c];
+              e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
+                                (uint32_t)((w >> 32) & 0xffff), (uint32_t)(w >> 48));
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane * 4 + u;
+          if (c < cols) {
+            in16[c] = 0ull;
+            if (fb) inF[c] = make_uint4(0, 0, 0, 0);
+          }
+        }
+        uint4 tot = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          tot = add4(tot, e[u]);
+          e[u] = tot;
+        }
+        uint4 incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint4 y = shfl_up4(incl, o);
+          if (lane >= o) incl = add4(incl, y);
+        }
+        const uint4 excl = add4(carry, make_uint4(incl.x - tot.x, incl.y - tot.y, incl.z - tot.z,
+                                                  incl.w - tot.w));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + lane * 4 + u;
+          if (c < cols) out[c] = add4(e[u], excl);
+        }
+        carry = add4(carry, shfl4(incl, 31));
+      }
+    }
+    __syncthreads();
+    // columns: thread (cell, lane) walks the rows; consecutive threads touch
+    // consecutive 32-bit words, so the walk is bank-conflict free
+    uint32_t* w32 = reinterpret_cast<uint32_t*>(s_slab);
+    for (int t = threadIdx.x; t < 4 * cols; t += blockDim.x) {
+      uint32_t acc = 0;
+      int r = 0;
+      for (; r + 4 <= rows; r += 4) {
+        const uint32_t v0 = w32[(r + 0) * cols * 4 + t], v1 = w32[(r + 1) * cols * 4 + t];
+        const uint32_t v2 = w32[(r + 2) * cols * 4 + t], v3 = w32[(r + 3) * cols * 4 + t];
+        acc += v0;
+        w32[(r + 0) * cols * 4 + t] = acc;
+        acc += v1;
+        w32[(r + 1) * cols * 4 + t] = acc;
+        acc += v2;
+        w32[(r + 2) * cols * 4 + t] = acc;
+        acc += v3;
+        w32[(r + 3) * cols * 4 + t] = acc;
+      }
+      for (; r < rows; ++r) {
+        acc += w32[r * cols * 4 + t];
+        w32[r * cols * 4 + t] = acc;
+      }
+    }
+    __syncthreads();
+    uint4* dst = T + base;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = s_slab[i];
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
@@ -696,7 +795,52 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
         }
       }
     }
+    // 1) cell indices of the row's walk (arithmetic only)
+    int64_t cFt[M], cPt[M];
     int64_t cF = a.cellsF - 1, cP = a.cellsP - 1;
+#pragma unroll
+    for (int t = 0; t < M - 2; ++t) {
+      cFt[t] = cF;
+      cPt[t] = cP;
+      if (t <= K - 3) {
+        const int m = (mdl >> (4 * t)) & 15u;
+        const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
+        cF -= dk * a.strideF[m];
+        if (NVP > 0 && m < a.DP) cP -= dk * a.strideP[m];
+        cFt[t] = cF;
+        cPt[t] = cP;
+      }
+    }
+    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
+    const int64_t c_row = s_begin + row * gL - a.cfg_begin;
+    const int64_t sL = a.strideF[mL];
+    const uint4* rowF = a.F + (cF - (int64_t)gL * sL);  // cell of threshold index kl: rowF + kl*sL
+    const int64_t sPL = (NVP > 0 && mL < a.DP) ? a.strideP[mL] : 0;
+    const int64_t rowP = cP - (int64_t)gL * sPL;
+    // 2) issue every load of the row (broadcast row cells + the lane's first
+    //    U config cells) before consuming any of them
+    constexpr int U = 4;
+    uint4 rF[M], rP[M][NVPX];
+#pragma unroll
+    for (int t = 0; t < M - 2; ++t) {
+      rF[t] = t <= K - 3 ? __ldg(a.F + cFt[t]) : totF;
+#pragma unroll
+      for (int v = 0; v < NVPX; ++v)
+        rP[t][v] = (NVP > 0 && t <= K - 3 && (int)((mdl >> (4 * t)) & 15u) < a.DP)
+                       ? __ldg(a.P + cPt[t] * NVP + v) : make_uint4(0, 0, 0, 0);
+    }
+    uint4 wF[U];
+    uint4 wP[U][NVPX];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kl = lane + 32 * u;
+      wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int v = 0; v < NVPX; ++v)
+        wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
+                                      : make_uint4(0, 0, 0, 0);
+    }
+    // 3) the row-shared part of the walk
     uint4 vF = totF;
     uint4 vP[NVPX];
 #pragma unroll
@@ -709,13 +853,10 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       if (t <= K - 3) {
         const int m = (mdl >> (4 * t)) & 15u;
         const uint32_t A = chan<M>(vF, vP, m);
-        const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
-        cF -= dk * a.strideF[m];
-        vF = __ldg(a.F + cF);
+        vF = rF[t];
         if (NVP > 0 && m < a.DP) {
-          cP -= dk * a.strideP[m];
 #pragma unroll
-          for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
+          for (int v = 0; v < NVPX; ++v) vP[v] = rP[t][v];
         }
         cp += A - chan<M>(vF, vP, m);
         fr[t + 1] = ddiv((double)vF.x, n);
@@ -724,25 +865,18 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
     }
     const uint32_t a_last = chan<M>(vF, vP, mL);
     const double costK = __ldg(a.cost1 + mK);
-    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
-    const int64_t c_row = s_begin + row * gL - a.cfg_begin;
-    // cell of threshold index kl: rowF + kl * sL (kl = gL would be "any")
-    const int64_t sL = a.strideF[mL];
-    const uint4* rowF = a.F + (cF - (int64_t)gL * sL);
-    const int64_t sPL = (NVP > 0 && mL < a.DP) ? a.strideP[mL] : 0;
-    const int64_t rowP = cP - (int64_t)gL * sPL;
-    constexpr int U = 4;  // configs per lane per pass, loads issued together
+    // 4) the lane's configs; rows longer than 32*U configs take more passes
     for (int base = 0; base < gL; base += 32 * U) {
-      uint4 wF[U];
-      uint4 wP[U][NVPX];
+      if (base > 0) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int kl = base + lane + 32 * u;
-        wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < U; ++u) {
+          const int kl = base + lane + 32 * u;
+          wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int v = 0; v < NVPX; ++v)
-          wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
-                                        : make_uint4(0, 0, 0, 0);
+          for (int v = 0; v < NVPX; ++v)
+            wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
+                                          : make_uint4(0, 0, 0, 0);
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -869,7 +1003,21 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
 cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
                          cudaStream_t st, unsigned long long* H16 = nullptr,
                          const uint32_t* flag = nullptr, bool h_f32 = true) {
-  if (H16) {  // main table: packed first pass along the last dim (vec == 1)
+  int fused = 0;  // trailing dims already scanned by the first pass
+  if (H16 && ndim >= 2 &&
+      (size_t)dims[ndim - 1] * dims[ndim - 2] * sizeof(uint4) <= kSlabSmemMax) {
+    const int rows = (int)dims[ndim - 2], cols = (int)dims[ndim - 1];
+    const size_t smem = (size_t)rows * cols * sizeof(uint4);
+    static std::atomic<int> smem_set{0};
+    cudaError_t e = ensure_smem(slab_first_kernel, smem_set, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t n_slabs = cells / ((int64_t)rows * cols);
+    const int64_t blocks = std::min<int64_t>(n_slabs, (int64_t)sm_count() * 2);
+    slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols);
+    e = cudaGetLastError();
+    if (e != cudaSuccess || ndim == 2) return e;
+    fused = 2;
+  } else if (H16) {  // main table: packed first pass along the last dim (vec == 1)
     const int64_t len = ndim == 0 ? 1 : dims[ndim - 1];
     const int64_t rows = cells / len;
     int64_t blocks = (rows * 32 + 255) / 256;
@@ -877,17 +1025,16 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     rowscan_first_kernel<<<(unsigned)blocks, 256, 0, st>>>(H16, H, flag, T, rows, (int)len);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || ndim <= 1) return e;
+    fused = 1;
   } else if (ndim == 0) {  // a single cell: convert, copy and re-zero
     rowscan_kernel<<<1, 32, 0, st>>>(H, T, vec, 1, h_f32 ? 1 : 0);
     return cudaGetLastError();
   }
   int64_t inner = vec;
   uint4* src = H;
-  if (H16) {
-    src = T;
-    inner *= dims[ndim - 1];
-  }
-  for (int d = ndim - 1 - (H16 ? 1 : 0); d >= 0; --d) {
+  for (int q = 0; q < fused; ++q) inner *= dims[ndim - 1 - q];
+  if (fused) src = T;
+  for (int d = ndim - 1 - fused; d >= 0; --d) {
     const int64_t len = dims[d];
     const int64_t outer = cells * vec / (len * inner);
     const int from_f32 = (src == H && h_f32) ? 1 : 0;
