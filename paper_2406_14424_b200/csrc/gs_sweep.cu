@@ -795,52 +795,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
         }
       }
     }
-    // 1) cell indices of the row's walk (arithmetic only)
-    int64_t cFt[M], cPt[M];
     int64_t cF = a.cellsF - 1, cP = a.cellsP - 1;
-#pragma unroll
-    for (int t = 0; t < M - 2; ++t) {
-      cFt[t] = cF;
-      cPt[t] = cP;
-      if (t <= K - 3) {
-        const int m = (mdl >> (4 * t)) & 15u;
-        const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
-        cF -= dk * a.strideF[m];
-        if (NVP > 0 && m < a.DP) cP -= dk * a.strideP[m];
-        cFt[t] = cF;
-        cPt[t] = cP;
-      }
-    }
-    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
-    const int64_t c_row = s_begin + row * gL - a.cfg_begin;
-    const int64_t sL = a.strideF[mL];
-    const uint4* rowF = a.F + (cF - (int64_t)gL * sL);  // cell of threshold index kl: rowF + kl*sL
-    const int64_t sPL = (NVP > 0 && mL < a.DP) ? a.strideP[mL] : 0;
-    const int64_t rowP = cP - (int64_t)gL * sPL;
-    // 2) issue every load of the row (broadcast row cells + the lane's first
-    //    U config cells) before consuming any of them
-    constexpr int U = 4;
-    uint4 rF[M], rP[M][NVPX];
-#pragma unroll
-    for (int t = 0; t < M - 2; ++t) {
-      rF[t] = t <= K - 3 ? __ldg(a.F + cFt[t]) : totF;
-#pragma unroll
-      for (int v = 0; v < NVPX; ++v)
-        rP[t][v] = (NVP > 0 && t <= K - 3 && (int)((mdl >> (4 * t)) & 15u) < a.DP)
-                       ? __ldg(a.P + cPt[t] * NVP + v) : make_uint4(0, 0, 0, 0);
-    }
-    uint4 wF[U];
-    uint4 wP[U][NVPX];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kl = lane + 32 * u;
-      wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int v = 0; v < NVPX; ++v)
-        wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
-                                      : make_uint4(0, 0, 0, 0);
-    }
-    // 3) the row-shared part of the walk
     uint4 vF = totF;
     uint4 vP[NVPX];
 #pragma unroll
@@ -853,10 +808,13 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       if (t <= K - 3) {
         const int m = (mdl >> (4 * t)) & 15u;
         const uint32_t A = chan<M>(vF, vP, m);
-        vF = rF[t];
+        const int64_t dk = (int64_t)(a.glen[m] - kk[t]);
+        cF -= dk * a.strideF[m];
+        vF = __ldg(a.F + cF);
         if (NVP > 0 && m < a.DP) {
+          cP -= dk * a.strideP[m];
 #pragma unroll
-          for (int v = 0; v < NVPX; ++v) vP[v] = rP[t][v];
+          for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
         }
         cp += A - chan<M>(vF, vP, m);
         fr[t + 1] = ddiv((double)vF.x, n);
@@ -865,18 +823,25 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
     }
     const uint32_t a_last = chan<M>(vF, vP, mL);
     const double costK = __ldg(a.cost1 + mK);
-    // 4) the lane's configs; rows longer than 32*U configs take more passes
+    const bool needP = NVP > 0 && (mL < a.DP || mK < a.DP);
+    const int64_t c_row = s_begin + row * gL - a.cfg_begin;
+    // cell of threshold index kl: rowF + kl * sL (kl = gL would be "any")
+    const int64_t sL = a.strideF[mL];
+    const uint4* rowF = a.F + (cF - (int64_t)gL * sL);
+    const int64_t sPL = (NVP > 0 && mL < a.DP) ? a.strideP[mL] : 0;
+    const int64_t rowP = cP - (int64_t)gL * sPL;
+    constexpr int U = 4;  // configs per lane per pass, loads issued together
     for (int base = 0; base < gL; base += 32 * U) {
-      if (base > 0) {
+      uint4 wF[U];
+      uint4 wP[U][NVPX];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int kl = base + lane + 32 * u;
-          wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
+      for (int u = 0; u < U; ++u) {
+        const int kl = base + lane + 32 * u;
+        wF[u] = kl < gL ? __ldg(rowF + (int64_t)kl * sL) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int v = 0; v < NVPX; ++v)
-            wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
-                                          : make_uint4(0, 0, 0, 0);
-        }
+        for (int v = 0; v < NVPX; ++v)
+          wP[u][v] = (needP && kl < gL) ? __ldg(a.P + (rowP + (int64_t)kl * sPL) * NVP + v)
+                                        : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
