@@ -79,6 +79,15 @@ __device__ __forceinline__ void merge_top2(C& m1, C& m2, C o1, C o2) {
 __device__ __forceinline__ double exp_term(float d) { return (double)expf(d); }
 __device__ __forceinline__ double exp_term(double d) { return exp(d); }
 
+// streaming 16-byte load: read once, keep it out of L1
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 // 16-byte vector of T
 template <typename T>
 struct Vec16 {
@@ -124,6 +133,69 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
   if (n == 1) {
     const double x0 = (double)to_float(row[0]);
     return KIND == GS_CERT_MARGIN ? x0 : 1.0;
+  }
+  constexpr int V = Vec16<T>::N;
+  constexpr int RV = 8;  // 16-byte vectors per lane held in registers
+  if (vec_ok && n / V <= 32 * RV) {
+    // register-resident row: every 16-byte load of the row is issued up
+    // front (8 per lane, 4 KB per warp in flight) and the row is read from
+    // HBM exactly once, whatever the certainty kind
+    const int lane = (int)lane_id();
+    const int nv = n / V;
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    uint4 buf[RV];
+#pragma unroll
+    for (int u = 0; u < RV; ++u) {
+      const int i = lane + 32 * u;
+      buf[u] = i < nv ? ldg_stream(rv + i) : make_uint4(0, 0, 0, 0);
+    }
+    const int tail = n - nv * V;
+    const bool has_tail = lane < tail;
+    const T tx = has_tail ? row[nv * V + lane] : row[0];
+    auto each = [&](auto&& f) {
+#pragma unroll
+      for (int u = 0; u < RV; ++u) {
+        if (lane + 32 * u < nv) {
+          const T* t = reinterpret_cast<const T*>(&buf[u]);
+#pragma unroll
+          for (int q = 0; q < V; ++q) f(t[q]);
+        }
+      }
+      if (has_tail) f(tx);
+    };
+    if (KIND == GS_CERT_MARGIN) {
+      C m1 = neg_inf<C>(), m2 = neg_inf<C>();
+      each([&](T x) { push_top2<C>((C)to_float(x), m1, m2); });
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const C o1 = __shfl_xor_sync(0xffffffffu, m1, o);
+        const C o2 = __shfl_xor_sync(0xffffffffu, m2, o);
+        merge_top2<C>(m1, m2, o1, o2);
+      }
+      return (double)m1 - (double)m2;
+    }
+    C m = neg_inf<C>();
+    each([&](T x) {
+      const C v = (C)to_float(x);
+      m = v > m ? v : m;
+    });
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const C y = __shfl_xor_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
+    }
+    double s = 0.0, t = 0.0;
+    each([&](T x) {
+      const C d = (C)to_float(x) - m;
+      const double e = exp_term(d);
+      s += e;
+      if (KIND == GS_CERT_ENTROPY) t += e * (double)d;
+    });
+    s = warp_sum(s);
+    if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / s;
+    t = warp_sum(t);
+    const double H = log(s) - t / s;
+    return 1.0 - H / log((double)n);
   }
   if (KIND == GS_CERT_MARGIN) {
     C m1 = neg_inf<C>(), m2 = neg_inf<C>();

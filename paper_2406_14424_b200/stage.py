@@ -36,6 +36,7 @@ class StageStepResult:
     deferred_idx: torch.Tensor    # i64 [n_deferred], batch order
     near_idx: torch.Tensor        # i64 [n_near], ascending
     next_payload: torch.Tensor | None  # [n_deferred, ...] gathered payload rows
+    counts: torch.Tensor | None = None  # device i64 [2]: n_deferred, n_near
 
 
 def _thr_tensor(thr, n: int, dev) -> torch.Tensor:
@@ -49,10 +50,13 @@ def _thr_tensor(thr, n: int, dev) -> torch.Tensor:
 
 def stage_step(scores: torch.Tensor, thr, is_last=None, *, kind: str = "margin",
                payload: torch.Tensor | None = None, near_eps: float = NEAR_EPS,
-               list_near: bool = True) -> StageStepResult:
+               list_near: bool = True, sync: bool = True) -> StageStepResult:
     """Gate one stage's batch.  scores: CUDA [n, n_cls] f32/f64/bf16 (row
     stride may exceed n_cls); thr: scalar or [n] f64; is_last: None or [n]
-    bool/u8; payload: optional CUDA tensor with leading dim n."""
+    bool/u8; payload: optional CUDA tensor with leading dim n.  With
+    sync=False nothing is read back: deferred_idx / near_idx are returned at
+    full capacity and `counts` (device i64 [2]: n_deferred, n_near) says how
+    much of each is valid."""
     if kind not in _lib.CERT_KINDS:
         raise ValueError(f"unknown certainty kind {kind!r}")
     dev = _lib.device()
@@ -96,10 +100,14 @@ def stage_step(scores: torch.Tensor, thr, is_last=None, *, kind: str = "margin",
         _lib.ptr(payload), row_bytes, _lib.ptr(nxt), ws.data_ptr(), ws.numel(),
         _lib.stream_ptr())
     _lib.check(rc, "stage_step")
+    if not sync:
+        return StageStepResult(cert=cert, stop=stop, deferred_idx=deferred,
+                               near_idx=near if list_near else deferred[:0],
+                               next_payload=nxt, counts=counts)
     nd, nn = (int(x) for x in counts.tolist())
     return StageStepResult(cert=cert, stop=stop, deferred_idx=deferred[:nd],
                            near_idx=near[:nn] if list_near else deferred[:0],
-                           next_payload=None if nxt is None else nxt[:nd])
+                           next_payload=None if nxt is None else nxt[:nd], counts=counts)
 
 
 @dataclass
