@@ -8,7 +8,8 @@
  *
  * oracle_evaluate_encoded restates _evaluate_numba
  *   /root/reference/pkg/src/gearserve/kernels.py:39-62
- * line for line: visits counted in f64 (+= 1.0, :52), stop test
+ * step for step: visits counted (the reference's f64 `+= 1.0`, :52, holds
+ * the same exact integers; counted here as int64), stop test
  * `s == ns-1 || certainty[r, m] >= thresholds[c, s]` (:53), correct added as
  * an integer (:54), epilogue frac = count / n_rec, mean_cost += frac *
  * cost1[m] in stage order, accuracy = n_correct / n_rec (:57-61).
@@ -22,6 +23,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdio.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -34,24 +36,30 @@ int oracle_max_threads(void) {
 #endif
 }
 
-static void eval_one(const double* cert, const uint8_t* corr, int64_t n_rec, int32_t M,
-                     const int32_t* sm, const double* thr, int32_t ns, int32_t L,
-                     const double* cost1, double* acc, double* cost, double* frac) {
+static void eval_one(const double* restrict cert, const uint8_t* restrict corr, int64_t n_rec,
+                     int32_t M, const int32_t* restrict sm, const double* restrict thr, int32_t ns,
+                     int32_t L, const double* restrict cost1, double* restrict acc,
+                     double* restrict cost, double* restrict frac) {
+  /* visits are counted as integers and converted once: the reference's
+     f64 `+= 1.0` holds the same exact integers (< 2^53) */
+  int64_t visits[64] = {0};
   int64_t n_correct = 0;
-  for (int32_t s = 0; s < L; ++s) frac[s] = 0.0;
   for (int64_t r = 0; r < n_rec; ++r) {
+    const double* row = cert + r * M;
+    const uint8_t* krow = corr + r * M;
     for (int32_t s = 0; s < ns; ++s) {
       const int32_t m = sm[s];
-      frac[s] += 1.0;
-      if (s == ns - 1 || cert[r * M + m] >= thr[s]) {
-        n_correct += corr[r * M + m];
+      visits[s] += 1;
+      if (s == ns - 1 || row[m] >= thr[s]) {
+        n_correct += krow[m];
         break;
       }
     }
   }
+  for (int32_t s = 0; s < L; ++s) frac[s] = 0.0;
   double mean = 0.0;
   for (int32_t s = 0; s < ns; ++s) {
-    const double f = frac[s] / (double)n_rec;
+    const double f = (double)visits[s] / (double)n_rec;
     frac[s] = f;
     mean += f * cost1[sm[s]];
   }
