@@ -49,6 +49,19 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// x / n for integer counts 0 <= x <= n < 2^26, correctly rounded, in three
+// FP64 ops instead of a full division: with rcp = RN(1/n) (IEEE division on
+// the host), q0 = RN(x * rcp) is within one ulp of x/n, the remainder
+// x - q0*n is exact in one FMA, and one FMA correction yields the correctly
+// rounded quotient (Markstein's theorem).  Counts never produce the
+// subnormal/overflow cases a general division has to check for.
+// tests/test_gpu_grid.py checks it exhaustively against __ddiv_rn.
+__device__ __forceinline__ double div_count(double x, double n, double rcp) {
+  const double q0 = __dmul_rn(x, rcp);
+  const double e = __fma_rn(-q0, n, x);
+  return __fma_rn(e, rcp, q0);
+}
+
 // ------------------------------------------------------- TMA bulk (1-D) --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

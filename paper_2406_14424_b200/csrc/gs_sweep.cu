@@ -677,6 +677,7 @@ struct EvalGridArgs {
   int64_t strideF[kMaxM];
   int64_t strideP[kMaxM];
   int64_t n_rec, cellsF, cellsP;
+  double rcp_n;  // RN(1 / n_rec), computed on the host
   int64_t cfg_begin, cfg_count;
   int64_t row_lo, row_hi;
   int64_t struct_begin[256 + 1];
@@ -705,7 +706,7 @@ __device__ __forceinline__ uint32_t chan(const uint4& vF, const uint4* vP, int m
 template <int M>
 __device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, const double* fr,
                                              int K, double frK, double mean, uint32_t correct,
-                                             double n) {
+                                             double n, double rcp) {
   if (a.frac) {
     double o[M];
 #pragma unroll
@@ -720,7 +721,7 @@ __device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, c
     }
   }
   if (a.cost) a.cost[i] = mean;
-  if (a.acc) a.acc[i] = ddiv((double)correct, n);
+  if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
   if (a.n_correct) a.n_correct[i] = correct;
 }
 
@@ -730,7 +731,8 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
   constexpr int NVPX = NVP > 0 ? NVP : 1;
   const int lane = (int)lane_id();
   const double n = (double)a.n_rec;
-  const double one = ddiv(n, n);  // first-stage fraction, as the reference computes it
+  const double rcp = a.rcp_n;
+  const double one = div_count(n, n, rcp);  // first-stage fraction: n / n
   const uint4 totF = __ldg(a.F + a.cellsF - 1);
   uint4 totP[NVPX];
 #pragma unroll
@@ -771,7 +773,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       const int64_t i = s_begin - a.cfg_begin;
       if (lane == 0 && i >= 0 && i < a.cfg_count) {
         const double mean = dadd(0.0, dmul(one, __ldg(a.cost1 + mK)));
-        store_config<M>(a, i, fr, 1, one, mean, chan<M>(totF, totP, mK), n);
+        store_config<M>(a, i, fr, 1, one, mean, chan<M>(totF, totP, mK), n, rcp);
       }
       continue;
     }
@@ -817,7 +819,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
           for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
         }
         cp += A - chan<M>(vF, vP, m);
-        fr[t + 1] = ddiv((double)vF.x, n);
+        fr[t + 1] = div_count((double)vF.x, n, rcp);
         mp = dadd(mp, dmul(fr[t + 1], __ldg(a.cost1 + ((mdl >> (4 * (t + 1))) & 15u))));
       }
     }
@@ -850,9 +852,9 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
         if (kl >= gL || i < 0 || i >= a.cfg_count) continue;
         const uint32_t correct =
             cp + a_last - chan<M>(wF[u], wP[u], mL) + chan<M>(wF[u], wP[u], mK);
-        const double frK = ddiv((double)wF[u].x, n);
+        const double frK = div_count((double)wF[u].x, n, rcp);
         const double mean = dadd(mp, dmul(frK, costK));
-        store_config<M>(a, i, fr, K, frK, mean, correct, n);
+        store_config<M>(a, i, fr, K, frK, mean, correct, n, rcp);
       }
     }
   }
@@ -1138,6 +1140,7 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
   for (int j = 0; j < p.D; ++j) a.strideF[j] = p.strideF[j];
   for (int j = 0; j < p.DP; ++j) a.strideP[j] = p.strideP[j];
   a.n_rec = n_rec;
+  a.rcp_n = 1.0 / (double)n_rec;
   a.cellsF = p.cellsF;
   a.cellsP = p.cellsP;
   a.cfg_begin = config_begin;

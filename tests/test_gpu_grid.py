@@ -103,6 +103,26 @@ def test_heavy_tie_cell_overflow_fallback(n_models):
     assert np.array_equal(res.accuracy.cpu().numpy(), want[0])
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 100, 997, 4096, 65535])
+def test_count_division_exhaustive(n):
+    """Every forward count 0..n and many correct counts appear once as a
+    config output: the kernel's FMA-corrected division must equal IEEE x/n
+    for all of them (the oracle divides with C `/`)."""
+    rng = np.random.default_rng(n)
+    vals = np.arange(1, n + 1) / n
+    cert = np.stack([rng.permutation(vals), rng.random(n)], axis=1)
+    corr = (rng.random((n, 2)) < 0.5).astype(np.uint8)
+    grids = [np.sort(vals), np.array([0.0])]
+    cost1 = np.array([3.0, 7.0])
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, cost1)
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1)
+    assert np.array_equal(frac, want[2]) and np.array_equal(acc, want[0])
+    assert np.array_equal(cost, want[1])
+    reach = np.rint(frac[:, 1] * n).astype(np.int64)
+    assert set(range(n)) <= set(reach.tolist()) | {0}
+
+
 def test_negative_singleton_certainty_bins_below_zero():
     """Singleton scores can be negative (cascades.certainty returns the score):
     such records sit below grid value 0 and forward at every threshold."""
