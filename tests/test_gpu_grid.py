@@ -103,7 +103,7 @@ def test_heavy_tie_cell_overflow_fallback(n_models):
     assert np.array_equal(res.accuracy.cpu().numpy(), want[0])
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 7, 100, 997, 4096, 65535])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 100, 997, 4096, 16000])
 def test_count_division_exhaustive(n):
     """Every forward count 0..n and many correct counts appear once as a
     config output: the kernel's FMA-corrected division must equal IEEE x/n
