@@ -71,6 +71,8 @@ struct Plan {
   int64_t struct_begin[256 + 1] = {};
   uint32_t struct_mask[256] = {};
   size_t offH16 = 0, offHF = 0, offF = 0, offHP = 0, offP = 0, offFlag = 0, bytes = 0;
+  bool walk = false;  // M == 4: fused b_0 prefix + full-structure scoring
+  size_t offFaces = 0;
 };
 
 int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
@@ -144,6 +146,13 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->offP = b16 + 2 * bF + bP;
   p->offFlag = b16 + 2 * bF + 2 * bP;
   p->bytes = p->offFlag + 256;
+  p->walk = M == 4 && p->dims[0] <= 160 &&
+            (size_t)p->dims[1] * p->dims[2] * 16 <= 200 * 1024 &&
+            (size_t)p->dims[0] * 72 * 16 <= 184 * 1024;
+  if (p->walk) {
+    p->offFaces = p->bytes;
+    p->bytes += bF;
+  }
   return GS_OK;
 }
 
@@ -860,6 +869,136 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
   }
 }
 
+// -------------------------------------------------------- fused walk (M=4) --
+// For four models the dominant structure is the full cascade (0,1,2,3): its
+// g0*g1*g2 configs are 96% of the enumeration and map one-to-one onto table
+// cells (k0, k1, k2).  walk_eval fuses the last prefix pass (along b_0) with
+// their scoring: a CTA owns a tile of kWalkTile consecutive cells of the
+// (b_1, b_2) plane, stages that tile for every k0 with 1-D TMA bulk copies
+// (one mbarrier), scans it along k0 in shared memory (threads = cell x step
+// group, two-level), and for each (k0, cell) writes the config's outputs
+// directly.  The row-shared cells the walk needs, (k0, k1, g2) and
+// (k0, g1, g2), are three extra running columns per CTA.  Only the "face"
+// cells (some index at its maximum) are written back: they are all the
+// smaller structures read, which the regular eval then scores.
+constexpr int kWalkTile = 72;   // max cells per tile (<= d2, so a tile spans <= 2 rows)
+constexpr int kWalkGroups = 7;  // step groups: 72 x 7 = 504 threads
+constexpr int kWalkMaxSteps = 160;
+
+struct WalkArgs {
+  int32_t d0, d1, d2;
+  int32_t tile;  // cells per CTA (<= kWalkTile and <= d2)
+  int64_t sb;    // first config of the full structure
+  int64_t cfg_begin, cfg_count;
+  int64_t n_rec;
+  double rcp_n;
+  const double* cost1;
+  const uint4* S;      // slab-prefixed table [d0][d1 * d2]
+  uint4* faces;        // full prefix, face cells only
+  const uint4* Pside;  // finished side table [d0] (c_0 in .x)
+  double* acc;
+  double* cost;
+  double* frac;
+  uint32_t* n_correct;
+};
+
+__global__ void __launch_bounds__(512) walk_eval_kernel(const __grid_constant__ WalkArgs a) {
+  extern __shared__ __align__(16) uint4 s_tile[];  // [d0][tile]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint4 s_grp[kWalkGroups][kWalkTile];
+  __shared__ uint4 s_ext[3][kWalkMaxSteps];  // running (k0, ra, g2), (k0, rb, g2), (k0, g1, g2)
+  __shared__ uint32_t s_side[kWalkMaxSteps];
+  const int d0 = a.d0, d1 = a.d1, d2 = a.d2;
+  const int g0 = d0 - 1, g1 = d1 - 1, g2 = d2 - 1;
+  const int plane = d1 * d2;
+  const int T = a.tile;
+  const int c0 = blockIdx.x * T;
+  const int w = min(T, plane - c0);
+  const int ra = c0 / d2, rb = (c0 + w - 1) / d2;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)(d0 * w * sizeof(uint4)));
+    for (int k0 = 0; k0 < d0; ++k0)
+      bulk_g2s(s_tile + k0 * T, a.S + (int64_t)k0 * plane + c0, (uint32_t)(w * sizeof(uint4)), &bar);
+  }
+  for (int i = tid; i < 3 * d0; i += blockDim.x) {
+    const int col = i / d0, k0 = i - col * d0;
+    const int row = col == 0 ? ra : (col == 1 ? rb : g1);
+    s_ext[col][k0] = a.S[(int64_t)k0 * plane + row * d2 + g2];
+  }
+  for (int k0 = tid; k0 < d0; k0 += blockDim.x) s_side[k0] = a.Pside[k0].x;
+  __syncthreads();
+  // prefix of the three extra columns along k0 (one warp per column)
+  for (int col = tid >> 5; col < 3; col += blockDim.x >> 5) {
+    const int lane = tid & 31;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (int base = 0; base < d0; base += 32) {
+      const int k0 = base + lane;
+      uint4 v = k0 < d0 ? s_ext[col][k0] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint4 y = shfl_up4(v, o);
+        if (lane >= o) v = add4(v, y);
+      }
+      v = add4(v, carry);
+      if (k0 < d0) s_ext[col][k0] = v;
+      carry = shfl4(v, 31);
+    }
+  }
+  mbar_wait(&bar, 0);
+  // two-level scan of the tile along k0: thread = (cell ci, step group q)
+  const int ci = tid % T, q = tid / T;  // threads past T * kWalkGroups only pad the warp
+  const int L = (d0 + kWalkGroups - 1) / kWalkGroups;
+  const int s0 = q * L, s1 = min(d0, s0 + L);
+  uint4 run = make_uint4(0, 0, 0, 0);
+  if (ci < w && q < kWalkGroups)
+    for (int k0 = s0; k0 < s1; ++k0) run = add4(run, s_tile[k0 * T + ci]);
+  if (q < kWalkGroups) s_grp[q][ci] = run;
+  __syncthreads();
+  if (ci >= w || q >= kWalkGroups) return;
+  uint4 P = make_uint4(0, 0, 0, 0);
+  for (int qq = 0; qq < q; ++qq) P = add4(P, s_grp[qq][ci]);
+  const int cell = c0 + ci;
+  const int k1 = cell / d2, k2 = cell - k1 * d2;
+  const int xcol = k1 == ra ? 0 : 1;
+  const double n = (double)a.n_rec, rcp = a.rcp_n;
+  const double one = div_count(n, n, rcp);
+  const double cA = __ldg(a.cost1 + 0), cB = __ldg(a.cost1 + 1), cC = __ldg(a.cost1 + 2),
+               cD = __ldg(a.cost1 + 3);
+  const double m0 = dadd(0.0, dmul(one, cA));
+  const uint32_t side_tot = s_side[g0];
+  const bool face_cell = k1 == g1 || k2 == g2;
+  const bool cfg_cell = k1 < g1 && k2 < g2;
+  for (int k0 = s0; k0 < s1; ++k0) {
+    P = add4(P, s_tile[k0 * T + ci]);  // full prefix P[k0][k1][k2]
+    if (face_cell || k0 == g0) a.faces[(int64_t)k0 * plane + cell] = P;
+    if (!cfg_cell || k0 == g0) continue;
+    const int64_t i = a.sb + ((int64_t)k0 * g1 + k1) * g2 + k2 - a.cfg_begin;
+    if (i < 0 || i >= a.cfg_count) continue;
+    const uint4 X0 = s_ext[2][k0];     // (k0, g1, g2): after stage 0
+    const uint4 X1 = s_ext[xcol][k0];  // (k0, k1, g2): after stage 1
+    // channels {cnt, c3, c2, c1}; c0 from the side table
+    const uint32_t correct = (side_tot - s_side[k0]) + (X0.w - X1.w) + (X1.z - P.z) + P.y;
+    const double f1 = div_count((double)X0.x, n, rcp);
+    const double f2 = div_count((double)X1.x, n, rcp);
+    const double f3 = div_count((double)P.x, n, rcp);
+    const double mean = dadd(dadd(dadd(m0, dmul(f1, cB)), dmul(f2, cC)), dmul(f3, cD));
+    if (a.frac) {
+      double2* row = reinterpret_cast<double2*>(a.frac + i * 4);
+      row[0] = make_double2(one, f1);
+      row[1] = make_double2(f2, f3);
+    }
+    if (a.cost) a.cost[i] = mean;
+    if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+    if (a.n_correct) a.n_correct[i] = correct;
+  }
+}
+
 // ---------------------------------------------------------------- decode --
 struct DecodeArgs {
   int32_t M, n_struct;
@@ -969,7 +1108,7 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
 // re-zeroes it) and writes T; later passes run in place on T.
 cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
                          cudaStream_t st, unsigned long long* H16 = nullptr,
-                         const uint32_t* flag = nullptr, bool h_f32 = true) {
+                         const uint32_t* flag = nullptr, bool h_f32 = true, int skip_leading = 0) {
   int fused = 0;  // trailing dims already scanned by the first pass
   if (H16 && ndim >= 2 &&
       (size_t)dims[ndim - 1] * dims[ndim - 2] * sizeof(uint4) <= kSlabSmemMax) {
@@ -982,7 +1121,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     const int64_t blocks = std::min<int64_t>(n_slabs, (int64_t)sm_count() * 2);
     slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols);
     e = cudaGetLastError();
-    if (e != cudaSuccess || ndim == 2) return e;
+    if (e != cudaSuccess || ndim - skip_leading == 2) return e;
     fused = 2;
   } else if (H16) {  // main table: packed first pass along the last dim (vec == 1)
     const int64_t len = ndim == 0 ? 1 : dims[ndim - 1];
@@ -1001,7 +1140,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
   uint4* src = H;
   for (int q = 0; q < fused; ++q) inner *= dims[ndim - 1 - q];
   if (fused) src = T;
-  for (int d = ndim - 1 - fused; d >= 0; --d) {
+  for (int d = ndim - 1 - fused; d >= skip_leading; --d) {
     const int64_t len = dims[d];
     const int64_t outer = cells * vec / (len * inner);
     const int from_f32 = (src == H && h_f32) ? 1 : 0;
@@ -1107,8 +1246,9 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
     default: return GS_EUNSUPPORTED;
   }
   GS_CUDA_TRY(e);
+  // with the fused walk the b_0 prefix is taken inside gs_grid_eval
   GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(F), reinterpret_cast<uint4*>(ws + p.offF), p.D,
-                           p.dims, p.cellsF, 1, st, H16, flag));
+                           p.dims, p.cellsF, 1, st, H16, flag, true, p.walk ? 1 : 0));
   if (p.DP > 0)
     GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), reinterpret_cast<uint4*>(ws + p.offP), p.DP,
                              p.dims, p.cellsP, p.NVP, st, nullptr, nullptr, false));
@@ -1154,17 +1294,48 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
     rows += (p.struct_begin[s + 1] - p.struct_begin[s]) / row_len(p, s);
   }
   a.row_begin[p.n_struct] = rows;
-  a.row_lo = global_row(p, a.row_begin, config_begin);
-  a.row_hi = global_row(p, a.row_begin, config_begin + config_count - 1) + 1;
   const uint8_t* ws = static_cast<const uint8_t*>(workspace);
-  a.F = reinterpret_cast<const uint4*>(ws + p.offF);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t reg_end = config_begin + config_count;  // regular eval covers [config_begin, reg_end)
+  if (p.walk) {
+    WalkArgs w{};
+    w.d0 = (int32_t)p.dims[0];
+    w.d1 = (int32_t)p.dims[1];
+    w.d2 = (int32_t)p.dims[2];
+    w.sb = p.struct_begin[p.n_struct - 1];
+    w.cfg_begin = config_begin;
+    w.cfg_count = config_count;
+    w.n_rec = n_rec;
+    w.rcp_n = 1.0 / (double)n_rec;
+    w.cost1 = cost1;
+    w.S = reinterpret_cast<const uint4*>(ws + p.offF);
+    w.faces = reinterpret_cast<uint4*>(const_cast<uint8_t*>(ws) + p.offFaces);
+    w.Pside = reinterpret_cast<const uint4*>(ws + p.offP);
+    w.acc = accuracy;
+    w.cost = mean_cost;
+    w.frac = forward_frac;
+    w.n_correct = n_correct;
+    w.tile = std::min(kWalkTile, w.d2);
+    const size_t smem = (size_t)w.d0 * w.tile * sizeof(uint4);
+    static std::atomic<int> smem_set{0};
+    GS_CUDA_TRY(ensure_smem(walk_eval_kernel, smem_set, (size_t)kWalkMaxSteps * kWalkTile * sizeof(uint4)));
+    const int plane = w.d1 * w.d2;
+    const int threads = (w.tile * kWalkGroups + 31) / 32 * 32;
+    walk_eval_kernel<<<(plane + w.tile - 1) / w.tile, threads, smem, st>>>(w);
+    GS_LAUNCH_CHECK();
+    reg_end = std::min<int64_t>(reg_end, w.sb);
+    if (reg_end <= config_begin) return GS_OK;
+  }
+  a.cfg_count = reg_end - config_begin;
+  a.row_lo = global_row(p, a.row_begin, config_begin);
+  a.row_hi = global_row(p, a.row_begin, reg_end - 1) + 1;
+  a.F = reinterpret_cast<const uint4*>(ws + (p.walk ? p.offFaces : p.offF));
   a.P = reinterpret_cast<const uint4*>(ws + p.offP);
   a.cost1 = cost1;
   a.acc = accuracy;
   a.cost = mean_cost;
   a.frac = forward_frac;
   a.n_correct = n_correct;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   switch (n_models) {
     case 1: e = launch_grid_eval<1>(a, st); break;
