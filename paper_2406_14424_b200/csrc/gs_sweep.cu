@@ -498,15 +498,79 @@ __global__ void __launch_bounds__(256) rowscan_first_kernel(unsigned long long* 
 // stores the slab once — one global read and one write for two dimensions.
 __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H16, uint4* HF,
                                                           const uint32_t* flag, uint4* T,
-                                                          int64_t n_slabs, int rows, int cols) {
+                                                          int64_t n_slabs, int rows, int cols,
+                                                          uint4* sideH, uint4* sideT, int side_len) {
   extern __shared__ __align__(16) uint4 s_slab[];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const bool fb = *flag != 0u;
   const int n = rows * cols;
+  if (blockIdx.x == 0 && warp == nwarps - 1 && side_len > 0) {
+    // a one-dimensional side table (4-model sweeps): scan it here too
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (int b = 0; b < side_len; b += 32) {
+      const int c = b + lane;
+      uint4 v = c < side_len ? sideH[c] : make_uint4(0, 0, 0, 0);
+      if (c < side_len) sideH[c] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint4 y = shfl_up4(v, o);
+        if (lane >= o) v = add4(v, y);
+      }
+      v = add4(v, carry);
+      if (c < side_len) sideT[c] = v;
+      carry = shfl4(v, 31);
+    }
+  }
+  // fast path: every row load of a warp issued before any is consumed
+  const bool pre = !fb && cols <= 128 && rows <= 4 * nwarps;
   for (int64_t slab = blockIdx.x; slab < n_slabs; slab += gridDim.x) {
     const int64_t base = slab * (int64_t)n;
-    for (int r = warp; r < rows; r += nwarps) {
+    if (pre) {
+      unsigned long long pv[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = warp + i * nwarps;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = lane * 4 + u;
+          pv[i][u] = (r < rows && c < cols) ? H16[base + (int64_t)r * cols + c] : 0ull;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = warp + i * nwarps;
+        if (r >= rows) break;  // uniform across the warp
+        uint4 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = lane * 4 + u;
+          const unsigned long long w = pv[i][u];
+          e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
+                            (uint32_t)((w >> 32) & 0xffff), (uint32_t)(w >> 48));
+          if (c < cols) H16[base + (int64_t)r * cols + c] = 0ull;
+        }
+        uint4 tot = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          tot = add4(tot, e[u]);
+          e[u] = tot;
+        }
+        uint4 incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint4 y = shfl_up4(incl, o);
+          if (lane >= o) incl = add4(incl, y);
+        }
+        const uint4 excl = make_uint4(incl.x - tot.x, incl.y - tot.y, incl.z - tot.z, incl.w - tot.w);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = lane * 4 + u;
+          if (c < cols) s_slab[r * cols + c] = add4(e[u], excl);
+        }
+      }
+    }
+    for (int r = pre ? rows : warp; r < rows; r += nwarps) {
       unsigned long long* in16 = H16 + base + (int64_t)r * cols;
       uint4* inF = HF + base + (int64_t)r * cols;
       uint4* out = s_slab + r * cols;
@@ -1078,6 +1142,7 @@ cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStr
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  if (n_rec < 65536) return cudaSuccess;  // no cell can reach 2^16 records
   auto k = grid_hist_kernel<M, Cell, 1>;  // no-op unless a cell passed 0xFFFF records
   static std::atomic<int> smem_set{0};
   cudaError_t e = ensure_smem(k, smem_set, smem);
@@ -1108,7 +1173,8 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
 // re-zeroes it) and writes T; later passes run in place on T.
 cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
                          cudaStream_t st, unsigned long long* H16 = nullptr,
-                         const uint32_t* flag = nullptr, bool h_f32 = true, int skip_leading = 0) {
+                         const uint32_t* flag = nullptr, bool h_f32 = true, int skip_leading = 0,
+                         uint4* sideH = nullptr, uint4* sideT = nullptr, int side_len = 0) {
   int fused = 0;  // trailing dims already scanned by the first pass
   if (H16 && ndim >= 2 &&
       (size_t)dims[ndim - 1] * dims[ndim - 2] * sizeof(uint4) <= kSlabSmemMax) {
@@ -1119,7 +1185,8 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     if (e != cudaSuccess) return e;
     const int64_t n_slabs = cells / ((int64_t)rows * cols);
     const int64_t blocks = std::min<int64_t>(n_slabs, (int64_t)sm_count() * 2);
-    slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols);
+    slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols,
+                                                            sideH, sideT, side_len);
     e = cudaGetLastError();
     if (e != cudaSuccess || ndim - skip_leading == 2) return e;
     fused = 2;
@@ -1247,9 +1314,15 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   }
   GS_CUDA_TRY(e);
   // with the fused walk the b_0 prefix is taken inside gs_grid_eval
+  // a 1-D side table (4 models) is scanned inside the slab pass
+  const bool fold_side = p.DP == 1 && p.NVP == 1 && p.D >= 2 &&
+                         (size_t)p.dims[p.D - 1] * p.dims[p.D - 2] * sizeof(uint4) <= kSlabSmemMax;
   GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(F), reinterpret_cast<uint4*>(ws + p.offF), p.D,
-                           p.dims, p.cellsF, 1, st, H16, flag, true, p.walk ? 1 : 0));
-  if (p.DP > 0)
+                           p.dims, p.cellsF, 1, st, H16, flag, true, p.walk ? 1 : 0,
+                           fold_side ? reinterpret_cast<uint4*>(P) : nullptr,
+                           fold_side ? reinterpret_cast<uint4*>(ws + p.offP) : nullptr,
+                           fold_side ? (int)p.cellsP : 0));
+  if (p.DP > 0 && !fold_side)
     GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), reinterpret_cast<uint4*>(ws + p.offP), p.DP,
                              p.dims, p.cellsP, p.NVP, st, nullptr, nullptr, false));
   return GS_OK;
