@@ -148,7 +148,7 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->bytes = p->offFlag + 256;
   p->walk = M == 4 && p->dims[0] <= 160 &&
             (size_t)p->dims[1] * p->dims[2] * 16 <= 200 * 1024 &&
-            (size_t)p->dims[0] * 72 * 16 <= 184 * 1024;
+            (size_t)p->dims[0] * 36 * 16 <= 92 * 1024;
   if (p->walk) {
     p->offFaces = p->bytes;
     p->bytes += bF;
@@ -499,7 +499,11 @@ __global__ void __launch_bounds__(256) rowscan_first_kernel(unsigned long long* 
 __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H16, uint4* HF,
                                                           const uint32_t* flag, uint4* T,
                                                           int64_t n_slabs, int rows, int cols,
-                                                          uint4* sideH, uint4* sideT, int side_len) {
+                                                          uint4* sideH, uint4* sideT, int side_len,
+                                                          int parts) {
+  // a slab may be split into `parts` column ranges, one CTA each: every CTA
+  // reads whole rows (for the row prefix) but keeps, scans and stores only
+  // its own columns, so twice the CTAs share the work
   extern __shared__ __align__(16) uint4 s_slab[];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -524,7 +528,11 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
   }
   // fast path: every row load of a warp issued before any is consumed
   const bool pre = !fb && cols <= 128 && rows <= 4 * nwarps;
-  for (int64_t slab = blockIdx.x; slab < n_slabs; slab += gridDim.x) {
+  const int hc = (cols + parts - 1) / parts;
+  for (int64_t item = blockIdx.x; item < n_slabs * parts; item += gridDim.x) {
+    const int64_t slab = item / parts;
+    const int cb = (int)(item - slab * parts) * hc;
+    const int ce = min(cols, cb + hc), wc = ce - cb;
     const int64_t base = slab * (int64_t)n;
     if (pre) {
       unsigned long long pv[4][4];
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
           const unsigned long long w = pv[i][u];
           e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
                             (uint32_t)((w >> 32) & 0xffff), (uint32_t)(w >> 48));
-          if (c < cols) H16[base + (int64_t)r * cols + c] = 0ull;
+          if (c >= cb && c < ce) H16[base + (int64_t)r * cols + c] = 0ull;
         }
         uint4 tot = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -566,14 +574,14 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = lane * 4 + u;
-          if (c < cols) s_slab[r * cols + c] = add4(e[u], excl);
+          if (c >= cb && c < ce) s_slab[r * wc + (c - cb)] = add4(e[u], excl);
         }
       }
     }
     for (int r = pre ? rows : warp; r < rows; r += nwarps) {
       unsigned long long* in16 = H16 + base + (int64_t)r * cols;
       uint4* inF = HF + base + (int64_t)r * cols;
-      uint4* out = s_slab + r * cols;
+      uint4* out = s_slab + r * wc - cb;
       uint4 carry = make_uint4(0, 0, 0, 0);
       for (int c0 = 0; c0 < cols; c0 += 128) {
         uint4 e[4];
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + lane * 4 + u;
-          if (c < cols) {
+          if (c >= cb && c < ce) {
             in16[c] = 0ull;
             if (fb) inF[c] = make_uint4(0, 0, 0, 0);
           }
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + lane * 4 + u;
-          if (c < cols) out[c] = add4(e[u], excl);
+          if (c >= cb && c < ce) out[c] = add4(e[u], excl);
         }
         carry = add4(carry, shfl4(incl, 31));
       }
@@ -626,29 +634,33 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
     // columns: thread (cell, lane) walks the rows; consecutive threads touch
     // consecutive 32-bit words, so the walk is bank-conflict free
     uint32_t* w32 = reinterpret_cast<uint32_t*>(s_slab);
-    for (int t = threadIdx.x; t < 4 * cols; t += blockDim.x) {
+    const int rw = wc * 4;  // 32-bit words per smem row
+    for (int t = threadIdx.x; t < rw; t += blockDim.x) {
       uint32_t acc = 0;
       int r = 0;
       for (; r + 4 <= rows; r += 4) {
-        const uint32_t v0 = w32[(r + 0) * cols * 4 + t], v1 = w32[(r + 1) * cols * 4 + t];
-        const uint32_t v2 = w32[(r + 2) * cols * 4 + t], v3 = w32[(r + 3) * cols * 4 + t];
+        const uint32_t v0 = w32[(r + 0) * rw + t], v1 = w32[(r + 1) * rw + t];
+        const uint32_t v2 = w32[(r + 2) * rw + t], v3 = w32[(r + 3) * rw + t];
         acc += v0;
-        w32[(r + 0) * cols * 4 + t] = acc;
+        w32[(r + 0) * rw + t] = acc;
         acc += v1;
-        w32[(r + 1) * cols * 4 + t] = acc;
+        w32[(r + 1) * rw + t] = acc;
         acc += v2;
-        w32[(r + 2) * cols * 4 + t] = acc;
+        w32[(r + 2) * rw + t] = acc;
         acc += v3;
-        w32[(r + 3) * cols * 4 + t] = acc;
+        w32[(r + 3) * rw + t] = acc;
       }
       for (; r < rows; ++r) {
-        acc += w32[r * cols * 4 + t];
-        w32[r * cols * 4 + t] = acc;
+        acc += w32[r * rw + t];
+        w32[r * rw + t] = acc;
       }
     }
     __syncthreads();
-    uint4* dst = T + base;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = s_slab[i];
+    uint4* dst = T + base + cb;
+    for (int i = threadIdx.x; i < rows * wc; i += blockDim.x) {
+      const int r = i / wc, j = i - r * wc;
+      dst[(int64_t)r * cols + j] = s_slab[i];
+    }
     __syncthreads();
   }
 }
@@ -945,8 +957,8 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
 // (k0, g1, g2), are three extra running columns per CTA.  Only the "face"
 // cells (some index at its maximum) are written back: they are all the
 // smaller structures read, which the regular eval then scores.
-constexpr int kWalkTile = 72;   // max cells per tile (<= d2, so a tile spans <= 2 rows)
-constexpr int kWalkGroups = 7;  // step groups: 72 x 7 = 504 threads
+constexpr int kWalkTile = 36;    // max cells per tile (<= d2, so a tile spans <= 2 rows)
+constexpr int kWalkGroups = 14;  // step groups: 36 x 14 = 504 threads
 constexpr int kWalkMaxSteps = 160;
 
 struct WalkArgs {
@@ -1179,14 +1191,16 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
   if (H16 && ndim >= 2 &&
       (size_t)dims[ndim - 1] * dims[ndim - 2] * sizeof(uint4) <= kSlabSmemMax) {
     const int rows = (int)dims[ndim - 2], cols = (int)dims[ndim - 1];
-    const size_t smem = (size_t)rows * cols * sizeof(uint4);
-    static std::atomic<int> smem_set{0};
-    cudaError_t e = ensure_smem(slab_first_kernel, smem_set, smem);
-    if (e != cudaSuccess) return e;
     const int64_t n_slabs = cells / ((int64_t)rows * cols);
-    const int64_t blocks = std::min<int64_t>(n_slabs, (int64_t)sm_count() * 2);
+    // split a slab across two CTAs when there are too few slabs to fill the GPU
+    const int parts = (cols >= 64 && n_slabs < 2 * sm_count()) ? 2 : 1;
+    const size_t smem = (size_t)rows * ((cols + parts - 1) / parts) * sizeof(uint4);
+    static std::atomic<int> smem_set{0};
+    cudaError_t e = ensure_smem(slab_first_kernel, smem_set, (size_t)kSlabSmemMax);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = std::min<int64_t>(n_slabs * parts, (int64_t)sm_count() * 4);
     slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols,
-                                                            sideH, sideT, side_len);
+                                                            sideH, sideT, side_len, parts);
     e = cudaGetLastError();
     if (e != cudaSuccess || ndim - skip_leading == 2) return e;
     fused = 2;
