@@ -296,8 +296,9 @@ def run_ours(args, world, rank, local):
                                   "frac": step_gbs / pk["hbm_gbs"]}},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
-            # per step: hist + one scan per main-table dim + one per side-table dim + eval
-            "gpu_launches": args.steps * (2 + (N_MODELS - 1) + max(0, N_MODELS - 3)),
+            # per step, as gs_grid_plan reports them (gs_grid_info)
+            "gpu_launches": args.steps * (sw.info.build_launches + sw.info.eval_launches),
+            "fast_path": bool(sw.info.fast_path),
             "parity_spot_check": check,
         }
         if stage is not None:

@@ -96,6 +96,10 @@ typedef struct gs_grid_info {
   int32_t n_structures;   /* 2^n_models - 1                              */
   int32_t max_len;        /* = n_models (forward_frac row width)         */
   size_t workspace_bytes; /* for gs_grid_build / eval                    */
+  int32_t build_launches; /* kernels one gs_grid_build enqueues           */
+  int32_t eval_launches;  /* kernels one full-range gs_grid_eval enqueues */
+  int32_t fast_path;      /* 1: four-model packed path (n_rec < 2^21)     */
+  int32_t reserved;
 } gs_grid_info;
 
 int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid_len,

@@ -39,7 +39,9 @@ DTYPES = {torch.float32: GS_F32, torch.float64: GS_F64, torch.bfloat16: GS_BF16}
 
 class gs_grid_info(ctypes.Structure):
     _fields_ = [("n_configs", c_int64), ("n_cells", c_int64), ("side_cells", c_int64),
-                ("n_structures", c_int32), ("max_len", c_int32), ("workspace_bytes", c_size_t)]
+                ("n_structures", c_int32), ("max_len", c_int32), ("workspace_bytes", c_size_t),
+                ("build_launches", c_int32), ("eval_launches", c_int32), ("fast_path", c_int32),
+                ("reserved", c_int32)]
 
 
 # symbol -> argtypes (all return c_int unless listed in _RESTYPES)

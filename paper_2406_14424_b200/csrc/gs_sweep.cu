@@ -50,6 +50,8 @@
 #include <atomic>
 
 #include "gs_common.cuh"
+#include "gs_grid4.cuh"
+#include "gs_grid_lut.cuh"
 
 namespace gs {
 namespace {
@@ -71,6 +73,7 @@ struct Plan {
   int64_t struct_begin[256 + 1] = {};
   uint32_t struct_mask[256] = {};
   size_t offH16 = 0, offHF = 0, offF = 0, offHP = 0, offP = 0, offFlag = 0, bytes = 0;
+  bool g4 = false;    // M == 4 fast path (gs_grid4.cu)
   bool walk = false;  // M == 4: fused b_0 prefix + full-structure scoring
   size_t offFaces = 0;
 };
@@ -146,6 +149,11 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->offP = b16 + 2 * bF + bP;
   p->offFlag = b16 + 2 * bF + 2 * bP;
   p->bytes = p->offFlag + 256;
+  p->g4 = grid4_supported(n_rec, M, p->glen);
+  if (p->g4) {
+    p->bytes = grid4_layout(p->glen).bytes;
+    return GS_OK;
+  }
   p->walk = M == 4 && p->dims[0] <= 160 &&
             (size_t)p->dims[1] * p->dims[2] * 16 <= 200 * 1024 &&
             (size_t)p->dims[0] * 36 * 16 <= 92 * 1024;
@@ -160,18 +168,6 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
                "f"(d)
                : "memory");
-}
-
-// #{g[i] <= x} for strictly increasing g (n >= 1).  Branch-free: the trip
-// count depends on n only, so a warp never diverges in the search.
-__device__ __forceinline__ int upper_count(const double* g, int n, double x) {
-  int base = 0, len = n;
-  while (len > 1) {
-    const int half = len >> 1;
-    base = (g[base + half - 1] <= x) ? base + half : base;
-    len -= half;
-  }
-  return base + (g[base] <= x ? 1 : 0);
 }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size,
@@ -210,21 +206,7 @@ struct HistArgs {
 // thread that moves a count from 0xFFFF sees it in the returned old value and
 // raises the flag).  MODE 1: exits at once unless the flag is up; then redoes
 // the main table with f32 vector reductions (exact below 2^24).
-// Bin lookup: per CTA, every forwarding model's grid is bucketed by a
-// monotone f64 map q(x) onto kLutBuckets buckets.  Grid values with q(g) <
-// q(x) are all <= x and those with q(g) > q(x) are all > x, so the exact
-// count #{g <= x} lies in [lb, ub) of x's bucket and only the grid values
-// sharing the bucket (usually none or one) are compared.  This replaces a
-// 7-step binary search of bank-conflicted 64-bit shared loads per model.
-constexpr int kLutBuckets = 2048;
-
-__device__ __forceinline__ int lut_bucket(double x, double lo, double hi, double scale) {
-  if (!(x >= lo)) return 0;  // below the grid (or NaN)
-  if (x >= hi) return kLutBuckets - 1;
-  const int q = (int)((x - lo) * scale);
-  return q > kLutBuckets - 1 ? kLutBuckets - 1 : q;
-}
-
+// Bin lookup: gs_grid_lut.cuh.
 template <int M, typename Cell, int MODE>
 __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
   if (MODE == 1 && *reinterpret_cast<volatile uint32_t*>(a.flag) == 0) return;
@@ -1263,6 +1245,23 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
   info->n_structures = p.n_struct;
   info->max_len = p.M;
   info->workspace_bytes = p.bytes;
+  info->fast_path = p.g4 ? 1 : 0;
+  if (p.g4) {
+    info->build_launches = 2;  // g4_hist, g4_prefix0
+    info->eval_launches = 1;   // g4_eval
+  } else {
+    // mirrors gs_grid_build / prefix_table / gs_grid_eval below
+    int b = 1 + (n_rec >= 65536 ? 1 : 0);
+    const bool slab = p.D >= 2 && (size_t)p.dims[p.D - 1] * p.dims[p.D - 2] * sizeof(uint4) <= kSlabSmemMax;
+    const int skip = p.walk ? 1 : 0;
+    if (p.D == 0) b += 1;
+    else if (slab) b += 1 + std::max(0, p.D - 2 - skip);
+    else b += 1 + std::max(0, p.D - 1 - skip);
+    const bool fold_side = p.DP == 1 && p.NVP == 1 && slab;
+    if (p.DP > 0 && !fold_side) b += std::max(1, p.DP);
+    info->build_launches = b;
+    info->eval_launches = p.walk ? 2 : 1;
+  }
   return GS_OK;
 }
 
@@ -1277,6 +1276,11 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
+  if (p.g4) {
+    GS_CUDA_TRY(grid4_build(certainty, correct, n_rec, grids, p.glen, ws,
+                            (flags & GS_GRID_WORKSPACE_DIRTY) != 0, st));
+    return GS_OK;
+  }
   float* F = reinterpret_cast<float*>(ws + p.offHF);
   uint32_t* P = reinterpret_cast<uint32_t*>(ws + p.offHP);
   auto* H16 = reinterpret_cast<unsigned long long*>(ws + p.offH16);
@@ -1358,6 +1362,12 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
   if ((accuracy && !aligned16(accuracy)) || (mean_cost && !aligned16(mean_cost)) ||
       (n_correct && !aligned16(n_correct)) || (forward_frac && !aligned16(forward_frac)))
     return GS_EINVAL;
+  if (p.g4) {
+    GS_CUDA_TRY(grid4_eval(n_rec, p.glen, p.struct_begin, p.struct_mask, p.n_struct, cost1,
+                           config_begin, config_count, accuracy, mean_cost, forward_frac, n_correct,
+                           static_cast<const uint8_t*>(workspace), static_cast<cudaStream_t>(stream)));
+    return GS_OK;
+  }
   EvalGridArgs a{};
   a.M = p.M;
   a.n_struct = p.n_struct;

@@ -164,3 +164,62 @@ def test_config2_shape_sampled_configs():
     assert np.array_equal(idx[again].cpu().numpy(), idx.cpu().numpy())
     keep = oracle.pareto_keep(res.accuracy.cpu().numpy(), res.mean_cost.cpu().numpy())
     assert np.array_equal(idx.cpu().numpy(), np.flatnonzero(keep))
+
+
+@pytest.mark.parametrize("n_rec,glen,ties", [
+    (1, (1, 1, 1, 1), False), (5, (2, 3, 1, 4), False), (400, (7, 1, 9, 3), True),
+    (2500, (12, 5, 8, 6), False), (3000, (20, 20, 20, 2), True), (1500, (3, 30, 2, 9), False),
+    (70_000, (33, 17, 40, 5), False)])
+def test_four_model_uneven_grids_vs_oracle(n_rec, glen, ties):
+    """The four-model fast path (gs_grid4.cu): every structure of the
+    enumeration, grids of different lengths per model (including a single
+    value), against the oracle walk over all configs."""
+    rng = np.random.default_rng(n_rec + sum(glen))
+    cert = rng.random((n_rec, 4))
+    if ties:
+        cert = np.round(cert, 1)
+    corr = (rng.random((n_rec, 4)) < 0.6).astype(np.uint8)
+    grids = []
+    for j, g in enumerate(glen):
+        q = np.quantile(cert[:, j], np.arange(1, g) / g) if g > 1 else []
+        vals = sorted({0.0} | {float(x) for x in q})
+        while len(vals) < g:  # ties collapsed quantiles: pad above the data
+            vals.append(vals[-1] + 1.0)
+        grids.append(np.array(vals[:g]))
+    cost1 = rng.uniform(10, 500, 4)
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, cost1)
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
+    assert np.array_equal(acc, want[0])
+    assert np.array_equal(cost, want[1])
+    assert np.array_equal(frac, want[2])
+    assert np.array_equal(nc / n_rec, want[0])
+    # repeat build + eval on the same workspace
+    sw.build()
+    again = sw.evaluate()
+    assert np.array_equal(again.accuracy.cpu().numpy(), want[0])
+    assert np.array_equal(again.forward_frac.cpu().numpy(), want[2])
+
+
+def test_four_models_past_packed_field_range():
+    """n_rec >= 2^21 leaves the 21-bit packed fast path for the general
+    path; sampled configs of every structure still match the oracle."""
+    from paper_2406_14424_b200.gridsweep import GridSweep, structures
+    rng = np.random.default_rng(21)
+    n = (1 << 21) + 3
+    cert = rng.random((n, 4))
+    corr = (rng.random((n, 4)) < 0.7).astype(np.uint8)
+    grids = [np.array(sorted({0.0} | set(np.quantile(cert[:, j], np.arange(1, 8) / 8).tolist())))
+             for j in range(4)]
+    cost1 = np.array([1.0, 4.0, 16.0, 64.0])
+    sw = GridSweep(cert, corr, grids, cost1)
+    res = sw.evaluate()
+    pick = []
+    for _, b, cnt in structures(4, sw.grid_len):
+        pick.extend(sorted(set(rng.integers(b, b + cnt, size=min(cnt, 12)).tolist())))
+    pick = np.array(pick)
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1, n_threads=8)
+    assert np.array_equal(res.accuracy.cpu().numpy()[pick], want[0])
+    assert np.array_equal(res.mean_cost.cpu().numpy()[pick], want[1])
+    assert np.array_equal(res.forward_frac.cpu().numpy()[pick], want[2])

@@ -1,5 +1,8 @@
+# grid tests + smoke + short bench + launch list (one GPU)
 set -x
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_grid.py -q -x > gpurun_out/pytest_grid.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_grid.log
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --skip-stage > gpurun_out/bench.log 2>&1
-TAG=prof_r1e KREGEX="grid_hist|slab_first|grid_eval|colscan" SKIP=0 COUNT=5 bash tools/gpu_prof.sh
+TAG=${TAG:-q}
+timeout 300 python __graft_entry__.py > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log
+timeout 900 python -m pytest tests -q -m gpu -x ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu ${BENCH_ARGS:-} > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$TAG.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --skip-stage > gpurun_out/ncu_bench_$TAG.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_bench_$TAG.log
