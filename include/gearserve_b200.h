@@ -108,6 +108,20 @@ int gs_grid_build(const double* certainty, const uint8_t* correct,
                   int64_t n_rec, int32_t n_models, const double* grids,
                   const int32_t* grid_len, void* workspace,
                   size_t workspace_bytes, int32_t flags, void* stream);
+/* Streamed build (gs_grid_info.fast_path == 1 only, else GS_EUNSUPPORTED):
+ * gs_grid_accumulate adds the n_chunk records at certainty / correct (a
+ * slice of the n_rec-record validation set) to the histogram, so host->device
+ * copies of later slices overlap the binning of earlier ones;
+ * gs_grid_finish turns the histogram of all n_rec records into the prefix
+ * tables.  gs_grid_build == gs_grid_accumulate(all) + gs_grid_finish.  The
+ * flags of the first accumulate of a build are those of gs_grid_build. */
+int gs_grid_accumulate(const double* certainty, const uint8_t* correct,
+                       int64_t n_chunk, int64_t n_rec, int32_t n_models,
+                       const double* grids, const int32_t* grid_len,
+                       void* workspace, size_t workspace_bytes, int32_t flags,
+                       void* stream);
+int gs_grid_finish(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
+                   void* workspace, size_t workspace_bytes, void* stream);
 /* Score configs [config_begin, config_begin + config_count).  Any output
  * pointer may be NULL to skip it.  n_correct receives the integer correct
  * count (accuracy * n_rec) used by the exact Pareto reduction. */

@@ -38,31 +38,37 @@ def _headers() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    """Compile every kernel source for sm_100a and link the shared library."""
+def build(verbose: bool = False, force: bool = False, phase_timing: bool = False) -> Path:
+    """Compile every kernel source for sm_100a and link the shared library.
+    phase_timing: a separate build (libgearserve_b200_phases.so, objects in
+    _objs_phases/) whose kernels stamp %globaltimer at phase boundaries
+    (GS_PHASE_TIMING; read back with gs_debug_phases) for tools/phase_probe.py."""
     nvcc = _nvcc()
-    BUILD.mkdir(exist_ok=True)
+    build_dir = BUILD.with_name("_objs_phases") if phase_timing else BUILD
+    lib_path = LIB.with_name("libgearserve_b200_phases.so") if phase_timing else LIB
+    extra = ["-DGS_PHASE_TIMING"] if phase_timing else []
+    build_dir.mkdir(exist_ok=True)
     hdr_mtime = max((p.stat().st_mtime for p in _headers()), default=0.0)
     objs = []
     for src in _sources():
-        obj = BUILD / (src.stem + ".o")
+        obj = build_dir / (src.stem + ".o")
         objs.append(obj)
         if (not force and obj.exists()
                 and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_mtime)):
             continue
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
     newest = max(o.stat().st_mtime for o in objs)
-    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or not lib_path.exists() or lib_path.stat().st_mtime < newest:
+        tmp = lib_path.with_suffix(".so.tmp")
         cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":

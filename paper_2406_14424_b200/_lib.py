@@ -17,7 +17,12 @@ from pathlib import Path
 import numpy as np
 import torch
 
-LIB_PATH = Path(__file__).resolve().with_name("libgearserve_b200.so")
+import os
+
+# GS_LIB_PATH selects another build of the same C ABI (e.g. the phase-timing
+# build tools/phase_probe.py makes); the default is the in-tree release build.
+LIB_PATH = Path(os.environ.get("GS_LIB_PATH") or
+                Path(__file__).resolve().with_name("libgearserve_b200.so"))
 
 GS_OK = 0
 GS_EINVAL = -1
@@ -56,6 +61,9 @@ _SIGNATURES = {
     "gs_grid_plan": [c_int64, c_int32, POINTER(c_int32), POINTER(gs_grid_info)],
     "gs_grid_build": [c_void_p, c_void_p, c_int64, c_int32, c_void_p, POINTER(c_int32),
                       c_void_p, c_size_t, c_int32, c_void_p],
+    "gs_grid_accumulate": [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p,
+                           POINTER(c_int32), c_void_p, c_size_t, c_int32, c_void_p],
+    "gs_grid_finish": [c_int64, c_int32, POINTER(c_int32), c_void_p, c_size_t, c_void_p],
     "gs_grid_eval": [c_int64, c_int32, POINTER(c_int32), c_void_p, c_int64, c_int64, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "gs_grid_decode": [c_int32, POINTER(c_int32), c_void_p, c_void_p, c_int64, c_void_p,

@@ -4,29 +4,35 @@
 // Same algorithm and outputs as the general path in gs_sweep.cu (dominance
 // counting over the bins b_j of the threshold grids, scored exactly like
 // _evaluate_numba, /root/reference/pkg/src/gearserve/kernels.py:39-62), laid
-// out so a whole sweep is three launches and every config is written by the
-// kernel that finishes its table slab:
+// out as three launches with no table pass that does not also do useful
+// arithmetic:
 //
-//   g4_hist      one pass over the records.  Per record ONE packed 64-bit
-//                reduction into the main table H[b0][b1][b2] = {cnt, c3, c2}
-//                (21-bit fields: exact for n_rec < 2^21, no carry possible,
-//                so no overflow check or fallback pass) and one into the
-//                small table H2[b0][b1] = {c1, c0} (32-bit fields).  A correct
-//                count c_j is only ever read where the dims after j are at
-//                "any", so c1 and c0 need only (b0, b1).
-//   g4_prefix0   inclusive prefix of H and H2 along b0 (strided dim): thread
-//                per (column, row segment), all loads of a segment in flight,
-//                segment carries through shared memory; re-zeroes H / H2.
-//   g4_eval      one CTA per (b0 slab k0, column part): the slab arrives by
-//                one TMA bulk copy, is row-prefixed along b2 in shared memory
-//                (a warp per row) and column-walked along b1 (thread per
-//                (b2 column, row segment)).  Each position (k1, k2) of slab k0
-//                is the table cell of the full cascade's config (k0, k1, k2);
-//                the same walk also scores every other structure that starts
-//                with model 0 at threshold k0 (their cells are the slab's
-//                last row / last column), and the "any" slab k0 = g0 scores
-//                every structure without model 0.  No face table, no second
-//                eval launch; the outputs of a slab are contiguous runs.
+//   g4_hist    one pass over the records: per record ONE 16-byte reduction
+//              (red.global.add.v4.f32, exact for counts < 2^24) of {1, k3,
+//              k2, k1} into H[b0][b1][b2], and model 0's correct bit into a
+//              per-CTA shared-memory row over b0 (c0 is only ever read where
+//              b1 and b2 are "any").  On B200 a v4 reduction costs the same
+//              as a scalar one (tools/micro_red.cu: 8.35 us per 1M into a
+//              1M-cell table), while a second reduction into a small hot
+//              table costs ~14 us more: one L2 operation per record is the
+//              design constraint.
+//   g4_plane   one CTA per b1: the (b0, b2) plane of H arrives by TMA bulk
+//              copies, is prefix-summed along b2 (a warp per row) and along
+//              b0 (thread per (b2 column, row segment)) in shared memory, and
+//              leaves as packed u64 {cnt, c3, c2} (21-bit fields, exact for
+//              n_rec < 2^21) plus R1[b0][b1] = the c1 channel at b2 = any.
+//              It re-zeroes H for the next build and turns the c0 row into
+//              its inclusive prefix P0.
+//   g4_eval    one CTA per (b0 slab k0, column part): the slab (already
+//              prefixed along b0 and b2) arrives by one TMA bulk copy; a
+//              column walk along b1 (thread per (b2 column, row segment))
+//              finishes the prefix and scores each position (k1, k2) as the
+//              full cascade's config (k0, k1, k2).  Row-shared terms (the
+//              stage-2 fraction, the partial mean cost, the partial correct
+//              count) are computed once per row.  The same walk scores every
+//              structure that starts with model 0 at threshold k0 (their
+//              cells are the slab's last row / column), and the "any" slab
+//              k0 = g0 scores every structure without model 0.
 //
 // Channels at a position (p0, p1, p2), "g" meaning any:
 //   cnt(p)  records with b0 <= p0, b1 <= p1, b2 <= p2
@@ -40,33 +46,65 @@
 #include <algorithm>
 #include <atomic>
 
+#include <cooperative_groups.h>
+
 #include "gs_grid4.cuh"
 #include "gs_grid_lut.cuh"
 
 namespace gs {
 namespace {
 
-constexpr uint64_t kF21 = (1ull << 21) - 1;
-constexpr int kHist4Threads = 1024;
-constexpr int kHist4Unroll = 4;
+namespace cg = cooperative_groups;
 
-__device__ __forceinline__ void red_add_u64(unsigned long long* addr, unsigned long long v) {
-  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+// Phase stamps (GS_PHASE_TIMING builds only, tools/phase_probe.py): thread 0
+// of each CTA records %globaltimer and clock64 at phase boundaries.
+constexpr int kPhaseKernels = 3, kPhaseCtas = 1024, kPhaseSlots = 8;
+#ifdef GS_PHASE_TIMING
+__device__ unsigned long long g_phase[kPhaseKernels * kPhaseCtas * kPhaseSlots * 2];
+__device__ __forceinline__ void phase(int kernel, int slot) {
+  if (threadIdx.x == 0 && blockIdx.x < kPhaseCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const size_t i = ((size_t)(kernel * kPhaseCtas + blockIdx.x) * kPhaseSlots + slot) * 2;
+    g_phase[i] = t;
+    g_phase[i + 1] = clock64();
+  }
+}
+#else
+__device__ __forceinline__ void phase(int, int) {}
+#endif
+
+constexpr uint64_t kF21 = (1ull << 21) - 1;
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+template <typename Kernel>
+cudaError_t ensure_smem4(Kernel k, std::atomic<int>& done, size_t bytes) {
+  if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.store((int)bytes, std::memory_order_release);
+  return e;
 }
 
 // ------------------------------------------------------------------ hist --
+constexpr int kHist4Threads = 1024;
+constexpr int kHist4Unroll = 4;
+constexpr int kMaxDim4 = 256;  // d0, d2 bound of this path
+
 struct G4HistArgs {
   const double* cert;
   const uint8_t* corr;
   int32_t n_rec;
   int32_t vec_ok;
   const double* grids;
-  int32_t goff[GS_MAX_MODELS];
-  int32_t glen[GS_MAX_MODELS];
-  int32_t n_grid;  // doubles of grids 0..2
-  int32_t d1, d2p, d1p;
-  unsigned long long* H;   // [d0][d1][d2p] {cnt, c3, c2}
-  unsigned long long* H2;  // [d0][d1p] {c1, c0}
+  int32_t glen[3];
+  int32_t d0, hp;
+  float* H;      // [d1][d0][hp] float4 {cnt, c3, c2, c1}
+  uint32_t* G0;  // [d0] model-0 correct counts per b0
 };
 
 struct Rec4 {
@@ -95,21 +133,24 @@ __device__ __forceinline__ Rec4 load_rec4(const G4HistArgs& a, int r) {
 }
 
 __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_constant__ G4HistArgs a) {
-  extern __shared__ __align__(16) double s_grid[];
-  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + a.n_grid);
-  __shared__ double s_par[3 * GS_MAX_MODELS];
+  extern __shared__ __align__(16) double s_grid[];  // grids 0..2, then the bucket tables
+  __shared__ uint32_t s_c0[kMaxDim4];
+  const int n_grid = a.glen[0] + a.glen[1] + a.glen[2];
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + n_grid);
+  phase(0, 0);
   const int stride = gridDim.x * kHist4Threads;
   int r0 = blockIdx.x * kHist4Threads + threadIdx.x;
-  // the first batch of records is in flight while the bin tables are built
+  // the first records are in flight while the bin tables are built
   Rec4 v[kHist4Unroll];
 #pragma unroll
   for (int u = 0; u < kHist4Unroll; ++u) {
     const int r = r0 + u * stride;
     if (r < a.n_rec) v[u] = load_rec4(a, r);
   }
-  const BinTables bt =
-      build_bin_tables<kHist4Threads>(a.grids, a.goff, a.glen, 3, a.n_grid, s_grid, s_lut, s_par);
-  const int d1 = a.d1, d2p = a.d2p, d1p = a.d1p;
+  for (int i = threadIdx.x; i < a.d0; i += kHist4Threads) s_c0[i] = 0u;
+  const BinTables<3> bt = build_bin_tables<3, kHist4Threads>(a.grids, a.glen, s_grid, s_lut);
+  phase(0, 1);
+  const int d0 = a.d0, hp = a.hp;
   while (r0 < a.n_rec) {
 #pragma unroll
     for (int u = 0; u < kHist4Unroll; ++u) {
@@ -118,11 +159,11 @@ __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_
       const int b1 = bt.bin(1, v[u].x1);
       const int b2 = bt.bin(2, v[u].x2);
       const uint32_t k = v[u].k;
-      const unsigned long long k0 = (k & 0xffu) != 0, k1 = (k & 0xff00u) != 0;
-      const unsigned long long k2 = (k & 0xff0000u) != 0, k3 = (k & 0xff000000u) != 0;
-      const int row = b0 * d1 + b1;
-      red_add_u64(a.H + (int64_t)row * d2p + b2, 1ull | (k3 << 21) | (k2 << 42));
-      if (k0 | k1) red_add_u64(a.H2 + b0 * d1p + b1, k1 | (k0 << 32));
+      const float k1 = (k & 0xff00u) ? 1.f : 0.f, k2 = (k & 0xff0000u) ? 1.f : 0.f;
+      const float k3 = (k & 0xff000000u) ? 1.f : 0.f;
+      const uint32_t cell = (uint32_t)(b1 * d0 + b0) * (uint32_t)hp + (uint32_t)b2;
+      red_add_v4(a.H + 4ull * cell, 1.f, k3, k2, k1);
+      if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
     }
     r0 += kHist4Unroll * stride;
 #pragma unroll
@@ -131,68 +172,163 @@ __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_
       if (r < a.n_rec) v[u] = load_rec4(a, r);
     }
   }
+  phase(0, 2);
+  __syncthreads();
+  phase(0, 3);
+  for (int i = threadIdx.x; i < a.d0; i += kHist4Threads)
+    if (s_c0[i]) atomicAdd(a.G0 + i, s_c0[i]);
+  phase(0, 4);
 }
 
-// --------------------------------------------------------------- prefix0 --
-constexpr int kPre4Threads = 256;
-constexpr int kPre4MaxSeg = 16;  // rows per thread
+// ----------------------------------------------------------------- plane --
+constexpr int kPlaneThreads = 1024;
 
-struct G4PrefixArgs {
-  unsigned long long* H;   // [d0][cols]
-  unsigned long long* S;
-  unsigned long long* H2;  // [d0][cols2]
-  unsigned long long* S2;
-  int32_t d0, cols, cols2;
-  int32_t nseg, seg_len, cpc;  // segments per column, rows per segment, columns per CTA
+struct G4PlaneArgs {
+  float* H;                  // [d1][d0][hp] float4, re-zeroed here
+  unsigned long long* S;     // [d0][d1][d2p] packed {cnt, c3, c2}
+  uint32_t* R1;              // [d0][d1p]
+  uint32_t* G0;              // [d0] raw c0, re-zeroed here
+  uint32_t* P0;              // [d0] inclusive prefix of G0
+  int32_t d0, d1, d2, d2p, d1p;
+  int32_t hp;                // histogram row pitch in cells (odd: conflict-free row walk)
+  int32_t half;              // b0 rows of the cluster's first CTA
+  int32_t ns2, seg2;         // b2 segments of the row walk
+  int32_t ns0, seg0;         // b0 segments of the column walk
 };
 
-__global__ void __launch_bounds__(kPre4Threads) g4_prefix0_kernel(const __grid_constant__ G4PrefixArgs a) {
-  __shared__ unsigned long long s_tot[kPre4Threads];
-  const int cl = threadIdx.x % a.cpc, seg = threadIdx.x / a.cpc;
-  const int c = blockIdx.x * a.cpc + cl;
-  const bool main = c < a.cols;
-  const bool live = c < a.cols + a.cols2 && seg < a.nseg;
-  unsigned long long* src = main ? a.H + c : a.H2 + (c - a.cols);
-  unsigned long long* dst = main ? a.S + c : a.S2 + (c - a.cols);
-  const uint32_t pitch = main ? a.cols : a.cols2;
-  const int r0 = seg * a.seg_len;
-  const int len = live ? max(0, min(a.seg_len, a.d0 - r0)) : 0;
-  src += (size_t)r0 * pitch;
-  dst += (size_t)r0 * pitch;
-  unsigned long long v[kPre4MaxSeg];
-  unsigned long long sum = 0;
-#pragma unroll
-  for (int i = 0; i < kPre4MaxSeg; ++i) v[i] = i < len ? src[i * pitch] : 0ull;
-#pragma unroll
-  for (int i = 0; i < kPre4MaxSeg; ++i) sum += v[i];
-  s_tot[threadIdx.x] = sum;
+__device__ __forceinline__ uint4 f4_to_u4(float4 f) {
+  return make_uint4(__float2uint_rn(f.x), __float2uint_rn(f.y), __float2uint_rn(f.z),
+                    __float2uint_rn(f.w));
+}
+__device__ __forceinline__ uint4 add4u(uint4 a, uint4 b) {
+  return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// The (b0, b2) plane of one b1 is contiguous in H ([b1][b0][hp]).  A
+// cluster of two CTAs owns it, split along b0: each CTA bulk-copies its half
+// of the rows, re-zeroes them, walks its rows along b2, and walks its
+// columns along b0; the first CTA hands its column totals to the second
+// through distributed shared memory as the b0 carry.  Both prefixes are
+// serial walks (one add per cell and channel, no shuffles), two-level so
+// that ~1000 threads share them, segment carries through shared memory.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 1)
+    g4_plane_kernel(const __grid_constant__ G4PlaneArgs a) {
+  extern __shared__ __align__(16) uint4 s_tile[];  // [rows][hp], segment sums, peer carry
+  __shared__ __align__(8) uint64_t bar;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int h = (int)cluster.block_rank();
+  const int b1 = blockIdx.x >> 1;
+  const int d0 = a.d0, d2 = a.d2, hp = a.hp;
+  const int r_beg = h ? a.half : 0, r_end = h ? d0 : a.half, nr = r_end - r_beg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kPlaneThreads / 32;
+  uint4* s_seg = s_tile + (size_t)a.half * hp;
+  uint4* s_carry = s_seg + kPlaneThreads;  // [d2] column totals of the first half (rank 1)
+  const uint32_t tile_bytes = (uint32_t)(nr * hp * sizeof(float4));
+  float4* H = reinterpret_cast<float4*>(a.H) + ((int64_t)b1 * d0 + r_beg) * hp;
+  const int64_t plane = (int64_t)a.d1 * a.d2p;  // S cells per b0 slab
+  phase(1, 0);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
   __syncthreads();
-  unsigned long long run = 0;
-  for (int s = 0; s < seg; ++s) run += s_tot[s * a.cpc + cl];
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, tile_bytes);
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t off = 0; off < tile_bytes; off += kChunk)
+      bulk_g2s(reinterpret_cast<uint8_t*>(s_tile) + off, reinterpret_cast<const uint8_t*>(H) + off,
+               min(kChunk, tile_bytes - off), &bar);
+  }
+  if (b1 == 0 && h == 0 && warp == nwarps - 1) {  // c0: inclusive prefix over b0, re-zero
+    uint32_t carry = 0;
+    for (int b = 0; b < d0; b += 32) {
+      const int i = b + lane;
+      uint32_t x = i < d0 ? a.G0[i] : 0u;
 #pragma unroll
-  for (int i = 0; i < kPre4MaxSeg; ++i) {
-    if (i < len) {
-      run += v[i];
-      dst[i * pitch] = run;
-      src[i * pitch] = 0ull;  // the next build starts from zero
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      x += carry;
+      if (i < d0) {
+        a.P0[i] = x;
+        a.G0[i] = 0u;
+      }
+      carry = __shfl_sync(0xffffffffu, x, 31);
     }
   }
+  mbar_wait(&bar, 0);
+  phase(1, 1);
+  // re-zero the histogram rows just read (the next build starts from zero)
+  for (int i = tid; i < nr * hp; i += kPlaneThreads) H[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  phase(1, 2);
+  // row walk along b2 (f32 counts -> u32 on the way)
+  {
+    const int r = tid % nr, s = tid / nr;
+    const bool live = s < a.ns2;
+    const int c_lo = s * a.seg2, c_hi = min(d2, c_lo + a.seg2);
+    uint4* row = s_tile + (size_t)r * hp;
+    uint4 sum = make_uint4(0, 0, 0, 0);
+    if (live)
+      for (int c = c_lo; c < c_hi; ++c) sum = add4u(sum, f4_to_u4(*reinterpret_cast<float4*>(row + c)));
+    if (live) s_seg[s * nr + r] = sum;
+    __syncthreads();
+    if (live) {
+      uint4 run = make_uint4(0, 0, 0, 0);
+      for (int q = 0; q < s; ++q) run = add4u(run, s_seg[q * nr + r]);
+      for (int c = c_lo; c < c_hi; ++c) {
+        run = add4u(run, f4_to_u4(*reinterpret_cast<float4*>(row + c)));
+        row[c] = run;
+      }
+    }
+    __syncthreads();
+  }
+  phase(1, 3);
+  // column walk along b0; the first half's column totals are the second's carry
+  const int c = tid % d2, s = tid / d2;
+  const bool live = s < a.ns0;
+  const int r_lo = s * a.seg0, r_hi = min(nr, r_lo + a.seg0);
+  uint4 sum = make_uint4(0, 0, 0, 0);
+  if (live)
+    for (int r = r_lo; r < r_hi; ++r) sum = add4u(sum, s_tile[(size_t)r * hp + c]);
+  if (live) s_seg[s * d2 + c] = sum;
+  __syncthreads();
+  if (h == 0 && s == 0) {
+    uint4 tot = make_uint4(0, 0, 0, 0);
+    for (int q = 0; q < a.ns0; ++q) tot = add4u(tot, s_seg[q * d2 + c]);
+    *cluster.map_shared_rank(s_carry + c, 1) = tot;
+  }
+  cluster.sync();
+  phase(1, 4);
+  if (!live) return;
+  uint4 P = h ? s_carry[c] : make_uint4(0, 0, 0, 0);
+  for (int q = 0; q < s; ++q) P = add4u(P, s_seg[q * d2 + c]);
+  unsigned long long* S = a.S + (int64_t)b1 * a.d2p + c;
+  for (int r = r_lo; r < r_hi; ++r) {
+    P = add4u(P, s_tile[(size_t)r * hp + c]);
+    const int64_t b0 = r_beg + r;
+    S[b0 * plane] = (unsigned long long)P.x | ((unsigned long long)P.y << 21) |
+                    ((unsigned long long)P.z << 42);
+    if (c == d2 - 1) a.R1[b0 * a.d1p + b1] = P.w;
+  }
+  phase(1, 5);
 }
 
 // ------------------------------------------------------------------ eval --
 constexpr int kEval4Threads = 512;
-constexpr int kEval4MaxRowCells = 8;  // cells per lane in the row prefix (d2 <= 256)
 
 struct G4EvalArgs {
   int32_t d0, d1, d2, d2p, d1p;
-  int32_t parts, width, nseg, seg_len;  // column parts per slab, columns per part, row segments
+  int32_t half, nseg, seg_len;          // rows of the cluster's first CTA, row segments
   int64_t sb[16];                       // first config of the structure with model mask m
   int64_t cfg_begin, cfg_count;
   int64_t n_rec;
   double rcp_n;
   const double* cost1;
-  const unsigned long long* S;   // b0-prefixed main table
-  const unsigned long long* S2;  // b0-prefixed {c1, c0}
+  const unsigned long long* S;  // prefixed along b0 and b2, packed {cnt, c3, c2}
+  const uint32_t* R1;           // [d0][d1p] C1 over b0 <= k0, b1, any b2
+  const uint32_t* P0;           // [d0] C0(k0)
   double* acc;
   double* cost;
   double* frac;
@@ -206,8 +342,37 @@ __device__ __forceinline__ Cell3 unpack3(unsigned long long v) {
   return {(uint32_t)(v & kF21), (uint32_t)((v >> 21) & kF21), (uint32_t)(v >> 42)};
 }
 
-// One config's outputs: frac row [1, f[0..K-2], 0 pad], mean built stage by
-// stage in the reference's order (src/kernels.py:57-60), acc = correct / n.
+// One config's outputs given its frac row and mean cost (the reference's
+// epilogue, src/kernels.py:57-61: frac = count / n, mean += frac * cost1 in
+// stage order, acc = correct / n).
+__device__ __forceinline__ void st_v4_f64(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+
+// ALL: accuracy, mean_cost and forward_frac all requested (the sweep's usual
+// call) and forward_frac 32-byte aligned: the frac row is one 256-bit store
+// (a warp writes 1 KB of whole lines; two 128-bit stores per row write every
+// line twice, half each time: tools/micro_store.cu, 14.5 vs 10.4 us for the
+// 52 B/config outputs of 1M configs).
+template <bool ALL>
+__device__ __forceinline__ void store4(const G4EvalArgs& a, int64_t i, double f0, double f1,
+                                       double f2, double f3, double mean, uint32_t correct,
+                                       double n, double rcp) {
+  if (ALL) {
+    st_v4_f64(a.frac + i * 4, f0, f1, f2, f3);
+  } else if (a.frac) {
+    double2* row = reinterpret_cast<double2*>(a.frac + i * 4);
+    row[0] = make_double2(f0, f1);
+    row[1] = make_double2(f2, f3);
+  }
+  if (ALL || a.cost) a.cost[i] = mean;
+  if (ALL || a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+  if (a.n_correct) a.n_correct[i] = correct;
+}
+
+// A config of K stages with reach counts reach[0..K-2] (after stages
+// 0..K-2) and stage costs cst[0..K-1], scored from scratch (edge cells).
 template <int K>
 __device__ __forceinline__ void put4(const G4EvalArgs& a, int64_t cfg, const uint32_t* reach,
                                      const double* cst, uint32_t correct, double n, double rcp,
@@ -221,195 +386,189 @@ __device__ __forceinline__ void put4(const G4EvalArgs& a, int64_t cfg, const uin
     fr[t] = div_count((double)reach[t - 1], n, rcp);
     mean = dadd(mean, dmul(fr[t], cst[t]));
   }
-  if (a.frac) {
-    double2* row = reinterpret_cast<double2*>(a.frac + i * 4);
-    row[0] = make_double2(fr[0], fr[1]);
-    row[1] = make_double2(fr[2], fr[3]);
-  }
-  if (a.cost) a.cost[i] = mean;
-  if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
-  if (a.n_correct) a.n_correct[i] = correct;
+  store4<false>(a, i, fr[0], fr[1], fr[2], fr[3], mean, correct, n, rcp);
 }
 
-__global__ void __launch_bounds__(kEval4Threads, 2) g4_eval_kernel(const __grid_constant__ G4EvalArgs a) {
-  extern __shared__ __align__(16) unsigned long long s_slab[];  // [d1][d2p]
+// A cluster of two CTAs owns slab k0, split along b1 (rows): each
+// bulk-copies its rows, sums its columns over them and hands the column
+// sums to the other CTA through distributed shared memory (rank 1 needs
+// rank 0's as its b1 carry; both need the other's column-g2 sum for the slab
+// total).  Then each walks its own rows.
+template <bool ALL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
+    g4_eval_kernel(const __grid_constant__ G4EvalArgs a) {
+  extern __shared__ __align__(16) unsigned long long s_slab[];  // [rows][d2p], then tables
   __shared__ __align__(8) uint64_t bar;
-  __shared__ unsigned long long s_colg[1024];  // prefix along b1 of column g2 (= row totals)
-  __shared__ uint32_t s_c1[1024];              // C1(k0, b1) prefix along b1
-  __shared__ unsigned long long s_seg[kEval4Threads];
-  __shared__ uint32_t s_c0[2];                 // C0(k0), C0(g0)
+  __shared__ uint32_t s_c0[2];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int h = (int)cluster.block_rank();
   const int d0 = a.d0, d1 = a.d1, d2 = a.d2, d2p = a.d2p;
   const int g0 = d0 - 1, g1 = d1 - 1, g2 = d2 - 1;
-  const int k0 = blockIdx.x / a.parts, part = blockIdx.x - k0 * a.parts;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kEval4Threads / 32;
+  const int k0 = blockIdx.x >> 1;
+  const int rb = h ? a.half : 0, re = h ? d1 : a.half, nr = re - rb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool any0 = k0 == g0;  // the "any" slab: structures without model 0
-  // skip a slab none of whose configs is in the requested range: a slab
-  // k0 < g0 scores structures (0,1) .. (0,1,2,3), the first starting at
-  // sb[3] + k0 and the last ending at sb[15] + (k0 + 1) g1 g2; the any slab
-  // scores the singletons (from config 0) through (1,2,3)
-  {
-    const int64_t lo = any0 ? 0 : a.sb[3] + k0;
-    const int64_t hi = any0 ? a.sb[14] + (int64_t)g1 * g2 : a.sb[15] + (int64_t)(k0 + 1) * g1 * g2;
-    if (hi <= a.cfg_begin || lo >= a.cfg_begin + a.cfg_count) return;
-  }
-  const uint32_t slab_bytes = (uint32_t)((int64_t)d1 * d2p * 8);
+  unsigned long long* s_colg = s_slab + (size_t)a.half * d2p;  // [half] row totals, prefixed
+  double* s_rowf = reinterpret_cast<double*>(s_colg + a.half);   // [half] row-shared fraction
+  double* s_rowm = s_rowf + a.half;                              // [half] partial mean cost
+  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(s_rowm + a.half);  // [nseg][d2]
+  unsigned long long* s_own = s_seg + (size_t)a.nseg * d2;       // [d2] column sums, own rows
+  unsigned long long* s_peer = s_own + d2;                       // [d2] column sums, other CTA
+  uint32_t* s_c1 = reinterpret_cast<uint32_t*>(s_peer + d2);     // [d1] C1 prefix along b1
+  uint32_t* s_rowc = s_c1 + d1;                                  // [half]
+  // skip a slab none of whose configs is in the requested range (both CTAs
+  // of the cluster decide alike): a slab k0 < g0 scores structures (0,1) ..
+  // (0,1,2,3), the first starting at sb[3] + k0 and the last ending at
+  // sb[15] + (k0 + 1) g1 g2; the any slab scores the singletons (from
+  // config 0) through (1,2,3)
+  const int64_t lo = any0 ? 0 : a.sb[3] + k0;
+  const int64_t hi = any0 ? a.sb[14] + (int64_t)g1 * g2 : a.sb[15] + (int64_t)(k0 + 1) * g1 * g2;
+  if (hi <= a.cfg_begin || lo >= a.cfg_begin + a.cfg_count) return;
+  const bool full = lo >= a.cfg_begin && hi <= a.cfg_begin + a.cfg_count;
+  phase(2, 0);
+  const uint32_t bytes = (uint32_t)((int64_t)nr * d2p * 8);
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_arrive_expect_tx(&bar, slab_bytes);
-    const unsigned long long* src = a.S + (int64_t)k0 * d1 * d2p;
+    mbar_arrive_expect_tx(&bar, bytes);
+    const unsigned long long* src = a.S + ((int64_t)k0 * d1 + rb) * d2p;
     constexpr uint32_t kChunk = 32768;
-    for (uint32_t off = 0; off < slab_bytes; off += kChunk)
+    for (uint32_t off = 0; off < bytes; off += kChunk)
       bulk_g2s(reinterpret_cast<uint8_t*>(s_slab) + off, reinterpret_cast<const uint8_t*>(src) + off,
-               min(kChunk, slab_bytes - off), &bar);
+               min(kChunk, bytes - off), &bar);
   }
-  // side channels while the slab is in flight: warp 1 -> C1 prefix and C0(k0),
-  // warp 2 -> C0(g0)
-  if (warp == 1 || warp == 2) {
-    const unsigned long long* row = a.S2 + (int64_t)(warp == 1 ? k0 : g0) * a.d1p;
-    uint32_t carry = 0, c0 = 0;
+  // while the slab is in flight: C1(k0, b1) prefix along b1 (warp 1), C0 (warp 2)
+  if (warp == 1) {
+    const uint32_t* row = a.R1 + (int64_t)k0 * a.d1p;
+    uint32_t carry = 0;
     for (int b = 0; b < d1; b += 32) {
       const int b1 = b + lane;
-      const unsigned long long w = b1 < d1 ? row[b1] : 0ull;
-      c0 += (uint32_t)(w >> 32);
-      if (warp == 1) {
-        uint32_t x = (uint32_t)w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
-        }
-        x += carry;
-        if (b1 < d1) s_c1[b1] = x;
-        carry = __shfl_sync(0xffffffffu, x, 31);
-      }
-    }
-    c0 = warp_sum(c0);
-    if (lane == 0) s_c0[warp - 1] = c0;
-  }
-  mbar_wait(&bar, 0);
-  // row prefix along b2, a warp per row, J consecutive cells per lane
-  {
-    const int J = (d2 + 31) / 32;
-    for (int r = warp; r < d1; r += nwarps) {
-      unsigned long long* row = s_slab + (int64_t)r * d2p;
-      unsigned long long e[kEval4MaxRowCells];
-      unsigned long long tot = 0;
-#pragma unroll
-      for (int j = 0; j < kEval4MaxRowCells; ++j) {
-        const int c = lane * J + j;
-        e[j] = (j < J && c < d2) ? row[c] : 0ull;
-        tot += e[j];
-        e[j] = tot;
-      }
-      unsigned long long incl = tot;
+      uint32_t x = b1 < d1 ? row[b1] : 0u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
       }
-      const unsigned long long excl = incl - tot;
-#pragma unroll
-      for (int j = 0; j < kEval4MaxRowCells; ++j) {
-        const int c = lane * J + j;
-        if (j < J && c < d2) row[c] = e[j] + excl;
-      }
+      x += carry;
+      if (b1 < d1) s_c1[b1] = x;
+      carry = __shfl_sync(0xffffffffu, x, 31);
     }
+  } else if (warp == 2 && lane == 0) {
+    s_c0[0] = a.P0[k0];
+    s_c0[1] = a.P0[g0];
   }
+  mbar_wait(&bar, 0);
+  phase(2, 1);
+  // column sums over this CTA's rows: thread (column col, row segment seg)
+  const int col = tid % d2, seg = tid / d2;
+  const bool live = seg < a.nseg;
+  const int r_lo = seg * a.seg_len, r_hi = min(nr, r_lo + a.seg_len);
+  unsigned long long ssum = 0;
+  if (live)
+    for (int r = r_lo; r < r_hi; ++r) ssum += s_slab[(size_t)r * d2p + col];
+  if (live) s_seg[seg * d2 + col] = ssum;
   __syncthreads();
-  // column g2 (row totals) prefix along b1 -> s_colg (warp 0); segment sums
-  // of the walked columns (every thread)
-  const int kc = tid % a.width, seg = tid / a.width;
-  const int k2 = part * a.width + kc;
-  const bool walker = kc < a.width && k2 < d2 && seg < a.nseg;
-  const int r_lo = seg * a.seg_len, r_hi = min(d1, r_lo + a.seg_len);
+  if (live && seg == 0) {
+    unsigned long long t = 0;
+    for (int q = 0; q < a.nseg; ++q) t += s_seg[q * d2 + col];
+    s_own[col] = t;
+    *cluster.map_shared_rank(s_peer + col, 1 - h) = t;
+  }
+  cluster.sync();
+  phase(2, 2);
+  // column g2 (row totals) prefix along b1 over own rows, after the carry
   if (warp == 0) {
-    unsigned long long carry = 0;
-    for (int b = 0; b < d1; b += 32) {
-      const int b1 = b + lane;
-      unsigned long long x = b1 < d1 ? s_slab[(int64_t)b1 * d2p + g2] : 0ull;
+    unsigned long long carry = h ? s_peer[g2] : 0ull;
+    for (int b = 0; b < nr; b += 32) {
+      const int r = b + lane;
+      unsigned long long x = r < nr ? s_slab[(size_t)r * d2p + g2] : 0ull;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
       x += carry;
-      if (b1 < d1) s_colg[b1] = x;
+      if (r < nr) s_colg[r] = x;
       carry = __shfl_sync(0xffffffffu, x, 31);
     }
   }
-  unsigned long long ssum = 0;
-  if (walker)
-    for (int r = r_lo; r < r_hi; ++r) ssum += s_slab[(int64_t)r * d2p + k2];
-  s_seg[tid] = ssum;
   __syncthreads();
-  if (!walker) return;
-  unsigned long long P = 0;
-  for (int s = 0; s < seg; ++s) P += s_seg[s * a.width + kc];
 
   const double n = (double)a.n_rec, rcp = a.rcp_n;
   const double one = div_count(n, n, rcp);
   const double c0c = __ldg(a.cost1 + 0), c1c = __ldg(a.cost1 + 1), c2c = __ldg(a.cost1 + 2),
                c3c = __ldg(a.cost1 + 3);
-  const Cell3 tot = unpack3(s_colg[g1]);
+  const Cell3 tot = unpack3(s_own[g2] + s_peer[g2]);  // slab total: (k0, g1, g2)
   const uint32_t C1g = s_c1[g1];
-  if (!any0) {
-    const uint32_t base0 = s_c0[1] - s_c0[0];  // model 0 completes b0 > k0
-    for (int k1 = r_lo; k1 < r_hi; ++k1) {
-      P += s_slab[(int64_t)k1 * d2p + k2];
-      const Cell3 p = unpack3(P);
-      if (k1 < g1) {
-        const Cell3 rg = unpack3(s_colg[k1]);
-        const uint32_t c01 = base0 + (C1g - s_c1[k1]);
-        if (k2 < g2) {  // (0,1,2,3)
-          const uint32_t reach[3] = {tot.cnt, rg.cnt, p.cnt};
-          const double cst[4] = {c0c, c1c, c2c, c3c};
-          put4<4>(a, a.sb[15] + ((int64_t)k0 * g1 + k1) * g2 + k2, reach, cst,
-                  c01 + (rg.c2 - p.c2) + p.c3, n, rcp, one);
-        } else {  // (0,1,2) and (0,1,3) at (k0, k1)
-          const uint32_t reach[2] = {tot.cnt, rg.cnt};
-          const double cst2[3] = {c0c, c1c, c2c}, cst3[3] = {c0c, c1c, c3c};
-          put4<3>(a, a.sb[7] + (int64_t)k0 * g1 + k1, reach, cst2, c01 + rg.c2, n, rcp, one);
-          put4<3>(a, a.sb[11] + (int64_t)k0 * g1 + k1, reach, cst3, c01 + rg.c3, n, rcp, one);
-        }
-      } else if (k2 < g2) {  // (0,2,3) at (k0, k2)
+  const uint32_t base0 = s_c0[1] - s_c0[0];  // slab k0: model 0 completes b0 > k0
+  const double f1 = div_count((double)tot.cnt, n, rcp);  // slab k0: after stage 0
+  const double m1 = dadd(dadd(0.0, dmul(one, c0c)), dmul(f1, c1c));
+  // row-shared terms of the longest structure of this slab:
+  //   slab k0: (0,1,2,3) -> frac[2] = cnt(k0,k1,g)/n, mean through stage 2,
+  //            correct through stage 1 plus C2(k0,k1,g)
+  //   any:     (1,2,3)   -> frac[1] = cnt(g,k1,g)/n, mean through stage 1,
+  //            correct of stage 0 (model 1) plus C2(g,k1,g)
+  for (int r = tid; r < nr; r += kEval4Threads) {
+    const int k1 = rb + r;
+    const Cell3 rg = unpack3(s_colg[r]);
+    const double fr = div_count((double)rg.cnt, n, rcp);
+    s_rowf[r] = fr;
+    if (!any0) {
+      s_rowm[r] = dadd(m1, dmul(fr, c2c));
+      s_rowc[r] = base0 + (C1g - s_c1[k1]) + rg.c2;
+    } else {
+      s_rowm[r] = dadd(dadd(0.0, dmul(one, c1c)), dmul(fr, c2c));
+      s_rowc[r] = (C1g - s_c1[k1]) + rg.c2;
+    }
+  }
+  __syncthreads();
+
+  phase(2, 3);
+  // edge cells, one thread each (their prefixes are already known):
+  //   last column (k2 = g2): row totals s_colg; last row (k1 = g1, rank 1):
+  //   column totals = carry + own column sums; corner: the slab total
+  for (int r = tid; r < nr; r += kEval4Threads) {
+    const int k1 = rb + r;
+    if (k1 >= g1) continue;
+    const Cell3 p = unpack3(s_colg[r]);
+    if (!any0) {  // (0,1,2) and (0,1,3) at (k0, k1)
+      const uint32_t reach[2] = {tot.cnt, p.cnt};
+      const uint32_t c01 = base0 + (C1g - s_c1[k1]);
+      const double cst2[3] = {c0c, c1c, c2c}, cst3[3] = {c0c, c1c, c3c};
+      put4<3>(a, a.sb[7] + (int64_t)k0 * g1 + k1, reach, cst2, c01 + p.c2, n, rcp, one);
+      put4<3>(a, a.sb[11] + (int64_t)k0 * g1 + k1, reach, cst3, c01 + p.c3, n, rcp, one);
+    } else {  // (1,2), (1,3) at k1
+      const uint32_t reach[1] = {p.cnt};
+      const uint32_t c1 = C1g - s_c1[k1];
+      const double cA[2] = {c1c, c2c}, cB[2] = {c1c, c3c};
+      put4<2>(a, a.sb[6] + k1, reach, cA, c1 + p.c2, n, rcp, one);
+      put4<2>(a, a.sb[10] + k1, reach, cB, c1 + p.c3, n, rcp, one);
+    }
+  }
+  if (h == 1) {
+    for (int k2 = tid; k2 < g2; k2 += kEval4Threads) {  // last row: P = (k0, g1, k2)
+      const Cell3 p = unpack3(s_own[k2] + s_peer[k2]);
+      if (!any0) {  // (0,2,3) at (k0, k2)
         const uint32_t reach[2] = {tot.cnt, p.cnt};
         const double cst[3] = {c0c, c2c, c3c};
-        put4<3>(a, a.sb[13] + (int64_t)k0 * g2 + k2, reach, cst,
-                base0 + (tot.c2 - p.c2) + p.c3, n, rcp, one);
-      } else {  // (0,1), (0,2), (0,3) at k0
+        put4<3>(a, a.sb[13] + (int64_t)k0 * g2 + k2, reach, cst, base0 + (tot.c2 - p.c2) + p.c3,
+                n, rcp, one);
+      } else {  // (2,3) at k2
+        const uint32_t reach[1] = {p.cnt};
+        const double cst[2] = {c2c, c3c};
+        put4<2>(a, a.sb[12] + k2, reach, cst, (tot.c2 - p.c2) + p.c3, n, rcp, one);
+      }
+    }
+    if (tid == kEval4Threads - 1) {
+      if (!any0) {  // (0,1), (0,2), (0,3) at k0
         const uint32_t reach[1] = {tot.cnt};
         const double cA[2] = {c0c, c1c}, cB[2] = {c0c, c2c}, cC[2] = {c0c, c3c};
         put4<2>(a, a.sb[3] + k0, reach, cA, base0 + C1g, n, rcp, one);
         put4<2>(a, a.sb[5] + k0, reach, cB, base0 + tot.c2, n, rcp, one);
         put4<2>(a, a.sb[9] + k0, reach, cC, base0 + tot.c3, n, rcp, one);
-      }
-    }
-  } else {
-    for (int k1 = r_lo; k1 < r_hi; ++k1) {
-      P += s_slab[(int64_t)k1 * d2p + k2];
-      const Cell3 p = unpack3(P);
-      if (k1 < g1) {
-        const Cell3 rg = unpack3(s_colg[k1]);
-        const uint32_t c1 = C1g - s_c1[k1];  // model 1 completes b1 > k1
-        if (k2 < g2) {  // (1,2,3) at (k1, k2)
-          const uint32_t reach[2] = {rg.cnt, p.cnt};
-          const double cst[3] = {c1c, c2c, c3c};
-          put4<3>(a, a.sb[14] + (int64_t)k1 * g2 + k2, reach, cst, c1 + (rg.c2 - p.c2) + p.c3, n,
-                  rcp, one);
-        } else {  // (1,2), (1,3) at k1
-          const uint32_t reach[1] = {rg.cnt};
-          const double cA[2] = {c1c, c2c}, cB[2] = {c1c, c3c};
-          put4<2>(a, a.sb[6] + k1, reach, cA, c1 + rg.c2, n, rcp, one);
-          put4<2>(a, a.sb[10] + k1, reach, cB, c1 + rg.c3, n, rcp, one);
-        }
-      } else if (k2 < g2) {  // (2,3) at k2
-        const uint32_t reach[1] = {p.cnt};
-        const double cst[2] = {c2c, c3c};
-        put4<2>(a, a.sb[12] + k2, reach, cst, (tot.c2 - p.c2) + p.c3, n, rcp, one);
       } else {  // singletons
         const uint32_t* none = nullptr;
         const double cA[1] = {c0c}, cB[1] = {c1c}, cC[1] = {c2c}, cD[1] = {c3c};
@@ -420,14 +579,31 @@ __global__ void __launch_bounds__(kEval4Threads, 2) g4_eval_kernel(const __grid_
       }
     }
   }
-}
+  phase(2, 4);
+  if (!live || col >= g2) return;
 
-template <typename Kernel>
-cudaError_t ensure_smem4(Kernel k, std::atomic<int>& done, size_t bytes) {
-  if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) done.store((int)bytes, std::memory_order_release);
-  return e;
+  // interior: the longest structure, one config per position (k1, k2),
+  // k1 < g1, k2 < g2; its index is row_base + k1 * g2
+  unsigned long long P = h ? s_peer[col] : 0ull;
+  for (int q = 0; q < seg; ++q) P += s_seg[q * d2 + col];
+  const int64_t row_base =
+      (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + col - a.cfg_begin;
+  const int r_end = min(r_hi, g1 - rb);
+  for (int r = r_lo; r < r_end; ++r) {
+    P += s_slab[(size_t)r * d2p + col];
+    const int64_t i = row_base + (int64_t)(rb + r) * g2;
+    if (!full && (i < 0 || i >= a.cfg_count)) continue;
+    const Cell3 p = unpack3(P);
+    const double f3 = div_count((double)p.cnt, n, rcp);
+    const double rf = s_rowf[r];
+    const double mean = dadd(s_rowm[r], dmul(f3, c3c));
+    const uint32_t correct = s_rowc[r] - p.c2 + p.c3;
+    if (!any0)
+      store4<ALL>(a, i, one, f1, rf, f3, mean, correct, n, rcp);
+    else
+      store4<ALL>(a, i, one, rf, f3, 0.0, mean, correct, n, rcp);
+  }
+  phase(2, 5);
 }
 
 }  // namespace
@@ -437,8 +613,13 @@ bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
   if (M != 4 || n_rec < 1 || n_rec >= kGrid4MaxRec) return false;
   const int64_t d0 = glen[0] + 1, d1 = glen[1] + 1, d2 = glen[2] + 1;
   const int64_t d2p = (d2 + 1) & ~1ll;
-  return d0 <= kPre4Threads && d1 <= 1024 && d2 <= 32 * kEval4MaxRowCells &&
-         d1 * d2p * 8 <= kGrid4SlabMax;
+  const int64_t grid_bytes = (int64_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * 4;
+  // plane tile [d0][d2p] x 16 B plus segment sums; eval slab [d1][d2p] x 8 B
+  const int64_t plane_smem = ((d0 + 1) / 2 * (d2 | 1) + kPlaneThreads + d2) * 16;
+  return d0 <= kMaxDim4 && d2 <= kMaxDim4 && d1 <= 4096 && grid_bytes <= 96 * 1024 &&
+         d2 <= kPlaneThreads && plane_smem <= (int64_t)kGrid4SlabMax &&
+         d2 <= kEval4Threads && d1 >= 2 &&
+         (d1 + 1) / 2 * (d2p * 8 + 28) + (kEval4Threads + 2 * d2) * 8 + d1 * 4 <= (int64_t)kGrid4SlabMax;
 }
 
 Grid4Layout grid4_layout(const int32_t* glen) {
@@ -447,70 +628,92 @@ Grid4Layout grid4_layout(const int32_t* glen) {
   L.d1 = glen[1] + 1;
   L.d2 = glen[2] + 1;
   L.d2p = (L.d2 + 1) & ~1;
-  L.d1p = (L.d1 + 1) & ~1;
-  const size_t bH = round_up((size_t)L.d0 * L.d1 * L.d2p * 8, 256);
-  const size_t bH2 = round_up((size_t)L.d0 * L.d1p * 8, 256);
+  L.d1p = (L.d1 + 3) & ~3;
+  L.hp = L.d2 | 1;
+  const size_t bH = round_up((size_t)L.d0 * L.d1 * L.hp * 16, 256);
+  const size_t bS = round_up((size_t)L.d0 * L.d1 * L.d2p * 8, 256);
+  const size_t bR1 = round_up((size_t)L.d0 * L.d1p * 4, 256);
+  const size_t bG = round_up((size_t)L.d0 * 4, 256);
   L.offH = 0;
-  L.offH2 = bH;
-  L.offS = bH + bH2;
-  L.offS2 = 2 * bH + bH2;
-  L.bytes = 2 * bH + 2 * bH2;
+  L.offG0 = bH;
+  L.offS = bH + bG;
+  L.offR1 = L.offS + bS;
+  L.offP0 = L.offR1 + bR1;
+  L.bytes = L.offP0 + bG;
   return L;
 }
 
-cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
-                        const int32_t* glen, uint8_t* ws, bool dirty, cudaStream_t st) {
+cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_chunk,
+                             const double* grids, const int32_t* glen, uint8_t* ws, bool dirty,
+                             cudaStream_t st) {
   const Grid4Layout L = grid4_layout(glen);
-  auto* H = reinterpret_cast<unsigned long long*>(ws + L.offH);
-  auto* H2 = reinterpret_cast<unsigned long long*>(ws + L.offH2);
+  float* H = reinterpret_cast<float*>(ws + L.offH);
+  uint32_t* G0 = reinterpret_cast<uint32_t*>(ws + L.offG0);
   if (dirty) {
-    cudaError_t e = cudaMemsetAsync(ws, 0, L.offS, st);  // H and H2
+    cudaError_t e = cudaMemsetAsync(ws, 0, L.offS, st);  // H and G0
     if (e != cudaSuccess) return e;
   }
   G4HistArgs h{};
   h.cert = cert;
   h.corr = corr;
-  h.n_rec = (int32_t)n_rec;
+  h.n_rec = (int32_t)n_chunk;
   h.vec_ok = aligned16(cert) && ((reinterpret_cast<uintptr_t>(corr) & 3u) == 0);
   h.grids = grids;
-  int off = 0;
-  for (int j = 0; j < 3; ++j) {
-    h.goff[j] = off;
-    h.glen[j] = glen[j];
-    off += glen[j];
-  }
-  h.n_grid = off;
-  h.d1 = L.d1;
-  h.d2p = L.d2p;
-  h.d1p = L.d1p;
+  for (int j = 0; j < 3; ++j) h.glen[j] = glen[j];
+  h.d0 = L.d0;
+  h.hp = L.hp;
   h.H = H;
-  h.H2 = H2;
-  const size_t smem = (size_t)h.n_grid * sizeof(double) + 3 * kLutBuckets * sizeof(uint32_t);
-  static std::atomic<int> smem_set{0};
-  cudaError_t e = ensure_smem4(g4_hist_kernel, smem_set, smem);
+  h.G0 = G0;
+  const size_t smem =
+      (size_t)(glen[0] + glen[1] + glen[2]) * sizeof(double) + 3 * kLutBuckets * sizeof(uint32_t);
+  static std::atomic<int> smem_hist{0};
+  cudaError_t e = ensure_smem4(g4_hist_kernel, smem_hist, smem);
   if (e != cudaSuccess) return e;
-  int64_t blocks = (n_rec + kHist4Threads * kHist4Unroll - 1) / (kHist4Threads * kHist4Unroll);
+  if (n_chunk == 0) return cudaSuccess;
+  int64_t blocks = (n_chunk + kHist4Threads * kHist4Unroll - 1) / (kHist4Threads * kHist4Unroll);
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, sm_count()));
   g4_hist_kernel<<<(unsigned)blocks, kHist4Threads, smem, st>>>(h);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
-  G4PrefixArgs p{};
+cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
+  const Grid4Layout L = grid4_layout(glen);
+  float* H = reinterpret_cast<float*>(ws + L.offH);
+  uint32_t* G0 = reinterpret_cast<uint32_t*>(ws + L.offG0);
+  cudaError_t e = cudaSuccess;
+
+  G4PlaneArgs p{};
   p.H = H;
   p.S = reinterpret_cast<unsigned long long*>(ws + L.offS);
-  p.H2 = H2;
-  p.S2 = reinterpret_cast<unsigned long long*>(ws + L.offS2);
+  p.R1 = reinterpret_cast<uint32_t*>(ws + L.offR1);
+  p.G0 = G0;
+  p.P0 = reinterpret_cast<uint32_t*>(ws + L.offP0);
   p.d0 = L.d0;
-  p.cols = L.d1 * L.d2p;
-  p.cols2 = L.d1p;
-  int nseg = 1;
-  while (nseg * kPre4MaxSeg < L.d0) nseg *= 2;
-  p.nseg = nseg;
-  p.seg_len = (L.d0 + nseg - 1) / nseg;
-  p.cpc = kPre4Threads / nseg;
-  const int64_t cols = (int64_t)p.cols + p.cols2;
-  g4_prefix0_kernel<<<(unsigned)((cols + p.cpc - 1) / p.cpc), kPre4Threads, 0, st>>>(p);
+  p.d1 = L.d1;
+  p.d2 = L.d2;
+  p.d2p = L.d2p;
+  p.d1p = L.d1p;
+  p.hp = L.hp;
+  p.half = (L.d0 + 1) / 2;
+  p.ns2 = std::max(1, std::min(kPlaneThreads / p.half, L.d2));
+  p.seg2 = (L.d2 + p.ns2 - 1) / p.ns2;
+  p.ns2 = (L.d2 + p.seg2 - 1) / p.seg2;
+  p.ns0 = std::max(1, std::min(kPlaneThreads / L.d2, p.half));
+  p.seg0 = (p.half + p.ns0 - 1) / p.ns0;
+  p.ns0 = (p.half + p.seg0 - 1) / p.seg0;
+  const size_t psmem = ((size_t)p.half * p.hp + kPlaneThreads + L.d2) * 16;
+  static std::atomic<int> smem_plane{0};
+  e = ensure_smem4(g4_plane_kernel, smem_plane, (size_t)kGrid4SlabMax);
+  if (e != cudaSuccess) return e;
+  g4_plane_kernel<<<(unsigned)(2 * L.d1), kPlaneThreads, psmem, st>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
+                        const int32_t* glen, uint8_t* ws, bool dirty, cudaStream_t st) {
+  cudaError_t e = grid4_accumulate(cert, corr, n_rec, grids, glen, ws, dirty, st);
+  if (e != cudaSuccess) return e;
+  return grid4_finish(glen, ws, st);
 }
 
 cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct_begin,
@@ -531,24 +734,37 @@ cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct
   a.rcp_n = 1.0 / (double)n_rec;
   a.cost1 = cost1;
   a.S = reinterpret_cast<const unsigned long long*>(ws + L.offS);
-  a.S2 = reinterpret_cast<const unsigned long long*>(ws + L.offS2);
+  a.R1 = reinterpret_cast<const uint32_t*>(ws + L.offR1);
+  a.P0 = reinterpret_cast<const uint32_t*>(ws + L.offP0);
   a.acc = acc;
   a.cost = cost;
   a.frac = frac;
   a.n_correct = n_correct;
-  // column parts so that every slab's walk spreads over >= 2 CTAs when the
-  // slabs alone cannot fill the GPU; row segments fill the CTA
-  a.parts = (L.d0 < 2 * sm_count() && L.d2 >= 16) ? 2 : 1;
-  a.width = (L.d2 + a.parts - 1) / a.parts;
-  a.nseg = std::max(1, std::min(kEval4Threads / a.width, L.d1));
-  a.seg_len = (L.d1 + a.nseg - 1) / a.nseg;
-  a.nseg = (L.d1 + a.seg_len - 1) / a.seg_len;
-  const size_t smem = (size_t)L.d1 * L.d2p * 8;
-  static std::atomic<int> smem_set{0};
-  cudaError_t e = ensure_smem4(g4_eval_kernel, smem_set, (size_t)kGrid4SlabMax);
+  a.half = (L.d1 + 1) / 2;
+  a.nseg = std::max(1, std::min(kEval4Threads / L.d2, a.half));
+  a.seg_len = (a.half + a.nseg - 1) / a.nseg;
+  a.nseg = (a.half + a.seg_len - 1) / a.seg_len;
+  const size_t smem = (size_t)a.half * L.d2p * 8 + (size_t)a.half * (8 + 8 + 8 + 4) +
+                      ((size_t)a.nseg + 2) * L.d2 * 8 + (size_t)L.d1 * 4;
+  const bool all = acc && cost && frac && (reinterpret_cast<uintptr_t>(frac) & 31u) == 0;
+  static std::atomic<int> smem_all{0}, smem_some{0};
+  cudaError_t e = all ? ensure_smem4(g4_eval_kernel<true>, smem_all, (size_t)kGrid4SlabMax)
+                      : ensure_smem4(g4_eval_kernel<false>, smem_some, (size_t)kGrid4SlabMax);
   if (e != cudaSuccess) return e;
-  g4_eval_kernel<<<(unsigned)(L.d0 * a.parts), kEval4Threads, smem, st>>>(a);
+  if (all)
+    g4_eval_kernel<true><<<(unsigned)(2 * L.d0), kEval4Threads, smem, st>>>(a);
+  else
+    g4_eval_kernel<false><<<(unsigned)(2 * L.d0), kEval4Threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 }  // namespace gs
+
+#ifdef GS_PHASE_TIMING
+// phase-timing builds only: copy the stamps [kernel][cta][slot][globaltimer,
+// clock64] to host memory (kPhaseKernels * kPhaseCtas * kPhaseSlots * 2 u64)
+extern "C" int gs_debug_phases(unsigned long long* host) {
+  if (cudaMemcpyFromSymbol(host, gs::g_phase, sizeof(gs::g_phase)) != cudaSuccess) return GS_ECUDA;
+  return GS_OK;
+}
+#endif

@@ -11,11 +11,17 @@ constexpr size_t kGrid4SlabMax = 200 * 1024;      // one (b1, b2) slab in shared
 
 struct Grid4Layout {
   int32_t d0, d1, d2, d2p, d1p;  // table dims (grid length + 1), padded pitches
-  size_t offH, offH2, offS, offS2, bytes;
+  int32_t hp;                    // histogram row pitch (odd)
+  size_t offH, offG0, offS, offR1, offP0, bytes;
 };
 
 bool grid4_supported(int64_t n_rec, int32_t n_models, const int32_t* grid_len);
 Grid4Layout grid4_layout(const int32_t* grid_len);
+// accumulate: add n_chunk records to the histogram; finish: prefix tables
+cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_chunk,
+                             const double* grids, const int32_t* grid_len, uint8_t* workspace,
+                             bool dirty, cudaStream_t st);
+cudaError_t grid4_finish(const int32_t* grid_len, uint8_t* workspace, cudaStream_t st);
 cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
                         const int32_t* grid_len, uint8_t* workspace, bool dirty, cudaStream_t st);
 cudaError_t grid4_eval(int64_t n_rec, const int32_t* grid_len, const int64_t* struct_begin,

@@ -38,92 +38,87 @@ __device__ __forceinline__ int upper_count(const double* g, int n, double x) {
   return base + (g[base] <= x ? 1 : 0);
 }
 
-// Shared-memory bin tables of D models: the grids (f64) and per model one
-// bucket table of (lb | ub << 16) entries.
+// Shared-memory bin tables of D models (four-model path).  The bucket map
+// is one clamp of a truncated affine f64 map: monotone non-decreasing in x
+// (each rounded step is), NaN -> bucket 0 (cvt.rzi of NaN is 0, and NaN >=
+// g is false for every g, so its bin 0 is exact), +-inf saturate.  An entry
+// holds the bucket's first grid index and how many grid values it holds
+// (usually 0 or 1), so a lookup is one LDS plus at most one f64 compare.
+__device__ __forceinline__ int bucket_of(double x, double lo, double scale) {
+  const int q = (int)__dmul_rn(__dadd_rn(x, -lo), scale);
+  return min(max(q, 0), kLutBuckets - 1);
+}
+
+template <int D>
 struct BinTables {
-  const double* grid;     // smem, concatenated grids
-  const uint32_t* lut;    // smem, [D][kLutBuckets]
-  const int32_t* goff;    // grid offsets (kernel params)
-  double lo[GS_MAX_MODELS], hi[GS_MAX_MODELS], scale[GS_MAX_MODELS];
+  const double* grid;   // smem, concatenated grids of models 0..D-1
+  const uint32_t* lut;  // smem, [D][kLutBuckets]: first index | count << 16
+  int goff[D];
+  double lo[D], scale[D];
 
   __device__ __forceinline__ int bin(int j, double x) const {
-    const uint32_t e = lut[j * kLutBuckets + lut_bucket(x, lo[j], hi[j], scale[j])];
-    const int lb = (int)(e & 0xffffu), ub = (int)(e >> 16);
-    return lb + (ub > lb ? upper_count(grid + goff[j] + lb, ub - lb, x) : 0);
+    const uint32_t e = lut[j * kLutBuckets + bucket_of(x, lo[j], scale[j])];
+    const int lb = (int)(e & 0xffffu), c = (int)(e >> 16);
+    const double* g = grid + goff[j] + lb;
+    if (c == 0) return lb;
+    if (c == 1) return lb + (g[0] <= x ? 1 : 0);
+    return lb + upper_count(g, c, x);
   }
 };
 
-// Build the bin tables of models 0..D-1 in shared memory.  Every thread of
-// the block must call it (it synchronises).  s_grid holds n_grid doubles,
-// s_lut D * kLutBuckets words, s_par 3 * D doubles.  THREADS = blockDim.x.
-template <int THREADS>
-__device__ __forceinline__ BinTables build_bin_tables(const double* grids, const int32_t* goff,
-                                                      const int32_t* glen, int D, int n_grid,
-                                                      double* s_grid, uint32_t* s_lut,
-                                                      double* s_par) {
-  static_assert(kLutBuckets % THREADS == 0 || THREADS % kLutBuckets == 0, "bucket split");
-  for (int i = threadIdx.x; i < n_grid; i += THREADS) s_grid[i] = grids[i];
-  for (int i = threadIdx.x; i < D * kLutBuckets; i += THREADS) s_lut[i] = 0u;
-  __syncthreads();
-  if ((int)threadIdx.x < D) {
-    const int j = threadIdx.x;
-    const double* g = s_grid + goff[j];
-    const int n = glen[j];
-    s_par[j] = g[0];
-    s_par[GS_MAX_MODELS + j] = g[n - 1];
-    s_par[2 * GS_MAX_MODELS + j] = n > 1 ? (double)kLutBuckets / (g[n - 1] - g[0]) : 0.0;
-  }
-  __syncthreads();
+// Build the tables in shared memory; every thread of the block calls it (two
+// barriers).  s_grid holds the D grids, s_lut D * kLutBuckets words.  Every
+// thread derives lo / scale itself.  Per model, a thread owns kLutBuckets /
+// THREADS consecutive buckets: one binary search (over the monotone bucket
+// index of the grid values) finds the first grid index of its first bucket,
+// then it walks its buckets and the grid values inside them.  The work is
+// balanced however unevenly the grid values fall into buckets.
+template <int D, int THREADS>
+__device__ __forceinline__ BinTables<D> build_bin_tables(const double* grids, const int32_t* glen,
+                                                         double* s_grid, uint32_t* s_lut) {
+  static_assert(kLutBuckets % THREADS == 0, "bucket split");
+  constexpr int per = kLutBuckets / THREADS;
+  BinTables<D> t;
+  int n_grid = 0;
+#pragma unroll
   for (int j = 0; j < D; ++j) {
-    const double lo = s_par[j], hi = s_par[GS_MAX_MODELS + j], sc = s_par[2 * GS_MAX_MODELS + j];
-    for (int i = threadIdx.x; i < glen[j]; i += THREADS)
-      atomicAdd(s_lut + j * kLutBuckets + lut_bucket(s_grid[goff[j] + i], lo, hi, sc), 1u);
+    t.goff[j] = n_grid;
+    n_grid += glen[j];
   }
+  for (int i = threadIdx.x; i < n_grid; i += THREADS) s_grid[i] = grids[i];
   __syncthreads();
-  // per model: exclusive scan of the bucket counts -> (lb, ub), whole block
-  {
-    __shared__ uint32_t s_wsum[THREADS / 32];
-    constexpr int per = kLutBuckets >= THREADS ? kLutBuckets / THREADS : 1;
-    const int warp = threadIdx.x >> 5, lane = (int)lane_id();
-    for (int j = 0; j < D; ++j) {
-      uint32_t* L = s_lut + j * kLutBuckets + threadIdx.x * per;
-      const bool own = (int)threadIdx.x * per < kLutBuckets;
-      uint32_t c[per], tot = 0;
+  const int q0 = threadIdx.x * per;
 #pragma unroll
-      for (int q = 0; q < per; ++q) {
-        c[q] = own ? L[q] : 0u;
-        tot += c[q];
+  for (int j = 0; j < D; ++j) {
+    const double* g = s_grid + t.goff[j];
+    const int n = glen[j];
+    const double lo = g[0];
+    const double scale = n > 1 ? (double)kLutBuckets / (g[n - 1] - g[0]) : 0.0;
+    t.lo[j] = lo;
+    t.scale[j] = scale;
+    // k = #{grid values whose bucket < q0}
+    int k = 0, len = n;
+    while (len > 0) {
+      const int half = len >> 1;
+      if (bucket_of(g[k + half], lo, scale) < q0) {
+        k += half + 1;
+        len -= half + 1;
+      } else {
+        len = half;
       }
-      uint32_t incl = tot;
+    }
+    uint32_t* L = s_lut + j * kLutBuckets;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) s_wsum[warp] = incl;
-      __syncthreads();
-      uint32_t run = incl - tot;
-      for (int w = 0; w < warp; ++w) run += s_wsum[w];
-      if (own) {
-#pragma unroll
-        for (int q = 0; q < per; ++q) {
-          L[q] = run | ((run + c[q]) << 16);
-          run += c[q];
-        }
-      }
-      __syncthreads();
+    for (int q = q0; q < q0 + per; ++q) {
+      int c = 0;
+      while (k + c < n && bucket_of(g[k + c], lo, scale) == q) ++c;
+      L[q] = (uint32_t)k | ((uint32_t)c << 16);
+      k += c;
     }
   }
-  BinTables t;
+  __syncthreads();
   t.grid = s_grid;
   t.lut = s_lut;
-  t.goff = goff;
-#pragma unroll
-  for (int j = 0; j < GS_MAX_MODELS; ++j) {
-    t.lo[j] = j < D ? s_par[j] : 0.0;
-    t.hi[j] = j < D ? s_par[GS_MAX_MODELS + j] : 0.0;
-    t.scale[j] = j < D ? s_par[2 * GS_MAX_MODELS + j] : 0.0;
-  }
   return t;
 }
 

@@ -1346,6 +1346,35 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   return GS_OK;
 }
 
+extern "C" int gs_grid_accumulate(const double* certainty, const uint8_t* correct, int64_t n_chunk,
+                                  int64_t n_rec, int32_t n_models, const double* grids,
+                                  const int32_t* grid_len, void* workspace, size_t workspace_bytes,
+                                  int32_t flags, void* stream) {
+  Plan p;
+  int rc = make_plan(n_rec, n_models, grid_len, &p);
+  if (rc != GS_OK) return rc;
+  if (!p.g4) return GS_EUNSUPPORTED;
+  GS_REQUIRE(n_chunk >= 0 && n_chunk <= n_rec && grids && (n_chunk == 0 || (certainty && correct)));
+  if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
+  GS_CUDA_TRY(grid4_accumulate(certainty, correct, n_chunk, grids, p.glen,
+                               static_cast<uint8_t*>(workspace),
+                               (flags & GS_GRID_WORKSPACE_DIRTY) != 0,
+                               static_cast<cudaStream_t>(stream)));
+  return GS_OK;
+}
+
+extern "C" int gs_grid_finish(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  Plan p;
+  int rc = make_plan(n_rec, n_models, grid_len, &p);
+  if (rc != GS_OK) return rc;
+  if (!p.g4) return GS_EUNSUPPORTED;
+  if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
+  GS_CUDA_TRY(grid4_finish(p.glen, static_cast<uint8_t*>(workspace),
+                           static_cast<cudaStream_t>(stream)));
+  return GS_OK;
+}
+
 extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
                             const double* cost1, int64_t config_begin, int64_t config_count,
                             double* accuracy, double* mean_cost, double* forward_frac,

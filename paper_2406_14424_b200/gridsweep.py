@@ -114,6 +114,53 @@ class GridSweep:
         _lib.check(rc, "grid build")
         self._built = True
 
+    def build_streamed(self, certainty_host: torch.Tensor, correct_host: torch.Tensor,
+                       chunks: int = 8) -> None:
+        """Build from HOST matrices (pinned torch tensors of this sweep's
+        shape), overlapping the host->device copy of each record slice with
+        the binning of the previous ones (gs_grid_accumulate per slice on the
+        current stream, copies on a side stream, then gs_grid_finish).  The
+        copies land in this sweep's device matrices.  Four-model fast path
+        only (gs_grid_info.fast_path)."""
+        if not self.info.fast_path:
+            raise ValueError("streamed build needs the four-model fast path "
+                             "(gs_grid_info.fast_path == 0 for this shape)")
+        if (tuple(certainty_host.shape) != tuple(self.cert.shape)
+                or tuple(correct_host.shape) != tuple(self.corr.shape)
+                or certainty_host.dtype != torch.float64 or correct_host.dtype != torch.uint8):
+            raise ValueError("host matrices must match the sweep's [n_rec, n_models] f64 / u8")
+        lib = _lib.load()
+        main = torch.cuda.current_stream()
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream()
+        copy = self._copy_stream
+        copy.wait_stream(main)  # earlier work on the device matrices is done
+        flags = 0 if self._clean else GS_GRID_WORKSPACE_DIRTY
+        bounds = np.linspace(0, self.n_rec, max(1, int(chunks)) + 1).astype(np.int64)
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            lo, hi = int(lo), int(hi)
+            if hi <= lo:
+                continue
+            with torch.cuda.stream(copy):
+                self.cert[lo:hi].copy_(certainty_host[lo:hi], non_blocking=True)
+                self.corr[lo:hi].copy_(correct_host[lo:hi], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(copy)
+            main.wait_event(done)
+            rc = lib.gs_grid_accumulate(self.cert[lo:].data_ptr(), self.corr[lo:].data_ptr(),
+                                        hi - lo, self.n_rec, self.n_models,
+                                        self.grids.data_ptr(), self._glen,
+                                        self.table.data_ptr(), self.table.numel(), flags,
+                                        main.cuda_stream)
+            _lib.check(rc, "grid accumulate")
+            flags = 0
+        self._clean = False  # the histogram holds records until finish
+        rc = lib.gs_grid_finish(self.n_rec, self.n_models, self._glen, self.table.data_ptr(),
+                                self.table.numel(), main.cuda_stream)
+        _lib.check(rc, "grid finish")
+        self._clean = True
+        self._built = True
+
     # -- scoring -----------------------------------------------------------
     def evaluate(self, begin: int = 0, count: int | None = None, *, accuracy: bool = True,
                  mean_cost: bool = True, forward_frac: bool = True,

@@ -223,3 +223,38 @@ def test_four_models_past_packed_field_range():
     assert np.array_equal(res.accuracy.cpu().numpy()[pick], want[0])
     assert np.array_equal(res.mean_cost.cpu().numpy()[pick], want[1])
     assert np.array_equal(res.forward_frac.cpu().numpy()[pick], want[2])
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_streamed_build_equals_build(chunks):
+    """gs_grid_accumulate over host slices (copies overlapped with binning)
+    + gs_grid_finish gives the same tables as one gs_grid_build."""
+    import torch
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    rng = np.random.default_rng(chunks)
+    cert, corr, grids, cost1 = _random_case(rng, 50_001, 4, 15)
+    ref = GridSweep(cert, corr, grids, cost1).evaluate(n_correct=True)
+    host_c = torch.from_numpy(cert).pin_memory()
+    host_k = torch.from_numpy(corr).pin_memory()
+    dev_c = torch.zeros(cert.shape, dtype=torch.float64, device="cuda")
+    dev_k = torch.zeros(corr.shape, dtype=torch.uint8, device="cuda")
+    sw = GridSweep(dev_c, dev_k, grids, cost1, build=False)
+    assert sw.info.fast_path == 1
+    for _ in range(2):  # a second streamed build on the same workspace
+        sw.build_streamed(host_c, host_k, chunks=chunks)
+        got = sw.evaluate(n_correct=True)
+        for a, b in ((got.accuracy, ref.accuracy), (got.mean_cost, ref.mean_cost),
+                     (got.forward_frac, ref.forward_frac), (got.n_correct, ref.n_correct)):
+            assert torch.equal(a, b)
+    assert torch.equal(dev_c.cpu(), host_c)
+
+
+def test_streamed_build_rejects_general_path():
+    import torch
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    rng = np.random.default_rng(3)
+    cert, corr, grids, cost1 = _random_case(rng, 1000, 3, 5)
+    sw = GridSweep(cert, corr, grids, cost1, build=False)
+    assert sw.info.fast_path == 0
+    with pytest.raises(ValueError):
+        sw.build_streamed(torch.from_numpy(cert), torch.from_numpy(corr))
