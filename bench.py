@@ -149,7 +149,7 @@ def run_ours(args, world, rank, local):
 
     from oracle import oracle
     from paper_2406_14424_b200 import distributed as gdist
-    from paper_2406_14424_b200.gridsweep import GridSweep, pareto_counts
+    from paper_2406_14424_b200.gridsweep import GridSweep, front_host, pareto_counts
 
     profiles, cert, corr, grids, cost1 = workload(seed=rank)  # one tenant per rank
     sw = GridSweep(cert, corr, grids, cost1, build=False)
@@ -158,6 +158,18 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", torch.cuda.current_device())
     out = None
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    flush_read = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def flush_l2():
+        """Evict the L2 between timed steps: write 512 MB (> 126 MB L2); with
+        --flush clean also read another 512 MB, so the L2 is left holding
+        clean lines and the next step does not pay the write-back of the
+        flush buffer's dirty lines (our data is evicted either way)."""
+        if args.flush == "none":
+            return
+        flush.zero_()
+        if args.flush == "clean":
+            flush_read.sum()
 
     sw.build()
     out = sw.evaluate()
@@ -178,7 +190,7 @@ def run_ours(args, world, rank, local):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(n)]
         for i in range(n):
-            flush.zero_()
+            flush_l2()
             ev[i][0].record(stream)
             graph.replay()
             ev[i][1].record(stream)
@@ -193,6 +205,18 @@ def run_ours(args, world, rank, local):
     value = world * C / (step_ms * 1e-3)
     build_ms = timed(g_build, args.steps)
     eval_ms = timed(g_eval, args.steps)
+    part_ms = {}
+    if sw.info.fast_path:
+        # each kernel alone (the plane graph replays over the histogram the
+        # hist graph leaves, so they alternate; the workspace stays valid)
+        g_hist = sw.capture(out, part="hist")
+        g_plane = sw.capture(out, part="plane")
+        hist_t, plane_t = [], []
+        for _ in range(args.steps):
+            hist_t += timed(g_hist, 1)
+            plane_t += timed(g_plane, 1)
+        part_ms = {"g4_hist": sum(hist_t) / args.steps, "g4_plane": sum(plane_t) / args.steps,
+                   "g4_eval": sum(eval_ms) / args.steps}
 
     # correctness spot-check of the timed outputs (rank 0, sampled configs)
     check = None
@@ -218,17 +242,17 @@ def run_ours(args, world, rank, local):
 
     def e2e_step():
         nonlocal e2e_out, d2h_total
-        # H2D of each record slice overlapped with the binning of the last
-        sw_e2e.build_streamed(pin_cert, pin_corr, chunks=8)
+        dcert.copy_(pin_cert, non_blocking=True)
+        dcorr.copy_(pin_corr, non_blocking=True)
+        sw_e2e.build()
         e2e_out = sw_e2e.evaluate(n_correct=True, out=e2e_out)
         idx = pareto_counts(e2e_out.n_correct, e2e_out.mean_cost, N_REC)
         front = gdist.gather_fronts(idx, e2e_out, world) if world > 1 else None
-        host = [idx.cpu(), e2e_out.accuracy[idx].cpu(), e2e_out.mean_cost[idx].cpu(),
-                e2e_out.forward_frac[idx].cpu()]
-        d2h_total = sum(t.numel() * t.element_size() for t in host)
+        rows = front_host(idx, e2e_out)  # one pinned D2H: [index, acc, cost, frac...]
+        d2h_total = rows.nbytes + 8  # + the front size
         if front is not None:
             d2h_total += front.numel() * front.element_size()
-        return host
+        return rows
 
     for _ in range(args.warmup):
         e2e_step()
@@ -237,7 +261,7 @@ def run_ours(args, world, rank, local):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        flush.zero_()  # same L2 state as the device-timed loop
+        flush_l2()  # same L2 state as the device-timed loop
         e2e_step()
     t1.record(stream)
     barrier(world)
@@ -247,7 +271,7 @@ def run_ours(args, world, rank, local):
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
-        flush.zero_()
+        flush_l2()
     f1.record(stream)
     torch.cuda.synchronize()
     flush_ms = f0.elapsed_time(f1) / args.steps
@@ -256,18 +280,25 @@ def run_ours(args, world, rank, local):
     # ---- stage step (config 3 shape: 1M x 1000-class f32 logits, entropy)
     stage = stage_bench(args, dev, flush) if (rank == 0 and not args.skip_stage) else None
 
-    # ---- roofline for the dominant kernel phase
+    # ---- roofline for the dominant kernel (each kernel timed alone above)
     pk = peaks()
     b_in = N_REC * N_MODELS * 9
     b_out = C * (16 + 8 * L)
     build_avg = sum(build_ms) / args.steps
     eval_avg = sum(eval_ms) / args.steps
-    if eval_avg >= build_avg:
-        dom, dom_bytes, dom_ms = "grid_eval_kernel (epilogue: acc, cost, frac per config)", b_out, eval_avg
+    alg_bytes = {"g4_hist": b_in, "g4_eval": b_out, "build": b_in, "eval": b_out}
+    if part_ms:
+        dom = max(("g4_hist", "g4_eval"), key=lambda k: part_ms[k])
+        dom_ms = part_ms[dom]
     else:
-        dom, dom_bytes, dom_ms = "grid build (hist + prefix scans)", b_in, build_avg
+        dom, dom_ms = ("eval", eval_avg) if eval_avg >= build_avg else ("build", build_avg)
+    dom_bytes = alg_bytes[dom]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_gbs = (b_in + b_out) / (step_ms * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "r1_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(dom)
 
     cpu = cpu_baseline(cert, corr, grids, cost1, args) if (rank == 0 and not args.no_cpu) else None
     if rank == 0:
@@ -278,18 +309,22 @@ def run_ours(args, world, rank, local):
             "data": "synthetic (reference make_validation semantics, default_rng(rank))",
             "config": {"workload": WORKLOAD, "n_records": N_REC, "n_models": N_MODELS,
                        "grid_levels": LEVELS, "n_configs_per_gpu": C,
-                       "cost_ratios": list(COST_RATIOS), "l2": "flushed (512 MB write) "
-                       "between timed steps", "parallelism": f"weak: 1 tenant sweep per GPU, "
+                       "cost_ratios": list(COST_RATIOS),
+                       "l2": {"write": "flushed between timed steps: 512 MB write",
+                              "clean": "flushed between timed steps: 512 MB write + 512 MB "
+                                       "read (clean lines left)",
+                              "none": "not flushed"}[args.flush], "parallelism": f"weak: 1 tenant sweep per GPU, "
                        f"NCCL all-gather of Pareto fronts in e2e ({world} ranks)"},
-            "breakdown_ms": {"build": build_avg, "eval": eval_avg},
+            "breakdown_ms": {"build": build_avg, "eval": eval_avg, **part_ms},
             "e2e": {"value": world * C / (e2e_ms * 1e-3), "unit": "config-evals/s",
                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h_total,
-                    "path": "GridSweep.build_streamed from pinned host matrices (8 slices, "
-                            "H2D overlapped with binning) -> eval -> pareto_counts -> D2H front"},
+                    "path": "GridSweep from pinned host matrices -> build -> eval -> "
+                            "pareto_counts -> D2H front rows"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                          "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                         "traffic": None, "algorithmic_bytes": dom_bytes,
+                         "traffic": traffic, "algorithmic_bytes": dom_bytes,
+                         "kernel_ms": dom_ms,
                          "peak_source": pk["source"],
                          "step": {"bytes": b_in + b_out, "achieved": step_gbs,
                                   "frac": step_gbs / pk["hbm_gbs"]}},
@@ -406,6 +441,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--skip-stage", action="store_true", help="skip the stage-step leg")
+    ap.add_argument("--flush", choices=["write", "clean", "none"], default="write",
+                    help="L2 eviction between timed steps (see flush_l2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="CPU time budget of the cpu_baseline sample")
     args = ap.parse_args()

@@ -92,7 +92,8 @@ cudaError_t ensure_smem4(Kernel k, std::atomic<int>& done, size_t bytes) {
 
 // ------------------------------------------------------------------ hist --
 constexpr int kHist4Threads = 1024;
-constexpr int kHist4Unroll = 4;
+constexpr int kHist4Unroll = 2;                          // records per thread per chunk
+constexpr int kHist4Chunk = kHist4Threads * kHist4Unroll;  // records per chunk
 constexpr int kMaxDim4 = 256;  // d0, d2 bound of this path
 
 struct G4HistArgs {
@@ -105,6 +106,7 @@ struct G4HistArgs {
   int32_t d0, hp;
   float* H;      // [d1][d0][hp] float4 {cnt, c3, c2, c1}
   uint32_t* G0;  // [d0] model-0 correct counts per b0
+  uint32_t* counters;  // [0] chunks handed out, [1] CTAs done (both 0 between launches)
 };
 
 struct Rec4 {
@@ -132,29 +134,59 @@ __device__ __forceinline__ Rec4 load_rec4(const G4HistArgs& a, int r) {
   return v;
 }
 
+// Records are taken in chunks of kHist4Chunk: a CTA's first chunk is its
+// block index (its loads go out before the bin tables are built), later ones
+// come from a global counter, one chunk ahead, so CTAs on slower SMs simply
+// take fewer chunks.  The last CTA to finish resets the counters.
 __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_constant__ G4HistArgs a) {
   extern __shared__ __align__(16) double s_grid[];  // grids 0..2, then the bucket tables
   __shared__ uint32_t s_c0[kMaxDim4];
+  __shared__ int s_next[2];
   const int n_grid = a.glen[0] + a.glen[1] + a.glen[2];
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + n_grid);
+  const int tid = threadIdx.x;
   phase(0, 0);
-  const int stride = gridDim.x * kHist4Threads;
-  int r0 = blockIdx.x * kHist4Threads + threadIdx.x;
-  // the first records are in flight while the bin tables are built
+  // grid values first, then the first chunk's records: the records stream
+  // in while the bin tables are built, and the grid loads are not queued
+  // behind them
+  constexpr int kGridRegs = 5;  // n_grid <= 5 * 1024 on this path
+  double gv[kGridRegs];
+#pragma unroll
+  for (int q = 0; q < kGridRegs; ++q) {
+    const int i = tid + q * kHist4Threads;
+    gv[q] = i < n_grid ? __ldg(a.grids + i) : 0.0;
+  }
+  int c = blockIdx.x;
   Rec4 v[kHist4Unroll];
 #pragma unroll
   for (int u = 0; u < kHist4Unroll; ++u) {
-    const int r = r0 + u * stride;
+    const int r = c * kHist4Chunk + u * kHist4Threads + tid;
     if (r < a.n_rec) v[u] = load_rec4(a, r);
   }
-  for (int i = threadIdx.x; i < a.d0; i += kHist4Threads) s_c0[i] = 0u;
-  const BinTables<3> bt = build_bin_tables<3, kHist4Threads>(a.grids, a.glen, s_grid, s_lut);
+  if (tid == 0) s_next[0] = gridDim.x + (int)atomicAdd(a.counters, 1u);
+#pragma unroll
+  for (int q = 0; q < kGridRegs; ++q) {
+    const int i = tid + q * kHist4Threads;
+    if (i < n_grid) s_grid[i] = gv[q];
+  }
+  for (int i = tid; i < a.d0; i += kHist4Threads) s_c0[i] = 0u;
+  __syncthreads();
+  const BinTables<3> bt = build_bin_tables<3, kHist4Threads>(a.glen, s_grid, s_lut);
   phase(0, 1);
   const int d0 = a.d0, hp = a.hp;
-  while (r0 < a.n_rec) {
+  int slot = 0;
+  while (c * kHist4Chunk < a.n_rec) {
+    const int cn = s_next[slot];
+    Rec4 nv[kHist4Unroll];
 #pragma unroll
     for (int u = 0; u < kHist4Unroll; ++u) {
-      if (r0 + u * stride >= a.n_rec) break;
+      const int r = cn * kHist4Chunk + u * kHist4Threads + tid;
+      if (r < a.n_rec) nv[u] = load_rec4(a, r);
+    }
+    if (tid == 0) s_next[slot ^ 1] = gridDim.x + (int)atomicAdd(a.counters, 1u);
+#pragma unroll
+    for (int u = 0; u < kHist4Unroll; ++u) {
+      if (c * kHist4Chunk + u * kHist4Threads + tid >= a.n_rec) break;
       const int b0 = bt.bin(0, v[u].x0);
       const int b1 = bt.bin(1, v[u].x1);
       const int b2 = bt.bin(2, v[u].x2);
@@ -165,23 +197,29 @@ __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_
       red_add_v4(a.H + 4ull * cell, 1.f, k3, k2, k1);
       if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
     }
-    r0 += kHist4Unroll * stride;
+    __syncthreads();  // s_next[slot ^ 1] visible; s_next[slot] free for reuse
 #pragma unroll
-    for (int u = 0; u < kHist4Unroll; ++u) {
-      const int r = r0 + u * stride;
-      if (r < a.n_rec) v[u] = load_rec4(a, r);
-    }
+    for (int u = 0; u < kHist4Unroll; ++u) v[u] = nv[u];
+    c = cn;
+    slot ^= 1;
   }
   phase(0, 2);
-  __syncthreads();
   phase(0, 3);
-  for (int i = threadIdx.x; i < a.d0; i += kHist4Threads)
+  for (int i = tid; i < a.d0; i += kHist4Threads)
     if (s_c0[i]) atomicAdd(a.G0 + i, s_c0[i]);
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.counters + 1, 1u) == gridDim.x - 1) {  // last CTA: reset for the next launch
+      a.counters[0] = 0u;
+      a.counters[1] = 0u;
+    }
+  }
   phase(0, 4);
 }
 
 // ----------------------------------------------------------------- plane --
-constexpr int kPlaneThreads = 1024;
+constexpr int kPlaneThreads = 512;
+constexpr int kZeroBytes = 16384;  // zero source of the bulk stores that re-zero H
 
 struct G4PlaneArgs {
   float* H;                  // [d1][d0][hp] float4, re-zeroed here
@@ -196,24 +234,31 @@ struct G4PlaneArgs {
   int32_t ns0, seg0;         // b0 segments of the column walk
 };
 
-__device__ __forceinline__ uint4 f4_to_u4(float4 f) {
-  return make_uint4(__float2uint_rn(f.x), __float2uint_rn(f.y), __float2uint_rn(f.z),
-                    __float2uint_rn(f.w));
+__device__ __forceinline__ float4 add4f(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
-__device__ __forceinline__ uint4 add4u(uint4 a, uint4 b) {
-  return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+// exact f32 integer in [0, 2^23) -> u32 without the conversion unit
+__device__ __forceinline__ uint32_t f2u_exact(float f) {
+  return __float_as_uint(f + 8388608.f) - 0x4B000000u;
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
 }
 
 // The (b0, b2) plane of one b1 is contiguous in H ([b1][b0][hp]).  A
 // cluster of two CTAs owns it, split along b0: each CTA bulk-copies its half
-// of the rows, re-zeroes them, walks its rows along b2, and walks its
-// columns along b0; the first CTA hands its column totals to the second
-// through distributed shared memory as the b0 carry.  Both prefixes are
-// serial walks (one add per cell and channel, no shuffles), two-level so
-// that ~1000 threads share them, segment carries through shared memory.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 1)
+// of the rows, re-zeroes them with bulk stores from a zeroed shared buffer,
+// walks its rows along b2 and its columns along b0; the first CTA hands its
+// column totals to the second through distributed shared memory as the b0
+// carry.  The counts stay f32 through both walks (exact below 2^24) and are
+// packed once.  Both walks are serial (one add per cell and channel, no
+// shuffles) and two-level so that the whole CTA shares them.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
     g4_plane_kernel(const __grid_constant__ G4PlaneArgs a) {
-  extern __shared__ __align__(16) uint4 s_tile[];  // [rows][hp], segment sums, peer carry
+  extern __shared__ __align__(16) float4 s_tile[];  // [rows][hp], seg sums, carry, zeros
   __shared__ __align__(8) uint64_t bar;
   cg::cluster_group cluster = cg::this_cluster();
   const int h = (int)cluster.block_rank();
@@ -222,8 +267,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 1)
   const int r_beg = h ? a.half : 0, r_end = h ? d0 : a.half, nr = r_end - r_beg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kPlaneThreads / 32;
-  uint4* s_seg = s_tile + (size_t)a.half * hp;
-  uint4* s_carry = s_seg + kPlaneThreads;  // [d2] column totals of the first half (rank 1)
+  float4* s_seg = s_tile + (size_t)a.half * hp;
+  float4* s_carry = s_seg + kPlaneThreads;  // [d2] column totals of the first half (rank 1)
+  float4* s_zero = s_carry + d2;            // kZeroBytes of zeros
   const uint32_t tile_bytes = (uint32_t)(nr * hp * sizeof(float4));
   float4* H = reinterpret_cast<float4*>(a.H) + ((int64_t)b1 * d0 + r_beg) * hp;
   const int64_t plane = (int64_t)a.d1 * a.d2p;  // S cells per b0 slab
@@ -232,6 +278,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 1)
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
+  for (int i = tid; i < kZeroBytes / 16; i += kPlaneThreads) s_zero[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  fence_proxy_async();  // the zero buffer is read by the async proxy (bulk stores)
   __syncthreads();
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar, tile_bytes);
@@ -260,25 +308,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 1)
   }
   mbar_wait(&bar, 0);
   phase(1, 1);
-  // re-zero the histogram rows just read (the next build starts from zero)
-  for (int i = tid; i < nr * hp; i += kPlaneThreads) H[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  // re-zero the histogram rows just read (the next build starts from zero):
+  // bulk stores from the zero buffer, issued by one thread, asynchronous
+  if (tid == 0) {
+    for (uint32_t off = 0; off < tile_bytes; off += kZeroBytes)
+      bulk_s2g(reinterpret_cast<uint8_t*>(H) + off, s_zero, min((uint32_t)kZeroBytes, tile_bytes - off));
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
   phase(1, 2);
-  // row walk along b2 (f32 counts -> u32 on the way)
+  // row walk along b2
   {
     const int r = tid % nr, s = tid / nr;
     const bool live = s < a.ns2;
     const int c_lo = s * a.seg2, c_hi = min(d2, c_lo + a.seg2);
-    uint4* row = s_tile + (size_t)r * hp;
-    uint4 sum = make_uint4(0, 0, 0, 0);
+    float4* row = s_tile + (size_t)r * hp;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live)
-      for (int c = c_lo; c < c_hi; ++c) sum = add4u(sum, f4_to_u4(*reinterpret_cast<float4*>(row + c)));
+      for (int c = c_lo; c < c_hi; ++c) sum = add4f(sum, row[c]);
     if (live) s_seg[s * nr + r] = sum;
     __syncthreads();
     if (live) {
-      uint4 run = make_uint4(0, 0, 0, 0);
-      for (int q = 0; q < s; ++q) run = add4u(run, s_seg[q * nr + r]);
+      float4 run = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < s; ++q) run = add4f(run, s_seg[q * nr + r]);
       for (int c = c_lo; c < c_hi; ++c) {
-        run = add4u(run, f4_to_u4(*reinterpret_cast<float4*>(row + c)));
+        run = add4f(run, row[c]);
         row[c] = run;
       }
     }
@@ -289,29 +342,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 1)
   const int c = tid % d2, s = tid / d2;
   const bool live = s < a.ns0;
   const int r_lo = s * a.seg0, r_hi = min(nr, r_lo + a.seg0);
-  uint4 sum = make_uint4(0, 0, 0, 0);
+  float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
   if (live)
-    for (int r = r_lo; r < r_hi; ++r) sum = add4u(sum, s_tile[(size_t)r * hp + c]);
+    for (int r = r_lo; r < r_hi; ++r) sum = add4f(sum, s_tile[(size_t)r * hp + c]);
   if (live) s_seg[s * d2 + c] = sum;
   __syncthreads();
   if (h == 0 && s == 0) {
-    uint4 tot = make_uint4(0, 0, 0, 0);
-    for (int q = 0; q < a.ns0; ++q) tot = add4u(tot, s_seg[q * d2 + c]);
+    float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < a.ns0; ++q) tot = add4f(tot, s_seg[q * d2 + c]);
     *cluster.map_shared_rank(s_carry + c, 1) = tot;
   }
   cluster.sync();
   phase(1, 4);
-  if (!live) return;
-  uint4 P = h ? s_carry[c] : make_uint4(0, 0, 0, 0);
-  for (int q = 0; q < s; ++q) P = add4u(P, s_seg[q * d2 + c]);
-  unsigned long long* S = a.S + (int64_t)b1 * a.d2p + c;
-  for (int r = r_lo; r < r_hi; ++r) {
-    P = add4u(P, s_tile[(size_t)r * hp + c]);
-    const int64_t b0 = r_beg + r;
-    S[b0 * plane] = (unsigned long long)P.x | ((unsigned long long)P.y << 21) |
-                    ((unsigned long long)P.z << 42);
-    if (c == d2 - 1) a.R1[b0 * a.d1p + b1] = P.w;
+  if (live) {
+    float4 P = h ? s_carry[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < s; ++q) P = add4f(P, s_seg[q * d2 + c]);
+    unsigned long long* S = a.S + (int64_t)b1 * a.d2p + c;
+    for (int r = r_lo; r < r_hi; ++r) {
+      P = add4f(P, s_tile[(size_t)r * hp + c]);
+      const int64_t b0 = r_beg + r;
+      S[b0 * plane] = (unsigned long long)f2u_exact(P.x) |
+                      ((unsigned long long)f2u_exact(P.y) << 21) |
+                      ((unsigned long long)f2u_exact(P.z) << 42);
+      if (c == d2 - 1) a.R1[b0 * a.d1p + b1] = f2u_exact(P.w);
+    }
   }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   phase(1, 5);
 }
 
@@ -527,43 +583,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   __syncthreads();
 
   phase(2, 3);
-  // edge cells, one thread each (their prefixes are already known):
-  //   last column (k2 = g2): row totals s_colg; last row (k1 = g1, rank 1):
-  //   column totals = carry + own column sums; corner: the slab total
-  for (int r = tid; r < nr; r += kEval4Threads) {
-    const int k1 = rb + r;
-    if (k1 >= g1) continue;
-    const Cell3 p = unpack3(s_colg[r]);
-    if (!any0) {  // (0,1,2) and (0,1,3) at (k0, k1)
-      const uint32_t reach[2] = {tot.cnt, p.cnt};
-      const uint32_t c01 = base0 + (C1g - s_c1[k1]);
-      const double cst2[3] = {c0c, c1c, c2c}, cst3[3] = {c0c, c1c, c3c};
-      put4<3>(a, a.sb[7] + (int64_t)k0 * g1 + k1, reach, cst2, c01 + p.c2, n, rcp, one);
-      put4<3>(a, a.sb[11] + (int64_t)k0 * g1 + k1, reach, cst3, c01 + p.c3, n, rcp, one);
-    } else {  // (1,2), (1,3) at k1
-      const uint32_t reach[1] = {p.cnt};
-      const uint32_t c1 = C1g - s_c1[k1];
-      const double cA[2] = {c1c, c2c}, cB[2] = {c1c, c3c};
-      put4<2>(a, a.sb[6] + k1, reach, cA, c1 + p.c2, n, rcp, one);
-      put4<2>(a, a.sb[10] + k1, reach, cB, c1 + p.c3, n, rcp, one);
-    }
-  }
-  if (h == 1) {
-    for (int k2 = tid; k2 < g2; k2 += kEval4Threads) {  // last row: P = (k0, g1, k2)
-      const Cell3 p = unpack3(s_own[k2] + s_peer[k2]);
-      if (!any0) {  // (0,2,3) at (k0, k2)
-        const uint32_t reach[2] = {tot.cnt, p.cnt};
-        const double cst[3] = {c0c, c2c, c3c};
-        put4<3>(a, a.sb[13] + (int64_t)k0 * g2 + k2, reach, cst, base0 + (tot.c2 - p.c2) + p.c3,
-                n, rcp, one);
-      } else {  // (2,3) at k2
-        const uint32_t reach[1] = {p.cnt};
-        const double cst[2] = {c2c, c3c};
-        put4<2>(a, a.sb[12] + k2, reach, cst, (tot.c2 - p.c2) + p.c3, n, rcp, one);
-      }
-    }
-    if (tid == kEval4Threads - 1) {
-      if (!any0) {  // (0,1), (0,2), (0,3) at k0
+  // Threads [0, nwalk) walk the interior (column w % g2, row segment
+  // w / g2); the spare threads score the edge cells meanwhile (their
+  // prefixes are already known): last column (k2 = g2) from the row totals
+  // s_colg; last row (k1 = g1, rank 1) from the column totals carry + own
+  // column sums; the corner from the slab total.
+  const int nwalk = a.nseg * g2;
+  if (tid >= nwalk) {
+    const int n_row = min(nr, g1 - rb);          // own rows k1 < g1
+    const int n_col = h == 1 ? g2 : 0;           // last-row cells
+    const int n_items = n_row + n_col + (h == 1 ? 1 : 0);
+    for (int e = tid - nwalk; e < n_items; e += kEval4Threads - nwalk) {
+      if (e < n_row) {
+        const int k1 = rb + e;
+        const Cell3 p = unpack3(s_colg[e]);
+        if (!any0) {  // (0,1,2) and (0,1,3) at (k0, k1)
+          const uint32_t reach[2] = {tot.cnt, p.cnt};
+          const uint32_t c01 = base0 + (C1g - s_c1[k1]);
+          const double cst2[3] = {c0c, c1c, c2c}, cst3[3] = {c0c, c1c, c3c};
+          put4<3>(a, a.sb[7] + (int64_t)k0 * g1 + k1, reach, cst2, c01 + p.c2, n, rcp, one);
+          put4<3>(a, a.sb[11] + (int64_t)k0 * g1 + k1, reach, cst3, c01 + p.c3, n, rcp, one);
+        } else {  // (1,2), (1,3) at k1
+          const uint32_t reach[1] = {p.cnt};
+          const uint32_t c1 = C1g - s_c1[k1];
+          const double cA[2] = {c1c, c2c}, cB[2] = {c1c, c3c};
+          put4<2>(a, a.sb[6] + k1, reach, cA, c1 + p.c2, n, rcp, one);
+          put4<2>(a, a.sb[10] + k1, reach, cB, c1 + p.c3, n, rcp, one);
+        }
+      } else if (e < n_row + n_col) {  // last row: P = (k0, g1, k2)
+        const int k2 = e - n_row;
+        const Cell3 p = unpack3(s_own[k2] + s_peer[k2]);
+        if (!any0) {  // (0,2,3) at (k0, k2)
+          const uint32_t reach[2] = {tot.cnt, p.cnt};
+          const double cst[3] = {c0c, c2c, c3c};
+          put4<3>(a, a.sb[13] + (int64_t)k0 * g2 + k2, reach, cst, base0 + (tot.c2 - p.c2) + p.c3,
+                  n, rcp, one);
+        } else {  // (2,3) at k2
+          const uint32_t reach[1] = {p.cnt};
+          const double cst[2] = {c2c, c3c};
+          put4<2>(a, a.sb[12] + k2, reach, cst, (tot.c2 - p.c2) + p.c3, n, rcp, one);
+        }
+      } else if (!any0) {  // (0,1), (0,2), (0,3) at k0
         const uint32_t reach[1] = {tot.cnt};
         const double cA[2] = {c0c, c1c}, cB[2] = {c0c, c2c}, cC[2] = {c0c, c3c};
         put4<2>(a, a.sb[3] + k0, reach, cA, base0 + C1g, n, rcp, one);
@@ -578,19 +638,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
         put4<1>(a, a.sb[8], none, cD, tot.c3, n, rcp, one);
       }
     }
+    return;
   }
   phase(2, 4);
-  if (!live || col >= g2) return;
 
   // interior: the longest structure, one config per position (k1, k2),
   // k1 < g1, k2 < g2; its index is row_base + k1 * g2
-  unsigned long long P = h ? s_peer[col] : 0ull;
-  for (int q = 0; q < seg; ++q) P += s_seg[q * d2 + col];
+  const int wc = tid % g2, ws = tid / g2;
+  const int w_lo = ws * a.seg_len, w_hi = min(nr, w_lo + a.seg_len);
+  unsigned long long P = h ? s_peer[wc] : 0ull;
+  for (int q = 0; q < ws; ++q) P += s_seg[q * d2 + wc];
   const int64_t row_base =
-      (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + col - a.cfg_begin;
-  const int r_end = min(r_hi, g1 - rb);
-  for (int r = r_lo; r < r_end; ++r) {
-    P += s_slab[(size_t)r * d2p + col];
+      (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + wc - a.cfg_begin;
+  const int r_end = min(w_hi, g1 - rb);
+  for (int r = w_lo; r < r_end; ++r) {
+    P += s_slab[(size_t)r * d2p + wc];
     const int64_t i = row_base + (int64_t)(rb + r) * g2;
     if (!full && (i < 0 || i >= a.cfg_count)) continue;
     const Cell3 p = unpack3(P);
@@ -614,8 +676,9 @@ bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
   const int64_t d0 = glen[0] + 1, d1 = glen[1] + 1, d2 = glen[2] + 1;
   const int64_t d2p = (d2 + 1) & ~1ll;
   const int64_t grid_bytes = (int64_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * 4;
+  if (glen[0] + glen[1] + glen[2] > 5 * kHist4Threads) return false;
   // plane tile [d0][d2p] x 16 B plus segment sums; eval slab [d1][d2p] x 8 B
-  const int64_t plane_smem = ((d0 + 1) / 2 * (d2 | 1) + kPlaneThreads + d2) * 16;
+  const int64_t plane_smem = ((d0 + 1) / 2 * (d2 | 1) + kPlaneThreads + d2) * 16 + kZeroBytes;
   return d0 <= kMaxDim4 && d2 <= kMaxDim4 && d1 <= 4096 && grid_bytes <= 96 * 1024 &&
          d2 <= kPlaneThreads && plane_smem <= (int64_t)kGrid4SlabMax &&
          d2 <= kEval4Threads && d1 >= 2 &&
@@ -639,7 +702,8 @@ Grid4Layout grid4_layout(const int32_t* glen) {
   L.offS = bH + bG;
   L.offR1 = L.offS + bS;
   L.offP0 = L.offR1 + bR1;
-  L.bytes = L.offP0 + bG;
+  L.offCnt = L.offP0 + bG;
+  L.bytes = L.offCnt + 256;
   return L;
 }
 
@@ -651,6 +715,8 @@ cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_
   uint32_t* G0 = reinterpret_cast<uint32_t*>(ws + L.offG0);
   if (dirty) {
     cudaError_t e = cudaMemsetAsync(ws, 0, L.offS, st);  // H and G0
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ws + L.offCnt, 0, 256, st);
     if (e != cudaSuccess) return e;
   }
   G4HistArgs h{};
@@ -664,13 +730,14 @@ cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_
   h.hp = L.hp;
   h.H = H;
   h.G0 = G0;
+  h.counters = reinterpret_cast<uint32_t*>(ws + L.offCnt);
   const size_t smem =
       (size_t)(glen[0] + glen[1] + glen[2]) * sizeof(double) + 3 * kLutBuckets * sizeof(uint32_t);
   static std::atomic<int> smem_hist{0};
   cudaError_t e = ensure_smem4(g4_hist_kernel, smem_hist, smem);
   if (e != cudaSuccess) return e;
   if (n_chunk == 0) return cudaSuccess;
-  int64_t blocks = (n_chunk + kHist4Threads * kHist4Unroll - 1) / (kHist4Threads * kHist4Unroll);
+  int64_t blocks = (n_chunk + kHist4Chunk - 1) / kHist4Chunk;
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, sm_count()));
   g4_hist_kernel<<<(unsigned)blocks, kHist4Threads, smem, st>>>(h);
   return cudaGetLastError();
@@ -701,7 +768,7 @@ cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
   p.ns0 = std::max(1, std::min(kPlaneThreads / L.d2, p.half));
   p.seg0 = (p.half + p.ns0 - 1) / p.ns0;
   p.ns0 = (p.half + p.seg0 - 1) / p.seg0;
-  const size_t psmem = ((size_t)p.half * p.hp + kPlaneThreads + L.d2) * 16;
+  const size_t psmem = ((size_t)p.half * p.hp + kPlaneThreads + L.d2) * 16 + kZeroBytes;
   static std::atomic<int> smem_plane{0};
   e = ensure_smem4(g4_plane_kernel, smem_plane, (size_t)kGrid4SlabMax);
   if (e != cudaSuccess) return e;
@@ -741,7 +808,10 @@ cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct
   a.frac = frac;
   a.n_correct = n_correct;
   a.half = (L.d1 + 1) / 2;
-  a.nseg = std::max(1, std::min(kEval4Threads / L.d2, a.half));
+  // the same row segments serve the column sums (d2 columns) and the
+  // interior walk (g2 columns), leaving >= 32 threads for the edge cells
+  const int g2w = std::max(1, L.d2 - 1);
+  a.nseg = std::max(1, std::min(std::min((kEval4Threads - 32) / g2w, kEval4Threads / L.d2), a.half));
   a.seg_len = (a.half + a.nseg - 1) / a.nseg;
   a.nseg = (a.half + a.seg_len - 1) / a.seg_len;
   const size_t smem = (size_t)a.half * L.d2p * 8 + (size_t)a.half * (8 + 8 + 8 + 4) +

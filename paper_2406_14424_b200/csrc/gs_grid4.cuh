@@ -12,7 +12,7 @@ constexpr size_t kGrid4SlabMax = 200 * 1024;      // one (b1, b2) slab in shared
 struct Grid4Layout {
   int32_t d0, d1, d2, d2p, d1p;  // table dims (grid length + 1), padded pitches
   int32_t hp;                    // histogram row pitch (odd)
-  size_t offH, offG0, offS, offR1, offP0, bytes;
+  size_t offH, offG0, offS, offR1, offP0, offCnt, bytes;
 };
 
 bool grid4_supported(int64_t n_rec, int32_t n_models, const int32_t* grid_len);

@@ -7,7 +7,8 @@
 // gs_pareto_counts (sweep outputs, O(n + n_rec), no sort).  Accuracy is the
 // integer correct count a in [0, n_rec] (acc = a / n_rec is monotone in a).
 //   mincost[a]  = min cost over items with count a            (u64 atomicMin)
-//   above[a]    = min cost over items with count > a          (suffix min)
+//   above[a]    = min cost over items with count > a          (suffix min,
+//                 stored beside mincost[a] as one 16-byte pair)
 //   keep(i)     = cost_i == mincost[a_i]  &&  cost_i < above[a_i]
 // (an item with the same count and lower cost, or a higher count and cost
 // <=, is exactly what dominates it).  Costs are compared through an
@@ -80,11 +81,11 @@ __global__ void chunk_min_kernel(const unsigned long long* v, int64_t len, unsig
   }
 }
 
-// above[k] = min(v[k+1 ..]) ; 256 threads x 8 entries per chunk.
+// pair[k] = {v[k], min(v[k+1 ..])} ; 256 threads x 8 entries per chunk.
+// (The select pass reads both for a count with one 16-byte load.)
 __global__ void __launch_bounds__(256) suffix_min_kernel(const unsigned long long* v, int64_t len,
                                                          const unsigned long long* chunk_min,
-                                                         int64_t n_chunks,
-                                                         unsigned long long* above) {
+                                                         int64_t n_chunks, ulonglong2* pair) {
   __shared__ unsigned long long s_warp[8];
   __shared__ unsigned long long s_carry;
   const int64_t b = blockIdx.x;
@@ -129,32 +130,73 @@ __global__ void __launch_bounds__(256) suffix_min_kernel(const unsigned long lon
   unsigned long long run = min(after_warp, after_thread);
 #pragma unroll
   for (int u = 7; u >= 0; --u) {
-    if (base + u < len) above[base + u] = run;
+    if (base + u < len) pair[base + u] = make_ulonglong2(x[u], run);
     run = min(run, x[u]);
   }
 }
 
+constexpr int kSelItems = 16;  // consecutive items per thread
+constexpr int kSelTile = 256 * kSelItems;
+
+// keep flags for kSelTile consecutive items per CTA (kSelItems per thread,
+// in order), block scan of the per-thread counts, decoupled look-back over
+// the (few) tiles, then each thread writes its kept indices in order.
 __global__ void __launch_bounds__(256) pareto_select_kernel(
     const uint32_t* n_correct, const double* cost, int64_t n, int64_t n_rec,
-    const unsigned long long* mincost, const unsigned long long* above, int64_t base_index,
+    const ulonglong2* pair, int64_t base_index,
     uint8_t* keep, int64_t* kept_idx, int64_t* n_kept, uint64_t* states,
     unsigned long long* counter, int64_t n_tiles) {
-  __shared__ uint32_t s_warp[64];
-  __shared__ uint64_t s_misc[4];
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint64_t s_excl;
   __shared__ int64_t s_tile;
   const int64_t tile = next_tile_id(counter, &s_tile);
-  const int64_t i = tile * blockDim.x + threadIdx.x;
-  bool k = false;
-  if (i < n) {
-    uint32_t a = n_correct[i];
-    if ((int64_t)a > n_rec) a = (uint32_t)n_rec;
-    const unsigned long long key = cost_key(cost[i]);
-    k = (mincost[a] == key) && (key < above[a]);
-    if (keep) keep[i] = k ? 1 : 0;
+  const int64_t i0 = tile * kSelTile + (int64_t)threadIdx.x * kSelItems;
+  uint32_t kmask = 0;
+#pragma unroll
+  for (int u = 0; u < kSelItems; ++u) {
+    const int64_t i = i0 + u;
+    if (i < n) {
+      uint32_t a = __ldg(n_correct + i);
+      if ((int64_t)a > n_rec) a = (uint32_t)n_rec;
+      const unsigned long long key = cost_key(__ldg(cost + i));
+      const ulonglong2 mb = pair[a];  // {min cost at a, min cost above a}
+      const bool k = (mb.x == key) && (key < mb.y);
+      kmask |= (uint32_t)k << u;
+      if (keep) keep[i] = k ? 1 : 0;
+    }
   }
-  const PairScan ps = block_pair_scan(k, false, states, tile, s_warp, s_misc);
-  if (k) kept_idx[ps.a_off] = base_index + i;
-  if (tile == n_tiles - 1 && threadIdx.x == 0) *n_kept = (int64_t)ps.a_total;
+  const uint32_t cnt = __popc(kmask);
+  const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < 8 ? s_warp[lane] : 0u, wi = w;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, wi, 7);
+    if (lane < 8) s_warp[lane] = wi - w;  // exclusive warp offsets
+    const uint64_t excl = lookback_exclusive(states, tile, (uint64_t)total);
+    if (lane == 0) {
+      s_excl = excl;
+      if (tile == n_tiles - 1) *n_kept = (int64_t)(excl + total);
+    }
+  }
+  __syncthreads();
+  int64_t out = (int64_t)s_excl + s_warp[warp] + (incl - cnt);
+  while (kmask) {
+    const int u = __ffs(kmask) - 1;
+    kmask &= kmask - 1;
+    kept_idx[out++] = base_index + i0 + u;
+  }
 }
 
 __global__ void __launch_bounds__(256) pareto_generic_kernel(const double* acc, const double* cost,
@@ -194,12 +236,12 @@ CountsWs counts_ws(int64_t n, int64_t n_rec) {
   CountsWs w;
   const int64_t len = n_rec + 1;
   const int64_t n_chunks = (len + kChunk - 1) / kChunk;
-  const int64_t n_tiles = (n + 255) / 256;
+  const int64_t n_tiles = (n + kSelTile - 1) / kSelTile;
   size_t off = 0;
   w.mincost = off;
   off += round_up((size_t)len * 8, 256);
   w.above = off;
-  off += round_up((size_t)len * 8, 256);
+  off += round_up((size_t)len * 16, 256);
   w.chunk_min = off;
   off += round_up((size_t)n_chunks * 8, 256);
   w.states = off;
@@ -237,13 +279,13 @@ extern "C" int gs_pareto_counts(const uint32_t* n_correct, const double* cost, i
   if (!workspace || workspace_bytes < w.total) return GS_EWORKSPACE;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   auto* mincost = reinterpret_cast<unsigned long long*>(ws + w.mincost);
-  auto* above = reinterpret_cast<unsigned long long*>(ws + w.above);
+  auto* pair = reinterpret_cast<ulonglong2*>(ws + w.above);
   auto* chunk_min = reinterpret_cast<unsigned long long*>(ws + w.chunk_min);
   auto* states = reinterpret_cast<uint64_t*>(ws + w.states);
   auto* counter = reinterpret_cast<unsigned long long*>(ws + w.counter);
   const int64_t len = n_rec + 1;
   const int64_t n_chunks = (len + kChunk - 1) / kChunk;
-  const int64_t n_tiles = (n + 255) / 256;
+  const int64_t n_tiles = (n + kSelTile - 1) / kSelTile;
   GS_CUDA_TRY(cudaMemsetAsync(mincost, 0xff, (size_t)len * 8, st));
   GS_CUDA_TRY(cudaMemsetAsync(states, 0, (size_t)n_tiles * 8, st));
   GS_CUDA_TRY(cudaMemsetAsync(counter, 0, 8, st));
@@ -252,11 +294,11 @@ extern "C" int gs_pareto_counts(const uint32_t* n_correct, const double* cost, i
   GS_LAUNCH_CHECK();
   chunk_min_kernel<<<(unsigned)n_chunks, 256, 0, st>>>(mincost, len, chunk_min);
   GS_LAUNCH_CHECK();
-  suffix_min_kernel<<<(unsigned)n_chunks, 256, 0, st>>>(mincost, len, chunk_min, n_chunks, above);
+  suffix_min_kernel<<<(unsigned)n_chunks, 256, 0, st>>>(mincost, len, chunk_min, n_chunks, pair);
   GS_LAUNCH_CHECK();
-  pareto_select_kernel<<<(unsigned)n_tiles, 256, 0, st>>>(n_correct, cost, n, n_rec, mincost, above,
-                                                          base_index, keep, kept_idx, n_kept, states,
-                                                          counter, n_tiles);
+  pareto_select_kernel<<<(unsigned)n_tiles, 256, 0, st>>>(n_correct, cost, n, n_rec, pair, base_index,
+                                                          keep, kept_idx, n_kept, states, counter,
+                                                          n_tiles);
   GS_LAUNCH_CHECK();
   return GS_OK;
 }

@@ -21,6 +21,7 @@
 // promoted to f64.  Max-softmax / entropy are extensions (no reference
 // oracle): exp in f32 (expf, <= 2 ulp), sums in f64.
 #include <algorithm>
+#include <cmath>
 
 #include "gs_common.cuh"
 
@@ -57,6 +58,12 @@ __device__ __forceinline__ double neg_inf<double>() {
   return __longlong_as_double(0xfff0000000000000ll);
 }
 
+// top two so far (duplicates count twice, NaN never enters: the sorted()
+// semantics of cascades.certainty on finite scores)
+__device__ __forceinline__ void push_top2(float x, float& m1, float& m2) {
+  m2 = fmaxf(m2, fminf(m1, x));  // three FMNMX, no branches
+  m1 = fmaxf(m1, x);
+}
 template <typename C>
 __device__ __forceinline__ void push_top2(C x, C& m1, C& m2) {
   if (x > m1) {
@@ -127,8 +134,9 @@ __device__ __forceinline__ void warp_for_each(const T* row, int n, bool vec_ok, 
 }
 
 // Certainty of one row, computed by a full warp; result valid in all lanes.
+// log_n: ln(n) precomputed by the caller for the entropy kind (<= 0: compute)
 template <typename T, int KIND>
-__device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok) {
+__device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok, double log_n = 0.0) {
   using C = typename Compute<T>::type;
   if (n == 1) {
     const double x0 = (double)to_float(row[0]);
@@ -185,17 +193,53 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
       m = y > m ? y : m;
     }
     double s = 0.0, t = 0.0;
-    each([&](T x) {
-      const C d = (C)to_float(x) - m;
-      const double e = exp_term(d);
-      s += e;
-      if (KIND == GS_CERT_ENTROPY) t += e * (double)d;
-    });
+    if constexpr (sizeof(C) == 4) {
+      // f32 rows: exp2 on the SFU, the terms of one 16-byte vector summed in
+      // f32 (all of one sign, so each group sum is within 3 ulp), the group
+      // sums accumulated in f64: half a conversion per element instead of
+      // two, and |cert error| stays far below the 5e-7 the tests allow
+      constexpr float kLog2e = 1.4426950408889634f;
+      auto term = [&](float x, float& e, float& d) {
+        d = x - m;
+        float y;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d * kLog2e));
+        e = y;
+      };
+#pragma unroll
+      for (int u = 0; u < RV; ++u) {
+        if (lane + 32 * u < nv) {
+          const T* tv = reinterpret_cast<const T*>(&buf[u]);
+          float s4 = 0.f, t4 = 0.f;
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            float e, d;
+            term((float)to_float(tv[q]), e, d);
+            s4 += e;
+            t4 = fmaf(e, d, t4);
+          }
+          s += (double)s4;
+          if (KIND == GS_CERT_ENTROPY) t += (double)t4;
+        }
+      }
+      if (has_tail) {
+        float e, d;
+        term((float)to_float(tx), e, d);
+        s += (double)e;
+        if (KIND == GS_CERT_ENTROPY) t += (double)e * (double)d;
+      }
+    } else {
+      each([&](T x) {
+        const C d = (C)to_float(x) - m;
+        const double e = exp_term(d);
+        s += e;
+        if (KIND == GS_CERT_ENTROPY) t += e * (double)d;
+      });
+    }
     s = warp_sum(s);
     if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / s;
     t = warp_sum(t);
     const double H = log(s) - t / s;
-    return 1.0 - H / log((double)n);
+    return 1.0 - H / (log_n > 0.0 ? log_n : log((double)n));
   }
   if (KIND == GS_CERT_MARGIN) {
     C m1 = neg_inf<C>(), m2 = neg_inf<C>();
@@ -309,11 +353,12 @@ struct StepArgs {
   unsigned long long* counter;
   int64_t n_tiles;
   int32_t rows_per_tile;
+  double log_n;  // ln(n_cls)
 };
 
 constexpr int kStepThreads = 256;
-constexpr int kWideRowsPerWarp = 8;
-constexpr int kWideTile = (kStepThreads / 32) * kWideRowsPerWarp;  // 64 rows
+constexpr int kWideRowsPerWarp = 32;
+constexpr int kWideTile = (kStepThreads / 32) * kWideRowsPerWarp;  // 256 rows: one per thread at the gate
 
 __device__ __forceinline__ void copy_payload_row(const uint8_t* src, uint8_t* dst, int64_t bytes,
                                                  bool vec) {
@@ -384,7 +429,8 @@ __global__ void __launch_bounds__(kStepThreads) stage_step_kernel(const __grid_c
     for (int k = 0; k < kWideRowsPerWarp; ++k) {
       const int lr = warp * kWideRowsPerWarp + k;
       if (lr < rows) {
-        const double c = warp_row_cert<T, KIND>(scores + (base + lr) * a.stride, a.n_cls, a.vec_ok);
+        const double c = warp_row_cert<T, KIND>(scores + (base + lr) * a.stride, a.n_cls, a.vec_ok,
+                                                a.log_n);
         if (lane_id() == 0) s_cert[lr] = c;
       }
     }
@@ -487,6 +533,7 @@ template <typename T, int KIND>
 cudaError_t launch_step(StepArgs a, cudaStream_t st) {
   const bool wide = a.n_cls >= 32;
   a.rows_per_tile = wide ? kWideTile : kStepThreads;
+  a.log_n = a.n_cls > 1 ? std::log((double)a.n_cls) : 0.0;
   a.n_tiles = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
   a.vec_ok = aligned16(a.scores) && ((a.stride * (int64_t)sizeof(T)) % 16 == 0);
   if (a.n_tiles > 0x7fffffff) return cudaErrorInvalidValue;

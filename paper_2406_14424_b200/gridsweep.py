@@ -189,12 +189,40 @@ class GridSweep:
         _lib.check(rc, "grid eval")
         return out
 
-    def capture(self, out: SweepResult, build: bool = True,
-                evaluate: bool = True) -> torch.cuda.CUDAGraph:
+    def histogram(self) -> None:
+        """The histogram half of build() (fast path): gs_grid_accumulate over
+        all records.  Leaves the workspace mid-build until finish()."""
+        lib = _lib.load()
+        flags = 0 if self._clean else GS_GRID_WORKSPACE_DIRTY
+        rc = lib.gs_grid_accumulate(self.cert.data_ptr(), self.corr.data_ptr(), self.n_rec,
+                                    self.n_rec, self.n_models, self.grids.data_ptr(), self._glen,
+                                    self.table.data_ptr(), self.table.numel(), flags,
+                                    _lib.stream_ptr())
+        _lib.check(rc, "grid accumulate")
+        self._clean = False
+
+    def finish(self) -> None:
+        """The prefix-table half of build() (fast path): gs_grid_finish."""
+        lib = _lib.load()
+        rc = lib.gs_grid_finish(self.n_rec, self.n_models, self._glen, self.table.data_ptr(),
+                                self.table.numel(), _lib.stream_ptr())
+        _lib.check(rc, "grid finish")
+        self._clean = True
+        self._built = True
+
+    def capture(self, out: SweepResult, build: bool = True, evaluate: bool = True,
+                part: str | None = None) -> torch.cuda.CUDAGraph:
         """CUDA graph of one sweep step (table build and/or scoring every
         config into `out`), so a step is one graph launch instead of a
-        Python-driven sequence of kernel launches."""
+        Python-driven sequence of kernel launches.  part = "hist" / "plane"
+        captures one half of the fast path's build alone (for timing)."""
         def body():
+            if part == "hist":
+                self.histogram()
+                return
+            if part == "plane":
+                self.finish()
+                return
             if build:
                 self.build()
             if evaluate:
@@ -247,21 +275,76 @@ class GridSweep:
         return out
 
 
+def front_rows(idx: torch.Tensor, res: SweepResult) -> torch.Tensor:
+    """Device [n_front, 3 + max_len] f64 rows (config index, accuracy,
+    mean_cost, forward_frac...) of the configs `idx` (absolute indices) of a
+    scored range, so a front leaves the device in one copy."""
+    local = idx - res.config_begin
+    cols = [idx.to(torch.float64)[:, None], res.accuracy[local][:, None],
+            res.mean_cost[local][:, None], res.forward_frac[local]]
+    return torch.cat(cols, dim=1)
+
+
+def front_host(idx: torch.Tensor, res: SweepResult) -> np.ndarray:
+    """front_rows copied to host memory in one pinned D2H: [n_front, 3 +
+    max_len] f64 (config index, accuracy, mean_cost, forward_frac...)."""
+    rows = front_rows(idx, res)
+    host = _pinned(rows.shape, rows.dtype)
+    host.copy_(rows, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy()
+
+
+_PINNED: dict = {}
+
+
+def _pinned(shape, dtype) -> torch.Tensor:
+    """A pinned host buffer of at least `shape`, reused across calls (one
+    per dtype, grown geometrically)."""
+    n = int(np.prod(shape))
+    buf = _PINNED.get(dtype)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1 << 16) * 2, dtype=dtype, pin_memory=True)
+        _PINNED[dtype] = buf
+    return buf[:n].view(*shape)
+
+
+class _ParetoScratch:
+    """Workspace, outputs and a pinned count slot of gs_pareto_counts for one
+    (n, n_rec, device), allocated once and reused."""
+
+    def __init__(self, n: int, n_rec: int, dev: torch.device):
+        lib = _lib.load()
+        nbytes = ctypes.c_size_t()
+        _lib.check(lib.gs_pareto_counts_workspace(n, n_rec, ctypes.byref(nbytes)), "pareto")
+        self.ws = _lib.workspace(nbytes.value)
+        self.kept = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        self.n_kept = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.n_host = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+
+
+_SCRATCH: dict = {}
+
+
 def pareto_counts(n_correct: torch.Tensor, mean_cost: torch.Tensor, n_rec: int,
                   base_index: int = 0, keep: torch.Tensor | None = None) -> torch.Tensor:
     """Indices (+base_index, ascending) of the exact Pareto front of points
-    given as integer correct counts and f64 costs (gs_pareto_counts)."""
+    given as integer correct counts and f64 costs (gs_pareto_counts).
+    Workspace and outputs are reused across calls of the same shape."""
     lib = _lib.load()
     n = int(n_correct.numel())
     dev = _lib.device()
-    nbytes = ctypes.c_size_t()
-    _lib.check(lib.gs_pareto_counts_workspace(n, n_rec, ctypes.byref(nbytes)), "pareto")
-    ws = _lib.workspace(nbytes.value)
-    kept = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-    n_kept = torch.zeros(1, dtype=torch.int64, device=dev)
+    key = (n, int(n_rec), dev.index)
+    sc = _SCRATCH.get(key)
+    if sc is None:
+        if len(_SCRATCH) > 8:
+            _SCRATCH.clear()
+        sc = _SCRATCH[key] = _ParetoScratch(n, n_rec, dev)
     rc = lib.gs_pareto_counts(n_correct.data_ptr() if n else None,
                               mean_cost.data_ptr() if n else None, n, n_rec, base_index,
-                              _lib.ptr(keep), kept.data_ptr(), n_kept.data_ptr(),
-                              ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+                              _lib.ptr(keep), sc.kept.data_ptr(), sc.n_kept.data_ptr(),
+                              sc.ws.data_ptr(), sc.ws.numel(), _lib.stream_ptr())
     _lib.check(rc, "pareto")
-    return kept[: int(n_kept.item())]
+    sc.n_host.copy_(sc.n_kept, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return sc.kept[: int(sc.n_host[0])].clone()

@@ -3,7 +3,7 @@ import sys, time
 import numpy as np, torch
 sys.path.insert(0, ".")
 import bench
-from paper_2406_14424_b200.gridsweep import GridSweep, pareto_counts
+from paper_2406_14424_b200.gridsweep import GridSweep, front_host, pareto_counts
 
 _, cert, corr, grids, cost1 = bench.workload(0)
 pc = torch.from_numpy(cert).pin_memory()
@@ -29,7 +29,7 @@ def step(build):
     build()
     out = sw.evaluate(n_correct=True, out=out)
     idx = pareto_counts(out.n_correct, out.mean_cost, sw.n_rec)
-    return [idx.cpu(), out.accuracy[idx].cpu(), out.mean_cost[idx].cpu(), out.forward_frac[idx].cpu()]
+    return front_host(idx, out)
 
 
 def timeit(f, n=20):
@@ -52,3 +52,9 @@ print("e2e plain      %.3f ms" % timeit(lambda: step(plain)))
 for k in (4, 8):
     print("e2e streamed %d %.3f ms" % (k, timeit(lambda: step(streamed(k)))))
 print("eval+pareto+d2h %.3f ms" % timeit(lambda: step(lambda: None)))
+plain()
+out = sw.evaluate(n_correct=True, out=out)
+print("eval only       %.3f ms" % timeit(lambda: sw.evaluate(n_correct=True, out=out)))
+print("pareto (+sync)  %.3f ms" % timeit(lambda: pareto_counts(out.n_correct, out.mean_cost, sw.n_rec)))
+idx = pareto_counts(out.n_correct, out.mean_cost, sw.n_rec)
+print("front rows+D2H  %.3f ms (n_front %d)" % (timeit(lambda: front_host(idx, out)), idx.numel()))

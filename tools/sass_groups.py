@@ -3,8 +3,10 @@ usage: sass_groups.py rep kernel_regex [min_count_to_print_lines]"""
 import csv, io, subprocess, sys, collections
 rep, kre = sys.argv[1], sys.argv[2]
 show = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kre}",
-                      "--launch-count", "1", "--print-source", "sass"], capture_output=True, text=True).stdout
+                      "--launch-skip", skip, "--launch-count", "1", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 c = {k: i for i, k in enumerate(hdr)}
