@@ -207,16 +207,27 @@ def run_ours(args, world, rank, local):
     eval_ms = timed(g_eval, args.steps)
     part_ms = {}
     if sw.info.fast_path:
-        # each kernel alone (the plane graph replays over the histogram the
-        # hist graph leaves, so they alternate; the workspace stays valid)
-        g_hist = sw.capture(out, part="hist")
-        g_plane = sw.capture(out, part="plane")
-        hist_t, plane_t = [], []
+        # per-kernel durations inside the real step: event-record nodes
+        # between the three kernels of one captured step graph
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        g_parts = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_parts):
+            evs[0].record()
+            sw.histogram()
+            evs[1].record()
+            sw.finish()
+            evs[2].record()
+            sw.evaluate(out=out)
+            evs[3].record()
+        acc = [0.0, 0.0, 0.0]
         for _ in range(args.steps):
-            hist_t += timed(g_hist, 1)
-            plane_t += timed(g_plane, 1)
-        part_ms = {"g4_hist": sum(hist_t) / args.steps, "g4_plane": sum(plane_t) / args.steps,
-                   "g4_eval": sum(eval_ms) / args.steps}
+            flush_l2()
+            g_parts.replay()
+            torch.cuda.synchronize()
+            for k in range(3):
+                acc[k] += evs[k].elapsed_time(evs[k + 1])
+        part_ms = {"g4_hist": acc[0] / args.steps, "g4_plane": acc[1] / args.steps,
+                   "g4_eval": acc[2] / args.steps}
 
     # correctness spot-check of the timed outputs (rank 0, sampled configs)
     check = None

@@ -203,6 +203,32 @@ int gs_stage_gate(const double* certainty, const uint8_t* correct,
                   int64_t* n_near, void* workspace, size_t workspace_bytes,
                   void* stream);
 
+/* ------------------------------------------------------------------------
+ * Validation ingest (host code, no GPU): the reference's validation JSONL
+ * (formats.load_validation, src/formats.py:75-97) parsed into columnar
+ * arrays with n_threads host threads.  gs_jsonl_open parses the file into a
+ * handle and reports the shape (or the failing 1-based line and a message);
+ * gs_jsonl_read fills caller arrays: sample_id [n], line_no [n] (optional),
+ * scores[m] -> [n, width[m]] f64 (zero padded), row_len [n, M] i32,
+ * correct [n, M] u8; gs_jsonl_close frees the handle.
+ * ---------------------------------------------------------------------- */
+#define GS_JSONL_MAX_MODELS 64
+
+typedef struct gs_jsonl_info {
+  int64_t n_records;
+  int32_t n_models;
+  int32_t width[GS_JSONL_MAX_MODELS];   /* max score-list length per model */
+  char model_ids[GS_JSONL_MAX_MODELS][64]; /* first record's key order  */
+  int64_t err_line;                     /* 1-based, 0 = no line        */
+  char error[256];
+} gs_jsonl_info;
+
+int gs_jsonl_open(const char* path, int32_t n_threads, void** handle,
+                  gs_jsonl_info* info);
+int gs_jsonl_read(void* handle, int64_t* sample_id, int64_t* line_no,
+                  double* const* scores, int32_t* row_len, uint8_t* correct);
+void gs_jsonl_close(void* handle);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,16 @@ class gs_grid_info(ctypes.Structure):
                 ("reserved", c_int32)]
 
 
+GS_JSONL_MAX_MODELS = 64
+
+
+class gs_jsonl_info(ctypes.Structure):
+    _fields_ = [("n_records", c_int64), ("n_models", c_int32),
+                ("width", c_int32 * GS_JSONL_MAX_MODELS),
+                ("model_ids", (ctypes.c_char * 64) * GS_JSONL_MAX_MODELS),
+                ("err_line", c_int64), ("error", ctypes.c_char * 256)]
+
+
 # symbol -> argtypes (all return c_int unless listed in _RESTYPES)
 _SIGNATURES = {
     "gs_version": [],
@@ -64,6 +74,9 @@ _SIGNATURES = {
     "gs_grid_accumulate": [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p,
                            POINTER(c_int32), c_void_p, c_size_t, c_int32, c_void_p],
     "gs_grid_finish": [c_int64, c_int32, POINTER(c_int32), c_void_p, c_size_t, c_void_p],
+    "gs_jsonl_open": [ctypes.c_char_p, c_int32, POINTER(c_void_p), POINTER(gs_jsonl_info)],
+    "gs_jsonl_read": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "gs_jsonl_close": [c_void_p],
     "gs_grid_eval": [c_int64, c_int32, POINTER(c_int32), c_void_p, c_int64, c_int64, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "gs_grid_decode": [c_int32, POINTER(c_int32), c_void_p, c_void_p, c_int64, c_void_p,
@@ -82,7 +95,8 @@ _SIGNATURES = {
                       c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_double,
                       c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
 }
-_RESTYPES = {"gs_strerror": ctypes.c_char_p, "gs_last_cuda_error": ctypes.c_char_p}
+_RESTYPES = {"gs_strerror": ctypes.c_char_p, "gs_last_cuda_error": ctypes.c_char_p,
+             "gs_jsonl_close": None}
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None

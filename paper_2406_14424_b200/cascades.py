@@ -107,7 +107,9 @@ def _device_matrices(validation, profiles: ProfileSet):
             c = c[:, cols] if isinstance(c, torch.Tensor) else np.asarray(c)[:, cols]
             cert = _lib.to_device(c, torch.float64)
         else:
-            cert = torch.stack([certainty_rows(validation.scores[m]) for m in order], dim=1)
+            rl = validation.row_len or {}
+            cert = torch.stack([certainty_rows(validation.scores[m], row_len=rl.get(m))
+                                for m in order], dim=1)
             cert = cert.contiguous()
     else:
         n, m_count = len(validation), len(order)

@@ -185,7 +185,8 @@ class ValidationArrays:
     score matrix [n, n_cls] (f32 / f64 / bf16, numpy or torch), plus a
     correctness column.  Accepted wherever a ValidationSet is."""
 
-    def __init__(self, model_ids, *, certainty=None, scores=None, correct=None):
+    def __init__(self, model_ids, *, certainty=None, scores=None, correct=None, row_len=None,
+                 sample_id=None):
         self.model_ids_ordered = tuple(model_ids)
         _require(len(self.model_ids_ordered) > 0, "validation covers no models")
         _require(len(set(self.model_ids_ordered)) == len(self.model_ids_ordered),
@@ -196,6 +197,8 @@ class ValidationArrays:
         self.certainty = certainty      # [n, M] or None
         self.scores = scores            # dict model_id -> [n, n_cls] or None
         self.correct = correct          # [n, M] u8 / bool
+        self.row_len = row_len          # dict model_id -> [n] int (ragged score rows) or None
+        self.sample_id = sample_id      # [n] int64 or None
         n = int(correct.shape[0])
         _require(n > 0, "validation set is empty")
         _require(tuple(correct.shape) == (n, len(self.model_ids_ordered)),

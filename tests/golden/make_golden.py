@@ -228,6 +228,60 @@ def engine_fixture(meta):
     meta["engine.npz"] = "gearserve.engine.EngineState.finish_batch on random multi-gear batches"
 
 
+INGEST_OK = """{"sample_id": 0, "models": {"a": {"scores": [0.1, 0.7, 0.2], "correct": true}, "b": {"scores": [0.5], "correct": false}}}
+
+{"models": {"b": {"correct": 1, "scores": [1e-5, -2.5e+3]}, "a": {"scores": [3, 4], "correct": 0}}, "sample_id": 7, "extra": [1, {"x": null}, "s"]}
+{"sample_id": 3.0, "models": {"a": {"scores": [NaN, 1.0], "correct": true, "note": "hi"}, "b": {"scores": [Infinity, -Infinity, 0.0], "correct": false}}}
+   
+{"sample_id": 12, "models": {"a": {"scores": [0.30000000000000004, "0.25"], "correct": false}, "b": {"scores": [5e-324, 1.7976931348623157e308], "correct": true}}}
+"""
+
+INGEST_BAD = {
+    "missing_correct": '{"sample_id": 0, "models": {"a": {"scores": [1.0], "correct": true}}}\n'
+                       '{"sample_id": 1, "models": {"a": {"scores": [1.0]}}}\n',
+    "empty_scores": '{"sample_id": 0, "models": {"a": {"scores": [1.0], "correct": true}}}\n\n'
+                    '{"sample_id": 1, "models": {"a": {"scores": [], "correct": true}}}\n',
+    "not_json": '{"sample_id": 0, "models": {"a": {"scores": [1.0], "correct": true}}}\n{oops\n',
+    "duplicate_id": '{"sample_id": 4, "models": {"a": {"scores": [1.0], "correct": true}}}\n'
+                    '{"sample_id": 4, "models": {"a": {"scores": [2.0], "correct": true}}}\n',
+    "model_mismatch": '{"sample_id": 0, "models": {"a": {"scores": [1.0], "correct": true}}}\n'
+                      '{"sample_id": 1, "models": {"b": {"scores": [1.0], "correct": true}}}\n',
+    "negative_id": '{"sample_id": -1, "models": {"a": {"scores": [1.0], "correct": true}}}\n',
+    "bad_score": '{"sample_id": 0, "models": {"a": {"scores": ["x"], "correct": true}}}\n',
+}
+
+
+def ingest_fixture(meta):
+    """gearserve.formats.load_validation (src/formats.py:75-97) on an
+    edge-case JSONL (blank lines, key order, extra keys, NaN / Infinity,
+    string scores, ragged and singleton score lists) and on malformed files
+    (the reference's error: ValueError, with the line number when the
+    reader names one)."""
+    from gearserve import formats as rf
+    ok = HERE / "ingest_ok.jsonl"
+    ok.write_text(INGEST_OK)
+    v = rf.load_validation(ok)
+    recs = [{"sample_id": r.sample_id,
+             "models": {m: {"scores": [repr(float(x)) for x in o.scores], "correct": o.correct}
+                        for m, o in r.outputs.items()}} for r in v.records]
+    bad = {}
+    for name, text in INGEST_BAD.items():
+        path = HERE / f"ingest_bad_{name}.jsonl"
+        path.write_text(text)
+        try:
+            rf.load_validation(path)
+            bad[name] = None
+        except ValueError as e:
+            msg = str(e)
+            line = None
+            if ": line " in msg:
+                line = int(msg.split(": line ")[1].split(":")[0])
+            bad[name] = {"line": line}
+    (HERE / "ingest.json").write_text(json.dumps({"ok": recs, "bad": bad}, indent=1) + "\n")
+    meta["ingest.json"] = ("gearserve.formats.load_validation on ingest_ok.jsonl and the "
+                           "ingest_bad_*.jsonl files")
+
+
 def main():
     meta = {"reference_src": REF_SRC, "numpy": np.__version__}
     kernels_fixtures(meta)
@@ -238,6 +292,7 @@ def main():
     grid_and_sampler_fixture(meta)
     synth_fixture(meta)
     engine_fixture(meta)
+    ingest_fixture(meta)
     (HERE / "MANIFEST.json").write_text(json.dumps(meta, indent=1) + "\n")
     print(json.dumps(meta, indent=1))
 

@@ -91,3 +91,29 @@ def test_sweep_grid_front_is_exact():
     # the decoded cascades score the same through the list path
     evs = cascades.evaluate_cascades(front.cascades, v, p)
     assert [e.accuracy for e in evs] == list(acc[keep])
+
+
+def test_jsonl_ingest_feeds_the_same_matrices(tmp_path):
+    """formats.load_validation_arrays (native reader + device certainty) gives
+    bit-identical matrices to the record path, and a sweep over them equals
+    the oracle walk."""
+    from paper_2406_14424_b200 import formats, synth
+    from paper_2406_14424_b200.cascades import matrices
+    from paper_2406_14424_b200.types import ModelOutput, ValidationRecord, ValidationSet
+    profiles = synth.make_profiles(n_models=3)
+    va = synth.binary_logit_arrays(profiles, 3000, 0.8, seed=4, dtype=np.float64)
+    vs = ValidationSet([ValidationRecord(
+        sample_id=i, outputs={m: ModelOutput(scores=tuple(float(x) for x in va.scores[m][i]),
+                                             correct=bool(va.correct[i, j]))
+                              for j, m in enumerate(profiles.model_ids)})
+        for i in range(3000)])
+    path = tmp_path / "v.jsonl"
+    formats.save_validation(vs, path)
+    arr = formats.load_validation_arrays(path)
+    c_ref, k_ref = matrices(vs, profiles)
+    c_arr, k_arr = matrices(arr, profiles)
+    assert np.array_equal(c_ref, c_arr) and np.array_equal(k_ref, k_arr)
+    col = tmp_path / "v.gsvc"
+    formats.save_validation_columnar(arr, col)
+    c_col, k_col = matrices(formats.load_validation_columnar(col), profiles)
+    assert np.array_equal(c_ref, c_col) and np.array_equal(k_ref, k_col)
