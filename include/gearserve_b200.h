@@ -204,6 +204,18 @@ int gs_stage_gate(const double* certainty, const uint8_t* correct,
                   void* stream);
 
 /* ------------------------------------------------------------------------
+ * Threshold-grid quantiles on the device: np.quantile(column, qs) with
+ * numpy's default "linear" method, bit-exact (cascades.build_threshold_grid,
+ * src/cascades.py:150-163).  column: device f64, n values at `stride`
+ * elements apart (a column of a row-major [n, M] matrix: stride = M);
+ * qs: HOST array of n_q values in [0, 1]; out: device f64 [n_q].
+ * ---------------------------------------------------------------------- */
+int gs_quantiles_workspace(int64_t n, int32_t n_q, size_t* bytes);
+int gs_quantiles(const double* column, int64_t n, int64_t stride,
+                 const double* qs, int32_t n_q, double* out, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
  * Validation ingest (host code, no GPU): the reference's validation JSONL
  * (formats.load_validation, src/formats.py:75-97) parsed into columnar
  * arrays with n_threads host threads.  gs_jsonl_open parses the file into a

@@ -294,3 +294,37 @@ def finish_batch(items, gears, cert, corr, rng, now):
             p = choose_weighted(g["cum_weights"][nxt], rng)
             forwarded.append((pos, int(g["replica_idx"][nxt][p])))
     return completed, forwarded
+
+
+def load_validation_jsonl(path):
+    """Restatement of the reference reader (src/formats.py:75-97): json.loads
+    per non-blank line, scores through float(), correct through bool(),
+    sample_id through int().  Returns (sample_ids, {model: [scores tuples]},
+    {model: [bool]}) in file order."""
+    import json
+    ids, scores, correct = [], {}, {}
+    with open(path) as f:
+        for lineno, line in enumerate(f, start=1):
+            line = line.strip()
+            if not line:
+                continue
+            try:
+                doc = json.loads(line)
+                outs = {mid: (tuple(float(s) for s in out["scores"]), bool(out["correct"]))
+                        for mid, out in doc["models"].items()}
+                sid = int(doc["sample_id"])
+            except (json.JSONDecodeError, KeyError, TypeError, ValueError) as e:
+                raise ValueError(f"{path}: line {lineno}: {e}")
+            ids.append(sid)
+            for mid, (sc, ok) in outs.items():
+                scores.setdefault(mid, []).append(sc)
+                correct.setdefault(mid, []).append(ok)
+    return ids, scores, correct
+
+
+def grid_values(cert_column, levels: int) -> tuple:
+    """build_threshold_grid's per-model grid (src/cascades.py:157-162) with
+    numpy on the host: {0} U np.quantile(col, k/levels), sorted."""
+    qs = [k / levels for k in range(1, levels)]
+    quants = np.quantile(np.asarray(cert_column, dtype=np.float64), qs)
+    return tuple(sorted({0.0} | {float(q) for q in quants}))

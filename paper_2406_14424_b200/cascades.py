@@ -21,6 +21,8 @@ the device (gridsweep.GridSweep), with an exact Pareto reduction.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -243,10 +245,34 @@ class ThresholdGrid:
                     raise ValueError(f"{mid}: grid not strictly increasing at {b}")
 
 
-def grid_values(cert_column: np.ndarray, levels: int) -> tuple[float, ...]:
-    """{0} U quantiles k/levels (numpy linear), sorted (reference :157-162)."""
+def quantiles(column, qs) -> np.ndarray:
+    """np.quantile(column, qs) (numpy "linear", bit-exact) computed on the
+    device (gs_quantiles: device sort + numpy's interpolation arithmetic).
+    column: a 1-D numpy array or CUDA tensor (any stride)."""
+    qs = np.ascontiguousarray(np.asarray(qs, dtype=np.float64).reshape(-1))
+    col = column if isinstance(column, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(column, dtype=np.float64)))
+    col = _lib.to_device(col, torch.float64) if col.device.type != "cuda" or \
+        col.dtype != torch.float64 else col
+    if col.ndim != 1 or col.numel() == 0:
+        raise ValueError("quantiles of an empty or non-1-D column")
+    n = int(col.numel())
+    lib = _lib.load()
+    nbytes = ctypes.c_size_t()
+    _lib.check(lib.gs_quantiles_workspace(n, qs.size, ctypes.byref(nbytes)), "quantiles")
+    ws = _lib.workspace(nbytes.value)
+    out = torch.empty(max(qs.size, 1), dtype=torch.float64, device=col.device)
+    rc = lib.gs_quantiles(col.data_ptr(), n, int(col.stride(0)), qs.ctypes.data, qs.size,
+                          out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr())
+    _lib.check(rc, "quantiles")
+    return out[: qs.size].cpu().numpy()
+
+
+def grid_values(cert_column, levels: int) -> tuple[float, ...]:
+    """{0} U quantiles k/levels (numpy linear), sorted (reference :157-162);
+    the quantiles are taken on the device."""
     qs = [k / levels for k in range(1, levels)]
-    quants = np.quantile(cert_column, qs)
+    quants = quantiles(cert_column, qs)
     return tuple(sorted({0.0} | {float(q) for q in quants}))
 
 
@@ -254,7 +280,7 @@ def build_threshold_grid(validation, profiles: ProfileSet, levels: int = 10) -> 
     """Per-model grids: 0 plus the certainty quantiles k/levels, k=1..levels-1."""
     if levels < 2:
         raise ValueError(f"levels must be >= 2, got {levels}")
-    cert, _ = matrices(validation, profiles)
+    cert, _ = _device_matrices(validation, profiles)
     return ThresholdGrid(per_model={mid: grid_values(cert[:, j], levels)
                                     for j, mid in enumerate(profiles.model_ids)})
 

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     from paper_2406_14424_b200 import _lib
     lib = _lib.load()
     header = (ROOT / "include" / "gearserve_b200.h").read_text()
-    declared = set(re.findall(r"^(?:int|const char\*)\s+(gs_\w+)\(", header, flags=re.M))
+    declared = set(re.findall(r"^(?:int|void|const char\*)\s+(gs_\w+)\(", header, flags=re.M))
     assert declared == set(_lib.exported_symbols())
     for name in declared:
         assert hasattr(lib, name), name
@@ -87,6 +87,7 @@ def test_structures_order_matches_oracle_enumeration():
             assert tuple(sm[c, : ns[c]]) == models
 
 
+@pytest.mark.gpu
 def test_threshold_grid_and_sampler_match_reference():
     from paper_2406_14424_b200 import cascades as gc
     from paper_2406_14424_b200.types import ModelProfile, ProfileSet
@@ -107,6 +108,7 @@ def test_threshold_grid_and_sampler_match_reference():
         assert got == json.loads(str(g[f"sample_{seed}"]))
 
 
+@pytest.mark.gpu
 def test_synth_sampler_on_acceptance_profiles():
     from paper_2406_14424_b200 import cascades as gc
     from paper_2406_14424_b200 import synth
