@@ -82,6 +82,32 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
+// Programmatic dependent launch: the plane and eval kernels are launched
+// with programmatic stream serialization, so their CTAs can be scheduled
+// (and run their prologue: barrier init, zero buffers, range checks) while
+// the previous kernel drains; griddepcontrol.wait then blocks until the
+// previous grid has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename Kernel, typename Args>
+cudaError_t launch_pdl(Kernel k, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       const Args& args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args);
+}
+
 template <typename Kernel>
 cudaError_t ensure_smem4(Kernel k, std::atomic<int>& done, size_t bytes) {
   if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
@@ -204,6 +230,7 @@ __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_
     slot ^= 1;
   }
   phase(0, 2);
+  pdl_release();
   phase(0, 3);
   for (int i = tid; i < a.d0; i += kHist4Threads)
     if (s_c0[i]) atomicAdd(a.G0 + i, s_c0[i]);
@@ -281,6 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
   for (int i = tid; i < kZeroBytes / 16; i += kPlaneThreads) s_zero[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   fence_proxy_async();  // the zero buffer is read by the async proxy (bulk stores)
   __syncthreads();
+  pdl_wait();  // the histogram is complete
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar, tile_bytes);
     constexpr uint32_t kChunk = 32768;
@@ -367,6 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
       if (c == d2 - 1) a.R1[b0 * a.d1p + b1] = f2u_exact(P.w);
     }
   }
+  pdl_release();
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   phase(1, 5);
 }
@@ -488,6 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();  // the prefix tables are complete
   if (tid == 0) {
     mbar_arrive_expect_tx(&bar, bytes);
     const unsigned long long* src = a.S + ((int64_t)k0 * d1 + rb) * d2p;
@@ -772,8 +802,7 @@ cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
   static std::atomic<int> smem_plane{0};
   e = ensure_smem4(g4_plane_kernel, smem_plane, (size_t)kGrid4SlabMax);
   if (e != cudaSuccess) return e;
-  g4_plane_kernel<<<(unsigned)(2 * L.d1), kPlaneThreads, psmem, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(g4_plane_kernel, (unsigned)(2 * L.d1), kPlaneThreads, psmem, st, p);
 }
 
 cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
@@ -821,11 +850,8 @@ cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct
   cudaError_t e = all ? ensure_smem4(g4_eval_kernel<true>, smem_all, (size_t)kGrid4SlabMax)
                       : ensure_smem4(g4_eval_kernel<false>, smem_some, (size_t)kGrid4SlabMax);
   if (e != cudaSuccess) return e;
-  if (all)
-    g4_eval_kernel<true><<<(unsigned)(2 * L.d0), kEval4Threads, smem, st>>>(a);
-  else
-    g4_eval_kernel<false><<<(unsigned)(2 * L.d0), kEval4Threads, smem, st>>>(a);
-  return cudaGetLastError();
+  return all ? launch_pdl(g4_eval_kernel<true>, (unsigned)(2 * L.d0), kEval4Threads, smem, st, a)
+             : launch_pdl(g4_eval_kernel<false>, (unsigned)(2 * L.d0), kEval4Threads, smem, st, a);
 }
 
 }  // namespace gs
