@@ -58,8 +58,8 @@ namespace cg = cooperative_groups;
 
 // Phase stamps (GS_PHASE_TIMING builds only, tools/phase_probe.py): thread 0
 // of each CTA records %globaltimer and clock64 at phase boundaries.
-constexpr int kPhaseKernels = 3, kPhaseCtas = 1024, kPhaseSlots = 8;
 #ifdef GS_PHASE_TIMING
+constexpr int kPhaseKernels = 3, kPhaseCtas = 1024, kPhaseSlots = 8;
 __device__ unsigned long long g_phase[kPhaseKernels * kPhaseCtas * kPhaseSlots * 2];
 __device__ __forceinline__ void phase(int kernel, int slot) {
   if (threadIdx.x == 0 && blockIdx.x < kPhaseCtas) {
@@ -118,7 +118,7 @@ cudaError_t ensure_smem4(Kernel k, std::atomic<int>& done, size_t bytes) {
 
 // ------------------------------------------------------------------ hist --
 constexpr int kHist4Threads = 1024;
-constexpr int kHist4Unroll = 2;                          // records per thread per chunk
+constexpr int kHist4Unroll = 1;                          // records per thread per chunk
 constexpr int kHist4Chunk = kHist4Threads * kHist4Unroll;  // records per chunk
 constexpr int kMaxDim4 = 256;  // d0, d2 bound of this path
 

@@ -173,7 +173,7 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
     };
     if (KIND == GS_CERT_MARGIN) {
       C m1 = neg_inf<C>(), m2 = neg_inf<C>();
-      each([&](T x) { push_top2<C>((C)to_float(x), m1, m2); });
+      each([&](T x) { push_top2((C)to_float(x), m1, m2); });
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const C o1 = __shfl_xor_sync(0xffffffffu, m1, o);
@@ -243,7 +243,7 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
   }
   if (KIND == GS_CERT_MARGIN) {
     C m1 = neg_inf<C>(), m2 = neg_inf<C>();
-    warp_for_each<T>(row, n, vec_ok, [&](T x) { push_top2<C>((C)to_float(x), m1, m2); });
+    warp_for_each<T>(row, n, vec_ok, [&](T x) { push_top2((C)to_float(x), m1, m2); });
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const C o1 = __shfl_xor_sync(0xffffffffu, m1, o);
@@ -287,7 +287,7 @@ __device__ __forceinline__ double thread_row_cert(const T* row, int n) {
   }
   if (KIND == GS_CERT_MARGIN) {
     C m1 = neg_inf<C>(), m2 = neg_inf<C>();
-    for (int j = 0; j < n; ++j) push_top2<C>((C)to_float(row[j]), m1, m2);
+    for (int j = 0; j < n; ++j) push_top2((C)to_float(row[j]), m1, m2);
     return (double)m1 - (double)m2;
   } else {
     C m = neg_inf<C>();
