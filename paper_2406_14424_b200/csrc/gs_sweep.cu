@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
                                                           const uint32_t* flag, uint4* T,
                                                           int64_t n_slabs, int rows, int cols,
                                                           uint4* sideH, uint4* sideT, int side_len,
-                                                          int parts) {
+                                                          int parts, int zero) {
   // a slab may be split into `parts` column ranges, one CTA each: every CTA
   // reads whole rows (for the row prefix) but keeps, scans and stores only
   // its own columns, so twice the CTAs share the work
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
           const unsigned long long w = pv[i][u];
           e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
                             (uint32_t)((w >> 32) & 0xffff), (uint32_t)(w >> 48));
-          if (c >= cb && c < ce) H16[base + (int64_t)r * cols + c] = 0ull;
+          if (zero && c >= cb && c < ce) H16[base + (int64_t)r * cols + c] = 0ull;
         }
         uint4 tot = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + lane * 4 + u;
-          if (c >= cb && c < ce) {
+          if (zero && c >= cb && c < ce) {
             in16[c] = 0ull;
             if (fb) inF[c] = make_uint4(0, 0, 0, 0);
           }
@@ -645,6 +645,14 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
     }
     __syncthreads();
   }
+}
+
+// re-zero the f32 fallback histogram, only if the overflow flag is up
+__global__ void zero_if_flag_kernel(uint4* HF, int64_t cells, const uint32_t* flag) {
+  if (*reinterpret_cast<const volatile uint32_t*>(flag) == 0u) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+       i += (int64_t)gridDim.x * blockDim.x)
+    HF[i] = make_uint4(0, 0, 0, 0);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1181,9 +1189,21 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     cudaError_t e = ensure_smem(slab_first_kernel, smem_set, (size_t)kSlabSmemMax);
     if (e != cudaSuccess) return e;
     const int64_t blocks = std::min<int64_t>(n_slabs * parts, (int64_t)sm_count() * 4);
+    // with two CTAs per slab each reads whole rows, so neither may re-zero
+    // the histogram in place (the other may not have read it yet): re-zero
+    // after the pass instead
     slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols,
-                                                            sideH, sideT, side_len, parts);
+                                                            sideH, sideT, side_len, parts,
+                                                            parts == 1 ? 1 : 0);
     e = cudaGetLastError();
+    if (e == cudaSuccess && parts > 1) {
+      e = cudaMemsetAsync(H16, 0, (size_t)cells * 8, st);
+      if (e == cudaSuccess) {
+        const int64_t zb = std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, (int64_t)sm_count() * 8));
+        zero_if_flag_kernel<<<(unsigned)zb, 256, 0, st>>>(H, cells, flag);
+        e = cudaGetLastError();
+      }
+    }
     if (e != cudaSuccess || ndim - skip_leading == 2) return e;
     fused = 2;
   } else if (H16) {  // main table: packed first pass along the last dim (vec == 1)
@@ -1255,7 +1275,11 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
     const bool slab = p.D >= 2 && (size_t)p.dims[p.D - 1] * p.dims[p.D - 2] * sizeof(uint4) <= kSlabSmemMax;
     const int skip = p.walk ? 1 : 0;
     if (p.D == 0) b += 1;
-    else if (slab) b += 1 + std::max(0, p.D - 2 - skip);
+    else if (slab) {
+      const int64_t n_slabs = p.cellsF / (p.dims[p.D - 1] * p.dims[p.D - 2]);
+      const bool two = p.dims[p.D - 1] >= 64 && n_slabs < 2 * sm_count();
+      b += 1 + (two ? 1 : 0) + std::max(0, p.D - 2 - skip);  // + zero_if_flag after a split pass
+    }
     else b += 1 + std::max(0, p.D - 1 - skip);
     const bool fold_side = p.DP == 1 && p.NVP == 1 && slab;
     if (p.DP > 0 && !fold_side) b += std::max(1, p.DP);

@@ -260,22 +260,26 @@ def test_streamed_build_rejects_general_path():
         sw.build_streamed(torch.from_numpy(cert), torch.from_numpy(corr))
 
 
-@pytest.mark.parametrize("glen", [(150, 40, 120, 10), (60, 300, 64, 5), (255, 3, 200, 2)])
+@pytest.mark.parametrize("glen", [(150, 40, 120, 10), (60, 300, 64, 5), (255, 3, 200, 2),
+                                  (150, 3, 200, 2), (10, 150, 5), (40, 250, 3)])
 def test_four_model_large_uneven_grids(glen):
     """Grids near and past the fast path's shared-memory bounds (the plan
-    falls back to the general path past them); sampled configs of every
-    structure against the oracle walk."""
+    falls back to the general path past them), and general-path slabs wide
+    enough to be split across two CTAs (which must not re-zero the histogram
+    in place: regression); sampled configs of every structure against the
+    oracle walk."""
     from paper_2406_14424_b200.gridsweep import GridSweep, structures
     rng = np.random.default_rng(sum(glen))
     n = 40_000
-    cert = rng.random((n, 4))
-    corr = (rng.random((n, 4)) < 0.6).astype(np.uint8)
+    m = len(glen)
+    cert = rng.random((n, m))
+    corr = (rng.random((n, m)) < 0.6).astype(np.uint8)
     grids = [np.concatenate([[0.0], np.sort(rng.random(g - 1))]) for g in glen]
-    cost1 = np.array([1.0, 3.0, 9.0, 27.0])
+    cost1 = np.array([1.0, 3.0, 9.0, 27.0])[:m]
     sw = GridSweep(cert, corr, grids, cost1)
     res = sw.evaluate(n_correct=True)
     pick = []
-    for _, b, cnt in structures(4, sw.grid_len):
+    for _, b, cnt in structures(m, sw.grid_len):
         pick.extend(sorted(set(rng.integers(b, b + cnt, size=min(cnt, 60)).tolist())))
     pick = np.array(pick)
     sm, thr, ns = (t.cpu().numpy() for t in sw.decode(pick))
