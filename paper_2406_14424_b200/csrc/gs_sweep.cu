@@ -802,6 +802,7 @@ __device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, c
 
 template <int M>
 __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ EvalGridArgs a) {
+  __shared__ double s_frac[8 * 32 * M];  // per-warp staging of forward_frac rows
   constexpr int NVP = M >= 4 ? (M - 3 + 3) / 4 : 0;
   constexpr int NVPX = NVP > 0 ? NVP : 1;
   const int lane = (int)lane_id();
@@ -924,12 +925,33 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
       for (int u = 0; u < U; ++u) {
         const int kl = base + lane + 32 * u;
         const int64_t i = c_row + kl;
-        if (kl >= gL || i < 0 || i >= a.cfg_count) continue;
+        const bool ok = kl < gL && i >= 0 && i < a.cfg_count;
         const uint32_t correct =
             cp + a_last - chan<M>(wF[u], wP[u], mL) + chan<M>(wF[u], wP[u], mK);
         const double frK = div_count((double)wF[u].x, n, rcp);
         const double mean = dadd(mp, dmul(frK, costK));
-        store_config<M>(a, i, fr, K, frK, mean, correct, n, rcp);
+        if (ok) {
+          if (a.cost) a.cost[i] = mean;
+          if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+          if (a.n_correct) a.n_correct[i] = correct;
+        }
+        // forward_frac: the warp's 32 consecutive [M]-rows go through a
+        // per-warp shared buffer and leave as M fully coalesced stores
+        // (strided per-lane rows cost M partial-line writes per row)
+        if (a.frac) {
+          double* buf = s_frac + (threadIdx.x >> 5) * (32 * M);
+#pragma unroll
+          for (int t = 0; t < M; ++t) buf[lane * M + t] = t < K - 1 ? fr[t] : (t == K - 1 ? frK : 0.0);
+          __syncwarp();
+          const int64_t i0 = c_row + base + 32 * u;  // config of lane 0
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            const int e = j * 32 + lane, src = e / M;
+            const int64_t is = i0 + src;
+            if (base + 32 * u + src < gL && is >= 0 && is < a.cfg_count) a.frac[i0 * M + e] = buf[e];
+          }
+          __syncwarp();
+        }
       }
     }
   }

@@ -17,6 +17,18 @@ __global__ void gen(uint32_t* idx, uint32_t* idx2, uint32_t ncell, uint32_t ncel
   }
 }
 
+__global__ void init_rec(double* cert, uint32_t* corr) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)r * 2654435761u;
+    for (int j = 0; j < 4; ++j) {
+      h ^= h >> 13;
+      h *= 2246822519u;
+      cert[4ll * r + j] = (h >> 8) * (1.0 / 16777216.0);
+    }
+    corr[r] = h & 0x01010101u;
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(1024) k(const uint32_t* idx, const uint32_t* idx2,
                                          unsigned long long* T64, unsigned long long* S64,
@@ -52,6 +64,38 @@ __global__ void __launch_bounds__(1024) k(const uint32_t* idx, const uint32_t* i
     __syncthreads();
     for (int i = threadIdx.x; i < 12288; i += blockDim.x)
       if (sm[i]) atomicAdd(T32 + i, sm[i]);
+  }
+}
+
+// record-stream variants: 1M records of 32 B certainty + 4 B correct
+template <int MODE>
+__global__ void __launch_bounds__(1024) k_rec(const double* cert, const uint32_t* corr, float* F4,
+                                              unsigned long long* sink) {
+  __shared__ uint32_t s_c0[256];
+  if (MODE == 2) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_c0[i] = 0;
+    __syncthreads();
+  }
+  double acc = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < N; r += gridDim.x * blockDim.x) {
+    const double2 p = __ldg(reinterpret_cast<const double2*>(cert + 4ll * r));
+    const double x2 = __ldg(cert + 4ll * r + 2);
+    const uint32_t k = __ldg(corr + r);
+    if (MODE == 0) {
+      acc += p.x + p.y + x2 + k;
+      continue;
+    }
+    const uint32_t h = (uint32_t)(p.x * 101.0) * 10201u + (uint32_t)(p.y * 101.0) * 101u +
+                       (uint32_t)(x2 * 101.0);
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(F4 + 4ull * (h % 1030301u)),
+                 "f"(1.f), "f"((float)(k & 1)), "f"((float)((k >> 8) & 1)), "f"((float)((k >> 16) & 1))
+                 : "memory");
+    if (MODE == 2 && (k >> 24)) atomicAdd(s_c0 + (h & 255u), 1u);
+  }
+  if (MODE == 0 && acc == 12345.0) sink[0] = 1;
+  if (MODE == 2) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) atomicAdd((uint32_t*)sink + i, s_c0[i]);
   }
 }
 
@@ -99,6 +143,38 @@ int main() {
     printf("  1 RED.64 / rec, 10K-cell table   %7.2f us\n", run<5>(blocks, idx, idx2, T64, S64, T32, F4, sink));
     printf("  RED.64 + smem ATOMS / rec        %7.2f us\n", run<6>(blocks, idx, idx2, T64, S64, T32, F4, sink));
     printf("  2 RED.32 / rec (1M + 4K cells)   %7.2f us\n", run<7>(blocks, idx, idx2, T64, S64, T32, F4, sink));
+  }
+  {
+    double* cert;
+    uint32_t* corr;
+    cudaMalloc(&cert, 32ll * N);
+    cudaMalloc(&corr, 4ll * N);
+    init_rec<<<592, 256>>>(cert, corr);
+    unsigned long long* sk;
+    cudaMalloc(&sk, 4096);
+    float* big;
+    cudaMalloc(&big, 256ll << 20);  // flush buffer
+    auto t = [&](auto f) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      float tot = 0;
+      for (int i = 0; i < 23; ++i) {
+        cudaMemsetAsync(big, 0, 256ll << 20);
+        cudaEventRecord(a);
+        f();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (i >= 3) tot += ms;
+      }
+      return tot * 1000.f / 20;
+    };
+    printf("record stream, 1M x 36 B, 148 x 1024 threads, L2 flushed:\n");
+    printf("  loads only                       %7.2f us\n", t([&] { k_rec<0><<<sms, 1024>>>(cert, corr, F4, sk); }));
+    printf("  loads + 1 RED.v4 / rec           %7.2f us\n", t([&] { k_rec<1><<<sms, 1024>>>(cert, corr, F4, sk); }));
+    printf("  loads + RED.v4 + smem c0 ATOMS   %7.2f us\n", t([&] { k_rec<2><<<sms, 1024>>>(cert, corr, F4, sk); }));
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status: %s\n", cudaGetErrorString(e));
