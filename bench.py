@@ -285,6 +285,24 @@ def run_ours(args, world, rank, local):
             d2h_total += front.numel() * front.element_size()
         return rows
 
+    e2e_pipelined = None
+    if world == 1:
+        # steady state of the public pipelined API: the H2D of set i+1 runs
+        # while set i is swept and its front read back (SweepPipeline);
+        # every step still copies its inputs in and its front rows out
+        from paper_2406_14424_b200.pipeline import SweepPipeline
+        pipe = SweepPipeline(N_REC, N_MODELS, grids, cost1, depth=3)
+        for _ in range(args.warmup):
+            pipe.submit(pin_cert, pin_corr)
+        pipe.drain()
+        torch.cuda.synchronize()
+        tp = time.perf_counter()
+        tickets = [pipe.submit(pin_cert, pin_corr) for _ in range(args.steps)]
+        rows = [pipe.result(t) for t in tickets]
+        torch.cuda.synchronize()
+        e2e_pipelined = (time.perf_counter() - tp) * 1e3 / args.steps
+        pipe_d2h = rows[-1].nbytes + 8
+        del pipe
     for _ in range(args.warmup):
         e2e_step()
     barrier(world)
@@ -347,11 +365,22 @@ def run_ours(args, world, rank, local):
                               "none": "not flushed"}[args.flush], "parallelism": f"weak: 1 tenant sweep per GPU, "
                        f"NCCL all-gather of Pareto fronts in e2e ({world} ranks)"},
             "breakdown_ms": {"build": build_avg, "eval": eval_avg, **part_ms},
-            "e2e": {"value": world * C / (e2e_ms * 1e-3), "unit": "config-evals/s",
-                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h_total,
-                    "path": "GridSweep from pinned host matrices -> build -> eval -> "
-                            "pareto_counts -> D2H front rows"},
+            "e2e": ({"value": C / (e2e_pipelined * 1e-3), "unit": "config-evals/s",
+                     "ms_per_step": e2e_pipelined, "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": pipe_d2h,
+                     "path": "SweepPipeline.submit/result from pinned host matrices: H2D of "
+                             "set i+1 on a copy stream while set i is built, scored, reduced "
+                             "to its exact Pareto front and the front rows read back; host "
+                             "wall clock over the steps, synchronized on both sides",
+                     "unpipelined": {"value": C / (e2e_ms * 1e-3), "ms_per_step": e2e_ms,
+                                     "path": "GridSweep from pinned host matrices -> build "
+                                             "-> eval -> pareto_counts -> D2H front rows"}}
+                    if e2e_pipelined is not None else
+                    {"value": world * C / (e2e_ms * 1e-3), "unit": "config-evals/s",
+                     "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h_total,
+                     "path": "GridSweep from pinned host matrices -> build -> eval -> "
+                             "pareto_counts -> D2H front rows (+ NCCL all-gather of fronts)"}),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                          "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                          "traffic": traffic, "algorithmic_bytes": dom_bytes,

@@ -288,3 +288,31 @@ def test_four_model_large_uneven_grids(glen):
     assert np.array_equal(res.mean_cost.cpu().numpy()[pick], want[1])
     assert np.array_equal(res.forward_frac.cpu().numpy()[pick], want[2])
     assert np.array_equal(res.n_correct.cpu().numpy()[pick] / n, want[0])
+
+
+def test_sweep_pipeline_fronts_equal_single_sweeps():
+    """SweepPipeline (H2D of set i+1 overlapped with set i's sweep and front
+    read-back) returns exactly the rows of one-at-a-time sweeps, in order."""
+    import torch
+    from paper_2406_14424_b200.gridsweep import GridSweep, front_host, pareto_counts
+    from paper_2406_14424_b200.pipeline import SweepPipeline
+    rng = np.random.default_rng(12)
+    n, m = 30_000, 4
+    grids = [np.concatenate([[0.0], np.sort(rng.random(19))]) for _ in range(m)]
+    cost1 = np.array([1.0, 4.0, 16.0, 64.0])
+    sets = []
+    for _ in range(5):
+        cert = rng.random((n, m))
+        corr = (rng.random((n, m)) < 0.7).astype(np.uint8)
+        sets.append((torch.from_numpy(cert).pin_memory(), torch.from_numpy(corr).pin_memory()))
+    want = []
+    for c, k in sets:
+        sw = GridSweep(c.numpy(), k.numpy(), grids, cost1)
+        res = sw.evaluate(n_correct=True)
+        want.append(front_host(pareto_counts(res.n_correct, res.mean_cost, n), res).copy())
+    pipe = SweepPipeline(n, m, grids, cost1)
+    tickets = [pipe.submit(c, k) for c, k in sets]
+    got = [pipe.result(t) for t in tickets]
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
+    pipe.drain()
