@@ -586,7 +586,7 @@ def run_reference(args, world, rank):
     threads = os.cpu_count() or 1
     sm, thr, ns = oracle.grid_configs(grids)
     rng = np.random.default_rng(3)
-    per_step = max(threads, 16)
+    per_step = max(threads, 16) * 8  # 8 configs per thread: thread start-up amortised
     for _ in range(args.warmup):
         p = rng.choice(sm.shape[0], size=per_step, replace=False)
         oracle.evaluate_encoded(cert, corr, sm[p], thr[p], ns[p], cost1, n_threads=threads)
