@@ -402,6 +402,8 @@ def run_ours(args, world, rank, local):
             line["ingest"] = _guarded(ingest_bench, args)
         if not args.skip_config4:
             line["config4b"] = _guarded(config4_bench, args, dev)
+        if not args.skip_config1:
+            line["config1"] = _guarded(config1_bench, args, dev)
         print(json.dumps(line), flush=True)
 
 
@@ -449,6 +451,57 @@ def stage_bench(args, dev, flush):
                      "frac": gbs / pk["hbm_gbs"], "launches_per_call": 1}
     out["workload"] = "cfg3 shape: 1M x 1000-class f32 logits, per-row thr, stable compaction"
     return out
+
+
+def config1_bench(args, dev):
+    """BASELINE configs[0] (the reference's CPU default): a 3-model cascade,
+    10k records, 100-level grids, the full product (C = 10,303) -- one CUDA
+    graph per sweep (build + eval), L2 flushed between steps; launch-bound by
+    design.  Beside it the oracle port of _evaluate_numba over all C configs
+    on all host threads (the reference's own CPU default, 1 core, takes
+    ~0.8 s: SURVEY 8d)."""
+    import torch
+
+    from oracle import oracle
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.cascades import grid_values
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    profiles = synth.make_profiles()
+    cert, corr = synth.validation_matrices(3, 10_000, 0.8, 0)
+    grids = [np.array(grid_values(cert[:, j], LEVELS)) for j in range(3)]
+    cost1 = profiles.cost1()
+    sw = GridSweep(cert, corr, grids, cost1)
+    out = sw.evaluate()
+    g = sw.capture(out)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        g.replay()
+    ts = []
+    for _ in range(max(args.steps, 10)):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = sum(ts) / len(ts)
+    sm, thr, ns = oracle.grid_configs(grids)
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=threads)
+    cpu_s = time.perf_counter() - t
+    ok = bool(np.array_equal(out.accuracy.cpu().numpy(), want[0]) and
+              np.array_equal(out.forward_frac.cpu().numpy(), want[2]))
+    del flush
+    return {"workload": "cfg1: 3-model cascade, 10k records, 100-level grids, full product",
+            "n_configs": sw.n_configs, "ms": ms, "config_evals_per_s": sw.n_configs / (ms * 1e-3),
+            "launches_per_step": sw.info.build_launches + sw.info.eval_launches,
+            "parity_full_product": ok,
+            "cpu_baseline": {"value": sw.n_configs / cpu_s, "unit": "config-evals/s",
+                             "cores": threads, "kind": "port",
+                             "sample": "all 10,303 configs x 10k records (oracle/oracle_eval.c)"}}
 
 
 def config4_bench(args, dev):
@@ -621,6 +674,7 @@ def main():
     ap.add_argument("--skip-stage", action="store_true", help="skip the stage-step leg")
     ap.add_argument("--skip-ingest", action="store_true", help="skip the ingest leg")
     ap.add_argument("--skip-config4", action="store_true", help="skip the 5-stage (cfg4b) leg")
+    ap.add_argument("--skip-config1", action="store_true", help="skip the 3-model cfg1 leg")
     ap.add_argument("--flush", choices=["write", "clean", "none"], default="write",
                     help="L2 eviction between timed steps (see flush_l2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,

@@ -58,8 +58,9 @@ __global__ void __launch_bounds__(1024) k(const uint32_t* idx, const uint32_t* i
       atomicAdd(sm + (__ldg(idx2 + r) % 12288u), 1u);
     }
     if (MODE == 7) atomicAdd(T32 + (c >> 1) * 2 + (c & 1), 1u), atomicAdd(T32 + 2 * 1048576 + (c % 4096), 1u);
+    if (MODE == 8) acc += atomicAdd(T64 + c, 1ull | (1ull << 16));  // ATOMG with the old value used
   }
-  if (MODE == 0 && acc == 12345) sink[0] = acc;
+  if ((MODE == 0 || MODE == 8) && acc == 12345) sink[0] = acc;
   if (MODE == 6) {
     __syncthreads();
     for (int i = threadIdx.x; i < 12288; i += blockDim.x)
@@ -143,6 +144,7 @@ int main() {
     printf("  1 RED.64 / rec, 10K-cell table   %7.2f us\n", run<5>(blocks, idx, idx2, T64, S64, T32, F4, sink));
     printf("  RED.64 + smem ATOMS / rec        %7.2f us\n", run<6>(blocks, idx, idx2, T64, S64, T32, F4, sink));
     printf("  2 RED.32 / rec (1M + 4K cells)   %7.2f us\n", run<7>(blocks, idx, idx2, T64, S64, T32, F4, sink));
+    printf("  1 ATOMG.64 / rec (old value used) %7.2f us\n", run<8>(blocks, idx, idx2, T64, S64, T32, F4, sink));
   }
   {
     double* cert;
