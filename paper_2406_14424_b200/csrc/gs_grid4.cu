@@ -400,6 +400,331 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
   phase(1, 5);
 }
 
+// ------------------------------------------------------ sorted build --
+// One-shot builds skip the global histogram: the reduction into a 16.5 MB
+// table is what held g4_hist above the streaming rate (one L2 reduction per
+// record, then a plane pass that re-reads and re-zeroes the table).  Here
+// g4_sort streams the records once and writes each as a 4-byte key
+// {b0, b2, k1, k2, k3, b1}, counting-sorted in shared memory by bucket
+// (b1, b0 half) within the CTA's record range, plus the range's bucket
+// offsets; g4_gather then builds each (b1, b0 half) plane in shared memory
+// from its bucket's keys (one shared 64-bit add of the packed {1, k3, k2}
+// per key), prefixes it along b2 and b0 and writes the same S / R1 / P0
+// tables as g4_plane.  Keys are 4 MB per 1M records and stay in L2.
+constexpr int kSortThreads = 1024;
+constexpr int kGatherThreads = 1024;
+constexpr int kSortMaxD1 = 1024;  // b1 takes 10 key bits
+constexpr int kSortSmemMax = 227 * 1024 - 4096;  // opt-in limit less the static arrays
+
+struct G4SortArgs {
+  const double* cert;
+  const uint8_t* corr;
+  int32_t n_rec;
+  int32_t vec_ok;
+  const double* grids;
+  int32_t glen[3];
+  int32_t d0, nb, per;         // buckets (one per b1), records per CTA
+  uint32_t* keys;              // [n_rec] sorted by bucket within each CTA's range
+  uint32_t* off;               // [parts][nb + 1] absolute key offsets of each bucket
+  uint32_t* G0;                // [d0] model-0 correct counts per b0
+};
+
+
+__global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_constant__ G4SortArgs a) {
+  extern __shared__ __align__(16) double s_grid[];  // grids, bucket tables, counts, keys
+  __shared__ uint32_t s_c0[kMaxDim4];
+  __shared__ uint32_t s_wsum[32];
+  const int n_grid = a.glen[0] + a.glen[1] + a.glen[2];
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + n_grid);
+  uint32_t* s_cnt = s_lut + 3 * kLutBuckets;           // [nb] -> bucket starts
+  uint32_t* s_key = s_cnt + ((a.nb + 3) & ~3);        // [per]
+  uint32_t* s_sorted = s_key + a.per;                 // [per]
+  uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_sorted + a.per);  // [per]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = blockIdx.x * a.per;
+  const int cnt = min(a.n_rec - r0, a.per);
+  phase(0, 0);
+  constexpr int kGridRegs = 5;
+  double gv[kGridRegs];
+#pragma unroll
+  for (int q = 0; q < kGridRegs; ++q) {
+    const int i = tid + q * kSortThreads;
+    gv[q] = i < n_grid ? __ldg(a.grids + i) : 0.0;
+  }
+  G4HistArgs ha{};
+  ha.cert = a.cert;
+  ha.corr = a.corr;
+  ha.vec_ok = a.vec_ok;
+  Rec4 v;
+  if (tid < cnt) v = load_rec4(ha, r0 + tid);
+#pragma unroll
+  for (int q = 0; q < kGridRegs; ++q) {
+    const int i = tid + q * kSortThreads;
+    if (i < n_grid) s_grid[i] = gv[q];
+  }
+  for (int i = tid; i < a.d0; i += kSortThreads) s_c0[i] = 0u;
+  for (int i = tid; i < a.nb; i += kSortThreads) s_cnt[i] = 0u;
+  __syncthreads();
+  const BinTables<3> bt = build_bin_tables<3, kSortThreads>(a.glen, s_grid, s_lut);
+  phase(0, 1);
+  for (int i = tid; i < cnt; i += kSortThreads) {
+    Rec4 nv;
+    if (i + kSortThreads < cnt) nv = load_rec4(ha, r0 + i + kSortThreads);
+    const uint32_t b0 = (uint32_t)bt.bin(0, v.x0);
+    const uint32_t b1 = (uint32_t)bt.bin(1, v.x1);
+    const uint32_t b2 = (uint32_t)bt.bin(2, v.x2);
+    const uint32_t k = v.k;
+    const uint32_t key = b0 | (b2 << 8) | ((k & 0xff00u) ? 1u << 16 : 0u) |
+                         ((k & 0xff0000u) ? 1u << 17 : 0u) | ((k & 0xff000000u) ? 1u << 18 : 0u) |
+                         (b1 << 19);
+    s_rank[i] = (uint16_t)atomicAdd(s_cnt + b1, 1u);
+    s_key[i] = key;
+    if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
+    v = nv;
+  }
+  phase(0, 2);
+  pdl_release();
+  __syncthreads();
+  // exclusive scan of the bucket counts (two per thread, nb <= 2 * kSortThreads)
+  {
+    const int i0 = 2 * tid, i1 = 2 * tid + 1;
+    const uint32_t t0 = i0 < a.nb ? s_cnt[i0] : 0u, t1 = i1 < a.nb ? s_cnt[i1] : 0u;
+    uint32_t x = t0 + t1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = s_wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_wsum[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t excl = x - (t0 + t1) + (warp ? s_wsum[warp - 1] : 0u);
+    uint32_t* off = a.off + (int64_t)blockIdx.x * (a.nb + 1);
+    if (i0 < a.nb) {
+      s_cnt[i0] = excl;
+      off[i0] = (uint32_t)r0 + excl;
+    }
+    if (i1 < a.nb) {
+      s_cnt[i1] = excl + t0;
+      off[i1] = (uint32_t)r0 + excl + t0;
+    }
+    if (tid == 0) off[a.nb] = (uint32_t)(r0 + cnt);
+  }
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kSortThreads) {
+    const uint32_t key = s_key[i];
+    s_sorted[s_cnt[key >> 19] + s_rank[i]] = key;
+  }
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kSortThreads) a.keys[r0 + i] = s_sorted[i];
+  for (int i = tid; i < a.d0; i += kSortThreads)
+    if (s_c0[i]) atomicAdd(a.G0 + i, s_c0[i]);
+  phase(0, 3);
+}
+
+struct G4GatherArgs {
+  const uint32_t* keys;
+  const uint32_t* off;        // [parts][nb + 1]
+  int32_t n_parts, nb;
+  unsigned long long* S;      // [d0][d1][d2p] packed {cnt, c3, c2}
+  uint32_t* R1;               // [d0][d1p]
+  uint32_t* G0;               // [d0] raw c0, re-zeroed here
+  uint32_t* P0;               // [d0] inclusive prefix of G0
+  int32_t d0, d1, d2, d2p, d1p;
+  int32_t hp;                 // plane row pitch in cells (odd: conflict-free row walk)
+  int32_t ns2, seg2;          // b2 segments of the row walk
+  int32_t ns0, seg0;          // b0 segments of the column walk
+};
+
+// One CTA per b1 builds the whole (b0, b2) plane (b1's bin holds ~1/d1 of
+// the records by construction of the quantile grids, so the CTAs are
+// balanced).  A thread takes one aligned 8-key octet of the key array at a
+// time (two 16-byte loads) and masks the keys outside this bucket's
+// segment; octets are numbered across the record ranges' segments and found
+// by a binary search over the per-range octet offsets.
+__global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __grid_constant__ G4GatherArgs a) {
+  extern __shared__ __align__(16) unsigned long long s_pl[];  // [d0][hp], then tables
+  __shared__ uint32_t s_wsum[kGatherThreads / 32];
+  __shared__ uint32_t s_total, s_noct;
+  const int b1 = blockIdx.x;
+  const int d0 = a.d0, d2 = a.d2, hp = a.hp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kGatherThreads / 32;
+  const int cells = d0 * hp;
+  uint32_t* s_w = reinterpret_cast<uint32_t*>(s_pl);                  // [cells] x 2 words
+  uint32_t* s_c2 = s_w + 2 * (size_t)cells;                           // [cells]
+  uint32_t* s_c1 = s_c2 + cells;                                      // [d0]
+  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(s_c1 + d0) + 15) & ~(uintptr_t)15);  // [kGatherThreads]
+  uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_seg + kGatherThreads);  // [parts] first key
+  uint32_t* s_end = s_beg + a.n_parts;                                // [parts] end key
+  uint32_t* s_opos = s_end + a.n_parts;                               // [parts + 1] first octet
+  phase(1, 0);
+  for (int i = tid; i < cells; i += kGatherThreads) {
+    s_pl[i] = 0ull;
+    s_c2[i] = 0u;
+  }
+  for (int i = tid; i < d0; i += kGatherThreads) s_c1[i] = 0u;
+  pdl_wait();  // keys, offsets and G0 are complete
+  if (b1 == 0 && warp == nwarps - 1) {  // c0: inclusive prefix over b0, re-zero
+    uint32_t carry = 0;
+    for (int b = 0; b < d0; b += 32) {
+      const int i = b + lane;
+      uint32_t x = i < d0 ? a.G0[i] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      x += carry;
+      if (i < d0) {
+        a.P0[i] = x;
+        a.G0[i] = 0u;
+      }
+      carry = __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  // this bucket's key segment in every record range and its octet count
+  uint32_t noct = 0, len = 0;
+  if (tid < a.n_parts) {
+    const uint32_t* o = a.off + (int64_t)tid * (a.nb + 1) + b1;
+    const uint32_t b = o[0], e = o[1];
+    s_beg[tid] = b;
+    s_end[tid] = e;
+    len = e - b;
+    noct = e > b ? ((e - 1) >> 3) - (b >> 3) + 1 : 0u;
+  }
+  uint32_t x = noct, y = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, x, o), u = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) x += t, y += u;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  if (tid == 0) s_total = 0u;
+  __syncthreads();
+  uint32_t wbase = 0;
+  for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
+  if (tid < a.n_parts) s_opos[tid] = wbase + x - noct;
+  if (tid == kGatherThreads - 1) s_noct = wbase + x;
+  if (lane == 31 && y) atomicAdd(&s_total, y);
+  __syncthreads();
+  phase(1, 1);
+  const uint32_t total = s_total, n_oct = s_noct;
+  const int n_parts = a.n_parts;
+  // shared 64-bit adds are CAS loops on sm_100: count in 32-bit words
+  // instead, {cnt | c3 << 16} in one word while no field can reach 2^16
+  // (fewer than 2^16 keys in the bucket), else cnt and c3 in the two words
+  // of the cell; c2 in its own word array; then pack once
+  const bool narrow = total < 65536u;
+  for (uint32_t m = tid; m < n_oct; m += kGatherThreads) {
+    int lo = 0, hi = n_parts;  // largest p with s_opos[p] <= m
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_opos[mid] <= m) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t beg = s_beg[lo], end = s_end[lo];
+    const uint32_t first = ((beg >> 3) + (m - s_opos[lo])) << 3;  // key index of the octet
+    const uint4* src = reinterpret_cast<const uint4*>(a.keys + first);
+    const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+    const uint32_t kv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t i = first + u;
+      if (i < beg || i >= end) continue;
+      const uint32_t key = kv[u];
+      const int r = (int)(key & 255u);
+      const int cell = r * hp + (int)((key >> 8) & 255u);
+      const uint32_t k3 = (key >> 18) & 1u;
+      if (narrow) {
+        atomicAdd(s_w + 2 * cell, 1u + (k3 << 16));
+      } else {
+        atomicAdd(s_w + 2 * cell, 1u);
+        if (k3) atomicAdd(s_w + 2 * cell + 1, 1u);
+      }
+      if (key & (1u << 17)) atomicAdd(s_c2 + cell, 1u);
+      if (key & (1u << 16)) atomicAdd(s_c1 + r, 1u);
+    }
+  }
+  __syncthreads();
+  phase(1, 2);
+  // row walk along b2, packing each cell to {cnt, c3, c2} as it is read
+  {
+    const int r = tid % d0, s = tid / d0;
+    const bool live = s < a.ns2;
+    const int c_lo = s * a.seg2, c_hi = min(d2, c_lo + a.seg2);
+    const int rb = r * hp;
+    auto packed = [&](int cell) -> unsigned long long {
+      const uint32_t w0 = s_w[2 * cell], w1 = s_w[2 * cell + 1];
+      const uint32_t cnt = narrow ? (w0 & 0xffffu) : w0, c3 = narrow ? (w0 >> 16) : w1;
+      return (unsigned long long)cnt | ((unsigned long long)c3 << 21) |
+             ((unsigned long long)s_c2[cell] << 42);
+    };
+    unsigned long long sum = 0;
+    if (live)
+      for (int c = c_lo; c < c_hi; ++c) sum += packed(rb + c);
+    if (live) s_seg[s * d0 + r] = sum;
+    __syncthreads();
+    if (live) {
+      unsigned long long run = 0;
+      for (int p = 0; p < s; ++p) run += s_seg[p * d0 + r];
+      for (int c = c_lo; c < c_hi; ++c) {
+        run += packed(rb + c);
+        s_pl[rb + c] = run;  // the cell's two words, read just above
+      }
+    }
+    __syncthreads();
+  }
+  phase(1, 3);
+  // column walk along b0 (prefix along b2 already in place); c1 prefix over b0
+  const int c = tid % d2, s = tid / d2;
+  const bool live = s < a.ns0;
+  const int r_lo = s * a.seg0, r_hi = min(d0, r_lo + a.seg0);
+  unsigned long long sum = 0;
+  if (live)
+    for (int r = r_lo; r < r_hi; ++r) sum += s_pl[(size_t)r * hp + c];
+  if (live) s_seg[s * d2 + c] = sum;
+  if (warp == nwarps - 1) {
+    uint32_t carry = 0;
+    for (int b = 0; b < d0; b += 32) {
+      const int r = b + lane;
+      uint32_t v = r < d0 ? s_c1[r] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      v += carry;
+      if (r < d0) a.R1[(int64_t)r * a.d1p + b1] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  pdl_release();
+  phase(1, 4);
+  if (live) {
+    unsigned long long P = 0;
+    for (int p = 0; p < s; ++p) P += s_seg[p * d2 + c];
+    unsigned long long* S = a.S + (int64_t)b1 * a.d2p + c;
+    const int64_t plane = (int64_t)a.d1 * a.d2p;
+    for (int r = r_lo; r < r_hi; ++r) {
+      P += s_pl[(size_t)r * hp + c];
+      S[(int64_t)r * plane] = P;
+    }
+  }
+  phase(1, 5);
+}
+
 // ------------------------------------------------------------------ eval --
 constexpr int kEval4Threads = 512;
 
@@ -715,7 +1040,29 @@ bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
          (d1 + 1) / 2 * (d2p * 8 + 28) + (kEval4Threads + 2 * d2) * 8 + d1 * 4 <= (int64_t)kGrid4SlabMax;
 }
 
-Grid4Layout grid4_layout(const int32_t* glen) {
+// Shared memory of the sorted build's two kernels (0 when it does not apply).
+struct SortPlan {
+  int parts, per;
+  size_t sort_smem, gather_smem;
+};
+
+SortPlan sort_plan(const Grid4Layout& L, const int32_t* glen, int64_t n_rec) {
+  SortPlan sp{};
+  if (L.d1 > kSortMaxD1 || n_rec < 1) return sp;
+  sp.parts = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), (n_rec + kSortThreads - 1) / kSortThreads));
+  sp.per = (int)(((n_rec + sp.parts - 1) / sp.parts + 31) & ~31ll);
+  sp.parts = (int)((n_rec + sp.per - 1) / sp.per);
+  sp.sort_smem = (size_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * 4 +
+                 (size_t)((L.nb + 3) & ~3) * 4 + (size_t)sp.per * 10;
+  sp.gather_smem = (size_t)L.d0 * L.hp * 12 + (size_t)L.d0 * 4 + 16 + kGatherThreads * 8 +
+                   (size_t)sp.parts * 12 + 4;
+  if (sp.sort_smem > (size_t)kSortSmemMax || sp.gather_smem > kGrid4SlabMax || sp.parts > kGatherThreads ||
+      L.d2 > kGatherThreads)
+    sp.sort_smem = sp.gather_smem = 0;
+  return sp;
+}
+
+Grid4Layout grid4_layout(const int32_t* glen, int64_t n_rec) {
   Grid4Layout L{};
   L.d0 = glen[0] + 1;
   L.d1 = glen[1] + 1;
@@ -723,6 +1070,8 @@ Grid4Layout grid4_layout(const int32_t* glen) {
   L.d2p = (L.d2 + 1) & ~1;
   L.d1p = (L.d1 + 3) & ~3;
   L.hp = L.d2 | 1;
+  L.nb = L.d1;
+  L.max_parts = sm_count();
   const size_t bH = round_up((size_t)L.d0 * L.d1 * L.hp * 16, 256);
   const size_t bS = round_up((size_t)L.d0 * L.d1 * L.d2p * 8, 256);
   const size_t bR1 = round_up((size_t)L.d0 * L.d1p * 4, 256);
@@ -733,14 +1082,17 @@ Grid4Layout grid4_layout(const int32_t* glen) {
   L.offR1 = L.offS + bS;
   L.offP0 = L.offR1 + bR1;
   L.offCnt = L.offP0 + bG;
-  L.bytes = L.offCnt + 256;
+  L.offKeys = L.offCnt + 256;
+  L.offOff = L.offKeys + round_up((size_t)std::max<int64_t>(n_rec, 1) * 4, 256);
+  L.bytes = L.offOff + round_up((size_t)L.max_parts * (L.nb + 1) * 4, 256);
+  L.sorted = sort_plan(L, glen, n_rec).sort_smem != 0;
   return L;
 }
 
 cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_chunk,
                              const double* grids, const int32_t* glen, uint8_t* ws, bool dirty,
                              cudaStream_t st) {
-  const Grid4Layout L = grid4_layout(glen);
+  const Grid4Layout L = grid4_layout(glen, n_chunk);
   float* H = reinterpret_cast<float*>(ws + L.offH);
   uint32_t* G0 = reinterpret_cast<uint32_t*>(ws + L.offG0);
   if (dirty) {
@@ -774,7 +1126,7 @@ cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_
 }
 
 cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
-  const Grid4Layout L = grid4_layout(glen);
+  const Grid4Layout L = grid4_layout(glen, 1);  // the table offsets do not depend on n_rec
   float* H = reinterpret_cast<float*>(ws + L.offH);
   uint32_t* G0 = reinterpret_cast<uint32_t*>(ws + L.offG0);
   cudaError_t e = cudaSuccess;
@@ -805,18 +1157,74 @@ cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
   return launch_pdl(g4_plane_kernel, (unsigned)(2 * L.d1), kPlaneThreads, psmem, st, p);
 }
 
+// One-shot build: the bucket-sorted kernels when their shared-memory plan
+// fits (the headline shapes), else histogram + plane.  Either way the
+// workspace is left as the streamed path expects it (H and G0 zero).
 cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
                         const int32_t* glen, uint8_t* ws, bool dirty, cudaStream_t st) {
-  cudaError_t e = grid4_accumulate(cert, corr, n_rec, grids, glen, ws, dirty, st);
-  if (e != cudaSuccess) return e;
-  return grid4_finish(glen, ws, st);
+  const Grid4Layout L = grid4_layout(glen, n_rec);
+  const SortPlan sp = sort_plan(L, glen, n_rec);
+  if (!L.sorted || sp.sort_smem == 0 || sp.parts > L.max_parts) {
+    cudaError_t e = grid4_accumulate(cert, corr, n_rec, grids, glen, ws, dirty, st);
+    if (e != cudaSuccess) return e;
+    return grid4_finish(glen, ws, st);
+  }
+  cudaError_t e;
+  if (dirty) {
+    if ((e = cudaMemsetAsync(ws, 0, L.offS, st)) != cudaSuccess) return e;  // H and G0
+    if ((e = cudaMemsetAsync(ws + L.offCnt, 0, 256, st)) != cudaSuccess) return e;
+  }
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ws + L.offKeys);
+  uint32_t* off = reinterpret_cast<uint32_t*>(ws + L.offOff);
+  uint32_t* G0 = reinterpret_cast<uint32_t*>(ws + L.offG0);
+  G4SortArgs a{};
+  a.cert = cert;
+  a.corr = corr;
+  a.n_rec = (int32_t)n_rec;
+  a.vec_ok = aligned16(cert) && ((reinterpret_cast<uintptr_t>(corr) & 3u) == 0);
+  a.grids = grids;
+  for (int j = 0; j < 3; ++j) a.glen[j] = glen[j];
+  a.d0 = L.d0;
+  a.nb = L.nb;
+  a.per = sp.per;
+  a.keys = keys;
+  a.off = off;
+  a.G0 = G0;
+  static std::atomic<int> smem_sort{0}, smem_gather{0};
+  if ((e = ensure_smem4(g4_sort_kernel, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
+  g4_sort_kernel<<<(unsigned)sp.parts, kSortThreads, sp.sort_smem, st>>>(a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  G4GatherArgs g{};
+  g.keys = keys;
+  g.off = off;
+  g.n_parts = sp.parts;
+  g.nb = L.nb;
+  g.S = reinterpret_cast<unsigned long long*>(ws + L.offS);
+  g.R1 = reinterpret_cast<uint32_t*>(ws + L.offR1);
+  g.G0 = G0;
+  g.P0 = reinterpret_cast<uint32_t*>(ws + L.offP0);
+  g.d0 = L.d0;
+  g.d1 = L.d1;
+  g.d2 = L.d2;
+  g.d2p = L.d2p;
+  g.d1p = L.d1p;
+  g.hp = L.hp;
+  g.ns2 = std::max(1, std::min(kGatherThreads / L.d0, L.d2));
+  g.seg2 = (L.d2 + g.ns2 - 1) / g.ns2;
+  g.ns2 = (L.d2 + g.seg2 - 1) / g.seg2;
+  g.ns0 = std::max(1, std::min(kGatherThreads / L.d2, L.d0));
+  g.seg0 = (L.d0 + g.ns0 - 1) / g.ns0;
+  g.ns0 = (L.d0 + g.seg0 - 1) / g.seg0;
+  if ((e = ensure_smem4(g4_gather_kernel, smem_gather, (size_t)kGrid4SlabMax)) != cudaSuccess) return e;
+  return launch_pdl(g4_gather_kernel, (unsigned)L.d1, kGatherThreads, sp.gather_smem, st, g);
 }
 
 cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct_begin,
                        const uint32_t* struct_mask, int n_struct, const double* cost1,
                        int64_t cfg_begin, int64_t cfg_count, double* acc, double* cost,
                        double* frac, uint32_t* n_correct, const uint8_t* ws, cudaStream_t st) {
-  const Grid4Layout L = grid4_layout(glen);
+  const Grid4Layout L = grid4_layout(glen, n_rec);
   G4EvalArgs a{};
   a.d0 = L.d0;
   a.d1 = L.d1;

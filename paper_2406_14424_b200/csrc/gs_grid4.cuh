@@ -12,11 +12,13 @@ constexpr size_t kGrid4SlabMax = 200 * 1024;      // one (b1, b2) slab in shared
 struct Grid4Layout {
   int32_t d0, d1, d2, d2p, d1p;  // table dims (grid length + 1), padded pitches
   int32_t hp;                    // histogram row pitch (odd)
-  size_t offH, offG0, offS, offR1, offP0, offCnt, bytes;
+  int32_t nb, max_parts;         // sorted build: buckets (2 per b1), record ranges
+  bool sorted;                   // one-shot builds take the bucket-sort kernels
+  size_t offH, offG0, offS, offR1, offP0, offCnt, offKeys, offOff, bytes;
 };
 
 bool grid4_supported(int64_t n_rec, int32_t n_models, const int32_t* grid_len);
-Grid4Layout grid4_layout(const int32_t* grid_len);
+Grid4Layout grid4_layout(const int32_t* grid_len, int64_t n_rec);
 // accumulate: add n_chunk records to the histogram; finish: prefix tables
 cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_chunk,
                              const double* grids, const int32_t* grid_len, uint8_t* workspace,

@@ -151,7 +151,7 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->bytes = p->offFlag + 256;
   p->g4 = grid4_supported(n_rec, M, p->glen);
   if (p->g4) {
-    p->bytes = grid4_layout(p->glen).bytes;
+    p->bytes = grid4_layout(p->glen, n_rec).bytes;
     return GS_OK;
   }
   p->walk = M == 4 && p->dims[0] <= 160 &&
@@ -1289,7 +1289,7 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
   info->workspace_bytes = p.bytes;
   info->fast_path = p.g4 ? 1 : 0;
   if (p.g4) {
-    info->build_launches = 2;  // g4_hist, g4_prefix0
+    info->build_launches = 2;  // g4_sort + g4_gather (one-shot) or g4_hist + g4_plane
     info->eval_launches = 1;   // g4_eval
   } else {
     // mirrors gs_grid_build / prefix_table / gs_grid_eval below

@@ -14,9 +14,9 @@ from paper_2406_14424_b200 import _lib  # noqa: E402
 from paper_2406_14424_b200.gridsweep import GridSweep  # noqa: E402
 
 K, CTAS, SLOTS = 3, 1024, 8
-names = ["g4_hist", "g4_plane", "g4_eval"]
-labels = [["start", "tables", "loop done", "bar", "end"],
-          ["start", "tile in", "zeroed", "row walk", "cluster", "end"],
+names = ["g4_sort", "g4_gather", "g4_eval"]
+labels = [["start", "tables", "loop done", "end"],
+          ["start", "segments", "plane built", "row walk", "cluster", "end"],
           ["start", "slab in", "cluster", "tables", "edges", "end"]]
 _, cert, corr, grids, cost1 = bench.workload(0)
 sw = GridSweep(cert, corr, grids, cost1, build=False)
