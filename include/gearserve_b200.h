@@ -88,6 +88,13 @@ int gs_eval_encoded(const double* certainty, const uint8_t* correct,
  * reused-for-something-else) workspace to have it zeroed first.
  * ---------------------------------------------------------------------- */
 #define GS_GRID_WORKSPACE_DIRTY 1
+/* Four-model path only (else GS_EUNSUPPORTED): run one of the build's two
+ * passes, for timing them apart.  RECORDS_PASS is the pass over the records
+ * (bucket sort into keys, or the histogram of the streamed variant) and
+ * must be followed by TABLES_PASS (keys / histogram -> prefix tables) on
+ * the same workspace before gs_grid_eval; neither flag = both passes. */
+#define GS_GRID_BUILD_RECORDS_PASS 2
+#define GS_GRID_BUILD_TABLES_PASS 4
 
 typedef struct gs_grid_info {
   int64_t n_configs;      /* total configs of the enumeration            */
@@ -98,7 +105,10 @@ typedef struct gs_grid_info {
   size_t workspace_bytes; /* for gs_grid_build / eval                    */
   int32_t build_launches; /* kernels one gs_grid_build enqueues           */
   int32_t eval_launches;  /* kernels one full-range gs_grid_eval enqueues */
-  int32_t fast_path;      /* 1: four-model packed path (n_rec < 2^21)     */
+  int32_t fast_path;      /* four-model packed path (n_rec < 2^21): 1,   */
+                          /* 2 when gs_grid_build takes the bucket-sort  */
+                          /* kernels (grid_len[1] < 1024, shared-memory  */
+                          /* plan fits); 0: general path                 */
   int32_t reserved;
 } gs_grid_info;
 
@@ -108,7 +118,7 @@ int gs_grid_build(const double* certainty, const uint8_t* correct,
                   int64_t n_rec, int32_t n_models, const double* grids,
                   const int32_t* grid_len, void* workspace,
                   size_t workspace_bytes, int32_t flags, void* stream);
-/* Streamed build (gs_grid_info.fast_path == 1 only, else GS_EUNSUPPORTED):
+/* Streamed build (gs_grid_info.fast_path != 0 only, else GS_EUNSUPPORTED):
  * gs_grid_accumulate adds the n_chunk records at certainty / correct (a
  * slice of the n_rec-record validation set) to the histogram, so host->device
  * copies of later slices overlap the binning of earlier ones;

@@ -45,6 +45,7 @@
 // and likewise for the shorter structures.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -430,6 +431,7 @@ struct G4SortArgs {
 };
 
 
+template <bool VEC>
 __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_constant__ G4SortArgs a) {
   extern __shared__ __align__(16) double s_grid[];  // grids, bucket tables, counts, keys
   __shared__ uint32_t s_c0[kMaxDim4];
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   G4HistArgs ha{};
   ha.cert = a.cert;
   ha.corr = a.corr;
-  ha.vec_ok = a.vec_ok;
+  ha.vec_ok = VEC ? 1 : 0;  // a compile-time branch in load_rec4
   Rec4 v;
   if (tid < cnt) v = load_rec4(ha, r0 + tid);
 #pragma unroll
@@ -465,24 +467,27 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   for (int i = tid; i < a.d0; i += kSortThreads) s_c0[i] = 0u;
   for (int i = tid; i < a.nb; i += kSortThreads) s_cnt[i] = 0u;
   __syncthreads();
-  const BinTables<3> bt = build_bin_tables<3, kSortThreads>(a.glen, s_grid, s_lut);
   phase(0, 1);
-  for (int i = tid; i < cnt; i += kSortThreads) {
-    Rec4 nv;
-    if (i + kSortThreads < cnt) nv = load_rec4(ha, r0 + i + kSortThreads);
-    const uint32_t b0 = (uint32_t)bt.bin(0, v.x0);
-    const uint32_t b1 = (uint32_t)bt.bin(1, v.x1);
-    const uint32_t b2 = (uint32_t)bt.bin(2, v.x2);
-    const uint32_t k = v.k;
+  const BinTables<3> bt = build_bin_tables<3, kSortThreads>(a.glen, s_grid, s_lut);
+  phase(0, 2);
+  auto put = [&](int i, double x0, double x1, double x2, uint32_t k) {
+    const uint32_t b0 = (uint32_t)bt.bin(0, x0);
+    const uint32_t b1 = (uint32_t)bt.bin(1, x1);
+    const uint32_t b2 = (uint32_t)bt.bin(2, x2);
     const uint32_t key = b0 | (b2 << 8) | ((k & 0xff00u) ? 1u << 16 : 0u) |
                          ((k & 0xff0000u) ? 1u << 17 : 0u) | ((k & 0xff000000u) ? 1u << 18 : 0u) |
                          (b1 << 19);
     s_rank[i] = (uint16_t)atomicAdd(s_cnt + b1, 1u);
     s_key[i] = key;
     if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
+  };
+  for (int i = tid; i < cnt; i += kSortThreads) {
+    Rec4 nv;
+    if (i + kSortThreads < cnt) nv = load_rec4(ha, r0 + i + kSortThreads);
+    put(i, v.x0, v.x1, v.x2, v.k);
     v = nv;
   }
-  phase(0, 2);
+  phase(0, 3);
   pdl_release();
   __syncthreads();
   // exclusive scan of the bucket counts (two per thread, nb <= 2 * kSortThreads)
@@ -520,6 +525,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
     if (tid == 0) off[a.nb] = (uint32_t)(r0 + cnt);
   }
   __syncthreads();
+  phase(0, 4);
   for (int i = tid; i < cnt; i += kSortThreads) {
     const uint32_t key = s_key[i];
     s_sorted[s_cnt[key >> 19] + s_rank[i]] = key;
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   for (int i = tid; i < cnt; i += kSortThreads) a.keys[r0 + i] = s_sorted[i];
   for (int i = tid; i < a.d0; i += kSortThreads)
     if (s_c0[i]) atomicAdd(a.G0 + i, s_c0[i]);
-  phase(0, 3);
+  phase(0, 5);
 }
 
 struct G4GatherArgs {
@@ -547,14 +553,11 @@ struct G4GatherArgs {
 
 // One CTA per b1 builds the whole (b0, b2) plane (b1's bin holds ~1/d1 of
 // the records by construction of the quantile grids, so the CTAs are
-// balanced).  A thread takes one aligned 8-key octet of the key array at a
-// time (two 16-byte loads) and masks the keys outside this bucket's
-// segment; octets are numbered across the record ranges' segments and found
-// by a binary search over the per-range octet offsets.
+// balanced).  A warp takes one record range's segment of the bucket at a
+// time, a key per lane.
 __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __grid_constant__ G4GatherArgs a) {
   extern __shared__ __align__(16) unsigned long long s_pl[];  // [d0][hp], then tables
-  __shared__ uint32_t s_wsum[kGatherThreads / 32];
-  __shared__ uint32_t s_total, s_noct;
+  __shared__ uint32_t s_total;
   const int b1 = blockIdx.x;
   const int d0 = a.d0, d2 = a.d2, hp = a.hp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -567,7 +570,6 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
       (reinterpret_cast<uintptr_t>(s_c1 + d0) + 15) & ~(uintptr_t)15);  // [kGatherThreads]
   uint32_t* s_beg = reinterpret_cast<uint32_t*>(s_seg + kGatherThreads);  // [parts] first key
   uint32_t* s_end = s_beg + a.n_parts;                                // [parts] end key
-  uint32_t* s_opos = s_end + a.n_parts;                               // [parts + 1] first octet
   phase(1, 0);
   for (int i = tid; i < cells; i += kGatherThreads) {
     s_pl[i] = 0ull;
@@ -593,94 +595,110 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
       carry = __shfl_sync(0xffffffffu, x, 31);
     }
   }
-  // this bucket's key segment in every record range and its octet count
-  uint32_t noct = 0, len = 0;
+  // this bucket's key segment in every record range
+  uint32_t len = 0;
   if (tid < a.n_parts) {
     const uint32_t* o = a.off + (int64_t)tid * (a.nb + 1) + b1;
     const uint32_t b = o[0], e = o[1];
     s_beg[tid] = b;
     s_end[tid] = e;
     len = e - b;
-    noct = e > b ? ((e - 1) >> 3) - (b >> 3) + 1 : 0u;
   }
-  uint32_t x = noct, y = len;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, x, o), u = __shfl_up_sync(0xffffffffu, y, o);
-    if (lane >= o) x += t, y += u;
-  }
-  if (lane == 31) s_wsum[warp] = x;
   if (tid == 0) s_total = 0u;
   __syncthreads();
-  uint32_t wbase = 0;
-  for (int w = 0; w < warp; ++w) wbase += s_wsum[w];
-  if (tid < a.n_parts) s_opos[tid] = wbase + x - noct;
-  if (tid == kGatherThreads - 1) s_noct = wbase + x;
-  if (lane == 31 && y) atomicAdd(&s_total, y);
+  const uint32_t wl = __reduce_add_sync(0xffffffffu, len);
+  if (lane == 0 && wl) atomicAdd(&s_total, wl);
   __syncthreads();
   phase(1, 1);
-  const uint32_t total = s_total, n_oct = s_noct;
+  const uint32_t total = s_total;
   const int n_parts = a.n_parts;
   // shared 64-bit adds are CAS loops on sm_100: count in 32-bit words
-  // instead, {cnt | c3 << 16} in one word while no field can reach 2^16
-  // (fewer than 2^16 keys in the bucket), else cnt and c3 in the two words
-  // of the cell; c2 in its own word array; then pack once
+  // instead, {cnt | c3 << 16, c2 | c1 << 16} while no field can reach 2^16
+  // (fewer than 2^16 keys in the bucket), else {cnt, c3} with c2 per cell
+  // and c1 per row apart; then pack once
   const bool narrow = total < 65536u;
-  for (uint32_t m = tid; m < n_oct; m += kGatherThreads) {
-    int lo = 0, hi = n_parts;  // largest p with s_opos[p] <= m
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_opos[mid] <= m) lo = mid;
-      else hi = mid;
-    }
-    const uint32_t beg = s_beg[lo], end = s_end[lo];
-    const uint32_t first = ((beg >> 3) + (m - s_opos[lo])) << 3;  // key index of the octet
-    const uint4* src = reinterpret_cast<const uint4*>(a.keys + first);
-    const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
-    const uint32_t kv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t i = first + u;
-      if (i < beg || i >= end) continue;
-      const uint32_t key = kv[u];
-      const int r = (int)(key & 255u);
-      const int cell = r * hp + (int)((key >> 8) & 255u);
-      const uint32_t k3 = (key >> 18) & 1u;
-      if (narrow) {
-        atomicAdd(s_w + 2 * cell, 1u + (k3 << 16));
-      } else {
-        atomicAdd(s_w + 2 * cell, 1u);
-        if (k3) atomicAdd(s_w + 2 * cell + 1, 1u);
-      }
+  auto count = [&](uint32_t key) {
+    const int r = (int)(key & 255u);
+    const int cell = r * hp + (int)((key >> 8) & 255u);
+    const uint32_t k3 = (key >> 18) & 1u;
+    if (narrow) {
+      atomicAdd(s_w + 2 * cell, 1u + (k3 << 16));
+      const uint32_t w1 = ((key >> 17) & 1u) | (key & (1u << 16));
+      if (w1) atomicAdd(s_w + 2 * cell + 1, w1);
+    } else {
+      atomicAdd(s_w + 2 * cell, 1u);
+      if (k3) atomicAdd(s_w + 2 * cell + 1, 1u);
       if (key & (1u << 17)) atomicAdd(s_c2 + cell, 1u);
       if (key & (1u << 16)) atomicAdd(s_c1 + r, 1u);
     }
+  };
+  // a warp per record range: its segment's first kHead keys are loaded one
+  // range ahead (kHead / 32 coalesced loads in flight per lane), the rest
+  // of a long segment inline
+  constexpr int kHead = 4;  // x 32 keys
+  constexpr uint32_t kNone = 0xffffffffu;
+  uint32_t nxt[kHead];
+  auto load_head = [&](int p, uint32_t (&k)[kHead]) {
+    const uint32_t b = p < n_parts ? s_beg[p] : 0u, e = p < n_parts ? s_end[p] : 0u;
+#pragma unroll
+    for (int j = 0; j < kHead; ++j) {
+      const uint32_t i = b + 32u * j + lane;
+      k[j] = i < e ? __ldg(a.keys + i) : kNone;
+    }
+  };
+  load_head(warp, nxt);
+  for (int p = warp; p < n_parts; p += nwarps) {
+    uint32_t cur[kHead];
+#pragma unroll
+    for (int j = 0; j < kHead; ++j) cur[j] = nxt[j];
+    load_head(p + nwarps, nxt);
+#pragma unroll
+    for (int j = 0; j < kHead; ++j)
+      if (cur[j] != kNone) count(cur[j]);
+    const uint32_t e = s_end[p];
+    for (uint32_t i = s_beg[p] + 32u * kHead + lane; i < e; i += 32u) count(__ldg(a.keys + i));
   }
   __syncthreads();
   phase(1, 2);
-  // row walk along b2, packing each cell to {cnt, c3, c2} as it is read
+  // row walk along b2, packing each cell to {cnt, c3, c2} (21-bit fields)
+  // as its prefix is stored.  Narrow: the 16-bit fields of the two words
+  // are prefixed by plain 64-bit adds (no field's sum reaches 2^16), and
+  // the row total's c1 field is the row's C1 count.
   {
     const int r = tid % d0, s = tid / d0;
     const bool live = s < a.ns2;
     const int c_lo = s * a.seg2, c_hi = min(d2, c_lo + a.seg2);
     const int rb = r * hp;
-    auto packed = [&](int cell) -> unsigned long long {
-      const uint32_t w0 = s_w[2 * cell], w1 = s_w[2 * cell + 1];
-      const uint32_t cnt = narrow ? (w0 & 0xffffu) : w0, c3 = narrow ? (w0 >> 16) : w1;
-      return (unsigned long long)cnt | ((unsigned long long)c3 << 21) |
-             ((unsigned long long)s_c2[cell] << 42);
-    };
     unsigned long long sum = 0;
-    if (live)
-      for (int c = c_lo; c < c_hi; ++c) sum += packed(rb + c);
-    if (live) s_seg[s * d0 + r] = sum;
+    if (live) {
+      if (narrow)
+        for (int c = c_lo; c < c_hi; ++c) sum += s_pl[rb + c];
+      else
+        for (int c = c_lo; c < c_hi; ++c) {
+          const int cell = rb + c;
+          sum += (unsigned long long)s_w[2 * cell] | ((unsigned long long)s_w[2 * cell + 1] << 21) |
+                 ((unsigned long long)s_c2[cell] << 42);
+        }
+      s_seg[s * d0 + r] = sum;
+    }
     __syncthreads();
     if (live) {
       unsigned long long run = 0;
       for (int p = 0; p < s; ++p) run += s_seg[p * d0 + r];
-      for (int c = c_lo; c < c_hi; ++c) {
-        run += packed(rb + c);
-        s_pl[rb + c] = run;  // the cell's two words, read just above
+      if (narrow) {
+        for (int c = c_lo; c < c_hi; ++c) {
+          run += s_pl[rb + c];
+          s_pl[rb + c] = (run & 0xffffull) | (((run >> 16) & 0xffffull) << 21) |
+                         (((run >> 32) & 0xffffull) << 42);
+        }
+        if (c_hi == d2) s_c1[r] = (uint32_t)(run >> 48);
+      } else {
+        for (int c = c_lo; c < c_hi; ++c) {
+          const int cell = rb + c;
+          run += (unsigned long long)s_w[2 * cell] | ((unsigned long long)s_w[2 * cell + 1] << 21) |
+                 ((unsigned long long)s_c2[cell] << 42);
+          s_pl[cell] = run;  // the cell's two words, read just above
+        }
       }
     }
     __syncthreads();
@@ -1161,16 +1179,16 @@ cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
 // fits (the headline shapes), else histogram + plane.  Either way the
 // workspace is left as the streamed path expects it (H and G0 zero).
 cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
-                        const int32_t* glen, uint8_t* ws, bool dirty, cudaStream_t st) {
+                        const int32_t* glen, uint8_t* ws, bool dirty, int passes, cudaStream_t st) {
   const Grid4Layout L = grid4_layout(glen, n_rec);
   const SortPlan sp = sort_plan(L, glen, n_rec);
+  cudaError_t e = cudaSuccess;
   if (!L.sorted || sp.sort_smem == 0 || sp.parts > L.max_parts) {
-    cudaError_t e = grid4_accumulate(cert, corr, n_rec, grids, glen, ws, dirty, st);
-    if (e != cudaSuccess) return e;
+    if (passes & 1) e = grid4_accumulate(cert, corr, n_rec, grids, glen, ws, dirty, st);
+    if (e != cudaSuccess || !(passes & 2)) return e;
     return grid4_finish(glen, ws, st);
   }
-  cudaError_t e;
-  if (dirty) {
+  if (dirty && (passes & 1)) {
     if ((e = cudaMemsetAsync(ws, 0, L.offS, st)) != cudaSuccess) return e;  // H and G0
     if ((e = cudaMemsetAsync(ws + L.offCnt, 0, 256, st)) != cudaSuccess) return e;
   }
@@ -1190,10 +1208,16 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   a.keys = keys;
   a.off = off;
   a.G0 = G0;
-  static std::atomic<int> smem_sort{0}, smem_gather{0};
-  if ((e = ensure_smem4(g4_sort_kernel, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
-  g4_sort_kernel<<<(unsigned)sp.parts, kSortThreads, sp.sort_smem, st>>>(a);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  static std::atomic<int> smem_sort{0}, smem_sort_s{0}, smem_gather{0};
+  if (!(passes & 1)) {
+  } else if (a.vec_ok) {
+    if ((e = ensure_smem4(g4_sort_kernel<true>, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
+    g4_sort_kernel<true><<<(unsigned)sp.parts, kSortThreads, sp.sort_smem, st>>>(a);
+  } else {
+    if ((e = ensure_smem4(g4_sort_kernel<false>, smem_sort_s, kSortSmemMax)) != cudaSuccess) return e;
+    g4_sort_kernel<false><<<(unsigned)sp.parts, kSortThreads, sp.sort_smem, st>>>(a);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess || !(passes & 2)) return e;
 
   G4GatherArgs g{};
   g.keys = keys;

@@ -24,8 +24,10 @@ cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_
                              const double* grids, const int32_t* grid_len, uint8_t* workspace,
                              bool dirty, cudaStream_t st);
 cudaError_t grid4_finish(const int32_t* grid_len, uint8_t* workspace, cudaStream_t st);
+// passes: bit 0 the records pass, bit 1 the tables pass (3 = the whole build)
 cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, const double* grids,
-                        const int32_t* grid_len, uint8_t* workspace, bool dirty, cudaStream_t st);
+                        const int32_t* grid_len, uint8_t* workspace, bool dirty, int passes,
+                        cudaStream_t st);
 cudaError_t grid4_eval(int64_t n_rec, const int32_t* grid_len, const int64_t* struct_begin,
                        const uint32_t* struct_mask, int n_struct, const double* cost1,
                        int64_t cfg_begin, int64_t cfg_count, double* acc, double* cost,

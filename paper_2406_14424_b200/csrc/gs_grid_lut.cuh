@@ -39,23 +39,20 @@ __device__ __forceinline__ int upper_count(const double* g, int n, double x) {
 }
 
 // Shared-memory bin tables of D models (four-model path).  The bucket map
-// is one clamp of a truncated affine f64 map: monotone non-decreasing in x
-// (each rounded step is), NaN -> bucket 0 (cvt.rzi of NaN is 0, and NaN >=
-// g is false for every g, so its bin 0 is exact), +-inf saturate.  An entry
-// holds the bucket's first grid index and how many grid values it holds
-// (usually 0 or 1), so a lookup is one LDS plus at most one f64 compare.
-//
-// The integer part is taken with the 2^52 magic-number trick instead of a
-// f64 -> s32 conversion (the conversion unit is the slow path): y is first
-// clamped to [-1, kLutBuckets] (NaN -> -1), so y + 2^52 is exact and its low
-// mantissa bits are round-to-nearest(y) — a monotone map, which is all the
-// bucketing needs (grid values and records go through the same function).
-__device__ __forceinline__ int bucket_of(double x, double lo, double scale) {
-  double y = __dmul_rn(__dadd_rn(x, -lo), scale);
-  y = fmin(fmax(y, -1.0), (double)kLutBuckets);
-  // low word of 2^52 + round(y) is round(y) (two's complement for y = -1)
-  const int q = __double2loint(__dadd_rn(y, 4503599627370496.0));
-  return min(max(q, 0), kLutBuckets - 1);
+// q(x) only has to be monotone non-decreasing (grid values and records go
+// through the same function; values sharing a bucket are compared exactly
+// in f64), so it is computed in f32: x rounded to f32 (monotone), minus the
+// grid's low end, times kLutBuckets / range (each rounded step monotone),
+// clamped to [0, kLutBuckets - 1] by fmaxf / fminf (NaN -> 0: NaN >= g is
+// false for every g, so its bin 0 is exact; +-inf saturate), and rounded to
+// an integer with the 2^23 magic-number add (exact below 2^22) instead of a
+// conversion instruction.  An entry holds the bucket's first grid index and
+// how many grid values it holds (usually 0 or 1), so a lookup is one LDS,
+// one f64 LDS and one f64 compare.
+__device__ __forceinline__ int bucket_of(double x, float lo, float scale) {
+  float y = __fmul_rn(__fsub_rn(__double2float_rn(x), lo), scale);
+  y = fminf(fmaxf(y, 0.f), (float)(kLutBuckets - 1));
+  return __float_as_int(__fadd_rn(y, 8388608.f)) - 0x4B000000;
 }
 
 template <int D>
@@ -63,15 +60,18 @@ struct BinTables {
   const double* grid;   // smem, concatenated grids of models 0..D-1
   const uint32_t* lut;  // smem, [D][kLutBuckets]: first index | count << 16
   int goff[D];
-  double lo[D], scale[D];
+  float lo[D], scale[D];
 
+  // the grid value at lb is read even for an empty bucket (lb <= n: at
+  // worst the first word past this model's grid, still shared memory) and
+  // only used when the bucket holds a value
   __device__ __forceinline__ int bin(int j, double x) const {
     const uint32_t e = lut[j * kLutBuckets + bucket_of(x, lo[j], scale[j])];
     const int lb = (int)(e & 0xffffu), c = (int)(e >> 16);
     const double* g = grid + goff[j] + lb;
-    if (c == 0) return lb;
-    if (c == 1) return lb + (g[0] <= x ? 1 : 0);
-    return lb + upper_count(g, c, x);
+    int b = lb + ((c != 0 && g[0] <= x) ? 1 : 0);
+    if (c > 1) b = lb + upper_count(g, c, x);
+    return b;
   }
 };
 
@@ -103,8 +103,9 @@ __device__ __forceinline__ BinTables<D> build_bin_tables(const int32_t* glen, do
     n_grid += glen[j];
     const double* g = s_grid + t.goff[j];
     const int n = glen[j];
-    t.lo[j] = g[0];
-    t.scale[j] = n > 1 ? (double)kLutBuckets / (g[n - 1] - g[0]) : 0.0;
+    t.lo[j] = __double2float_rn(g[0]);
+    const float range = __fsub_rn(__double2float_rn(g[n - 1]), t.lo[j]);
+    t.scale[j] = range > 0.f ? __fdiv_rn((float)kLutBuckets, range) : 0.f;
   }
   const int q0 = threadIdx.x * per;
 #pragma unroll
@@ -118,7 +119,7 @@ __device__ __forceinline__ BinTables<D> build_bin_tables(const int32_t* glen, do
     for (int q = 1; q < D; ++q) j += i >= t.goff[q] ? 1 : 0;
     // register arrays indexed by a runtime j would go to local memory
     int goff = t.goff[0];
-    double lo = t.lo[0], scale = t.scale[0];
+    float lo = t.lo[0], scale = t.scale[0];
 #pragma unroll
     for (int q = 1; q < D; ++q)
       if (j == q) {

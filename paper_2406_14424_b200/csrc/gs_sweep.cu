@@ -1287,7 +1287,7 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
   info->n_structures = p.n_struct;
   info->max_len = p.M;
   info->workspace_bytes = p.bytes;
-  info->fast_path = p.g4 ? 1 : 0;
+  info->fast_path = p.g4 ? (grid4_layout(p.glen, n_rec).sorted ? 2 : 1) : 0;
   if (p.g4) {
     info->build_launches = 2;  // g4_sort + g4_gather (one-shot) or g4_hist + g4_plane
     info->eval_launches = 1;   // g4_eval
@@ -1322,11 +1322,16 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   if (!workspace || workspace_bytes < p.bytes) return GS_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const int passes = (flags & (GS_GRID_BUILD_RECORDS_PASS | GS_GRID_BUILD_TABLES_PASS)) == 0
+                         ? 3
+                         : ((flags & GS_GRID_BUILD_RECORDS_PASS) ? 1 : 0) |
+                               ((flags & GS_GRID_BUILD_TABLES_PASS) ? 2 : 0);
   if (p.g4) {
     GS_CUDA_TRY(grid4_build(certainty, correct, n_rec, grids, p.glen, ws,
-                            (flags & GS_GRID_WORKSPACE_DIRTY) != 0, st));
+                            (flags & GS_GRID_WORKSPACE_DIRTY) != 0, passes, st));
     return GS_OK;
   }
+  if (passes != 3) return GS_EUNSUPPORTED;
   float* F = reinterpret_cast<float*>(ws + p.offHF);
   uint32_t* P = reinterpret_cast<uint32_t*>(ws + p.offHP);
   auto* H16 = reinterpret_cast<unsigned long long*>(ws + p.offH16);

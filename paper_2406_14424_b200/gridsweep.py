@@ -30,6 +30,8 @@ from . import _lib
 from .types import Cascade
 
 GS_GRID_WORKSPACE_DIRTY = 1
+GS_GRID_BUILD_RECORDS_PASS = 2
+GS_GRID_BUILD_TABLES_PASS = 4
 
 
 def structures(n_models: int, grid_len: Sequence[int]) -> list[tuple[tuple[int, ...], int, int]]:
@@ -103,16 +105,27 @@ class GridSweep:
             self.build()
 
     # -- table -------------------------------------------------------------
-    def build(self) -> None:
+    def build(self, part: str | None = None) -> None:
+        """Fill the prefix tables from the device matrices.  part = "records"
+        / "tables" runs one of the build's two passes (four-model path; for
+        timing them apart), "records" first."""
         lib = _lib.load()
         flags = 0 if self._clean else GS_GRID_WORKSPACE_DIRTY
+        if part == "records":
+            flags |= GS_GRID_BUILD_RECORDS_PASS
+        elif part == "tables":
+            flags = GS_GRID_BUILD_TABLES_PASS
+        elif part is not None:
+            raise ValueError(f"unknown build part {part!r}")
         rc = lib.gs_grid_build(self.cert.data_ptr(), self.corr.data_ptr(), self.n_rec,
                                self.n_models, self.grids.data_ptr(), self._glen,
                                self.table.data_ptr(), self.table.numel(), flags,
                                _lib.stream_ptr())
-        self._clean = rc == _lib.GS_OK
+        if rc != _lib.GS_OK:
+            self._clean = False
         _lib.check(rc, "grid build")
-        self._built = True
+        self._clean = part != "records"
+        self._built = part != "records"
 
     def build_streamed(self, certainty_host: torch.Tensor, correct_host: torch.Tensor,
                        chunks: int = 8) -> None:
@@ -214,14 +227,11 @@ class GridSweep:
                 part: str | None = None) -> torch.cuda.CUDAGraph:
         """CUDA graph of one sweep step (table build and/or scoring every
         config into `out`), so a step is one graph launch instead of a
-        Python-driven sequence of kernel launches.  part = "hist" / "plane"
-        captures one half of the fast path's build alone (for timing)."""
+        Python-driven sequence of kernel launches.  part = "records" /
+        "tables" captures one pass of the build alone (for timing)."""
         def body():
-            if part == "hist":
-                self.histogram()
-                return
-            if part == "plane":
-                self.finish()
+            if part in ("records", "tables"):
+                self.build(part=part)
                 return
             if build:
                 self.build()

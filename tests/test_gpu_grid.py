@@ -239,7 +239,7 @@ def test_streamed_build_equals_build(chunks):
     dev_c = torch.zeros(cert.shape, dtype=torch.float64, device="cuda")
     dev_k = torch.zeros(corr.shape, dtype=torch.uint8, device="cuda")
     sw = GridSweep(dev_c, dev_k, grids, cost1, build=False)
-    assert sw.info.fast_path == 1
+    assert sw.info.fast_path == 2  # one-shot builds take the bucket-sort kernels
     for _ in range(2):  # a second streamed build on the same workspace
         sw.build_streamed(host_c, host_k, chunks=chunks)
         got = sw.evaluate(n_correct=True)
@@ -316,3 +316,56 @@ def test_sweep_pipeline_fronts_equal_single_sweeps():
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
     pipe.drain()
+
+
+def _equal_results(a, b):
+    import torch
+    for x, y in ((a.accuracy, b.accuracy), (a.mean_cost, b.mean_cost),
+                 (a.forward_frac, b.forward_frac), (a.n_correct, b.n_correct)):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("skew", [False, True])
+def test_sorted_build_matches_streamed_build(skew):
+    """The bucket-sort build (gs_grid_build) and the histogram build
+    (gs_grid_accumulate + gs_grid_finish) give identical tables, alternating
+    on one workspace.  skew: 80% of the records share model 1's bin, so that
+    bucket holds > 2^16 keys (the gather's wide counters)."""
+    import torch
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    rng = np.random.default_rng(17)
+    n = 300_000 if skew else 60_000
+    cert, corr, grids, cost1 = _random_case(rng, n, 4, 20)
+    if skew:
+        cert[: 4 * n // 5, 1] = 0.5
+        q = np.quantile(cert[:, 1], np.arange(1, 20) / 20)
+        grids[1] = np.array(sorted({0.0} | {float(x) for x in q}))
+    sw = GridSweep(cert, corr, grids, cost1, build=False)
+    assert sw.info.fast_path == 2
+    host_c = torch.from_numpy(cert).pin_memory()
+    host_k = torch.from_numpy(corr).pin_memory()
+    sw.build()
+    a = sw.evaluate(n_correct=True)
+    sw.build_streamed(host_c, host_k, chunks=3)
+    b = sw.evaluate(n_correct=True)
+    _equal_results(a, b)
+    sw.build()
+    _equal_results(sw.evaluate(n_correct=True), b)
+    # spot check against the oracle walk
+    pick = np.sort(rng.choice(sw.n_configs, size=48, replace=False))
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1, n_threads=8)
+    assert np.array_equal(a.accuracy.cpu().numpy()[pick], want[0])
+    assert np.array_equal(a.mean_cost.cpu().numpy()[pick], want[1])
+
+
+def test_build_passes_split():
+    """GS_GRID_BUILD_RECORDS_PASS then GS_GRID_BUILD_TABLES_PASS == one build."""
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    rng = np.random.default_rng(5)
+    cert, corr, grids, cost1 = _random_case(rng, 40_000, 4, 30)
+    sw = GridSweep(cert, corr, grids, cost1)
+    a = sw.evaluate(n_correct=True)
+    sw.build(part="records")
+    sw.build(part="tables")
+    _equal_results(sw.evaluate(n_correct=True), a)

@@ -15,15 +15,21 @@ from paper_2406_14424_b200.gridsweep import GridSweep  # noqa: E402
 
 K, CTAS, SLOTS = 3, 1024, 8
 names = ["g4_sort", "g4_gather", "g4_eval"]
-labels = [["start", "tables", "loop done", "end"],
+labels = [["start", "grid in", "tables", "loop done", "scanned", "end"],
           ["start", "segments", "plane built", "row walk", "cluster", "end"],
           ["start", "slab in", "cluster", "tables", "edges", "end"]]
 _, cert, corr, grids, cost1 = bench.workload(0)
 sw = GridSweep(cert, corr, grids, cost1, build=False)
 out = None
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+flush_read = torch.empty(512 << 20, dtype=torch.uint8, device="cuda").fill_(1)
+mode = os.environ.get("PHASE_FLUSH", "write")  # write | clean | none
+print(f"# flush before each build: {mode}")
 for _ in range(5):
-    flush.zero_()
+    if mode != "none":
+        flush.zero_()
+    if mode == "clean":
+        flush_read.sum()
     sw.build()
     out = sw.evaluate(out=out)
 torch.cuda.synchronize()
