@@ -69,6 +69,12 @@ __device__ __forceinline__ void phase(int kernel, int slot) {
     const size_t i = ((size_t)(kernel * kPhaseCtas + blockIdx.x) * kPhaseSlots + slot) * 2;
     g_phase[i] = t;
     g_phase[i + 1] = clock64();
+    if (slot == 0) {  // the CTA's SM in the last slot
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const size_t j = ((size_t)(kernel * kPhaseCtas + blockIdx.x) * kPhaseSlots + kPhaseSlots - 1) * 2;
+      g_phase[j + 1] = smid;
+    }
   }
 }
 #else
@@ -632,31 +638,36 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
       if (key & (1u << 16)) atomicAdd(s_c1 + r, 1u);
     }
   };
-  // a warp per record range: its segment's first kHead keys are loaded one
-  // range ahead (kHead / 32 coalesced loads in flight per lane), the rest
-  // of a long segment inline
-  constexpr int kHead = 4;  // x 32 keys
+  // a warp per record range: the first kHead x 32 keys of the segments of
+  // kBatch ranges are loaded at once (kHead * kBatch coalesced loads in
+  // flight per lane, one latency for the whole batch), the rest of a long
+  // segment inline
+  constexpr int kHead = 3, kBatch = 5;
   constexpr uint32_t kNone = 0xffffffffu;
-  uint32_t nxt[kHead];
-  auto load_head = [&](int p, uint32_t (&k)[kHead]) {
-    const uint32_t b = p < n_parts ? s_beg[p] : 0u, e = p < n_parts ? s_end[p] : 0u;
+  for (int p0 = warp; p0 < n_parts; p0 += nwarps * kBatch) {
+    uint32_t k[kBatch][kHead];
 #pragma unroll
-    for (int j = 0; j < kHead; ++j) {
-      const uint32_t i = b + 32u * j + lane;
-      k[j] = i < e ? __ldg(a.keys + i) : kNone;
+    for (int m = 0; m < kBatch; ++m) {
+      const int p = p0 + m * nwarps;
+      const uint32_t b = p < n_parts ? s_beg[p] : 0u, e = p < n_parts ? s_end[p] : 0u;
+#pragma unroll
+      for (int j = 0; j < kHead; ++j) {
+        const uint32_t i = b + 32u * j + lane;
+        k[m][j] = i < e ? __ldg(a.keys + i) : kNone;
+      }
     }
-  };
-  load_head(warp, nxt);
-  for (int p = warp; p < n_parts; p += nwarps) {
-    uint32_t cur[kHead];
 #pragma unroll
-    for (int j = 0; j < kHead; ++j) cur[j] = nxt[j];
-    load_head(p + nwarps, nxt);
+    for (int m = 0; m < kBatch; ++m)
 #pragma unroll
-    for (int j = 0; j < kHead; ++j)
-      if (cur[j] != kNone) count(cur[j]);
-    const uint32_t e = s_end[p];
-    for (uint32_t i = s_beg[p] + 32u * kHead + lane; i < e; i += 32u) count(__ldg(a.keys + i));
+      for (int j = 0; j < kHead; ++j)
+        if (k[m][j] != kNone) count(k[m][j]);
+#pragma unroll 1
+    for (int m = 0; m < kBatch; ++m) {
+      const int p = p0 + m * nwarps;
+      if (p >= n_parts) break;
+      const uint32_t e = s_end[p];
+      for (uint32_t i = s_beg[p] + 32u * kHead + lane; i < e; i += 32u) count(__ldg(a.keys + i));
+    }
   }
   __syncthreads();
   phase(1, 2);
@@ -728,7 +739,6 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
     }
   }
   __syncthreads();
-  pdl_release();
   phase(1, 4);
   if (live) {
     unsigned long long P = 0;
@@ -740,6 +750,10 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
       S[(int64_t)r * plane] = P;
     }
   }
+  // the eval is released only once every plane is written: launched
+  // earlier, its clusters would be placed around this kernel's CTAs and the
+  // last ones could miss the first wave
+  pdl_release();
   phase(1, 5);
 }
 
@@ -748,7 +762,7 @@ constexpr int kEval4Threads = 512;
 
 struct G4EvalArgs {
   int32_t d0, d1, d2, d2p, d1p;
-  int32_t half, nseg, seg_len;          // rows of the cluster's first CTA, row segments
+  int32_t rows, nseg, seg_len;          // b1 rows per CTA of the cluster, row segments
   int64_t sb[16];                       // first config of the structure with model mask m
   int64_t cfg_begin, cfg_count;
   int64_t n_rec;
@@ -817,13 +831,16 @@ __device__ __forceinline__ void put4(const G4EvalArgs& a, int64_t cfg, const uin
   store4<false>(a, i, fr[0], fr[1], fr[2], fr[3], mean, correct, n, rcp);
 }
 
-// A cluster of two CTAs owns slab k0, split along b1 (rows): each
+// A cluster of CL CTAs owns slab k0, split along b1 (rows): each
 // bulk-copies its rows, sums its columns over them and hands the column
-// sums to the other CTA through distributed shared memory (rank 1 needs
-// rank 0's as its b1 carry; both need the other's column-g2 sum for the slab
-// total).  Then each walks its own rows.
-template <bool ALL>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
+// sums to every CTA of the cluster through distributed shared memory (a
+// rank's b1 carry is the sum over the ranks before it; the slab total over
+// all of them).  Then each walks its own rows.  Four CTAs of 256 threads
+// per slab (B200: up to 148 four-CTA clusters resident, 101 needed for
+// 100-level grids, so the grid is one wave even when launched around the
+// previous kernel's last CTAs) and a walk of a quarter slab per CTA.
+template <bool ALL, int THREADS, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THREADS)
     g4_eval_kernel(const __grid_constant__ G4EvalArgs a) {
   extern __shared__ __align__(16) unsigned long long s_slab[];  // [rows][d2p], then tables
   __shared__ __align__(8) uint64_t bar;
@@ -832,19 +849,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   const int h = (int)cluster.block_rank();
   const int d0 = a.d0, d1 = a.d1, d2 = a.d2, d2p = a.d2p;
   const int g0 = d0 - 1, g1 = d1 - 1, g2 = d2 - 1;
-  const int k0 = blockIdx.x >> 1;
-  const int rb = h ? a.half : 0, re = h ? d1 : a.half, nr = re - rb;
+  const int k0 = blockIdx.x / CL;
+  const int rb = h * a.rows, re = min(d1, rb + a.rows), nr = re - rb;
+  const bool last = re == d1;  // owns row g1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool any0 = k0 == g0;  // the "any" slab: structures without model 0
-  unsigned long long* s_colg = s_slab + (size_t)a.half * d2p;  // [half] row totals, prefixed
-  double* s_rowf = reinterpret_cast<double*>(s_colg + a.half);   // [half] row-shared fraction
-  double* s_rowm = s_rowf + a.half;                              // [half] partial mean cost
-  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(s_rowm + a.half);  // [nseg][d2]
-  unsigned long long* s_own = s_seg + (size_t)a.nseg * d2;       // [d2] column sums, own rows
-  unsigned long long* s_peer = s_own + d2;                       // [d2] column sums, other CTA
-  uint32_t* s_c1 = reinterpret_cast<uint32_t*>(s_peer + d2);     // [d1] C1 prefix along b1
-  uint32_t* s_rowc = s_c1 + d1;                                  // [half]
-  // skip a slab none of whose configs is in the requested range (both CTAs
+  unsigned long long* s_colg = s_slab + (size_t)a.rows * d2p;  // [rows] row totals, prefixed
+  double* s_rowf = reinterpret_cast<double*>(s_colg + a.rows);   // [rows] row-shared fraction
+  double* s_rowm = s_rowf + a.rows;                              // [rows] partial mean cost
+  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(s_rowm + a.rows);  // [nseg][d2]
+  unsigned long long* s_sums = s_seg + (size_t)a.nseg * d2;      // [CL][d2] column sums per rank
+  unsigned long long* s_carry = s_sums + (size_t)CL * d2;        // [d2] over the ranks before
+  unsigned long long* s_tot = s_carry + d2;                      // [d2] over the slab
+  uint32_t* s_c1 = reinterpret_cast<uint32_t*>(s_tot + d2);      // [d1] C1 prefix along b1
+  uint32_t* s_rowc = s_c1 + d1;                                  // [rows]
+  // skip a slab none of whose configs is in the requested range (all CTAs
   // of the cluster decide alike): a slab k0 < g0 scores structures (0,1) ..
   // (0,1,2,3), the first starting at sb[3] + k0 and the last ending at
   // sb[15] + (k0 + 1) g1 g2; the any slab scores the singletons (from
@@ -854,7 +873,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   if (hi <= a.cfg_begin || lo >= a.cfg_begin + a.cfg_count) return;
   const bool full = lo >= a.cfg_begin && hi <= a.cfg_begin + a.cfg_count;
   phase(2, 0);
-  const uint32_t bytes = (uint32_t)((int64_t)nr * d2p * 8);
+  // every CTA of the cluster must be running before its shared memory is
+  // written by the others: arrive now, wait before the first remote write
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  const uint32_t bytes = (uint32_t)((int64_t)max(nr, 0) * d2p * 8);
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -900,17 +922,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
     for (int r = r_lo; r < r_hi; ++r) ssum += s_slab[(size_t)r * d2p + col];
   if (live) s_seg[seg * d2 + col] = ssum;
   __syncthreads();
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (live && seg == 0) {
     unsigned long long t = 0;
     for (int q = 0; q < a.nseg; ++q) t += s_seg[q * d2 + col];
-    s_own[col] = t;
-    *cluster.map_shared_rank(s_peer + col, 1 - h) = t;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(s_sums + h * d2 + col, r) = t;
   }
   cluster.sync();
+  if (tid < d2) {
+    unsigned long long c = 0, t = 0;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      const unsigned long long v = s_sums[r * d2 + tid];
+      if (r < h) c += v;
+      t += v;
+    }
+    s_carry[tid] = c;
+    s_tot[tid] = t;
+  }
+  __syncthreads();
+  if (nr <= 0) return;  // a rank past the slab's last row (small d1) only adds zeros
   phase(2, 2);
   // column g2 (row totals) prefix along b1 over own rows, after the carry
   if (warp == 0) {
-    unsigned long long carry = h ? s_peer[g2] : 0ull;
+    unsigned long long carry = s_carry[g2];
     for (int b = 0; b < nr; b += 32) {
       const int r = b + lane;
       unsigned long long x = r < nr ? s_slab[(size_t)r * d2p + g2] : 0ull;
@@ -930,7 +966,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   const double one = div_count(n, n, rcp);
   const double c0c = __ldg(a.cost1 + 0), c1c = __ldg(a.cost1 + 1), c2c = __ldg(a.cost1 + 2),
                c3c = __ldg(a.cost1 + 3);
-  const Cell3 tot = unpack3(s_own[g2] + s_peer[g2]);  // slab total: (k0, g1, g2)
+  const Cell3 tot = unpack3(s_tot[g2]);  // slab total: (k0, g1, g2)
   const uint32_t C1g = s_c1[g1];
   const uint32_t base0 = s_c0[1] - s_c0[0];  // slab k0: model 0 completes b0 > k0
   const double f1 = div_count((double)tot.cnt, n, rcp);  // slab k0: after stage 0
@@ -940,7 +976,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   //            correct through stage 1 plus C2(k0,k1,g)
   //   any:     (1,2,3)   -> frac[1] = cnt(g,k1,g)/n, mean through stage 1,
   //            correct of stage 0 (model 1) plus C2(g,k1,g)
-  for (int r = tid; r < nr; r += kEval4Threads) {
+  for (int r = tid; r < nr; r += THREADS) {
     const int k1 = rb + r;
     const Cell3 rg = unpack3(s_colg[r]);
     const double fr = div_count((double)rg.cnt, n, rcp);
@@ -959,14 +995,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   // Threads [0, nwalk) walk the interior (column w % g2, row segment
   // w / g2); the spare threads score the edge cells meanwhile (their
   // prefixes are already known): last column (k2 = g2) from the row totals
-  // s_colg; last row (k1 = g1, rank 1) from the column totals carry + own
-  // column sums; the corner from the slab total.
+  // s_colg; last row (k1 = g1, last rank) from the slab's column totals;
+  // the corner from the slab total.
   const int nwalk = a.nseg * g2;
   if (tid >= nwalk) {
     const int n_row = min(nr, g1 - rb);          // own rows k1 < g1
-    const int n_col = h == 1 ? g2 : 0;           // last-row cells
-    const int n_items = n_row + n_col + (h == 1 ? 1 : 0);
-    for (int e = tid - nwalk; e < n_items; e += kEval4Threads - nwalk) {
+    const int n_col = last ? g2 : 0;             // last-row cells
+    const int n_items = n_row + n_col + (last ? 1 : 0);
+    for (int e = tid - nwalk; e < n_items; e += THREADS - nwalk) {
       if (e < n_row) {
         const int k1 = rb + e;
         const Cell3 p = unpack3(s_colg[e]);
@@ -985,7 +1021,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
         }
       } else if (e < n_row + n_col) {  // last row: P = (k0, g1, k2)
         const int k2 = e - n_row;
-        const Cell3 p = unpack3(s_own[k2] + s_peer[k2]);
+        const Cell3 p = unpack3(s_tot[k2]);
         if (!any0) {  // (0,2,3) at (k0, k2)
           const uint32_t reach[2] = {tot.cnt, p.cnt};
           const double cst[3] = {c0c, c2c, c3c};
@@ -1019,7 +1055,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kEval4Threads, 2)
   // k1 < g1, k2 < g2; its index is row_base + k1 * g2
   const int wc = tid % g2, ws = tid / g2;
   const int w_lo = ws * a.seg_len, w_hi = min(nr, w_lo + a.seg_len);
-  unsigned long long P = h ? s_peer[wc] : 0ull;
+  unsigned long long P = s_carry[wc];
   for (int q = 0; q < ws; ++q) P += s_seg[q * d2 + wc];
   const int64_t row_base =
       (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + wc - a.cfg_begin;
@@ -1055,7 +1091,7 @@ bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
   return d0 <= kMaxDim4 && d2 <= kMaxDim4 && d1 <= 4096 && grid_bytes <= 96 * 1024 &&
          d2 <= kPlaneThreads && plane_smem <= (int64_t)kGrid4SlabMax &&
          d2 <= kEval4Threads && d1 >= 2 &&
-         (d1 + 1) / 2 * (d2p * 8 + 28) + (kEval4Threads + 2 * d2) * 8 + d1 * 4 <= (int64_t)kGrid4SlabMax;
+         (d1 + 1) / 2 * (d2p * 8 + 28) + (kEval4Threads + 4 * d2) * 8 + d1 * 4 <= (int64_t)kGrid4SlabMax;
 }
 
 // Shared memory of the sorted build's two kernels (0 when it does not apply).
@@ -1244,6 +1280,35 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   return launch_pdl(g4_gather_kernel, (unsigned)L.d1, kGatherThreads, sp.gather_smem, st, g);
 }
 
+// Row split of a slab over the CL CTAs of a cluster: rows per CTA, and row
+// segments that serve both the column sums (d2 columns) and the interior
+// walk (g2 columns), leaving >= 32 threads for the edge cells.
+template <int THREADS, int CL>
+void eval_split(G4EvalArgs& a, const Grid4Layout& L) {
+  a.rows = (L.d1 + CL - 1) / CL;
+  const int g2w = std::max(1, L.d2 - 1);
+  a.nseg = std::max(1, std::min(std::min((THREADS - 32) / g2w, THREADS / L.d2), a.rows));
+  a.seg_len = (a.rows + a.nseg - 1) / a.nseg;
+  a.nseg = (a.rows + a.seg_len - 1) / a.seg_len;
+}
+
+template <int THREADS, int CL>
+size_t eval_smem(G4EvalArgs a, const Grid4Layout& L) {
+  eval_split<THREADS, CL>(a, L);
+  return (size_t)a.rows * L.d2p * 8 + (size_t)a.rows * (8 + 8 + 8 + 4) +
+         ((size_t)a.nseg + CL + 2) * L.d2 * 8 + (size_t)L.d1 * 4;
+}
+
+template <bool ALL, int THREADS, int CL>
+cudaError_t launch_eval(G4EvalArgs a, const Grid4Layout& L, cudaStream_t st) {
+  eval_split<THREADS, CL>(a, L);
+  const size_t smem = eval_smem<THREADS, CL>(a, L);
+  static std::atomic<int> done{0};
+  cudaError_t e = ensure_smem4(g4_eval_kernel<ALL, THREADS, CL>, done, (size_t)kGrid4SlabMax);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(g4_eval_kernel<ALL, THREADS, CL>, (unsigned)(CL * L.d0), THREADS, smem, st, a);
+}
+
 cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct_begin,
                        const uint32_t* struct_mask, int n_struct, const double* cost1,
                        int64_t cfg_begin, int64_t cfg_count, double* acc, double* cost,
@@ -1268,22 +1333,14 @@ cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct
   a.cost = cost;
   a.frac = frac;
   a.n_correct = n_correct;
-  a.half = (L.d1 + 1) / 2;
-  // the same row segments serve the column sums (d2 columns) and the
-  // interior walk (g2 columns), leaving >= 32 threads for the edge cells
-  const int g2w = std::max(1, L.d2 - 1);
-  a.nseg = std::max(1, std::min(std::min((kEval4Threads - 32) / g2w, kEval4Threads / L.d2), a.half));
-  a.seg_len = (a.half + a.nseg - 1) / a.nseg;
-  a.nseg = (a.half + a.seg_len - 1) / a.seg_len;
-  const size_t smem = (size_t)a.half * L.d2p * 8 + (size_t)a.half * (8 + 8 + 8 + 4) +
-                      ((size_t)a.nseg + 2) * L.d2 * 8 + (size_t)L.d1 * 4;
   const bool all = acc && cost && frac && (reinterpret_cast<uintptr_t>(frac) & 31u) == 0;
-  static std::atomic<int> smem_all{0}, smem_some{0};
-  cudaError_t e = all ? ensure_smem4(g4_eval_kernel<true>, smem_all, (size_t)kGrid4SlabMax)
-                      : ensure_smem4(g4_eval_kernel<false>, smem_some, (size_t)kGrid4SlabMax);
-  if (e != cudaSuccess) return e;
-  return all ? launch_pdl(g4_eval_kernel<true>, (unsigned)(2 * L.d0), kEval4Threads, smem, st, a)
-             : launch_pdl(g4_eval_kernel<false>, (unsigned)(2 * L.d0), kEval4Threads, smem, st, a);
+  // four CTAs of 256 threads per slab when the slab is tall enough, else
+  // two of 512
+  const bool four = L.d1 >= 16 && L.d2 <= 224 && eval_smem<256, 4>(a, L) <= kGrid4SlabMax;
+  if (four)
+    return all ? launch_eval<true, 256, 4>(a, L, st) : launch_eval<false, 256, 4>(a, L, st);
+  return all ? launch_eval<true, kEval4Threads, 2>(a, L, st)
+             : launch_eval<false, kEval4Threads, 2>(a, L, st);
 }
 
 }  // namespace gs
