@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kHist4Threads, 1) g4_hist_kernel(const __grid_
   __shared__ uint32_t s_c0[kMaxDim4];
   __shared__ int s_next[2];
   const int n_grid = a.glen[0] + a.glen[1] + a.glen[2];
-  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + n_grid);
+  void* s_lut = s_grid + n_grid;  // [3][kLutBuckets] entries
   const int tid = threadIdx.x;
   phase(0, 0);
   // grid values first, then the first chunk's records: the records stream
@@ -443,11 +443,10 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   __shared__ uint32_t s_c0[kMaxDim4];
   __shared__ uint32_t s_wsum[32];
   const int n_grid = a.glen[0] + a.glen[1] + a.glen[2];
-  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_grid + n_grid);
-  uint32_t* s_cnt = s_lut + 3 * kLutBuckets;           // [nb] -> bucket starts
+  void* s_lut = s_grid + n_grid;                       // [3][kLutBuckets] entries
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(s_lut) + 3 * kLutBuckets * kLutEntryBytes);  // [nb]
   uint32_t* s_key = s_cnt + ((a.nb + 3) & ~3);        // [per]
   uint32_t* s_sorted = s_key + a.per;                 // [per]
-  uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_sorted + a.per);  // [per]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r0 = blockIdx.x * a.per;
   const int cnt = min(a.n_rec - r0, a.per);
@@ -463,8 +462,9 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   ha.cert = a.cert;
   ha.corr = a.corr;
   ha.vec_ok = VEC ? 1 : 0;  // a compile-time branch in load_rec4
-  Rec4 v;
+  Rec4 v, w;  // two records per thread in flight from the start
   if (tid < cnt) v = load_rec4(ha, r0 + tid);
+  if (tid + kSortThreads < cnt) w = load_rec4(ha, r0 + tid + kSortThreads);
 #pragma unroll
   for (int q = 0; q < kGridRegs; ++q) {
     const int i = tid + q * kSortThreads;
@@ -483,15 +483,23 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
     const uint32_t key = b0 | (b2 << 8) | ((k & 0xff00u) ? 1u << 16 : 0u) |
                          ((k & 0xff0000u) ? 1u << 17 : 0u) | ((k & 0xff000000u) ? 1u << 18 : 0u) |
                          (b1 << 19);
-    s_rank[i] = (uint16_t)atomicAdd(s_cnt + b1, 1u);
+    atomicAdd(s_cnt + b1, 1u);  // count only: the rank is taken in the scatter
     s_key[i] = key;
     if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
   };
-  for (int i = tid; i < cnt; i += kSortThreads) {
-    Rec4 nv;
-    if (i + kSortThreads < cnt) nv = load_rec4(ha, r0 + i + kSortThreads);
+  // three records per trip in a rotation of three registers sets, each
+  // loaded two records ahead (no register moves)
+  constexpr int T = kSortThreads;
+  for (int i = tid; i < cnt; i += 3 * T) {
+    Rec4 x;
+    if (i + 2 * T < cnt) x = load_rec4(ha, r0 + i + 2 * T);
     put(i, v.x0, v.x1, v.x2, v.k);
-    v = nv;
+    if (i + 3 * T < cnt) v = load_rec4(ha, r0 + i + 3 * T);
+    if (i + T >= cnt) break;
+    put(i + T, w.x0, w.x1, w.x2, w.k);
+    if (i + 4 * T < cnt) w = load_rec4(ha, r0 + i + 4 * T);
+    if (i + 2 * T >= cnt) break;
+    put(i + 2 * T, x.x0, x.x1, x.x2, x.k);
   }
   phase(0, 3);
   pdl_release();
@@ -534,7 +542,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   phase(0, 4);
   for (int i = tid; i < cnt; i += kSortThreads) {
     const uint32_t key = s_key[i];
-    s_sorted[s_cnt[key >> 19] + s_rank[i]] = key;
+    s_sorted[atomicAdd(s_cnt + (key >> 19), 1u)] = key;
   }
   __syncthreads();
   for (int i = tid; i < cnt; i += kSortThreads) a.keys[r0 + i] = s_sorted[i];
@@ -1084,7 +1092,7 @@ bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
   if (M != 4 || n_rec < 1 || n_rec >= kGrid4MaxRec) return false;
   const int64_t d0 = glen[0] + 1, d1 = glen[1] + 1, d2 = glen[2] + 1;
   const int64_t d2p = (d2 + 1) & ~1ll;
-  const int64_t grid_bytes = (int64_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * 4;
+  const int64_t grid_bytes = (int64_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * kLutEntryBytes;
   if (glen[0] + glen[1] + glen[2] > 5 * kHist4Threads) return false;
   // plane tile [d0][d2p] x 16 B plus segment sums; eval slab [d1][d2p] x 8 B
   const int64_t plane_smem = ((d0 + 1) / 2 * (d2 | 1) + kPlaneThreads + d2) * 16 + kZeroBytes;
@@ -1106,8 +1114,8 @@ SortPlan sort_plan(const Grid4Layout& L, const int32_t* glen, int64_t n_rec) {
   sp.parts = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), (n_rec + kSortThreads - 1) / kSortThreads));
   sp.per = (int)(((n_rec + sp.parts - 1) / sp.parts + 31) & ~31ll);
   sp.parts = (int)((n_rec + sp.per - 1) / sp.per);
-  sp.sort_smem = (size_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * 4 +
-                 (size_t)((L.nb + 3) & ~3) * 4 + (size_t)sp.per * 10;
+  sp.sort_smem = (size_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * kLutEntryBytes +
+                 (size_t)((L.nb + 3) & ~3) * 4 + (size_t)sp.per * 8;
   sp.gather_smem = (size_t)L.d0 * L.hp * 12 + (size_t)L.d0 * 4 + 16 + kGatherThreads * 8 +
                    (size_t)sp.parts * 12 + 4;
   if (sp.sort_smem > (size_t)kSortSmemMax || sp.gather_smem > kGrid4SlabMax || sp.parts > kGatherThreads ||
@@ -1168,7 +1176,7 @@ cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_
   h.G0 = G0;
   h.counters = reinterpret_cast<uint32_t*>(ws + L.offCnt);
   const size_t smem =
-      (size_t)(glen[0] + glen[1] + glen[2]) * sizeof(double) + 3 * kLutBuckets * sizeof(uint32_t);
+      (size_t)(glen[0] + glen[1] + glen[2]) * sizeof(double) + 3 * kLutBuckets * kLutEntryBytes;
   static std::atomic<int> smem_hist{0};
   cudaError_t e = ensure_smem4(g4_hist_kernel, smem_hist, smem);
   if (e != cudaSuccess) return e;

@@ -18,6 +18,7 @@
 namespace gs {
 
 constexpr int kLutBuckets = 2048;
+constexpr int kLutEntryBytes = 8;
 
 __device__ __forceinline__ int lut_bucket(double x, double lo, double hi, double scale) {
   if (!(x >= lo)) return 0;  // below the grid (or NaN)
@@ -49,28 +50,34 @@ __device__ __forceinline__ int upper_count(const double* g, int n, double x) {
 // conversion instruction.  An entry holds the bucket's first grid index and
 // how many grid values it holds (usually 0 or 1), so a lookup is one LDS,
 // one f64 LDS and one f64 compare.
-__device__ __forceinline__ int bucket_of(double x, float lo, float scale) {
-  float y = __fmul_rn(__fsub_rn(__double2float_rn(x), lo), scale);
+__device__ __forceinline__ int bucket_of_f(float xf, float lo, float scale) {
+  float y = __fmul_rn(__fsub_rn(xf, lo), scale);
   y = fminf(fmaxf(y, 0.f), (float)(kLutBuckets - 1));
   return __float_as_int(__fadd_rn(y, 8388608.f)) - 0x4B000000;
 }
+__device__ __forceinline__ int bucket_of(double x, float lo, float scale) {
+  return bucket_of_f(__double2float_rn(x), lo, scale);
+}
 
+// An entry is {first grid index | count << 16, f32 of the bucket's first
+// grid value}: with one value in the bucket (the usual case) the f32
+// compare decides unless the two round to the same f32 (monotone rounding:
+// xf > gf implies x > g, xf < gf implies x < g), and only then, or for NaN
+// or several values, the exact f64 compare runs.
 template <int D>
 struct BinTables {
-  const double* grid;   // smem, concatenated grids of models 0..D-1
-  const uint32_t* lut;  // smem, [D][kLutBuckets]: first index | count << 16
+  const double* grid;  // smem, concatenated grids of models 0..D-1
+  const uint2* lut;    // smem, [D][kLutBuckets]
   int goff[D];
   float lo[D], scale[D];
 
-  // the grid value at lb is read even for an empty bucket (lb <= n: at
-  // worst the first word past this model's grid, still shared memory) and
-  // only used when the bucket holds a value
   __device__ __forceinline__ int bin(int j, double x) const {
-    const uint32_t e = lut[j * kLutBuckets + bucket_of(x, lo[j], scale[j])];
-    const int lb = (int)(e & 0xffffu), c = (int)(e >> 16);
-    const double* g = grid + goff[j] + lb;
-    int b = lb + ((c != 0 && g[0] <= x) ? 1 : 0);
-    if (c > 1) b = lb + upper_count(g, c, x);
+    const float xf = __double2float_rn(x);
+    const uint2 e = lut[j * kLutBuckets + bucket_of_f(xf, lo[j], scale[j])];
+    const int lb = (int)(e.x & 0xffffu), c = (int)(e.x >> 16);
+    const float gf = __uint_as_float(e.y);
+    int b = lb + ((c != 0 && xf > gf) ? 1 : 0);
+    if (c > 1 || (c == 1 && !(xf > gf) && !(xf < gf))) b = lb + upper_count(grid + goff[j] + lb, c, x);
     return b;
   }
 };
@@ -78,7 +85,8 @@ struct BinTables {
 // Build the tables in shared memory; every thread of the block calls it.
 // s_grid must already hold the D grids (loaded by the caller, so it can
 // order the grid loads ahead of its own record loads) and be synchronised;
-// s_lut holds D * kLutBuckets words.  Every thread derives lo / scale
+// s_lut holds D * kLutBuckets 8-byte entries (kLutEntryBytes); the first
+// half serves as 32-bit scratch until the entries are written.  Every thread derives lo / scale
 // itself.  Three steps, no serial loops over buckets or grid values:
 //   1. every bucket's entry := n (empty);
 //   2. one thread per grid value: the first value of each occupied bucket
@@ -90,7 +98,8 @@ struct BinTables {
 //      lb(q)) << 16.
 template <int D, int THREADS>
 __device__ __forceinline__ BinTables<D> build_bin_tables(const int32_t* glen, double* s_grid,
-                                                         uint32_t* s_lut) {
+                                                         void* s_lut_mem) {
+  uint32_t* s_lut = static_cast<uint32_t*>(s_lut_mem);
   static_assert(kLutBuckets % THREADS == 0, "bucket split");
   constexpr int per = kLutBuckets / THREADS;
   constexpr int nwarps = THREADS / 32;
@@ -155,21 +164,46 @@ __device__ __forceinline__ BinTables<D> build_bin_tables(const int32_t* glen, do
     tmin[j] = lane == 31 ? 0xffffffffu : after;
   }
   __syncthreads();
+  // across warps: warp j turns model j's warp minima into "minimum over the
+  // warps after this one" (a suffix minimum by shuffles, not a serial loop)
+  if (warp < D) {
+    const uint32_t m = lane < nwarps ? s_wmin[warp][lane] : 0xffffffffu;
+    uint32_t incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_down_sync(0xffffffffu, incl, o);
+      if (lane + o < 32) incl = min(incl, y);
+    }
+    const uint32_t after = __shfl_down_sync(0xffffffffu, incl, 1);
+    __syncwarp();
+    if (lane < nwarps) s_wmin[warp][lane] = lane == 31 ? 0xffffffffu : after;
+  }
+  __syncthreads();
+  uint2 entry[D][per];
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    uint32_t after = tmin[j];
-    for (int w = warp + 1; w < nwarps; ++w) after = min(after, s_wmin[j][w]);
+    const uint32_t after = min(tmin[j], s_wmin[j][warp]);
     // lb(q) for the thread's buckets, lb of the bucket after the last
     uint32_t lb[per + 1];
     lb[per] = min(after, (uint32_t)glen[j]);
 #pragma unroll
     for (int q = 0; q < per; ++q) lb[q] = min(v[j][q], after);
 #pragma unroll
-    for (int q = 0; q < per; ++q) s_lut[j * kLutBuckets + q0 + q] = lb[q] | ((lb[q + 1] - lb[q]) << 16);
+    for (int q = 0; q < per; ++q) {
+      const uint32_t c = lb[q + 1] - lb[q];
+      const float gf = c ? __double2float_rn(s_grid[t.goff[j] + lb[q]]) : 0.f;
+      entry[j][q] = make_uint2(lb[q] | (c << 16), __float_as_uint(gf));
+    }
   }
+  __syncthreads();  // every scratch word is read: the entries overwrite them
+  uint2* s_entry = static_cast<uint2*>(s_lut_mem);
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int q = 0; q < per; ++q) s_entry[j * kLutBuckets + q0 + q] = entry[j][q];
   __syncthreads();
   t.grid = s_grid;
-  t.lut = s_lut;
+  t.lut = s_entry;
   return t;
 }
 
