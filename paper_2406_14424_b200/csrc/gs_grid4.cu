@@ -431,13 +431,31 @@ struct G4SortArgs {
   const double* grids;
   int32_t glen[3];
   int32_t d0, nb, per;         // buckets (one per b1), records per CTA
+  int32_t off_ring;            // byte offset of the cp.async record ring (RING variant)
   uint32_t* keys;              // [n_rec] sorted by bucket within each CTA's range
   uint32_t* off;               // [parts][nb + 1] absolute key offsets of each bucket
   uint32_t* G0;                // [d0] model-0 correct counts per b0
 };
 
 
-template <bool VEC>
+constexpr int kRing = 3;  // records per thread in flight through the shared-memory ring
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// RING: each thread keeps kRing records in flight through a shared-memory
+// ring filled by cp.async (no registers held), from before the bin tables
+// are built until the range ends, so the records stream at the HBM rate
+// while the tables are built; else (unaligned inputs, or no room) a
+// rotation of register sets, two records ahead.
+template <bool VEC, bool RING>
 __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_constant__ G4SortArgs a) {
   extern __shared__ __align__(16) double s_grid[];  // grids, bucket tables, counts, keys
   __shared__ uint32_t s_c0[kMaxDim4];
@@ -462,9 +480,24 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   ha.cert = a.cert;
   ha.corr = a.corr;
   ha.vec_ok = VEC ? 1 : 0;  // a compile-time branch in load_rec4
-  Rec4 v, w;  // two records per thread in flight from the start
-  if (tid < cnt) v = load_rec4(ha, r0 + tid);
-  if (tid + kSortThreads < cnt) w = load_rec4(ha, r0 + tid + kSortThreads);
+  constexpr int T = kSortThreads;
+  double* s_rc = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(s_grid) + a.off_ring);  // [kRing][T][4]
+  uint32_t* s_rk = reinterpret_cast<uint32_t*>(s_rc + (size_t)kRing * T * 4);                 // [kRing][T]
+  auto issue = [&](int slot, int i) {  // record i of the range into this thread's slot
+    if (i < cnt) {
+      const double* src = a.cert + (int64_t)(r0 + i) * 4;
+      double* dst = s_rc + ((size_t)slot * T + tid) * 4;
+      cp_async16(dst, src);
+      cp_async16(dst + 2, src + 2);
+      cp_async4(s_rk + slot * T + tid, a.corr + (int64_t)(r0 + i) * 4);
+    }
+    cp_async_commit();  // one group per record, empty past the range
+  };
+  Rec4 v, w;  // register variant: two records per thread in flight from the start
+  if (!RING) {
+    if (tid < cnt) v = load_rec4(ha, r0 + tid);
+    if (tid + kSortThreads < cnt) w = load_rec4(ha, r0 + tid + kSortThreads);
+  }
 #pragma unroll
   for (int q = 0; q < kGridRegs; ++q) {
     const int i = tid + q * kSortThreads;
@@ -474,6 +507,12 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   for (int i = tid; i < a.nb; i += kSortThreads) s_cnt[i] = 0u;
   __syncthreads();
   phase(0, 1);
+  // the ring fills while the tables are built (issued only now: queued
+  // behind the records of every SM, the grid values would arrive late)
+  if (RING) {
+#pragma unroll
+    for (int q = 0; q < kRing; ++q) issue(q, tid + q * T);
+  }
   const BinTables<3> bt = build_bin_tables<3, kSortThreads>(a.glen, s_grid, s_lut);
   phase(0, 2);
   auto put = [&](int i, double x0, double x1, double x2, uint32_t k) {
@@ -487,9 +526,22 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
     s_key[i] = key;
     if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
   };
+  if (RING) {
+    int slot = 0;
+    for (int i = tid; i < cnt; i += T) {
+      cp_async_wait<kRing - 1>();  // this record's group is complete
+      const double* rc = s_rc + ((size_t)slot * T + tid) * 4;
+      const double2 p = *reinterpret_cast<const double2*>(rc);
+      const double x2 = rc[2];
+      const uint32_t k = s_rk[slot * T + tid];
+      issue(slot, i + kRing * T);
+      put(i, p.x, p.y, x2, k);
+      slot = slot == kRing - 1 ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
+  } else
   // three records per trip in a rotation of three registers sets, each
   // loaded two records ahead (no register moves)
-  constexpr int T = kSortThreads;
   for (int i = tid; i < cnt; i += 3 * T) {
     Rec4 x;
     if (i + 2 * T < cnt) x = load_rec4(ha, r0 + i + 2 * T);
@@ -1104,7 +1156,8 @@ bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
 
 // Shared memory of the sorted build's two kernels (0 when it does not apply).
 struct SortPlan {
-  int parts, per;
+  int parts, per, off_ring;
+  bool ring;
   size_t sort_smem, gather_smem;
 };
 
@@ -1116,6 +1169,10 @@ SortPlan sort_plan(const Grid4Layout& L, const int32_t* glen, int64_t n_rec) {
   sp.parts = (int)((n_rec + sp.per - 1) / sp.per);
   sp.sort_smem = (size_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * kLutEntryBytes +
                  (size_t)((L.nb + 3) & ~3) * 4 + (size_t)sp.per * 8;
+  sp.off_ring = (int)round_up(sp.sort_smem, 128);
+  const size_t ring_bytes = (size_t)kRing * kSortThreads * 36;
+  sp.ring = sp.off_ring + ring_bytes <= (size_t)kSortSmemMax;
+  if (sp.ring) sp.sort_smem = sp.off_ring + ring_bytes;
   sp.gather_smem = (size_t)L.d0 * L.hp * 12 + (size_t)L.d0 * 4 + 16 + kGatherThreads * 8 +
                    (size_t)sp.parts * 12 + 4;
   if (sp.sort_smem > (size_t)kSortSmemMax || sp.gather_smem > kGrid4SlabMax || sp.parts > kGatherThreads ||
@@ -1252,14 +1309,21 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   a.keys = keys;
   a.off = off;
   a.G0 = G0;
-  static std::atomic<int> smem_sort{0}, smem_sort_s{0}, smem_gather{0};
+  static std::atomic<int> smem_sort{0}, smem_sort_r{0}, smem_sort_s{0}, smem_gather{0};
+  a.off_ring = sp.off_ring;
+  // the ring's cp.async copies want 16-byte aligned rows and 4-byte correct words
+  const bool ring = sp.ring && a.vec_ok;
+  const size_t smem = ring ? sp.sort_smem : (size_t)sp.off_ring;
   if (!(passes & 1)) {
+  } else if (ring) {
+    if ((e = ensure_smem4(g4_sort_kernel<true, true>, smem_sort_r, kSortSmemMax)) != cudaSuccess) return e;
+    g4_sort_kernel<true, true><<<(unsigned)sp.parts, kSortThreads, smem, st>>>(a);
   } else if (a.vec_ok) {
-    if ((e = ensure_smem4(g4_sort_kernel<true>, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
-    g4_sort_kernel<true><<<(unsigned)sp.parts, kSortThreads, sp.sort_smem, st>>>(a);
+    if ((e = ensure_smem4(g4_sort_kernel<true, false>, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
+    g4_sort_kernel<true, false><<<(unsigned)sp.parts, kSortThreads, smem, st>>>(a);
   } else {
-    if ((e = ensure_smem4(g4_sort_kernel<false>, smem_sort_s, kSortSmemMax)) != cudaSuccess) return e;
-    g4_sort_kernel<false><<<(unsigned)sp.parts, kSortThreads, sp.sort_smem, st>>>(a);
+    if ((e = ensure_smem4(g4_sort_kernel<false, false>, smem_sort_s, kSortSmemMax)) != cudaSuccess) return e;
+    g4_sort_kernel<false, false><<<(unsigned)sp.parts, kSortThreads, smem, st>>>(a);
   }
   if ((e = cudaGetLastError()) != cudaSuccess || !(passes & 2)) return e;
 
