@@ -369,3 +369,31 @@ def test_build_passes_split():
     sw.build(part="records")
     sw.build(part="tables")
     _equal_results(sw.evaluate(n_correct=True), a)
+
+
+@pytest.mark.parametrize("n_rec", [5, 1025, 3 * 1024 + 7, 150_001])
+def test_sorted_build_unaligned_inputs(n_rec):
+    """The bucket-sort build reads records through a cp.async ring when the
+    rows are 16-byte aligned and the correct words 4-byte aligned, else with
+    scalar loads: views offset by 8 B (certainty) and 1 B (correct) take the
+    second path and must give the same tables (and the oracle's values)."""
+    import torch
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    rng = np.random.default_rng(n_rec)
+    cert, corr, grids, cost1 = _random_case(rng, n_rec, 4, 9)
+    a = GridSweep(cert, corr, grids, cost1)
+    assert a.info.fast_path == 2
+    big_c = torch.empty(n_rec * 4 + 1, dtype=torch.float64, device="cuda")
+    big_k = torch.empty(n_rec * 4 + 1, dtype=torch.uint8, device="cuda")
+    vc = big_c[1:].view(n_rec, 4)
+    vk = big_k[1:].view(n_rec, 4)
+    vc.copy_(torch.from_numpy(cert))
+    vk.copy_(torch.from_numpy(corr))
+    assert vc.data_ptr() % 16 == 8 and vk.data_ptr() % 4 == 1
+    b = GridSweep(vc, vk, grids, cost1)
+    assert b.cert.data_ptr() == vc.data_ptr()
+    _equal_results(a.evaluate(n_correct=True), b.evaluate(n_correct=True))
+    if n_rec <= 5000:
+        sm, thr, ns = oracle.grid_configs(grids)
+        want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
+        assert np.array_equal(b.evaluate().accuracy.cpu().numpy(), want[0])
