@@ -957,6 +957,121 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
   }
 }
 
+// ------------------------------------------------ full cascade (M = 5) --
+// For five models the full cascade (0,1,2,3,4) holds g0 g1 g2 g3 of the
+// configs (95% at 100-level grids) and its config (k0, k1, k2, k3) reads the
+// table at (k0,g,g,g), (k0,k1,g,g), (k0,k1,k2,g) and (k0,k1,k2,k3).  A CTA
+// owns one (k0, k1) pair: its row-shared terms (two fractions, the partial
+// mean through stage 2, the correct counts of models 0-2) once per CTA; a
+// warp per k2 row loads the row's d3 cells (contiguous, the last one being
+// (k0,k1,k2,g)) and scores its g3 configs, which are consecutive in the
+// enumeration; forward_frac rows (40 B, not vector aligned) go through a
+// per-warp shared buffer and leave as coalesced 8-byte stores.  The regular
+// eval scores the other structures.
+constexpr int kFull5Threads = 256;
+constexpr int kFull5MaxRow = 128;  // g3 bound of the per-warp frac buffer (40 KB static)
+
+struct Full5Args {
+  int32_t g0, g1, g2, g3, d1;
+  int64_t sF0, sF1, sF2;  // F strides of dims 0..2 (dim 3 contiguous)
+  int64_t sb;             // first config of the full cascade
+  int64_t cfg_begin, cfg_count;
+  int64_t n_rec;
+  double rcp_n;
+  const double* cost1;
+  const uint4* F;  // {cnt, c4, c3, c2} fully prefixed
+  const uint4* P;  // side table over (b0, b1): {c0, c1, -, -}
+  double* acc;
+  double* cost;
+  double* frac;
+  uint32_t* n_correct;
+};
+
+__global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_constant__ Full5Args a) {
+  __shared__ double s_frac[kFull5Threads / 32][kFull5MaxRow * 5];
+  const int k0 = blockIdx.x / a.g1, k1 = blockIdx.x % a.g1;
+  const int g1 = a.g1, g2 = a.g2, g3 = a.g3;
+  const int64_t cta_first = a.sb + ((int64_t)k0 * g1 + k1) * g2 * g3;
+  const int64_t cta_end = cta_first + (int64_t)g2 * g3;
+  if (cta_end <= a.cfg_begin || cta_first >= a.cfg_begin + a.cfg_count) return;
+  const bool full = cta_first >= a.cfg_begin && cta_end <= a.cfg_begin + a.cfg_count;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double n = (double)a.n_rec, rcp = a.rcp_n;
+  const double one = div_count(n, n, rcp);
+  const double c0 = __ldg(a.cost1), c1 = __ldg(a.cost1 + 1), c2 = __ldg(a.cost1 + 2),
+               c3 = __ldg(a.cost1 + 3), c4 = __ldg(a.cost1 + 4);
+  const uint4 Fk0 = __ldg(a.F + k0 * a.sF0 + (int64_t)g1 * a.sF1 + (int64_t)g2 * a.sF2 + g3);
+  const uint4 Fk01 = __ldg(a.F + k0 * a.sF0 + (int64_t)k1 * a.sF1 + (int64_t)g2 * a.sF2 + g3);
+  const uint4 Pgg = __ldg(a.P + (int64_t)a.g0 * a.d1 + g1);
+  const uint4 Pk0 = __ldg(a.P + (int64_t)k0 * a.d1 + g1);
+  const uint4 Pk01 = __ldg(a.P + (int64_t)k0 * a.d1 + k1);
+  const double fr1 = div_count((double)Fk0.x, n, rcp);
+  const double fr2 = div_count((double)Fk01.x, n, rcp);
+  const double m2 = dadd(dadd(dadd(0.0, dmul(one, c0)), dmul(fr1, c1)), dmul(fr2, c2));
+  // models 0, 1 complete between their positions; model 2's count before k2
+  const uint32_t base = (Pgg.x - Pk0.x) + (Pk0.y - Pk01.y) + Fk01.w;
+  double* buf = s_frac[warp];
+  constexpr int U = (kFull5MaxRow + 32) / 32;  // cells per lane (d3 = g3 + 1 <= 32 U)
+  for (int k2 = warp; k2 < g2; k2 += kFull5Threads / 32) {
+    const uint4* row = a.F + k0 * a.sF0 + (int64_t)k1 * a.sF1 + (int64_t)k2 * a.sF2;
+    uint4 cell[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k3 = lane + 32 * u;
+      cell[u] = k3 <= g3 ? __ldg(row + k3) : make_uint4(0, 0, 0, 0);
+    }
+    uint4 rc = make_uint4(0, 0, 0, 0);  // (k0, k1, k2, g): the row's last cell
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4 t = make_uint4(__shfl_sync(0xffffffffu, cell[u].x, g3 & 31),
+                                 __shfl_sync(0xffffffffu, cell[u].y, g3 & 31),
+                                 __shfl_sync(0xffffffffu, cell[u].z, g3 & 31),
+                                 __shfl_sync(0xffffffffu, cell[u].w, g3 & 31));
+      if (u == (g3 >> 5)) rc = t;
+    }
+    const double fr3 = div_count((double)rc.x, n, rcp);
+    const double m3 = dadd(m2, dmul(fr3, c3));
+    const uint32_t cr = base - rc.w + rc.z;  // through model 2, plus model 3's count before k3
+    const int64_t i0 = cta_first + (int64_t)k2 * g3 - a.cfg_begin;  // config of k3 = 0
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k3 = lane + 32 * u;
+      if (k3 < g3) {
+        const uint4 c = cell[u];
+        const double fr4 = div_count((double)c.x, n, rcp);
+        const double mean = dadd(m3, dmul(fr4, c4));
+        const uint32_t correct = cr - c.z + c.y;
+        const int64_t i = i0 + k3;
+        if (full || (i >= 0 && i < a.cfg_count)) {
+          if (a.cost) a.cost[i] = mean;
+          if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+          if (a.n_correct) a.n_correct[i] = correct;
+        }
+        double* f = buf + k3 * 5;
+        f[0] = one;
+        f[1] = fr1;
+        f[2] = fr2;
+        f[3] = fr3;
+        f[4] = fr4;
+      }
+    }
+    __syncwarp();
+    if (a.frac) {
+      double* dst = a.frac + i0 * 5;
+      const int ne = g3 * 5;
+      if (full) {
+        for (int e = lane; e < ne; e += 32) dst[e] = buf[e];
+      } else {
+        for (int e = lane; e < ne; e += 32) {
+          const int64_t i = i0 + e / 5;
+          if (i >= 0 && i < a.cfg_count) dst[e] = buf[e];
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // -------------------------------------------------------- fused walk (M=4) --
 // For four models the dominant structure is the full cascade (0,1,2,3): its
 // g0*g1*g2 configs are 96% of the enumeration and map one-to-one onto table
@@ -1306,7 +1421,7 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
     const bool fold_side = p.DP == 1 && p.NVP == 1 && slab;
     if (p.DP > 0 && !fold_side) b += std::max(1, p.DP);
     info->build_launches = b;
-    info->eval_launches = p.walk ? 2 : 1;
+    info->eval_launches = (p.walk || (p.M == 5 && p.glen[3] <= kFull5MaxRow)) ? 2 : 1;
   }
   return GS_OK;
 }
@@ -1501,6 +1616,36 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
     walk_eval_kernel<<<(plane + w.tile - 1) / w.tile, threads, smem, st>>>(w);
     GS_LAUNCH_CHECK();
     reg_end = std::min<int64_t>(reg_end, w.sb);
+    if (reg_end <= config_begin) return GS_OK;
+  }
+  if (p.M == 5 && p.glen[3] <= kFull5MaxRow && p.cellsP > 0) {
+    // the full cascade (the last structure): full5_eval_kernel
+    Full5Args f{};
+    f.g0 = p.glen[0];
+    f.g1 = p.glen[1];
+    f.g2 = p.glen[2];
+    f.g3 = p.glen[3];
+    f.d1 = (int32_t)p.dims[1];
+    f.sF0 = p.strideF[0];
+    f.sF1 = p.strideF[1];
+    f.sF2 = p.strideF[2];
+    f.sb = p.struct_begin[p.n_struct - 1];
+    f.cfg_begin = config_begin;
+    f.cfg_count = config_count;
+    f.n_rec = n_rec;
+    f.rcp_n = 1.0 / (double)n_rec;
+    f.cost1 = cost1;
+    f.F = reinterpret_cast<const uint4*>(ws + p.offF);
+    f.P = reinterpret_cast<const uint4*>(ws + p.offP);
+    f.acc = accuracy;
+    f.cost = mean_cost;
+    f.frac = forward_frac;
+    f.n_correct = n_correct;
+    if (config_begin + config_count > f.sb) {
+      full5_eval_kernel<<<(unsigned)((int64_t)f.g0 * f.g1), kFull5Threads, 0, st>>>(f);
+      GS_LAUNCH_CHECK();
+    }
+    reg_end = std::min<int64_t>(reg_end, f.sb);
     if (reg_end <= config_begin) return GS_OK;
   }
   a.cfg_count = reg_end - config_begin;

@@ -66,19 +66,35 @@ def test_random_grids_vs_oracle(n_rec, n_models, levels, ties):
     assert np.array_equal(idx.cpu().numpy(), np.flatnonzero(keep))
 
 
-def test_config_ranges_equal_full_sweep():
+@pytest.mark.parametrize("n_models", [4, 5])
+def test_config_ranges_equal_full_sweep(n_models):
+    """Ranges of the enumeration (crossing the full cascade's start, inside
+    one of its (k0, k1) blocks, ...) score exactly like the full sweep."""
     rng = np.random.default_rng(9)
-    cert, corr, grids, cost1 = _random_case(rng, 4000, 4, 9)
+    cert, corr, grids, cost1 = _random_case(rng, 4000, n_models, 9)
     from paper_2406_14424_b200.gridsweep import GridSweep
     sw = GridSweep(cert, corr, grids, cost1)
-    full = sw.evaluate()
+    full = sw.evaluate(n_correct=True)
     n = sw.n_configs
-    for begin, count in ((0, 1), (3, 100), (n - 7, 7), (123, n - 200), (5, 3)):
+    sb = n - int(np.prod([len(g) for g in grids[:-1]]))  # first config of the full cascade
+    if n_models == 5:  # the full-cascade kernel's whole answer, against the oracle
+        sm, thr, ns = oracle.grid_configs(grids)
+        pick = np.sort(rng.choice(np.arange(sb, n), size=64, replace=False))
+        want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1, n_threads=8)
+        assert np.array_equal(full.accuracy.cpu().numpy()[pick], want[0])
+        assert np.array_equal(full.mean_cost.cpu().numpy()[pick], want[1])
+        assert np.array_equal(full.forward_frac.cpu().numpy()[pick], want[2])
+    for begin, count in ((0, 1), (3, 100), (n - 7, 7), (123, n - 200), (5, 3),
+                         (sb - 5, 20), (sb + 17, 101), (sb + 64 * 8 + 3, 700)):
+        begin = min(begin, n - 1)
+        count = min(count, n - begin)
         part = sw.evaluate(begin, count)
         assert np.array_equal(part.accuracy.cpu().numpy(),
                               full.accuracy[begin:begin + count].cpu().numpy())
         assert np.array_equal(part.forward_frac.cpu().numpy(),
                               full.forward_frac[begin:begin + count].cpu().numpy())
+        assert np.array_equal(part.mean_cost.cpu().numpy(),
+                              full.mean_cost[begin:begin + count].cpu().numpy())
 
 
 @pytest.mark.parametrize("n_models", [2, 4])
