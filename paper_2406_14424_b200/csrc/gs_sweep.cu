@@ -966,10 +966,11 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
 // warp per k2 row loads the row's d3 cells (contiguous, the last one being
 // (k0,k1,k2,g)) and scores its g3 configs, which are consecutive in the
 // enumeration; forward_frac rows (40 B, not vector aligned) go through a
-// per-warp shared buffer and leave as coalesced 8-byte stores.  The regular
+// per-warp shared buffer and the row's block leaves as coalesced 16-byte
+// stores.  The regular
 // eval scores the other structures.
 constexpr int kFull5Threads = 256;
-constexpr int kFull5MaxRow = 128;  // g3 bound of the per-warp frac buffer (40 KB static)
+constexpr int kFull5MaxRow = 128;  // g3 bound (per-warp frac buffer: 40 KB static)
 
 struct Full5Args {
   int32_t g0, g1, g2, g3, d1;
@@ -988,7 +989,7 @@ struct Full5Args {
 };
 
 __global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_constant__ Full5Args a) {
-  __shared__ double s_frac[kFull5Threads / 32][kFull5MaxRow * 5];
+  __shared__ double s_frac[kFull5Threads / 32][kFull5MaxRow * 5];  // the warp's row of frac rows
   const int k0 = blockIdx.x / a.g1, k1 = blockIdx.x % a.g1;
   const int g1 = a.g1, g2 = a.g2, g3 = a.g3;
   const int64_t cta_first = a.sb + ((int64_t)k0 * g1 + k1) * g2 * g3;
@@ -1060,7 +1061,15 @@ __global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_
       double* dst = a.frac + i0 * 5;
       const int ne = g3 * 5;
       if (full) {
-        for (int e = lane; e < ne; e += 32) dst[e] = buf[e];
+        // 16-byte stores from the first 16-byte boundary of the block
+        const int head = (reinterpret_cast<uintptr_t>(dst) & 15u) ? 1 : 0;
+        if (head && lane == 0) dst[0] = buf[0];
+        const int npair = (ne - head) / 2;
+        for (int q = lane; q < npair; q += 32) {
+          const int e = head + 2 * q;
+          *reinterpret_cast<double2*>(dst + e) = make_double2(buf[e], buf[e + 1]);
+        }
+        if (((ne - head) & 1) && lane == 0) dst[ne - 1] = buf[ne - 1];
       } else {
         for (int e = lane; e < ne; e += 32) {
           const int64_t i = i0 + e / 5;
