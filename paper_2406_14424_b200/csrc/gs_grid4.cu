@@ -45,7 +45,6 @@
 // and likewise for the shorter structures.
 #include <algorithm>
 #include <atomic>
-#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -412,12 +411,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
 // table is what held g4_hist above the streaming rate (one L2 reduction per
 // record, then a plane pass that re-reads and re-zeroes the table).  Here
 // g4_sort streams the records once and writes each as a 4-byte key
-// {b0, b2, k1, k2, k3, b1}, counting-sorted in shared memory by bucket
-// (b1, b0 half) within the CTA's record range, plus the range's bucket
-// offsets; g4_gather then builds each (b1, b0 half) plane in shared memory
-// from its bucket's keys (one shared 64-bit add of the packed {1, k3, k2}
-// per key), prefixes it along b2 and b0 and writes the same S / R1 / P0
-// tables as g4_plane.  Keys are 4 MB per 1M records and stay in L2.
+// {b0, b2, k1, k2, k3, b1}, counting-sorted in shared memory by b1 within
+// the CTA's record range, plus the range's bucket offsets; g4_gather then
+// builds each b1's (b0, b2) plane in shared memory from its bucket's keys
+// (32-bit shared atomics on 16-bit packed counters), prefixes it along b2
+// and b0 and writes the same S / R1 / P0 tables as g4_plane.  Keys are
+// 4 MB per 1M records and stay in L2.
 constexpr int kSortThreads = 1024;
 constexpr int kGatherThreads = 1024;
 constexpr int kSortMaxD1 = 1024;  // b1 takes 10 key bits
