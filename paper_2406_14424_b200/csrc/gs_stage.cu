@@ -133,14 +133,32 @@ __device__ __forceinline__ void warp_for_each(const T* row, int n, bool vec_ok, 
   }
 }
 
-// Certainty of one row, computed by a full warp; result valid in all lanes.
-// log_n: ln(n) precomputed by the caller for the entropy kind (<= 0: compute)
+// The two reduced quantities a row's certainty is finished from (valid in
+// all lanes): margin {top, second}; max-softmax {sum of exp(x - max), -};
+// entropy {that sum, sum of exp(x - max) (x - max)}.  finish_cert turns
+// them into the certainty; the stage step finishes 32 rows in one pass
+// (lane k the warp's k-th row) instead of once per row: the f64 log and
+// divisions of the entropy were a quarter of its instructions.
+struct RowPair {
+  double x, y;
+};
+
+template <int KIND>
+__device__ __forceinline__ double finish_cert(RowPair p, int n, double log_n) {
+  if (KIND == GS_CERT_MARGIN) return p.x - p.y;
+  if (n == 1) return 1.0;
+  if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / p.x;
+  const double H = log(p.x) - p.y / p.x;
+  return 1.0 - H / (log_n > 0.0 ? log_n : log((double)n));
+}
+
+// Certainty pair of one row, computed by a full warp.
 template <typename T, int KIND>
-__device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok, double log_n = 0.0) {
+__device__ __forceinline__ RowPair warp_row_pair(const T* row, int n, bool vec_ok) {
   using C = typename Compute<T>::type;
   if (n == 1) {
     const double x0 = (double)to_float(row[0]);
-    return KIND == GS_CERT_MARGIN ? x0 : 1.0;
+    return {KIND == GS_CERT_MARGIN ? x0 : 1.0, 0.0};
   }
   constexpr int V = Vec16<T>::N;
   constexpr int RV = 8;  // 16-byte vectors per lane held in registers
@@ -180,7 +198,7 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
         const C o2 = __shfl_xor_sync(0xffffffffu, m2, o);
         merge_top2<C>(m1, m2, o1, o2);
       }
-      return (double)m1 - (double)m2;
+      return {(double)m1, (double)m2};
     }
     C m = neg_inf<C>();
     each([&](T x) {
@@ -236,10 +254,8 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
       });
     }
     s = warp_sum(s);
-    if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / s;
-    t = warp_sum(t);
-    const double H = log(s) - t / s;
-    return 1.0 - H / (log_n > 0.0 ? log_n : log((double)n));
+    if (KIND == GS_CERT_ENTROPY) t = warp_sum(t);
+    return {s, t};
   }
   if (KIND == GS_CERT_MARGIN) {
     C m1 = neg_inf<C>(), m2 = neg_inf<C>();
@@ -250,7 +266,7 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
       const C o2 = __shfl_xor_sync(0xffffffffu, m2, o);
       merge_top2<C>(m1, m2, o1, o2);
     }
-    return (double)m1 - (double)m2;
+    return {(double)m1, (double)m2};
   } else {
     C m = neg_inf<C>();
     warp_for_each<T>(row, n, vec_ok, [&](T x) {
@@ -270,11 +286,16 @@ __device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok
       if (KIND == GS_CERT_ENTROPY) t += e * (double)d;
     });
     s = warp_sum(s);
-    if (KIND == GS_CERT_MAX_SOFTMAX) return 1.0 / s;
-    t = warp_sum(t);
-    const double H = log(s) - t / s;
-    return 1.0 - H / log((double)n);
+    if (KIND == GS_CERT_ENTROPY) t = warp_sum(t);
+    return {s, t};
   }
+}
+
+// Certainty of one row, computed by a full warp; result valid in all lanes.
+// log_n: ln(n) precomputed by the caller for the entropy kind (<= 0: compute)
+template <typename T, int KIND>
+__device__ __forceinline__ double warp_row_cert(const T* row, int n, bool vec_ok, double log_n = 0.0) {
+  return finish_cert<KIND>(warp_row_pair<T, KIND>(row, n, vec_ok), n, log_n);
 }
 
 // Certainty of one row computed by one thread.
@@ -426,14 +447,19 @@ __global__ void __launch_bounds__(kStepThreads) stage_step_kernel(const __grid_c
   double cert = 0.0;
   if (WIDE) {
     const int warp = threadIdx.x >> 5;
+    // lane k keeps the pair of the warp's k-th row; one finishing pass
+    static_assert(kWideRowsPerWarp == 32, "a row per lane");
+    const int lane = (int)lane_id();
+    RowPair mine{0.0, 0.0};
     for (int k = 0; k < kWideRowsPerWarp; ++k) {
       const int lr = warp * kWideRowsPerWarp + k;
       if (lr < rows) {
-        const double c = warp_row_cert<T, KIND>(scores + (base + lr) * a.stride, a.n_cls, a.vec_ok,
-                                                a.log_n);
-        if (lane_id() == 0) s_cert[lr] = c;
+        const RowPair p = warp_row_pair<T, KIND>(scores + (base + lr) * a.stride, a.n_cls, a.vec_ok);
+        if (lane == k) mine = p;
       }
     }
+    const int lr = warp * kWideRowsPerWarp + lane;
+    if (lr < rows) s_cert[lr] = finish_cert<KIND>(mine, a.n_cls, a.log_n);
     __syncthreads();
     if ((int)threadIdx.x < rows) cert = s_cert[threadIdx.x];
   } else {
