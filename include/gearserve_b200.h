@@ -132,6 +132,21 @@ int gs_grid_accumulate(const double* certainty, const uint8_t* correct,
                        void* stream);
 int gs_grid_finish(int64_t n_rec, int32_t n_models, const int32_t* grid_len,
                    void* workspace, size_t workspace_bytes, void* stream);
+/* Many small three-model sweeps in one launch (config 1 stacked: the
+ * reference's CPU default is launch-bound alone).  n_sets validation sets of
+ * n_rec records each, certainty [n_sets][n_rec][3] f64 and correct
+ * [n_sets][n_rec][3] u8 row-major on the DEVICE, per-set grids
+ * [n_sets][grid_len[0] + grid_len[1] + grid_len[2]] f64 on the DEVICE (each
+ * strictly increasing), grid_len [3] on the HOST, cost1 [3] on the DEVICE.
+ * Outputs [n_sets][C] (accuracy, mean_cost) and [n_sets][C][3]
+ * (forward_frac), C = 3 + 2 g0 + g1 + g0 g1, every config of each set's
+ * enumeration in gs_grid_eval's order and with its values.  GS_EUNSUPPORTED
+ * unless n_models == 3, (g0 + 1)(g1 + 1) <= 12800 and n_rec < 2^31. */
+int gs_grid_sweep_batched(const double* certainty, const uint8_t* correct,
+                          int64_t n_sets, int64_t n_rec, int32_t n_models,
+                          const double* grids, const int32_t* grid_len,
+                          const double* cost1, double* accuracy, double* mean_cost,
+                          double* forward_frac, void* stream);
 /* Score configs [config_begin, config_begin + config_count).  Any output
  * pointer may be NULL to skip it.  n_correct receives the integer correct
  * count (accuracy * n_rec) used by the exact Pareto reduction. */

@@ -80,6 +80,8 @@ _SIGNATURES = {
     "gs_jsonl_open": [ctypes.c_char_p, c_int32, POINTER(c_void_p), POINTER(gs_jsonl_info)],
     "gs_jsonl_read": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "gs_jsonl_close": [c_void_p],
+    "gs_grid_sweep_batched": [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p,
+                              POINTER(c_int32), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "gs_grid_eval": [c_int64, c_int32, POINTER(c_int32), c_void_p, c_int64, c_int64, c_void_p,
                      c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "gs_grid_decode": [c_int32, POINTER(c_int32), c_void_p, c_void_p, c_int64, c_void_p,

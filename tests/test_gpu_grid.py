@@ -413,3 +413,44 @@ def test_sorted_build_unaligned_inputs(n_rec):
         sm, thr, ns = oracle.grid_configs(grids)
         want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
         assert np.array_equal(b.evaluate().accuracy.cpu().numpy(), want[0])
+
+
+@pytest.mark.parametrize("n_rec,levels,ties", [(10_000, 100, False), (777, 12, True), (1, 3, False)])
+def test_batched_three_model_sweeps_match_single(n_rec, levels, ties):
+    """gs_grid_sweep_batched: each set's rows equal that set's own
+    GridSweep (one launch for every set, a CTA per set)."""
+    from paper_2406_14424_b200.gridsweep import GridSweep, sweep_batched
+    rng = np.random.default_rng(n_rec + levels)
+    sets = [_random_case(rng, n_rec, 3, levels, ties) for _ in range(5)]
+    # one grid-length triple for the batch: trim every set's grids to the shortest
+    glen = [min(len(s[2][j]) for s in sets) for j in range(3)]
+    grids = [[s[2][j][:glen[j]] for j in range(3)] for s in sets]
+    cost1 = sets[0][3]
+    cert = np.stack([s[0] for s in sets])
+    corr = np.stack([s[1] for s in sets])
+    res = sweep_batched(cert, corr, grids, cost1)
+    for i in range(len(sets)):
+        ref = GridSweep(cert[i], corr[i], grids[i], cost1).evaluate()
+        assert torch_equal(res.accuracy[i], ref.accuracy)
+        assert torch_equal(res.mean_cost[i], ref.mean_cost)
+        assert torch_equal(res.forward_frac[i], ref.forward_frac)
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
+
+
+def test_batched_sweep_config1_golden():
+    """Set 0 of a batch is config 1 (the reference's golden values)."""
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.gridsweep import sweep_batched
+    g = golden("config1.npz")
+    cert0, corr0 = synth.validation_matrices(3, 10_000, 0.8, 0)
+    cert1, corr1 = synth.validation_matrices(3, 10_000, 0.8, 1)
+    grids = [g["grid0"], g["grid1"], g["grid2"]]
+    res = sweep_batched(np.stack([cert0, cert1]), np.stack([corr0, corr1]), [grids, grids],
+                        g["cost1"])
+    assert np.array_equal(res.accuracy[0].cpu().numpy(), g["acc"])
+    assert np.array_equal(res.mean_cost[0].cpu().numpy(), g["cost"])
+    assert np.array_equal(res.forward_frac[0].cpu().numpy(), g["frac"])
