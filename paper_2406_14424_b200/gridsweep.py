@@ -360,51 +360,68 @@ def pareto_counts(n_correct: torch.Tensor, mean_cost: torch.Tensor, n_rec: int,
     return sc.kept[: int(sc.n_host[0])].clone()
 
 
+class BatchedSweep:
+    """Full grid sweeps of many three-model validation sets, one launch per
+    run() (gs_grid_sweep_batched): certainty [R, n, 3] f64, correct
+    [R, n, 3] u8, grids [R][3] per-set grids (each strictly increasing; the
+    three lengths shared by every set), cost1 [3].  run() fills [R, C]
+    accuracy / mean_cost and [R, C, 3] forward_frac, each row equal to that
+    set's GridSweep(...).evaluate() (config 1 stacked: the reference's CPU
+    default is launch-bound as one sweep).  The constructor does the host
+    work (validation, grid upload), so run() is one C call."""
+
+    def __init__(self, certainty, correct, grids, cost1):
+        self.cert = _lib.to_device(certainty, torch.float64)
+        self.corr = _lib.to_device(correct, torch.uint8)
+        if (self.cert.ndim != 3 or self.cert.shape[2] != 3
+                or tuple(self.corr.shape) != tuple(self.cert.shape)):
+            raise ValueError("certainty and correct must both be [n_sets, n_records, 3]")
+        self.n_sets, self.n_rec = int(self.cert.shape[0]), int(self.cert.shape[1])
+        if len(grids) != self.n_sets:
+            raise ValueError(f"need {self.n_sets} grid triples, got {len(grids)}")
+        glen = None
+        flat = []
+        for s_idx, triple in enumerate(grids):
+            if len(triple) != 3:
+                raise ValueError(f"set {s_idx}: need 3 grids")
+            lens = []
+            for j, g in enumerate(triple):
+                g = np.asarray(g.cpu() if isinstance(g, torch.Tensor) else g, dtype=np.float64)
+                if g.ndim != 1 or g.size == 0 or np.any(np.diff(g) <= 0):
+                    raise ValueError(f"set {s_idx} grid {j} must be a non-empty strictly "
+                                     "increasing 1-D array")
+                lens.append(int(g.size))
+                flat.append(g)
+            if glen is None:
+                glen = lens
+            elif lens != glen:
+                raise ValueError("every set's grids must have the same lengths")
+        self.grid_len = glen
+        self._glen = _lib.int32_array(glen)
+        self.grids = _lib.to_device(np.concatenate(flat), torch.float64)
+        self.cost1 = _lib.to_device(np.asarray(cost1, dtype=np.float64), torch.float64)
+        if self.cost1.numel() != 3:
+            raise ValueError("cost1 must have 3 entries")
+        g0, g1, _ = glen
+        self.n_configs = 3 + 2 * g0 + g1 + g0 * g1
+        dev = self.cert.device
+        self.out = SweepResult(
+            accuracy=torch.empty((self.n_sets, self.n_configs), dtype=torch.float64, device=dev),
+            mean_cost=torch.empty((self.n_sets, self.n_configs), dtype=torch.float64, device=dev),
+            forward_frac=torch.empty((self.n_sets, self.n_configs, 3), dtype=torch.float64,
+                                     device=dev),
+            n_correct=None, config_begin=0)
+
+    def run(self) -> SweepResult:
+        o = self.out
+        rc = _lib.load().gs_grid_sweep_batched(
+            self.cert.data_ptr(), self.corr.data_ptr(), self.n_sets, self.n_rec, 3,
+            self.grids.data_ptr(), self._glen, self.cost1.data_ptr(), o.accuracy.data_ptr(),
+            o.mean_cost.data_ptr(), o.forward_frac.data_ptr(), _lib.stream_ptr())
+        _lib.check(rc, "batched grid sweep")
+        return o
+
+
 def sweep_batched(certainty, correct, grids, cost1) -> SweepResult:
-    """Full grid sweeps of many three-model validation sets in one launch
-    (gs_grid_sweep_batched): certainty [R, n, 3] f64, correct [R, n, 3] u8,
-    grids [R, 3] per-set grids (each strictly increasing; the three lengths
-    shared by every set), cost1 [3].  Returns [R, C] accuracy / mean_cost and
-    [R, C, 3] forward_frac, each row equal to GridSweep(...).evaluate() of
-    that set (config 1 stacked: the reference's CPU default is launch-bound
-    as one sweep)."""
-    cert = _lib.to_device(certainty, torch.float64)
-    corr = _lib.to_device(correct, torch.uint8)
-    if cert.ndim != 3 or cert.shape[2] != 3 or tuple(corr.shape) != tuple(cert.shape):
-        raise ValueError("certainty and correct must both be [n_sets, n_records, 3]")
-    n_sets, n_rec = int(cert.shape[0]), int(cert.shape[1])
-    if len(grids) != n_sets:
-        raise ValueError(f"need {n_sets} grid triples, got {len(grids)}")
-    glen = None
-    flat = []
-    for s_idx, triple in enumerate(grids):
-        if len(triple) != 3:
-            raise ValueError(f"set {s_idx}: need 3 grids")
-        lens = []
-        for j, g in enumerate(triple):
-            g = np.asarray(g.cpu() if isinstance(g, torch.Tensor) else g, dtype=np.float64)
-            if g.ndim != 1 or g.size == 0 or np.any(np.diff(g) <= 0):
-                raise ValueError(f"set {s_idx} grid {j} must be a non-empty strictly increasing 1-D array")
-            lens.append(int(g.size))
-            flat.append(g)
-        if glen is None:
-            glen = lens
-        elif lens != glen:
-            raise ValueError("every set's grids must have the same lengths")
-    g_dev = _lib.to_device(np.concatenate(flat), torch.float64)
-    c_dev = _lib.to_device(np.asarray(cost1, dtype=np.float64), torch.float64)
-    if c_dev.numel() != 3:
-        raise ValueError("cost1 must have 3 entries")
-    g0, g1, _ = glen
-    n_cfg = 3 + 2 * g0 + g1 + g0 * g1
-    dev = cert.device
-    acc = torch.empty((n_sets, n_cfg), dtype=torch.float64, device=dev)
-    cost = torch.empty((n_sets, n_cfg), dtype=torch.float64, device=dev)
-    frac = torch.empty((n_sets, n_cfg, 3), dtype=torch.float64, device=dev)
-    rc = _lib.load().gs_grid_sweep_batched(cert.data_ptr(), corr.data_ptr(), n_sets, n_rec, 3,
-                                           g_dev.data_ptr(), _lib.int32_array(glen),
-                                           c_dev.data_ptr(), acc.data_ptr(), cost.data_ptr(),
-                                           frac.data_ptr(), _lib.stream_ptr())
-    _lib.check(rc, "batched grid sweep")
-    return SweepResult(accuracy=acc, mean_cost=cost, forward_frac=frac, n_correct=None,
-                       config_begin=0)
+    """BatchedSweep(...).run(): every set's full sweep in one launch."""
+    return BatchedSweep(certainty, correct, grids, cost1).run()

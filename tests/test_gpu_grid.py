@@ -415,10 +415,12 @@ def test_sorted_build_unaligned_inputs(n_rec):
         assert np.array_equal(b.evaluate().accuracy.cpu().numpy(), want[0])
 
 
-@pytest.mark.parametrize("n_rec,levels,ties", [(10_000, 100, False), (777, 12, True), (1, 3, False)])
+@pytest.mark.parametrize("n_rec,levels,ties", [(10_000, 100, False), (777, 12, True), (1, 3, False),
+                                              (70_000, 20, True)])
 def test_batched_three_model_sweeps_match_single(n_rec, levels, ties):
     """gs_grid_sweep_batched: each set's rows equal that set's own
-    GridSweep (one launch for every set, a CTA per set)."""
+    GridSweep (one launch for every set, a CTA per set; 16-bit packed
+    counters below 2^16 records, 32-bit ones from there)."""
     from paper_2406_14424_b200.gridsweep import GridSweep, sweep_batched
     rng = np.random.default_rng(n_rec + levels)
     sets = [_random_case(rng, n_rec, 3, levels, ties) for _ in range(5)]
