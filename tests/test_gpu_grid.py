@@ -277,7 +277,9 @@ def test_streamed_build_rejects_general_path():
 
 
 @pytest.mark.parametrize("glen", [(150, 40, 120, 10), (60, 300, 64, 5), (255, 3, 200, 2),
-                                  (150, 3, 200, 2), (10, 150, 5), (40, 250, 3)])
+                                  (150, 3, 200, 2), (10, 150, 5), (40, 250, 3),
+                                  (6, 1000, 9, 3), (6, 1500, 9, 3), (3, 14, 9, 3),
+                                  (30, 30, 30, 30, 30)])
 def test_four_model_large_uneven_grids(glen):
     """Grids near and past the fast path's shared-memory bounds (the plan
     falls back to the general path past them), and general-path slabs wide
@@ -291,7 +293,7 @@ def test_four_model_large_uneven_grids(glen):
     cert = rng.random((n, m))
     corr = (rng.random((n, m)) < 0.6).astype(np.uint8)
     grids = [np.concatenate([[0.0], np.sort(rng.random(g - 1))]) for g in glen]
-    cost1 = np.array([1.0, 3.0, 9.0, 27.0])[:m]
+    cost1 = np.array([1.0, 3.0, 9.0, 27.0, 81.0])[:m]
     sw = GridSweep(cert, corr, grids, cost1)
     res = sw.evaluate(n_correct=True)
     pick = []
