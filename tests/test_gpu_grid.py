@@ -458,3 +458,25 @@ def test_batched_sweep_config1_golden():
     assert np.array_equal(res.accuracy[0].cpu().numpy(), g["acc"])
     assert np.array_equal(res.mean_cost[0].cpu().numpy(), g["cost"])
     assert np.array_equal(res.forward_frac[0].cpu().numpy(), g["frac"])
+
+
+def test_sorted_build_near_record_limit():
+    """2M records (just under the packed fields' 2^21): the sort's record
+    ranges no longer leave room for the cp.async ring, so the register path
+    runs; tables equal the histogram build's."""
+    import torch
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    rng = np.random.default_rng(21)
+    n = 2_000_000
+    cert, corr, grids, cost1 = _random_case(rng, n, 4, 20)
+    sw = GridSweep(cert, corr, grids, cost1, build=False)
+    assert sw.info.fast_path == 2
+    sw.build()
+    a = sw.evaluate(n_correct=True)
+    sw.build_streamed(torch.from_numpy(cert).pin_memory(), torch.from_numpy(corr).pin_memory(),
+                      chunks=2)
+    _equal_results(sw.evaluate(n_correct=True), a)
+    pick = np.sort(rng.choice(sw.n_configs, size=12, replace=False))
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1, n_threads=8)
+    assert np.array_equal(a.accuracy.cpu().numpy()[pick], want[0])
