@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   __shared__ uint32_t s_c0[kMaxDim4];
   __shared__ uint32_t s_wsum[32];
   const int n_grid = a.glen[0] + a.glen[1] + a.glen[2];
-  void* s_lut = s_grid + n_grid;                       // [3][kLutBuckets] entries
+  void* s_lut = s_grid + ((n_grid + 1) & ~1);           // [3][kLutBuckets] entries (16 B aligned)
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(s_lut) + 3 * kLutBuckets * kLutEntryBytes);  // [nb]
   uint32_t* s_key = s_cnt + ((a.nb + 3) & ~3);        // [per]
   uint32_t* s_sorted = s_key + a.per;                 // [per]
@@ -518,12 +518,13 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
     const uint32_t b0 = (uint32_t)bt.bin(0, x0);
     const uint32_t b1 = (uint32_t)bt.bin(1, x1);
     const uint32_t b2 = (uint32_t)bt.bin(2, x2);
+    // bit 29: model 0's correct bit, counted per b0 in the scatter (one
+    // shared atomic less in the streaming loop); the gather ignores it
     const uint32_t key = b0 | (b2 << 8) | ((k & 0xff00u) ? 1u << 16 : 0u) |
                          ((k & 0xff0000u) ? 1u << 17 : 0u) | ((k & 0xff000000u) ? 1u << 18 : 0u) |
-                         (b1 << 19);
+                         (b1 << 19) | ((k & 0xffu) ? 1u << 29 : 0u);
     atomicAdd(s_cnt + b1, 1u);  // count only: the rank is taken in the scatter
     s_key[i] = key;
-    if (k & 0xffu) atomicAdd(s_c0 + b0, 1u);
   };
   if (RING) {
     int slot = 0;
@@ -593,12 +594,21 @@ __global__ void __launch_bounds__(kSortThreads, 1) g4_sort_kernel(const __grid_c
   phase(0, 4);
   for (int i = tid; i < cnt; i += kSortThreads) {
     const uint32_t key = s_key[i];
-    s_sorted[atomicAdd(s_cnt + (key >> 19), 1u)] = key;
+    s_sorted[atomicAdd(s_cnt + ((key >> 19) & 1023u), 1u)] = key;
+    if (key & (1u << 29)) atomicAdd(s_c0 + (key & 255u), 1u);
   }
+  fence_proxy_async();  // the scattered keys are read next by the async proxy
   __syncthreads();
-  for (int i = tid; i < cnt; i += kSortThreads) a.keys[r0 + i] = s_sorted[i];
+  // the range's keys leave by one bulk copy (16-byte multiple) plus a tail
+  const int bulk = cnt & ~3;
+  if (tid == 0 && bulk > 0) {
+    bulk_s2g(a.keys + r0, s_sorted, (uint32_t)bulk * 4u);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  for (int i = bulk + tid; i < cnt; i += kSortThreads) a.keys[r0 + i] = s_sorted[i];
   for (int i = tid; i < a.d0; i += kSortThreads)
     if (s_c0[i]) atomicAdd(a.G0 + i, s_c0[i]);
+  if (tid == 0 && bulk > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   phase(0, 5);
 }
 
@@ -1166,7 +1176,7 @@ SortPlan sort_plan(const Grid4Layout& L, const int32_t* glen, int64_t n_rec) {
   sp.parts = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), (n_rec + kSortThreads - 1) / kSortThreads));
   sp.per = (int)(((n_rec + sp.parts - 1) / sp.parts + 31) & ~31ll);
   sp.parts = (int)((n_rec + sp.per - 1) / sp.per);
-  sp.sort_smem = (size_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * kLutEntryBytes +
+  sp.sort_smem = (size_t)((glen[0] + glen[1] + glen[2] + 1) & ~1) * 8 + 3 * kLutBuckets * kLutEntryBytes +
                  (size_t)((L.nb + 3) & ~3) * 4 + (size_t)sp.per * 8;
   sp.off_ring = (int)round_up(sp.sort_smem, 128);
   const size_t ring_bytes = (size_t)kRing * kSortThreads * 36;
