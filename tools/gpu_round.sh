@@ -13,7 +13,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:stag
 python tools/traffic.py gpurun_out/traffic_$TAG.json gpurun_out/full_$TAG.ncu-rep gpurun_out/stage_$TAG.ncu-rep > /dev/null 2>&1 && cp gpurun_out/traffic_$TAG.json profiles/r1_traffic.json
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$TAG.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_bench_$TAG.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --skip-config1 > gpurun_out/ncu_bench_$TAG.log 2>&1
 timeout 300 python tools/phase_probe.py > gpurun_out/phase_$TAG.txt 2>&1
 timeout 300 python tools/e2e_probe.py > gpurun_out/e2e_$TAG.txt 2>&1
 timeout 300 python tools/launch_probe.py > gpurun_out/launch_probe_$TAG.txt 2>&1
