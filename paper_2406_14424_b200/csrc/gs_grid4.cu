@@ -1129,6 +1129,33 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THR
   const int64_t row_base =
       (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + wc - a.cfg_begin;
   const int r_end = min(w_hi, g1 - rb);
+  if (ALL && full && !a.n_correct) {
+    // the usual sweep: every output of the slab requested, the configs of
+    // consecutive rows g2 apart -- walk three output pointers
+    const int64_t i0 = row_base + (int64_t)(rb + w_lo) * g2;
+    double* pf = a.frac + i0 * 4;
+    double* pc = a.cost + i0;
+    double* pa = a.acc + i0;
+    for (int r = w_lo; r < r_end; ++r) {
+      P += s_slab[(size_t)r * d2p + wc];
+      const Cell3 p = unpack3(P);
+      const double f3 = div_count((double)p.cnt, n, rcp);
+      const double rf = s_rowf[r];
+      const double mean = dadd(s_rowm[r], dmul(f3, c3c));
+      const uint32_t correct = s_rowc[r] - p.c2 + p.c3;
+      if (!any0)
+        st_v4_f64(pf, one, f1, rf, f3);
+      else
+        st_v4_f64(pf, one, rf, f3, 0.0);
+      *pc = mean;
+      *pa = div_count((double)correct, n, rcp);
+      pf += 4 * (int64_t)g2;
+      pc += g2;
+      pa += g2;
+    }
+    phase(2, 5);
+    return;
+  }
   for (int r = w_lo; r < r_end; ++r) {
     P += s_slab[(size_t)r * d2p + wc];
     const int64_t i = row_base + (int64_t)(rb + r) * g2;
