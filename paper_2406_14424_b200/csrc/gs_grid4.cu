@@ -812,11 +812,14 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
   if (live) {
     unsigned long long P = 0;
     for (int p = 0; p < s; ++p) P += s_seg[p * d2 + c];
-    unsigned long long* S = a.S + (int64_t)b1 * a.d2p + c;
     const int64_t plane = (int64_t)a.d1 * a.d2p;
-    for (int r = r_lo; r < r_hi; ++r) {
-      P += s_pl[(size_t)r * hp + c];
-      S[(int64_t)r * plane] = P;
+    unsigned long long* dst = a.S + (int64_t)b1 * a.d2p + c + (int64_t)r_lo * plane;
+    const unsigned long long* src = s_pl + (size_t)r_lo * hp + c;
+    for (int r = r_lo; r < r_hi; ++r) {  // pointers stepped, no per-row index math
+      P += *src;
+      *dst = P;
+      src += hp;
+      dst += plane;
     }
   }
   // the eval is released only once every plane is written: launched
