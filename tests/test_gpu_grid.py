@@ -480,3 +480,22 @@ def test_sorted_build_near_record_limit():
     sm, thr, ns = oracle.grid_configs(grids)
     want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1, n_threads=8)
     assert np.array_equal(a.accuracy.cpu().numpy()[pick], want[0])
+
+
+def test_batched_sweep_rejects_bad_input():
+    from paper_2406_14424_b200.gridsweep import BatchedSweep
+    rng = np.random.default_rng(2)
+    cert = rng.random((2, 50, 3))
+    corr = (rng.random((2, 50, 3)) < 0.5).astype(np.uint8)
+    g = [np.array([0.0, 0.5]), np.array([0.0, 0.3, 0.6]), np.array([0.0])]
+    cost1 = [1.0, 2.0, 3.0]
+    with pytest.raises(ValueError):  # one grid triple for two sets
+        BatchedSweep(cert, corr, [g], cost1)
+    with pytest.raises(ValueError):  # lengths differ between sets
+        BatchedSweep(cert, corr, [g, [g[0], g[1][:2], g[2]]], cost1)
+    with pytest.raises(ValueError):  # not increasing
+        BatchedSweep(cert, corr, [g, [g[0][::-1], g[1], g[2]]], cost1)
+    with pytest.raises(ValueError):  # four models
+        BatchedSweep(rng.random((2, 50, 4)), np.zeros((2, 50, 4), np.uint8), [g, g], cost1)
+    res = BatchedSweep(cert, corr, [g, g], cost1).run()
+    assert tuple(res.accuracy.shape) == (2, 3 + 2 * 2 + 3 + 2 * 3)
