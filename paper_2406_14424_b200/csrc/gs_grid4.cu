@@ -4,35 +4,35 @@
 // Same algorithm and outputs as the general path in gs_sweep.cu (dominance
 // counting over the bins b_j of the threshold grids, scored exactly like
 // _evaluate_numba, /root/reference/pkg/src/gearserve/kernels.py:39-62), laid
-// out as three launches with no table pass that does not also do useful
-// arithmetic:
+// out as three launches.  A one-shot build (gs_grid_build):
 //
-//   g4_hist    one pass over the records: per record ONE 16-byte reduction
-//              (red.global.add.v4.f32, exact for counts < 2^24) of {1, k3,
-//              k2, k1} into H[b0][b1][b2], and model 0's correct bit into a
-//              per-CTA shared-memory row over b0 (c0 is only ever read where
-//              b1 and b2 are "any").  On B200 a v4 reduction costs the same
-//              as a scalar one (tools/micro_red.cu: 8.35 us per 1M into a
-//              1M-cell table), while a second reduction into a small hot
-//              table costs ~14 us more: one L2 operation per record is the
-//              design constraint.
-//   g4_plane   one CTA per b1: the (b0, b2) plane of H arrives by TMA bulk
-//              copies, is prefix-summed along b2 (a warp per row) and along
-//              b0 (thread per (b2 column, row segment)) in shared memory, and
-//              leaves as packed u64 {cnt, c3, c2} (21-bit fields, exact for
-//              n_rec < 2^21) plus R1[b0][b1] = the c1 channel at b2 = any.
-//              It re-zeroes H for the next build and turns the c0 row into
-//              its inclusive prefix P0.
-//   g4_eval    one CTA per (b0 slab k0, column part): the slab (already
-//              prefixed along b0 and b2) arrives by one TMA bulk copy; a
-//              column walk along b1 (thread per (b2 column, row segment))
-//              finishes the prefix and scores each position (k1, k2) as the
-//              full cascade's config (k0, k1, k2).  Row-shared terms (the
-//              stage-2 fraction, the partial mean cost, the partial correct
-//              count) are computed once per row.  The same walk scores every
-//              structure that starts with model 0 at threshold k0 (their
-//              cells are the slab's last row / column), and the "any" slab
-//              k0 = g0 scores every structure without model 0.
+//   g4_sort    one pass over the records (148 CTAs, a contiguous range each,
+//              streamed through a cp.async shared-memory ring): bins by
+//              per-CTA bucket tables, each record a 4-byte key {b0, b2, k1,
+//              k2, k3, b1, k0}, counting-sorted by b1 in shared memory; one
+//              bulk copy of the range's keys and its bucket offsets out.
+//   g4_gather  one CTA per b1: the bucket's key segments of every range,
+//              counted into the (b0, b2) plane in shared memory (16-bit
+//              packed counters, 32-bit atomics), prefixed along b2 and b0 and
+//              written as packed u64 {cnt, c3, c2} (21-bit fields, exact for
+//              n_rec < 2^21) plus R1[b0][b1] (the c1 channel at b2 = any) and
+//              the prefix P0 of model 0's correct counts per b0.
+//
+// The streamed build (gs_grid_accumulate / gs_grid_finish, and shapes the
+// sorted plan does not fit) uses g4_hist (one red.global.add.v4.f32 of
+// {1, k3, k2, k1} per record into H[b1][b0][b2]) and g4_plane (the same
+// plane prefix from H, re-zeroing it).  Both leave the same S / R1 / P0.
+//
+//   g4_eval    a cluster of CTAs per b0 slab k0, split along b1: each
+//              bulk-copies its rows of S[k0], exchanges column sums through
+//              distributed shared memory (the b1 carry), then a column walk
+//              along b1 finishes the prefix and scores each position
+//              (k1, k2) as the full cascade's config (k0, k1, k2), with
+//              row-shared terms (the stage-2 fraction, the partial mean cost,
+//              the partial correct count) once per row.  Spare threads score
+//              every structure that starts with model 0 at threshold k0
+//              (their cells are the slab's last row / column), and the "any"
+//              slab k0 = g0 scores every structure without model 0.
 //
 // Channels at a position (p0, p1, p2), "g" meaning any:
 //   cnt(p)  records with b0 <= p0, b1 <= p1, b2 <= p2
