@@ -264,7 +264,9 @@ def run_ours(args, world, rank, local):
                                        n_threads=os.cpu_count() or 1)
         got_acc = out.accuracy.cpu().numpy()[pick]
         got_cost = out.mean_cost.cpu().numpy()[pick]
-        check = bool(np.array_equal(got_acc, want[0]) and np.array_equal(got_cost, want[1]))
+        got_frac = out.forward_frac.cpu().numpy()[pick]
+        check = bool(np.array_equal(got_acc, want[0]) and np.array_equal(got_cost, want[1])
+                     and np.array_equal(got_frac, want[2]))
 
     # ---- e2e through the public API from host buffers (+ front all-gather)
     pin_cert = torch.from_numpy(cert).pin_memory()

@@ -228,6 +228,22 @@ int gs_stage_gate(const double* certainty, const uint8_t* correct,
                   int64_t* n_near, void* workspace, size_t workspace_bytes,
                   void* stream);
 
+/* The same gate for one small online batch (EngineState.finish_batch on a
+ * batch of <= max_profiled_batch items, src/engine.py:355-383) as ONE call:
+ * one H2D of the packed items, the gate, one D2H of the packed outcome.
+ *   host_in  (pinned) {row i64[n], thr f64[n], model i32[n], is_last u8[n]}
+ *   host_out (pinned) {n_deferred i64, n_near i64, stop u8[n], correct u8[n],
+ *                      pad to 8, near i64[n]}
+ *   dev_buf  device scratch of gs_stage_gate_packed_bytes(n).dev_bytes
+ *   sync     != 0: cudaStreamSynchronize before returning (host_out valid) */
+int gs_stage_gate_packed_bytes(int64_t n_items, size_t* host_in_bytes,
+                               size_t* host_out_bytes, size_t* dev_bytes);
+int gs_stage_gate_packed(const double* certainty, const uint8_t* correct,
+                         int64_t n_rec, int32_t n_models, const void* host_in,
+                         int64_t n_items, double near_eps, void* host_out,
+                         void* dev_buf, size_t dev_bytes, int32_t sync,
+                         void* stream);
+
 /* ------------------------------------------------------------------------
  * Threshold-grid quantiles on the device: np.quantile(column, qs) with
  * numpy's default "linear" method, bit-exact (cascades.build_threshold_grid,

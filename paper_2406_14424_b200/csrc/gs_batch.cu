@@ -242,14 +242,9 @@ extern "C" int gs_grid_sweep_batched(const double* certainty, const uint8_t* cor
   if (g0 + g1 > 2 * 1024) return GS_EUNSUPPORTED;
   const bool packed = n_rec < 65536;
   const size_t smem = (size_t)cells * (packed ? 8 : 16) + (size_t)(g0 + g1) * 8;
-  static std::atomic<bool> attr{false};
-  if (!attr.load(std::memory_order_acquire)) {
-    GS_CUDA_TRY(cudaFuncSetAttribute(batch3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(kBatchMaxCells * 16 + 2 * 1024 * 8)));
-    GS_CUDA_TRY(cudaFuncSetAttribute(batch3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(kBatchMaxCells * 8 + 2 * 1024 * 8)));
-    attr.store(true, std::memory_order_release);
-  }
+  static SmemAttr attr_wide, attr_packed;
+  GS_CUDA_TRY(ensure_smem(batch3_kernel<false>, attr_wide, (size_t)(kBatchMaxCells * 16 + 2 * 1024 * 8)));
+  GS_CUDA_TRY(ensure_smem(batch3_kernel<true>, attr_packed, (size_t)(kBatchMaxCells * 8 + 2 * 1024 * 8)));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (packed)
     batch3_kernel<true><<<(unsigned)n_sets, kBatchThreads, smem, st>>>(a);

@@ -9,15 +9,21 @@ static thread_local const char* t_last_cuda_error = "no error";
 
 void set_cuda_error(cudaError_t e) { t_last_cuda_error = cudaGetErrorString(e); }
 
-int sm_count() {
-  static std::atomic<int> cached{0};
-  int v = cached.load(std::memory_order_relaxed);
-  if (v > 0) return v;
+int current_device() {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  return dev;
+}
+
+int sm_count() {
+  static std::atomic<int> cached[kMaxDevices];  // per device, 0 = not read yet
+  const int dev = current_device();
+  std::atomic<int>* slot = dev < kMaxDevices ? &cached[dev] : nullptr;
+  int v = slot ? slot->load(std::memory_order_relaxed) : 0;
+  if (v > 0) return v;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
     v = 148;
-  cached.store(v, std::memory_order_relaxed);
+  if (slot) slot->store(v, std::memory_order_relaxed);
   return v;
 }
 

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/gearserve_b200.h"
 
 namespace gs {
@@ -39,9 +41,38 @@ __host__ __device__ inline bool aligned16(const void* p) {
 
 inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Number of SMs of the current device (cached per process; read-only after
-// first use, so safe to call from any thread).
+// Devices a process can drive through this library (one process may use
+// several GPUs, e.g. one executor thread per device: src/serving.py:121-139).
+constexpr int kMaxDevices = 64;
+
+// Ordinal of the calling thread's current device (0 if it cannot be read).
+int current_device();
+
+// Number of SMs of the current device (cached per device; safe to call from
+// any thread).
 int sm_count();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current
+// device only, so the "already set" high-water mark is kept per device: a
+// kernel first launched on device 1 gets its attribute there too.  Once set
+// for a size, later calls (e.g. inside a CUDA-graph capture) issue nothing.
+struct SmemAttr {
+  std::atomic<int> bytes[kMaxDevices];  // zero-initialised (static storage)
+};
+
+template <typename Kernel>
+cudaError_t ensure_smem(Kernel k, SmemAttr& attr, size_t bytes) {
+  const int dev = current_device();
+  std::atomic<int>& slot = attr.bytes[(dev >= 0 && dev < kMaxDevices) ? dev : 0];
+  if ((int)bytes <= slot.load(std::memory_order_acquire) && dev < kMaxDevices) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && dev < kMaxDevices) {
+    int cur = slot.load(std::memory_order_relaxed);
+    while ((int)bytes > cur && !slot.compare_exchange_weak(cur, (int)bytes)) {
+    }
+  }
+  return e;
+}
 
 // ------------------------------------------------------------ f64 epilogue --
 // Explicit round-to-nearest intrinsics so nvcc cannot fuse a*b+c into a DFMA.
@@ -217,7 +248,8 @@ __device__ __forceinline__ PairScan block_pair_scan(bool a, bool b, uint64_t* st
       s_warp[32 + lane] = ib - cb;
     }
     const uint64_t agg = (uint64_t)ta | ((uint64_t)tb << 31);
-    const uint64_t excl = lookback_exclusive(states, tile, agg);
+    // states == nullptr: a single-tile launch, nothing before it
+    const uint64_t excl = states ? lookback_exclusive(states, tile, agg) : 0;
     if (lane == 0) {
       s_misc[0] = excl & kLbFieldMask;
       s_misc[1] = (excl >> 31) & kLbFieldMask;
@@ -237,7 +269,9 @@ __device__ __forceinline__ PairScan block_pair_scan(bool a, bool b, uint64_t* st
 
 // Dynamic tile id (guarantees every predecessor tile has started, so the
 // look-back cannot deadlock).  One thread takes it, the block reads it.
+// counter == nullptr: a single-tile launch (tile 0, no workspace).
 __device__ __forceinline__ int64_t next_tile_id(unsigned long long* counter, int64_t* s_tile) {
+  if (counter == nullptr) return 0;
   if (threadIdx.x == 0) *s_tile = (int64_t)atomicAdd(counter, 1ull);
   __syncthreads();
   return *s_tile;

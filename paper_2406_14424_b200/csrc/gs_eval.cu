@@ -201,12 +201,9 @@ __global__ void eval_finalize_kernel(const uint32_t* counts, const int32_t* stag
 template <int MAXL>
 cudaError_t launch_eval(const EvalArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   auto k = eval_list_kernel<MAXL>;
-  static std::atomic<int> smem_set{0};
-  if ((int)smem > smem_set.load()) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    smem_set.store((int)smem);
-  }
+  static SmemAttr smem_set;
+  cudaError_t e = ensure_smem(k, smem_set, smem);
+  if (e != cudaSuccess) return e;
   k<<<grid, kEvalThreads, smem, st>>>(a);
   return cudaGetLastError();
 }

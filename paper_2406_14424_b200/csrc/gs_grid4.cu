@@ -114,13 +114,6 @@ cudaError_t launch_pdl(Kernel k, unsigned grid, unsigned block, size_t smem, cud
   return cudaLaunchKernelEx(&cfg, k, args);
 }
 
-template <typename Kernel>
-cudaError_t ensure_smem4(Kernel k, std::atomic<int>& done, size_t bytes) {
-  if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) done.store((int)bytes, std::memory_order_release);
-  return e;
-}
 
 // ------------------------------------------------------------------ hist --
 constexpr int kHist4Threads = 1024;
@@ -1273,8 +1266,8 @@ cudaError_t grid4_accumulate(const double* cert, const uint8_t* corr, int64_t n_
   h.counters = reinterpret_cast<uint32_t*>(ws + L.offCnt);
   const size_t smem =
       (size_t)(glen[0] + glen[1] + glen[2]) * sizeof(double) + 3 * kLutBuckets * kLutEntryBytes;
-  static std::atomic<int> smem_hist{0};
-  cudaError_t e = ensure_smem4(g4_hist_kernel, smem_hist, smem);
+  static SmemAttr smem_hist;
+  cudaError_t e = ensure_smem(g4_hist_kernel, smem_hist, smem);
   if (e != cudaSuccess) return e;
   if (n_chunk == 0) return cudaSuccess;
   int64_t blocks = (n_chunk + kHist4Chunk - 1) / kHist4Chunk;
@@ -1309,8 +1302,8 @@ cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
   p.seg0 = (p.half + p.ns0 - 1) / p.ns0;
   p.ns0 = (p.half + p.seg0 - 1) / p.seg0;
   const size_t psmem = ((size_t)p.half * p.hp + kPlaneThreads + L.d2) * 16 + kZeroBytes;
-  static std::atomic<int> smem_plane{0};
-  e = ensure_smem4(g4_plane_kernel, smem_plane, (size_t)kGrid4SlabMax);
+  static SmemAttr smem_plane;
+  e = ensure_smem(g4_plane_kernel, smem_plane, (size_t)kGrid4SlabMax);
   if (e != cudaSuccess) return e;
   return launch_pdl(g4_plane_kernel, (unsigned)(2 * L.d1), kPlaneThreads, psmem, st, p);
 }
@@ -1348,20 +1341,20 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   a.keys = keys;
   a.off = off;
   a.G0 = G0;
-  static std::atomic<int> smem_sort{0}, smem_sort_r{0}, smem_sort_s{0}, smem_gather{0};
+  static SmemAttr smem_sort, smem_sort_r, smem_sort_s, smem_gather;
   a.off_ring = sp.off_ring;
   // the ring's cp.async copies want 16-byte aligned rows and 4-byte correct words
   const bool ring = sp.ring && a.vec_ok;
   const size_t smem = ring ? sp.sort_smem : (size_t)sp.off_ring;
   if (!(passes & 1)) {
   } else if (ring) {
-    if ((e = ensure_smem4(g4_sort_kernel<true, true>, smem_sort_r, kSortSmemMax)) != cudaSuccess) return e;
+    if ((e = ensure_smem(g4_sort_kernel<true, true>, smem_sort_r, kSortSmemMax)) != cudaSuccess) return e;
     g4_sort_kernel<true, true><<<(unsigned)sp.parts, kSortThreads, smem, st>>>(a);
   } else if (a.vec_ok) {
-    if ((e = ensure_smem4(g4_sort_kernel<true, false>, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
+    if ((e = ensure_smem(g4_sort_kernel<true, false>, smem_sort, kSortSmemMax)) != cudaSuccess) return e;
     g4_sort_kernel<true, false><<<(unsigned)sp.parts, kSortThreads, smem, st>>>(a);
   } else {
-    if ((e = ensure_smem4(g4_sort_kernel<false, false>, smem_sort_s, kSortSmemMax)) != cudaSuccess) return e;
+    if ((e = ensure_smem(g4_sort_kernel<false, false>, smem_sort_s, kSortSmemMax)) != cudaSuccess) return e;
     g4_sort_kernel<false, false><<<(unsigned)sp.parts, kSortThreads, smem, st>>>(a);
   }
   if ((e = cudaGetLastError()) != cudaSuccess || !(passes & 2)) return e;
@@ -1387,7 +1380,7 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   g.ns0 = std::max(1, std::min(kGatherThreads / L.d2, L.d0));
   g.seg0 = (L.d0 + g.ns0 - 1) / g.ns0;
   g.ns0 = (L.d0 + g.seg0 - 1) / g.seg0;
-  if ((e = ensure_smem4(g4_gather_kernel, smem_gather, (size_t)kGrid4SlabMax)) != cudaSuccess) return e;
+  if ((e = ensure_smem(g4_gather_kernel, smem_gather, (size_t)kGrid4SlabMax)) != cudaSuccess) return e;
   return launch_pdl(g4_gather_kernel, (unsigned)L.d1, kGatherThreads, sp.gather_smem, st, g);
 }
 
@@ -1414,8 +1407,8 @@ template <bool ALL, int THREADS, int CL>
 cudaError_t launch_eval(G4EvalArgs a, const Grid4Layout& L, cudaStream_t st) {
   eval_split<THREADS, CL>(a, L);
   const size_t smem = eval_smem<THREADS, CL>(a, L);
-  static std::atomic<int> done{0};
-  cudaError_t e = ensure_smem4(g4_eval_kernel<ALL, THREADS, CL>, done, (size_t)kGrid4SlabMax);
+  static SmemAttr done;
+  cudaError_t e = ensure_smem(g4_eval_kernel<ALL, THREADS, CL>, done, (size_t)kGrid4SlabMax);
   if (e != cudaSuccess) return e;
   return launch_pdl(g4_eval_kernel<ALL, THREADS, CL>, (unsigned)(CL * L.d0), THREADS, smem, st, a);
 }

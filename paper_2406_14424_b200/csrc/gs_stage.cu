@@ -627,9 +627,14 @@ extern "C" int gs_stage_step(const void* scores, int32_t dtype, int64_t n_rows, 
     return GS_OK;
   }
   GS_REQUIRE(scores && thr && deferred_idx);
-  const size_t need = step_ws_bytes(n_rows);
-  if (!workspace || workspace_bytes < need) return GS_EWORKSPACE;
-  GS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, st));
+  // one tile (<= 256 narrow rows, <= kWideTile wide rows) needs no tile
+  // counter or look-back states: no workspace memset
+  const bool single = n_rows <= (n_cls >= 32 ? (int64_t)kWideTile : (int64_t)kStepThreads);
+  if (!single) {
+    const size_t need = step_ws_bytes(n_rows);
+    if (!workspace || workspace_bytes < need) return GS_EWORKSPACE;
+    GS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, st));
+  }
   StepArgs a{};
   a.scores = scores;
   a.n_rows = n_rows;
@@ -648,8 +653,8 @@ extern "C" int gs_stage_step(const void* scores, int32_t dtype, int64_t n_rows, 
   a.payload_bytes = payload_row_bytes;
   a.next_payload = static_cast<uint8_t*>(next_payload);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  a.counter = reinterpret_cast<unsigned long long*>(ws);
-  a.states = reinterpret_cast<uint64_t*>(ws + 256);
+  a.counter = single ? nullptr : reinterpret_cast<unsigned long long*>(ws);
+  a.states = single ? nullptr : reinterpret_cast<uint64_t*>(ws + 256);
   cudaError_t e;
   switch (dtype) {
     case GS_F32: e = dispatch_step<float>(kind, a, st); break;
@@ -677,9 +682,12 @@ extern "C" int gs_stage_gate(const double* certainty, const uint8_t* correct, in
     return GS_OK;
   }
   GS_REQUIRE(certainty && correct && row && model && thr && deferred_idx);
-  const size_t need = step_ws_bytes(n_items);
-  if (!workspace || workspace_bytes < need) return GS_EWORKSPACE;
-  GS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, st));
+  const int64_t n_tiles = (n_items + 255) / 256;
+  if (n_tiles > 1) {  // one tile needs no tile counter or look-back states
+    const size_t need = step_ws_bytes(n_items);
+    if (!workspace || workspace_bytes < need) return GS_EWORKSPACE;
+    GS_CUDA_TRY(cudaMemsetAsync(workspace, 0, need, st));
+  }
   GateArgs a{};
   a.cert = certainty;
   a.corr = correct;
@@ -698,10 +706,66 @@ extern "C" int gs_stage_gate(const double* certainty, const uint8_t* correct, in
   a.near_idx = near_idx;
   a.n_near = n_near;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  a.counter = reinterpret_cast<unsigned long long*>(ws);
-  a.states = reinterpret_cast<uint64_t*>(ws + 256);
-  a.n_tiles = (n_items + 255) / 256;
+  a.counter = n_tiles > 1 ? reinterpret_cast<unsigned long long*>(ws) : nullptr;
+  a.states = n_tiles > 1 ? reinterpret_cast<uint64_t*>(ws + 256) : nullptr;
+  a.n_tiles = n_tiles;
   stage_gate_kernel<<<(unsigned)a.n_tiles, 256, 0, st>>>(a);
   GS_LAUNCH_CHECK();
+  return GS_OK;
+}
+
+// Packed small-batch gate (the online path: batches of 1-8 items,
+// src/synth.py:30): the batch's items arrive in ONE pinned host buffer
+// {row i64[n], thr f64[n], model i32[n], is_last u8[n]}, the outcome leaves
+// in ONE pinned host buffer {n_deferred i64, n_near i64, stop u8[n],
+// correct u8[n], (8-aligned) near i64[n]}: one H2D, one kernel, one D2H on
+// the caller's stream, then (sync != 0) a stream synchronize.  dev_buf holds
+// the device copies (gs_stage_gate_packed_bytes) and, for n > 256, the
+// look-back workspace.
+static size_t packed_in_bytes(int64_t n) { return (size_t)n * 21; }
+static size_t packed_out_bytes(int64_t n) { return round_up(16 + 2 * (size_t)n, 8) + 8 * (size_t)n; }
+
+extern "C" int gs_stage_gate_packed_bytes(int64_t n_items, size_t* host_in_bytes,
+                                          size_t* host_out_bytes, size_t* dev_bytes) {
+  GS_REQUIRE(n_items >= 0);
+  const size_t in = packed_in_bytes(n_items), out = packed_out_bytes(n_items);
+  if (host_in_bytes) *host_in_bytes = in;
+  if (host_out_bytes) *host_out_bytes = out;
+  if (dev_bytes)
+    *dev_bytes = round_up(in, 256) + round_up(out, 256) + round_up((size_t)n_items * 8 + 8, 256) +
+                 step_ws_bytes(n_items);
+  return GS_OK;
+}
+
+extern "C" int gs_stage_gate_packed(const double* certainty, const uint8_t* correct,
+                                    int64_t n_rec, int32_t n_models, const void* host_in,
+                                    int64_t n_items, double near_eps, void* host_out,
+                                    void* dev_buf, size_t dev_bytes, int32_t sync,
+                                    void* stream) {
+  GS_REQUIRE(n_items >= 0 && host_out);
+  size_t need = 0;
+  gs_stage_gate_packed_bytes(n_items, nullptr, nullptr, &need);
+  if (!dev_buf || dev_bytes < need) return GS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t in = packed_in_bytes(n_items), out = packed_out_bytes(n_items);
+  uint8_t* d_in = static_cast<uint8_t*>(dev_buf);
+  uint8_t* d_out = d_in + round_up(in, 256);
+  uint8_t* d_def = d_out + round_up(out, 256);
+  uint8_t* d_ws = d_def + round_up((size_t)n_items * 8 + 8, 256);
+  if (n_items > 0) {
+    GS_REQUIRE(host_in);
+    GS_CUDA_TRY(cudaMemcpyAsync(d_in, host_in, in, cudaMemcpyHostToDevice, st));
+  }
+  int64_t* counts = reinterpret_cast<int64_t*>(d_out);
+  const int64_t n = n_items;
+  const int rc = gs_stage_gate(
+      certainty, correct, n_rec, n_models, reinterpret_cast<const int64_t*>(d_in),
+      reinterpret_cast<const int32_t*>(d_in + 16 * n), reinterpret_cast<const double*>(d_in + 8 * n),
+      d_in + 20 * n, n, d_out + 16, d_out + 16 + n, reinterpret_cast<int64_t*>(d_def), counts,
+      near_eps, reinterpret_cast<int64_t*>(d_out + round_up(16 + 2 * (size_t)n, 8)), counts + 1, d_ws,
+      step_ws_bytes(n), stream);
+  if (rc != GS_OK) return rc;
+  GS_CUDA_TRY(cudaMemcpyAsync(host_out, d_out, out, cudaMemcpyDeviceToHost, st));
+  if (sync) GS_CUDA_TRY(cudaStreamSynchronize(st));
   return GS_OK;
 }

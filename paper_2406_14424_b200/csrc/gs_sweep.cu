@@ -172,13 +172,6 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size,
 // so later calls (e.g. inside a CUDA-graph capture) issue no attribute calls.
-template <typename Kernel>
-cudaError_t ensure_smem(Kernel k, std::atomic<int>& done, size_t bytes) {
-  if ((int)bytes <= done.load(std::memory_order_acquire)) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) done.store((int)bytes, std::memory_order_release);
-  return e;
-}
 
 // ------------------------------------------------------------------ hist --
 struct HistArgs {
@@ -1283,7 +1276,7 @@ cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStr
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 4));
   {
     auto k = grid_hist_kernel<M, Cell, 0>;
-    static std::atomic<int> smem_set{0};
+    static SmemAttr smem_set;
     cudaError_t e = ensure_smem(k, smem_set, smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)blocks, kHistThreads, smem, st>>>(h);
@@ -1292,7 +1285,7 @@ cudaError_t launch_hist_t(const HistArgs& h, int64_t n_rec, size_t smem, cudaStr
   }
   if (n_rec < 65536) return cudaSuccess;  // no cell can reach 2^16 records
   auto k = grid_hist_kernel<M, Cell, 1>;  // no-op unless a cell passed 0xFFFF records
-  static std::atomic<int> smem_set{0};
+  static SmemAttr smem_set;
   cudaError_t e = ensure_smem(k, smem_set, smem);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)std::min<int64_t>(blocks, sm_count()), kHistThreads, smem, st>>>(h);
@@ -1331,7 +1324,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     // split a slab across two CTAs when there are too few slabs to fill the GPU
     const int parts = (cols >= 64 && n_slabs < 2 * sm_count()) ? 2 : 1;
     const size_t smem = (size_t)rows * ((cols + parts - 1) / parts) * sizeof(uint4);
-    static std::atomic<int> smem_set{0};
+    static SmemAttr smem_set;
     cudaError_t e = ensure_smem(slab_first_kernel, smem_set, (size_t)kSlabSmemMax);
     if (e != cudaSuccess) return e;
     const int64_t blocks = std::min<int64_t>(n_slabs * parts, (int64_t)sm_count() * 4);
@@ -1379,7 +1372,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
       rowscan_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, T, outer, (int)len, from_f32);
     } else {
       const size_t smem = (size_t)kColChunk * kColTile * sizeof(uint4);
-      static std::atomic<int> smem_set{0};
+      static SmemAttr smem_set;
       cudaError_t e = ensure_smem(colscan_kernel, smem_set, smem);
       if (e != cudaSuccess) return e;
       const int64_t tiles = outer * ((inner + kColTile - 1) / kColTile);
@@ -1618,7 +1611,7 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
     w.n_correct = n_correct;
     w.tile = std::min(kWalkTile, w.d2);
     const size_t smem = (size_t)w.d0 * w.tile * sizeof(uint4);
-    static std::atomic<int> smem_set{0};
+    static SmemAttr smem_set;
     GS_CUDA_TRY(ensure_smem(walk_eval_kernel, smem_set, (size_t)kWalkMaxSteps * kWalkTile * sizeof(uint4)));
     const int plane = w.d1 * w.d2;
     const int threads = (w.tile * kWalkGroups + 31) / 32 * 32;

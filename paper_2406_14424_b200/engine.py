@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .stage import stage_gate
+from .stage import GateBatcher
 
 
 @dataclass
@@ -153,10 +153,11 @@ class StageRouter:
     """
 
     def __init__(self, tables: GearTables, cert, corr, replica_device, seed: int = 0,
-                 rng: np.random.Generator | None = None):
+                 rng: np.random.Generator | None = None, near_keep: int = 4096):
         self.tables = tables
         self.cert = _lib.to_device(cert, torch.float64)
         self.corr = _lib.to_device(corr, torch.uint8)
+        self.gate = GateBatcher(self.cert, self.corr)
         self.replica_device = np.asarray(replica_device, dtype=np.int64)
         self.queues = [deque() for _ in range(len(self.replica_device))]
         self.rng = rng if rng is not None else np.random.default_rng(seed)
@@ -165,7 +166,10 @@ class StageRouter:
         self.in_flight = 0
         self.window_latencies: list[int] = []
         self.window_correct = 0
-        self.near_threshold: list[int] = []  # request ids gated within 1e-6
+        # request ids gated within 1e-6 of their threshold: the most recent
+        # near_keep of them (bounded for long-running routers), and a count
+        self.near_threshold: deque[int] = deque(maxlen=near_keep)
+        self.n_near_threshold = 0
 
     def finish_batch(self, device_idx: int, items: list[Item], now: int) -> set[int]:
         """Complete certain items, forward the rest (batch order kept);
@@ -181,11 +185,11 @@ class StageRouter:
         model = t._model[gear, stage]
         thr = t._thr[gear, stage]
         last = stage == t._n_stages[gear] - 1
-        res = stage_gate(self.cert, self.corr, rows, model, thr, last)
-        stop = res.stop.cpu().numpy().astype(bool)
-        correct = res.correct.cpu().numpy()
-        fwd = res.deferred_idx.cpu().numpy()
-        self.near_threshold.extend(items[i].request_id for i in res.near_idx.cpu().numpy())
+        # one H2D of the packed items, the device gate, one D2H of the outcome
+        stop, correct, near = self.gate.gate(rows, model, thr, last)
+        fwd = np.flatnonzero(~stop)  # batch order, as the kernel compacts them
+        self.n_near_threshold += len(near)
+        self.near_threshold.extend(items[i].request_id for i in near)
         for i in np.flatnonzero(stop):
             it = items[i]
             ok = bool(correct[i])

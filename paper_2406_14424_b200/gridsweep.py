@@ -193,6 +193,8 @@ class GridSweep:
                 torch.empty((count, self.max_len), **f64) if forward_frac else None,
                 torch.empty(count, dtype=torch.int32, device=dev) if n_correct else None,
                 begin)
+        else:
+            _check_out(out, count, self.max_len, dev)
         out.config_begin = begin
         lib = _lib.load()
         rc = lib.gs_grid_eval(self.n_rec, self.n_models, self._glen, self.cost1.data_ptr(),
@@ -254,6 +256,9 @@ class GridSweep:
         if res is None:
             res = self.evaluate(begin, count, accuracy=True, mean_cost=True,
                                 forward_frac=True, n_correct=True)
+        elif res.n_correct is None or res.mean_cost is None:
+            raise ValueError("pareto(res=...) needs a result scored with n_correct=True "
+                             "and mean_cost")
         idx = pareto_counts(res.n_correct, res.mean_cost, self.n_rec, base_index=res.config_begin)
         return idx, res
 
@@ -285,6 +290,22 @@ class GridSweep:
         return out
 
 
+def _check_out(out: SweepResult, count: int, max_len: int, dev: torch.device) -> None:
+    """A caller-supplied SweepResult must hold `count` configs in the layout
+    gs_grid_eval writes (the C call receives no output sizes)."""
+    specs = (("accuracy", out.accuracy, torch.float64, (count,)),
+             ("mean_cost", out.mean_cost, torch.float64, (count,)),
+             ("forward_frac", out.forward_frac, torch.float64, (count, max_len)),
+             ("n_correct", out.n_correct, torch.int32, (count,)))
+    for name, t, dtype, shape in specs:
+        if t is None:
+            continue
+        if t.dtype != dtype or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"out.{name} must be a contiguous {dtype} tensor on {dev}")
+        if tuple(t.shape) != shape:
+            raise ValueError(f"out.{name} has shape {tuple(t.shape)}, the range needs {shape}")
+
+
 def front_rows(idx: torch.Tensor, res: SweepResult) -> torch.Tensor:
     """Device [n_front, 3 + max_len] f64 rows (config index, accuracy,
     mean_cost, forward_frac...) of the configs `idx` (absolute indices) of a
@@ -302,7 +323,7 @@ def front_host(idx: torch.Tensor, res: SweepResult) -> np.ndarray:
     host = _pinned(rows.shape, rows.dtype)
     host.copy_(rows, non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    return host.numpy()
+    return host.numpy().copy()  # the pinned staging buffer is reused by the next call
 
 
 _PINNED: dict = {}

@@ -1,0 +1,182 @@
+"""Bind the reference `gearserve` package's hot path to the B200 library.
+
+This is the reference-side binding INTEGRATION.md §2 describes, applied
+in-process to an unmodified `gearserve` import (no reference file edited):
+
+  gearserve.kernels.evaluate_encoded      (src/kernels.py:93-108)
+      -> kernels.evaluate_encoded (gs_eval_encoded, bit-exact walk)
+  gearserve.cascades.matrices             (src/cascades.py:44-63)
+      -> one batched device certainty launch (gs_certainty), host copies
+         cached on the ValidationSet exactly where the reference caches them
+         (also the name engine.py imports, src/engine.py:22)
+  gearserve.cascades.certainty            (src/cascades.py:20-28)
+      -> gs_certainty (also the name serving.py imports, src/serving.py:25)
+  gearserve.cascades.pareto_filter        (src/cascades.py:116-129)
+      -> gs_pareto_generic (also the name planner.py imports, :25-33)
+  gearserve.engine.EngineState.finish_batch (src/engine.py:355-383)
+      -> the gate on the device, one packed H2D / kernel / D2H per batch
+         (gs_stage_gate_packed); completions, queue appends and the shared
+         Generator's draws in the reference's order.
+
+Everything that is not on the hot path (planner SP2-SP4, the LP, the event
+loop, the threaded server, formats, CLI) stays the reference's own code.
+`install()` returns the counters of calls routed to the library, so a test
+can prove the GPU path actually ran.
+"""
+
+from __future__ import annotations
+
+import importlib
+from collections import Counter
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import cascades as b200_cascades
+from . import kernels as b200_kernels
+from .stage import GateBatcher
+
+CALLS: Counter = Counter()
+_INSTALLED: dict = {}
+
+
+def _evaluate_encoded(certainty, correct, stage_model, thresholds, n_stages, cost1):
+    CALLS["evaluate_encoded"] += 1
+    return b200_kernels.evaluate_encoded(certainty, correct, stage_model, thresholds,
+                                         n_stages, cost1)
+
+
+def _certainty(scores) -> float:
+    CALLS["certainty"] += 1
+    return b200_cascades.certainty(scores)
+
+
+def _matrices(validation, profiles):
+    """Reference cascades.matrices: same cache key, same error, same arrays."""
+    key = profiles.model_ids
+    cached = validation._matrix_cache.get(key)
+    if cached is not None:
+        return cached
+    missing = set(key) - validation.model_ids
+    if missing:
+        raise ValueError(f"validation set lacks records for models {sorted(missing)}")
+    CALLS["matrices"] += 1
+    cert, corr = b200_cascades._device_matrices(validation, profiles)
+    host = (cert.cpu().numpy(), corr.cpu().numpy())
+    validation._matrix_cache[key] = host
+    return host
+
+
+def _pareto_filter(evals):
+    CALLS["pareto_filter"] += 1
+    return b200_cascades.pareto_filter(evals)
+
+
+class _PlanGate:
+    """Device view of one CompiledPlan: certainty / correct matrices and the
+    per-gear (stage -> model, threshold, n_stages) tables of _CompiledGear
+    (src/engine.py:175-193), plus the packed gate."""
+
+    def __init__(self, comp):
+        self.batcher = GateBatcher(torch.from_numpy(np.ascontiguousarray(comp.cert)),
+                                   torch.from_numpy(np.ascontiguousarray(comp.corr)),
+                                   capacity=max(8, max(comp.max_batch)))
+        n = len(comp.gears)
+        L = max(len(g.stage_model_idx) for g in comp.gears)
+        self.model = np.zeros((n, L), dtype=np.int32)
+        self.thr = np.zeros((n, L), dtype=np.float64)
+        self.n_stages = np.zeros(n, dtype=np.int64)
+        for gi, g in enumerate(comp.gears):
+            k = len(g.stage_model_idx)
+            self.model[gi, :k] = g.stage_model_idx
+            self.thr[gi, : k - 1] = [float(t) for t in g.stage_thresholds[:-1]]
+            self.n_stages[gi] = k
+
+
+def _plan_gate(comp) -> _PlanGate:
+    pg = getattr(comp, "_b200_gate", None)
+    if pg is None or pg.batcher.cert.device.index != torch.cuda.current_device():
+        pg = _PlanGate(comp)
+        comp._b200_gate = pg
+    return pg
+
+
+def _make_finish_batch(engine_mod):
+    RequestRecord = engine_mod.RequestRecord
+    choose_weighted = engine_mod.choose_weighted
+
+    def finish_batch(self, device_idx, items, now):
+        """EngineState.finish_batch with the gate on the device (reference
+        src/engine.py:355-383; same records, queue order and RNG draws)."""
+        comp = self.compiled
+        self.device_busy[device_idx] = False
+        self.in_flight -= len(items)
+        touched = {device_idx}
+        if not items:
+            return touched
+        CALLS["finish_batch"] += 1
+        pg = _plan_gate(comp)
+        n = len(items)
+        gear = np.fromiter((it.gear_idx for it in items), dtype=np.int64, count=n)
+        stage = np.fromiter((it.stage for it in items), dtype=np.int64, count=n)
+        rows = np.fromiter((it.row for it in items), dtype=np.int64, count=n)
+        stop, correct, _ = pg.batcher.gate(rows, pg.model[gear, stage], pg.thr[gear, stage],
+                                           stage == pg.n_stages[gear] - 1)
+        for i, it in enumerate(items):
+            if stop[i]:
+                ok = bool(correct[i])
+                self.request_records.append(RequestRecord(
+                    request_id=it.request_id, arrival_us=it.arrival_us, completion_us=now,
+                    stages_executed=it.stage + 1, correct=ok, gear_index=it.gear_idx))
+                self.completed += 1
+                self._window_latencies.append(now - it.arrival_us)
+                self._window_correct += 1 if ok else 0
+            else:
+                g = comp.gears[it.gear_idx]
+                it.stage += 1
+                pos = choose_weighted(g.stage_cum_weights[it.stage], self.rng)
+                ridx = int(g.stage_replica_idx[it.stage][pos])
+                self.queues[ridx].append(it)
+                touched.add(comp.device_of[ridx])
+        return touched
+
+    return finish_batch
+
+
+def install(package: str = "gearserve", engine_gate: bool = True) -> Counter:
+    """Route the reference package's hot path to the B200 library (no CPU
+    fallback: the first routed call raises if the library or the GPU is
+    missing).  Idempotent; returns the call counters."""
+    if package in _INSTALLED:
+        return CALLS
+    _lib.load()
+    kernels = importlib.import_module(f"{package}.kernels")
+    cascades = importlib.import_module(f"{package}.cascades")
+    engine = importlib.import_module(f"{package}.engine")
+    planner = importlib.import_module(f"{package}.planner")
+    serving = importlib.import_module(f"{package}.serving")
+    saved = [(kernels, "evaluate_encoded", kernels.evaluate_encoded),
+             (cascades, "certainty", cascades.certainty),
+             (cascades, "matrices", cascades.matrices),
+             (cascades, "pareto_filter", cascades.pareto_filter),
+             (engine, "matrices", engine.matrices),
+             (planner, "pareto_filter", planner.pareto_filter),
+             (serving, "certainty", serving.certainty)]
+    kernels.evaluate_encoded = _evaluate_encoded
+    cascades.certainty = _certainty
+    cascades.matrices = _matrices
+    cascades.pareto_filter = _pareto_filter
+    engine.matrices = _matrices
+    planner.pareto_filter = _pareto_filter
+    serving.certainty = _certainty
+    if engine_gate:
+        saved.append((engine.EngineState, "finish_batch", engine.EngineState.finish_batch))
+        engine.EngineState.finish_batch = _make_finish_batch(engine)
+    _INSTALLED[package] = saved
+    return CALLS
+
+
+def uninstall(package: str = "gearserve") -> None:
+    for obj, name, value in reversed(_INSTALLED.pop(package, [])):
+        setattr(obj, name, value)

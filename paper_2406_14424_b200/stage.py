@@ -149,3 +149,62 @@ def stage_gate(cert: torch.Tensor, corr: torch.Tensor, row, model, thr, is_last=
     nd, nn = (int(x) for x in counts.tolist())
     return GateResult(stop=stop, correct=correct, deferred_idx=deferred[:nd],
                       near_idx=near[:nn])
+
+
+class GateBatcher:
+    """The gate for small online batches as ONE native call per batch
+    (gs_stage_gate_packed): the items go to the device in one pinned H2D,
+    the outcome comes back in one pinned D2H, buffers reused across calls.
+
+    The reference gates a batch of <= max_profiled_batch items (4-8,
+    src/synth.py:30) per finish_batch (src/engine.py:355-383); at that size
+    a gate is latency-bound, so what matters is the number of host<->device
+    transfers and launches per batch: one copy in, one kernel, one copy out.
+    """
+
+    def __init__(self, cert: torch.Tensor, corr: torch.Tensor, capacity: int = 64,
+                 near_eps: float = NEAR_EPS):
+        self.cert = _lib.to_device(cert, torch.float64)
+        self.corr = _lib.to_device(corr, torch.uint8)
+        if self.cert.ndim != 2 or tuple(self.corr.shape) != tuple(self.cert.shape):
+            raise ValueError("cert and corr must both be [n_records, n_models]")
+        self.n_rec, self.n_models = int(self.cert.shape[0]), int(self.cert.shape[1])
+        self.near_eps = float(near_eps)
+        self.cap = 0
+        self._grow(max(1, int(capacity)))
+
+    def _grow(self, n: int) -> None:
+        lib = _lib.load()
+        hin, hout, dev = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.check(lib.gs_stage_gate_packed_bytes(n, ctypes.byref(hin), ctypes.byref(hout),
+                                                  ctypes.byref(dev)), "gate batch")
+        self.h_in = torch.empty(max(hin.value, 8), dtype=torch.uint8, pin_memory=True)
+        self.h_out = torch.empty(max(hout.value, 16), dtype=torch.uint8, pin_memory=True)
+        self.d_buf = _lib.workspace(dev.value)
+        self._in = self.h_in.numpy()
+        self._out = self.h_out.numpy()
+        self.cap = n
+
+    def gate(self, rows, model, thr, is_last):
+        """(stop bool[n], correct u8[n], near positions i64) for one batch;
+        rows i64, model i32, thr f64, is_last bool — host arrays."""
+        n = len(rows)
+        if n > self.cap:
+            self._grow(max(n, 2 * self.cap))
+        b = self._in
+        b[: 8 * n].view(np.int64)[:] = rows
+        b[8 * n: 16 * n].view(np.float64)[:] = thr
+        b[16 * n: 20 * n].view(np.int32)[:] = model
+        b[20 * n: 21 * n] = is_last
+        rc = _lib.load().gs_stage_gate_packed(
+            self.cert.data_ptr(), self.corr.data_ptr(), self.n_rec, self.n_models,
+            self.h_in.data_ptr(), n, self.near_eps, self.h_out.data_ptr(), self.d_buf.data_ptr(),
+            self.d_buf.numel(), 1, _lib.stream_ptr())
+        _lib.check(rc, "gate batch")
+        o = self._out
+        n_near = int(o[8:16].view(np.int64)[0])
+        stop = o[16: 16 + n].astype(bool)
+        correct = o[16 + n: 16 + 2 * n].copy()
+        near_off = (16 + 2 * n + 7) // 8 * 8
+        near = o[near_off: near_off + 8 * n_near].view(np.int64).copy()
+        return stop, correct, near

@@ -118,3 +118,28 @@ def test_stage_gate_vs_oracle():
     assert np.array_equal(res.deferred_idx.cpu().numpy(), deferred)
     assert np.array_equal(res.near_idx.cpu().numpy(), near)
     assert np.array_equal(res.correct.cpu().numpy(), np.where(stop, corr[rows, models], 0))
+
+
+def test_gate_batcher_matches_stage_gate():
+    """The packed one-call gate (gs_stage_gate_packed) equals stage_gate on
+    tiny online batches and on batches past one tile (look-back path)."""
+    import torch
+
+    from paper_2406_14424_b200.stage import GateBatcher, stage_gate
+    rng = np.random.default_rng(5)
+    cert = np.round(rng.random((500, 3)), 2)
+    corr = (rng.random((500, 3)) < 0.6).astype(np.uint8)
+    dc, dk = torch.from_numpy(cert).cuda(), torch.from_numpy(corr).cuda()
+    gb = GateBatcher(dc, dk, capacity=4)
+    for n in (1, 3, 8, 255, 256, 257, 1000, 0):
+        rows = rng.integers(0, 500, n)
+        model = rng.integers(0, 3, n).astype(np.int32)
+        thr = np.round(rng.random(n), 2)
+        last = rng.random(n) < 0.2
+        stop, correct, near = gb.gate(rows, model, thr, last)
+        ref = stage_gate(dc, dk, rows, model, thr, last)
+        assert np.array_equal(stop, ref.stop.cpu().numpy().astype(bool))
+        assert np.array_equal(correct, ref.correct.cpu().numpy())
+        assert np.array_equal(near, ref.near_idx.cpu().numpy())
+        want = (cert[rows, model] >= thr) | last
+        assert np.array_equal(stop, want)
