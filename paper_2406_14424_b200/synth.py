@@ -136,3 +136,33 @@ def imagenet_logits(n_samples: int, n_cls: int = 1000, n_models: int = 3, seed: 
         out.append(x.to(dtype))
         correct.append(right.to(torch.uint8))
     return out, torch.stack(correct, dim=1), labels
+
+
+def kernels_bench_problem(n_records: int = 4000, n_models: int = 6, n_cascades: int = 200,
+                          seed: int = 0):
+    """The reference's own operator benchmark problem
+    (pkg/benchmarks/bench_kernels.py:25-49, the published 5.3 ms numba /
+    17.0 ms numpy point at records=4000 models=6 cascades=200): the same
+    Generator draws in the same order, returned as evaluate_encoded's
+    positional arguments (certainty, correct, stage_model, thresholds,
+    n_stages, cost1)."""
+    rng = np.random.default_rng(seed)
+    mids = [f"m{j}" for j in range(n_models)]
+    cost1 = np.array([int(rng.integers(1_000, 60_000)) for _ in mids], dtype=np.float64)
+    index = {m: j for j, m in enumerate(mids)}
+    stages_list, thr_list = [], []
+    for _ in range(n_cascades):
+        k = int(rng.integers(1, n_models + 1))
+        stages_list.append(tuple(rng.permutation(mids)[:k]))
+        thr_list.append(tuple(float(x) for x in rng.random(k - 1)))
+    max_len = max(len(s) for s in stages_list)
+    stage_model = np.full((n_cascades, max_len), -1, dtype=np.int32)
+    thresholds = np.zeros((n_cascades, max_len))
+    n_stages = np.zeros(n_cascades, dtype=np.int32)
+    for ci, (s, t) in enumerate(zip(stages_list, thr_list)):
+        n_stages[ci] = len(s)
+        stage_model[ci, : len(s)] = [index[m] for m in s]
+        thresholds[ci, : len(t)] = t
+    certainty = rng.random((n_records, n_models))
+    correct = (rng.random((n_records, n_models)) < 0.7).astype(np.uint8)
+    return certainty, correct, stage_model, thresholds, n_stages, cost1

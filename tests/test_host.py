@@ -156,3 +156,46 @@ def test_product_refuses_to_run_without_cuda():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         kernels.evaluate_encoded(np.zeros((2, 1)), np.zeros((2, 1)), np.zeros((1, 1)),
                                  np.zeros((1, 1)), np.ones(1), np.ones(1))
+
+
+def test_kernels_bench_problem_matches_golden_generator():
+    """synth.kernels_bench_problem (bench.py's list-path leg) draws the same
+    problem as the golden generator restating bench_kernels.py:25-49."""
+    from golden_inputs import bench_problem
+    from paper_2406_14424_b200 import synth
+    for args in ((4000, 6, 200, 0), (50, 3, 17, 5)):
+        a = synth.kernels_bench_problem(*args)
+        b = bench_problem(*args)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+def test_refbinding_patches_reference_package():
+    """refbinding.install routes the unmodified reference's hot-path names
+    to this package (checked without a GPU: only the binding, no compute)."""
+    import importlib
+    import os
+    import sys
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "gearserve").is_dir():
+        pytest.skip("reference not installed in baseline/_ref (tools/install_reference.sh)")
+    sys.path.insert(0, str(ref))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    try:
+        from paper_2406_14424_b200 import refbinding
+        gk = importlib.import_module("gearserve.kernels")
+        ge = importlib.import_module("gearserve.engine")
+        orig = (gk.evaluate_encoded, ge.EngineState.finish_batch)
+        refbinding.install("gearserve")
+        try:
+            assert gk.evaluate_encoded is refbinding._evaluate_encoded
+            assert importlib.import_module("gearserve.planner").pareto_filter is \
+                refbinding._pareto_filter
+            assert importlib.import_module("gearserve.serving").certainty is refbinding._certainty
+            assert ge.matrices is refbinding._matrices
+            assert ge.EngineState.finish_batch is not orig[1]
+        finally:
+            refbinding.uninstall("gearserve")
+        assert (gk.evaluate_encoded, ge.EngineState.finish_batch) == orig
+    finally:
+        sys.path.remove(str(ref))
