@@ -333,8 +333,7 @@ def run_ours(args, world, rank, local):
     flush_ms = f0.elapsed_time(f1) / args.steps
     e2e_ms = max(e2e_ms - flush_ms, 1e-6)
 
-    # ---- stage step (config 3 shape: 1M x 1000-class f32 logits, entropy)
-    stage = _guarded(stage_bench, args, dev, flush) if (rank == 0 and not args.skip_stage) else None
+    stage = None
 
     # ---- roofline for the dominant kernel (each kernel timed alone above)
     pk = peaks()
@@ -411,6 +410,13 @@ def run_ours(args, world, rank, local):
             line["config4b"] = _guarded(config4_bench, args, dev)
         if not args.skip_config1:
             line["config1"] = _guarded(config1_bench, args, dev)
+        if not args.skip_list:
+            line["list_path"] = _guarded(list_path_bench, args, dev)
+        if not args.skip_config3:
+            line["config3"] = c3 = _guarded(config3_bench, args, dev)
+            if "entropy" in c3:  # the online stage step at the config-3 shape
+                line["stage_step"] = {k: c3[k]["stage_step"] for k in ("entropy", "margin")}
+        line["host"] = host_info()
         print(json.dumps(line), flush=True)
 
 
@@ -422,42 +428,6 @@ def _guarded(fn, *a):
         import traceback
         traceback.print_exc(file=sys.stderr)
         return {"error": f"{type(e).__name__}: {e}"}
-
-
-def stage_bench(args, dev, flush):
-    """Config-3 shape stage step: 1M rows x 1000-class f32 logits (4 GB),
-    entropy certainty, per-row thresholds, compaction of deferred rows."""
-    import torch
-
-    from paper_2406_14424_b200.stage import stage_step
-    n, c = N_REC, 1000
-    g = torch.Generator(device=dev)
-    g.manual_seed(0)
-    x = torch.randn((n, c), generator=g, device=dev, dtype=torch.float32)
-    thr = torch.full((n,), 0.05, dtype=torch.float64, device=dev)
-    out = {}
-    pk = peaks()
-    for kind in ("entropy", "margin"):
-        for _ in range(max(args.warmup, 1)):
-            r = stage_step(x, thr, kind=kind, sync=False)
-        torch.cuda.synchronize()
-        k = max(args.steps, 5)
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(k):  # back to back: the input (4 GB) is far larger than L2
-            r = stage_step(x, thr, kind=kind, sync=False)
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / k
-        d = int(r.counts[0].item())
-        bytes_ = n * c * 4 + n * (8 + 8 + 1) + d * 8
-        gbs = bytes_ / (ms * 1e-3) / 1e9
-        out[kind] = {"samples_per_s": n / (ms * 1e-3), "ms": ms, "deferred": d,
-                     "algorithmic_bytes": bytes_, "achieved_gbs": gbs,
-                     "frac": gbs / pk["hbm_gbs"], "launches_per_call": 1}
-    out["workload"] = "cfg3 shape: 1M x 1000-class f32 logits, per-row thr, stable compaction"
-    return out
 
 
 def config1_bench(args, dev):
@@ -538,12 +508,45 @@ def config1_bench(args, dev):
         one = GridSweep(cert_r[seed], corr_r[seed], gs_[seed], cost1).evaluate()
         ok_r = ok_r and bool(torch.equal(one.accuracy, res.accuracy[seed]) and
                              torch.equal(one.forward_frac, res.forward_frac[seed]))
+    # e2e: the public API from pinned host matrices each step (H2D, build,
+    # score every config, exact front, front rows D2H)
+    from paper_2406_14424_b200.gridsweep import front_host
+    pin_c = torch.from_numpy(cert).pin_memory()
+    pin_k = torch.from_numpy(corr).pin_memory()
+    dc, dk = torch.empty_like(pin_c, device=dev), torch.empty_like(pin_k, device=dev)
+    sw_e = GridSweep(dc, dk, grids, cost1, build=False)
+    e_out = None
+
+    def e2e_step():
+        nonlocal e_out
+        dc.copy_(pin_c, non_blocking=True)
+        dk.copy_(pin_k, non_blocking=True)
+        sw_e.build()
+        e_out = sw_e.evaluate(n_correct=True, out=e_out)
+        idx, _ = sw_e.pareto(res=e_out)
+        return front_host(idx, e_out)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    te = []
+    for _ in range(max(args.steps, 10)):
+        t = time.perf_counter()
+        rows = e2e_step()
+        te.append(time.perf_counter() - t)
+    te.sort()
+    e2e_ms = te[len(te) // 2] * 1e3
     b_r = R * (10_000 * 3 * 9 + n_cfg_r * (16 + 8 * 3))
     del flush, cert_r, corr_r, res, bs
     return {"workload": "cfg1: 3-model cascade, 10k records, 100-level grids, full product",
             "n_configs": sw.n_configs, "ms": ms, "config_evals_per_s": sw.n_configs / (ms * 1e-3),
             "launches_per_step": sw.info.build_launches + sw.info.eval_launches,
             "parity_full_product": ok,
+            "e2e": {"value": sw.n_configs / (e2e_ms * 1e-3), "unit": "config-evals/s",
+                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(cert.nbytes + corr.nbytes),
+                    "d2h_bytes_per_step": int(rows.nbytes),
+                    "path": "GridSweep from pinned host matrices: H2D, build, eval, pareto, "
+                            "front rows D2H; host wall clock, median"},
             "stacked": {"sets": R, "ms": ms_r, "config_evals_per_s": R * n_cfg_r / (ms_r * 1e-3),
                         "launches_per_step": 1, "algorithmic_bytes": b_r,
                         "achieved_gbs": b_r / (ms_r * 1e-3) / 1e9,
@@ -596,6 +599,12 @@ def config4_bench(args, dev):
     ok = bool(np.array_equal(out.accuracy[torch.from_numpy(pick).to(dev)].cpu().numpy(), want[0])
               and np.array_equal(out.mean_cost[torch.from_numpy(pick).to(dev)].cpu().numpy(),
                                  want[1]))
+    threads = os.cpu_count() or 1
+    pick_c = np.sort(rng.choice(c, size=threads * 16, replace=False))
+    csm, cthr, cns = (t.cpu().numpy() for t in sw.decode(pick_c))
+    t = time.perf_counter()
+    oracle.evaluate_encoded(cert, corr, csm, cthr, cns, cost1, n_threads=threads)
+    cpu_rate = len(pick_c) / (time.perf_counter() - t)
     out_bytes = c * (16 + 8 * m)
     gbs = (out_bytes + n * m * 9) / (ms * 1e-3) / 1e9
     del out
@@ -605,7 +614,10 @@ def config4_bench(args, dev):
             "algorithmic_bytes": out_bytes + n * m * 9, "achieved_gbs": gbs,
             "frac": gbs / peaks()["hbm_gbs"], "fast_path": bool(sw.info.fast_path),
             "parity_spot_check": ok, "timing": "best of 3 (build + full eval), no L2 flush "
-                                               "(5.9 GB of outputs per step)"}
+                                               "(5.9 GB of outputs per step)",
+            "cpu_baseline": {"value": cpu_rate, "unit": "config-evals/s", "cores": threads,
+                             "kind": "port", "sample": f"{len(pick_c)} random configs x 100k "
+                                                       "records, oracle/oracle_eval.c"}}
 
 
 def ingest_bench(args, n=200_000):
@@ -658,6 +670,327 @@ def ingest_bench(args, n=200_000):
             "cpu_baseline": {"records_per_s": 20_000 / ref_dt, "cores": 1, "kind": "port",
                              "sample": "20k lines, oracle.load_validation_jsonl (json.loads "
                                        "per line, src/formats.py:75-97)"}}
+
+
+def host_info() -> dict:
+    """CPU model, logical cores and this process's affinity."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = os.cpu_count()
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "affinity": aff}
+
+
+def _ref_gearserve():
+    """The unmodified reference from baseline/_ref (tools/install_reference.sh)
+    when it travelled with the snapshot and numba imports; else None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "gearserve").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/gs_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.append(str(ref))
+    try:
+        from gearserve import kernels as ref_kernels
+        return ref_kernels
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def list_path_bench(args, dev):
+    """The operator the reference exposes, kernels.evaluate_encoded (list
+    path, gs_eval_encoded), at (a) the reference's published benchmark point
+    (bench_kernels.py: records=4000 models=6 cascades=200; numba 5.3 ms,
+    numpy 17.0 ms on one core, README.md:131-135) through the numpy-in /
+    numpy-out drop-in, and (b) SP1's shape: 2000 sampled cascades
+    (sample_cascades over the cfg2 100-level grids) x 1M records, device
+    resident.  CPU: the oracle port on one core (a) / all cores (b), and the
+    reference's own numba walk when baseline/_ref is present."""
+    import torch
+
+    from oracle import oracle
+    from paper_2406_14424_b200 import kernels, synth
+    from paper_2406_14424_b200.cascades import encode_cascades, sample_cascades
+    from paper_2406_14424_b200.cascades import ThresholdGrid
+
+    out = {}
+    prob = synth.kernels_bench_problem(4000, 6, 200, 0)
+    got = kernels.evaluate_encoded(*prob)
+    want = oracle.evaluate_encoded(*prob, n_threads=1)
+    ok = all(np.array_equal(a, b) for a, b in zip(got, want))
+    ts = []
+    for _ in range(max(args.steps, 10)):
+        t = time.perf_counter()
+        kernels.evaluate_encoded(*prob)
+        ts.append(time.perf_counter() - t)
+    ts.sort()
+    dev_args = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in prob]
+    for _ in range(3):
+        kernels.evaluate_encoded_device(*dev_args)
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(args.steps, 10)
+    a_ev.record()
+    for _ in range(k):
+        kernels.evaluate_encoded_device(*dev_args)
+    b_ev.record()
+    torch.cuda.synchronize()
+    dev_ms = a_ev.elapsed_time(b_ev) / k
+    t = time.perf_counter()
+    for _ in range(5):
+        oracle.evaluate_encoded(*prob, n_threads=1)
+    port_ms = (time.perf_counter() - t) / 5 * 1e3
+    pub = {"records": 4000, "models": 6, "cascades": 200,
+           "e2e_ms_median": ts[len(ts) // 2] * 1e3, "e2e_ms_best": ts[0] * 1e3,
+           "device_ms": dev_ms, "bit_exact_vs_oracle": ok,
+           "published_numba_ms": 5.3, "published_numpy_ms": 17.0,
+           "e2e_speedup_vs_published_numba": 5.3 / (ts[len(ts) // 2] * 1e3),
+           "path": "kernels.evaluate_encoded: numpy in (H2D), gs_eval_encoded, numpy out (D2H); "
+                   "device_ms = evaluate_encoded_device on resident tensors (CUDA events)",
+           "cpu_baseline": {"value": port_ms, "unit": "ms/call", "cores": 1, "kind": "port",
+                            "sample": "the whole problem, oracle/oracle_eval.c, 1 thread"}}
+    ref = _ref_gearserve()
+    if ref is not None and getattr(ref, "HAS_NUMBA", False):
+        ref._evaluate_numba(*prob)  # JIT / cache load
+        t = time.perf_counter()
+        for _ in range(5):
+            r = ref._evaluate_numba(*prob)
+        pub["reference_numba"] = {"value": (time.perf_counter() - t) / 5 * 1e3, "unit": "ms/call",
+                                  "cores": 1, "kind": "reference",
+                                  "bit_exact": all(np.array_equal(x, y) for x, y in zip(r, got)),
+                                  "sample": "baseline/_ref gearserve.kernels._evaluate_numba, as shipped"}
+    out["published_point"] = pub
+
+    # (b) SP1 shape: 2000 sampled cascades x the cfg2 records
+    profiles, cert, corr, grids, cost1 = workload(seed=0)
+    grid = ThresholdGrid({m: tuple(float(x) for x in grids[j])
+                          for j, m in enumerate(profiles.model_ids)})
+    cascs = sample_cascades(profiles, grid, 2000, rng_seed=0)
+    sm, thr, ns = encode_cascades(cascs, profiles)
+    dcert = torch.from_numpy(cert).to(dev)
+    dcorr = torch.from_numpy(corr).to(dev)
+    dsm, dthr, dns = (torch.from_numpy(x).to(dev) for x in (sm, thr, ns))
+    dcost = torch.from_numpy(cost1).to(dev)
+    kernels.evaluate_encoded_device(dcert, dcorr, dsm, dthr, dns, dcost)
+    a_ev.record()
+    for _ in range(3):
+        r = kernels.evaluate_encoded_device(dcert, dcorr, dsm, dthr, dns, dcost)
+    b_ev.record()
+    torch.cuda.synchronize()
+    sp1_ms = a_ev.elapsed_time(b_ev) / 3
+    pick = np.arange(0, len(cascs), max(1, len(cascs) // 64))
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    want = oracle.evaluate_encoded(cert, corr, sm[pick], thr[pick], ns[pick], cost1,
+                                   n_threads=threads)
+    cpu_dt = time.perf_counter() - t
+    ok_b = bool(np.array_equal(r[0].cpu().numpy()[pick], want[0]) and
+                np.array_equal(r[2].cpu().numpy()[pick], want[2]))
+    steps = int(ns.astype(np.int64).sum())  # upper bound of stage visits per record
+    out["sp1_shape"] = {
+        "cascades": len(cascs), "records": N_REC, "device_ms": sp1_ms,
+        "config_evals_per_s": len(cascs) / (sp1_ms * 1e-3),
+        "record_config_pairs_per_s": len(cascs) * N_REC / (sp1_ms * 1e-3),
+        "bound": "issue (O(C*N*stages) walk: one thread per cascade, records broadcast from "
+                 "shared memory; the HBM bytes are N*M*9 = 36 MB, ~6 us)",
+        "stage_visits_upper_bound": steps * N_REC,
+        "parity_spot_check": ok_b,
+        "cpu_baseline": {"value": len(pick) / cpu_dt, "unit": "config-evals/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{len(pick)} of the {len(cascs)} cascades x 1M records, "
+                                   "oracle/oracle_eval.c"}}
+    del dcert, dcorr
+    return out
+
+
+def config3_bench(args, dev):
+    """BASELINE configs[2]: an ImageNet-shaped 3-model cascade (ResNet-
+    18/50/152 stand-ins), 1M samples, 1000-class f32 logits per model
+    (synth.imagenet_logits; correct = argmax == label).  One step: the
+    certainty of every logit row of the three models (entropy, the config's
+    named kind; margin = the reference's Eq. 5) into the [N, 3] matrix, the
+    device quantile grids (levels 100), the full grid sweep (C = 10,303) and
+    its exact Pareto front.  Beside it the stage step at thresholds chosen at
+    the 35th certainty percentile (so about a third of the rows defer and
+    compaction runs), and the reference's certainty on the CPU."""
+    import torch
+
+    from oracle import oracle
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.cascades import certainty_rows, grid_values
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    from paper_2406_14424_b200.stage import stage_step
+
+    n, n_cls, m = N_REC, 1000, 3
+    logits, _, labels = synth.imagenet_logits(n, n_cls, m, seed=0, device=dev)
+    corr = torch.stack([(x.argmax(dim=1) == labels).to(torch.uint8) for x in logits], 1)
+    corr = corr.contiguous()
+    cost1 = np.array([1.8, 4.1, 11.5]) * 1000.0  # ResNet-18/50/152 GFLOP ratios, µs
+    pk = peaks()
+    out = {"workload": "cfg3: 3 x [1M, 1000] f32 logits (ResNet-18/50/152 stand-ins), "
+                       "certainty -> [N,3] matrices -> 100-level device grids -> full sweep "
+                       "(C = 10,303) -> exact Pareto front",
+           "correct": "argmax(logits) == label (setup, untimed)"}
+    for kind in ("entropy", "margin"):
+        def step():
+            cert = torch.stack([certainty_rows(x, kind=kind) for x in logits], 1).contiguous()
+            grids = [grid_values(cert[:, j], LEVELS) for j in range(m)]
+            sw = GridSweep(cert, corr, grids, cost1)
+            idx, res = sw.pareto()
+            return cert, sw, idx, res
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(3, min(args.steps, 5))):
+            t = time.perf_counter()
+            cert, sw, idx, res = step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t)
+        ms = min(ts) * 1e3
+        # certainty phase alone (the bytes: the logits), CUDA events
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record()
+        for x in logits:
+            certainty_rows(x, kind=kind)
+        b_ev.record()
+        torch.cuda.synchronize()
+        cert_ms = a_ev.elapsed_time(b_ev)
+        bytes_ = m * n * (n_cls * 4 + 8)
+        gbs = bytes_ / (cert_ms * 1e-3) / 1e9
+        # parity: the sweep against the oracle walk on sampled configs,
+        # certainty against the f64 numpy oracle on sampled rows
+        rng = np.random.default_rng(3)
+        rows = np.sort(rng.choice(n, 2000, replace=False))
+        lg = [x[torch.from_numpy(rows).to(dev)].cpu().numpy() for x in logits]
+        fn = oracle.entropy_rows if kind == "entropy" else oracle.margin_rows
+        c_ref = np.stack([fn(z) for z in lg], 1)
+        c_got = cert.cpu().numpy()[rows]
+        cert_ok = bool(np.max(np.abs(c_got - c_ref)) <= 5e-7) if kind == "entropy" else \
+            bool(np.array_equal(c_got, c_ref))
+        pick = np.sort(rng.choice(sw.n_configs, 64, replace=False))
+        sm, thr, ns = (t.cpu().numpy() for t in sw.decode(pick))
+        want = oracle.evaluate_encoded(cert.cpu().numpy(), corr.cpu().numpy(), sm, thr, ns, cost1,
+                                       n_threads=os.cpu_count() or 1)
+        sweep_ok = bool(np.array_equal(res.accuracy.cpu().numpy()[pick], want[0]))
+        out[kind] = {"ms_per_step": ms, "logit_rows_per_s": m * n / (ms * 1e-3),
+                     "certainty_ms": cert_ms, "certainty_rows_per_s": m * n / (cert_ms * 1e-3),
+                     "certainty_roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"],
+                                            "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                                            "algorithmic_bytes": bytes_},
+                     "front_size": int(idx.numel()), "n_configs": sw.n_configs,
+                     "certainty_check": cert_ok, "sweep_spot_check": sweep_ok,
+                     "timing": "host wall clock around the synchronized pipeline, best of "
+                               f"{len(ts)}; certainty_ms by CUDA events"}
+        # stage step of model 0 at its 35th certainty percentile
+        thr_v = float(np.quantile(cert[:, 0].cpu().numpy(), 0.35))
+        thr_t = torch.full((n,), thr_v, dtype=torch.float64, device=dev)
+        for _ in range(2):
+            r = stage_step(logits[0], thr_t, kind=kind, sync=False)
+        a_ev.record()
+        for _ in range(5):
+            r = stage_step(logits[0], thr_t, kind=kind, sync=False)
+        b_ev.record()
+        torch.cuda.synchronize()
+        st_ms = a_ev.elapsed_time(b_ev) / 5
+        d = int(r.counts[0].item())
+        b_st = n * n_cls * 4 + n * (8 + 1) + d * 8
+        out[kind]["stage_step"] = {
+            "ms": st_ms, "samples_per_s": n / (st_ms * 1e-3), "threshold": thr_v, "deferred": d,
+            "deferred_frac": d / n, "algorithmic_bytes": b_st,
+            "frac": b_st / (st_ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    # e2e: logits from pinned host memory (H2D inside the timed region),
+    # certainty + sweep + front, the front rows read back
+    out["e2e"] = _guarded(config3_e2e, logits, corr, cost1, dev)
+    # CPU: the reference's certainty (sorted() per row, src/cascades.py:20-28)
+    # on 2000 rows, and f64 numpy margin / entropy on 50k rows, one core
+    lg0 = logits[0][:50_000].cpu().numpy()
+    t = time.perf_counter()
+    for i in range(2000):
+        oracle.certainty(lg0[i].tolist())
+    ref_rate = 2000 / (time.perf_counter() - t)
+    t = time.perf_counter()
+    oracle.margin_rows(lg0)
+    np_margin = 50_000 / (time.perf_counter() - t)
+    t = time.perf_counter()
+    oracle.entropy_rows(lg0)
+    np_entropy = 50_000 / (time.perf_counter() - t)
+    out["cpu_baseline"] = {"value": ref_rate, "unit": "rows/s", "cores": 1, "kind": "port",
+                           "sample": "2000 rows of model 0: cascades.certainty semantics "
+                                     "(sorted per row, oracle.certainty)",
+                           "numpy_f64_margin_rows_per_s": np_margin,
+                           "numpy_f64_entropy_rows_per_s": np_entropy}
+    del logits
+    torch.cuda.empty_cache()
+    return out
+
+
+def config3_e2e(logits, corr, cost1, dev):
+    """Config 3 end to end from HOST logits: pinned [N, 1000] f32 per model,
+    streamed to the device in row chunks on a copy stream while the previous
+    chunk's certainty runs, then grids, sweep, front, front rows to host."""
+    import psutil
+    import torch
+
+    from paper_2406_14424_b200.cascades import certainty_rows, grid_values
+    from paper_2406_14424_b200.gridsweep import GridSweep, front_host
+
+    n, n_cls = logits[0].shape
+    need = len(logits) * n * n_cls * 4
+    if psutil.virtual_memory().available < 3 * need:
+        return {"skipped": f"host memory: {psutil.virtual_memory().available / 1e9:.0f} GB free"}
+    host = [torch.empty((n, n_cls), dtype=torch.float32, pin_memory=True) for _ in logits]
+    for h, x in zip(host, logits):
+        h.copy_(x)
+    chunk = 65536
+    bufs = [torch.empty((chunk, n_cls), dtype=torch.float32, device=dev) for _ in range(2)]
+    copy = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    cert = torch.empty((n, len(logits)), dtype=torch.float64, device=dev)
+    evs = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+
+    def step():
+        k = 0
+        for j, h in enumerate(host):
+            for lo in range(0, n, chunk):
+                hi = min(n, lo + chunk)
+                b = k % 2
+                with torch.cuda.stream(copy):
+                    copy.wait_event(free[b])
+                    bufs[b][: hi - lo].copy_(h[lo:hi], non_blocking=True)
+                    evs[b].record(copy)
+                main.wait_event(evs[b])
+                cert[lo:hi, j] = certainty_rows(bufs[b][: hi - lo], kind="entropy")
+                free[b].record(main)
+                k += 1
+        c = cert.contiguous()
+        grids = [grid_values(c[:, j], LEVELS) for j in range(len(host))]
+        sw = GridSweep(c, corr, grids, cost1)
+        idx, res = sw.pareto()
+        return front_host(idx, res)
+
+    step()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        rows = step()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t)
+    ms = min(ts) * 1e3
+    return {"ms_per_step": ms, "logit_rows_per_s": len(host) * n / (ms * 1e-3),
+            "h2d_bytes_per_step": need, "d2h_bytes_per_step": int(rows.nbytes),
+            "path": "pinned host logits -> 64k-row chunks H2D on a copy stream overlapped with "
+                    "certainty_rows (entropy) -> grid_values -> GridSweep.pareto -> front_host; "
+                    "host wall clock, best of 3"}
 
 
 def cpu_baseline(cert, corr, grids, cost1, args):
@@ -728,6 +1061,8 @@ def main():
     ap.add_argument("--skip-ingest", action="store_true", help="skip the ingest leg")
     ap.add_argument("--skip-config4", action="store_true", help="skip the 5-stage (cfg4b) leg")
     ap.add_argument("--skip-config1", action="store_true", help="skip the 3-model cfg1 leg")
+    ap.add_argument("--skip-list", action="store_true", help="skip the list-path legs")
+    ap.add_argument("--skip-config3", action="store_true", help="skip the cfg3 cascade leg")
     ap.add_argument("--flush", choices=["write", "clean", "none"], default="write",
                     help="L2 eviction between timed steps (see flush_l2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
