@@ -244,6 +244,89 @@ int gs_stage_gate_packed(const double* certainty, const uint8_t* correct,
                          void* dev_buf, size_t dev_bytes, int32_t sync,
                          void* stream);
 
+
+/* ------------------------------------------------------------------------
+ * Replay engine: engine.run (src/engine.py:452-520) in virtual-clock mode on
+ * the device, for many independent runs per launch (config-5 trace replays,
+ * the planner's simulator probes src/planner.py:293-356).  Each run is one
+ * sequential event loop -- arrivals (EngineState.submit :299-319), batch
+ * completions (finish_batch :355-383: the certainty gate and the replica
+ * draws), measurement ticks (tick / maybe_switch_gear :389-410, :123-133)
+ * and dispatch (scan_device / choose_dispatch :321-353, :248-253) -- with
+ * numpy's PCG64 stream reproduced on the device, so records, windows,
+ * queues and the final generator state equal the reference's.
+ * ---------------------------------------------------------------------- */
+typedef struct gs_engine_plan {
+  const double* cert;            /* [n_records, n_cols] CompiledPlan.cert  */
+  const uint8_t* corr;           /* [n_records, n_cols] CompiledPlan.corr  */
+  int64_t n_records;
+  int32_t n_cols;                /* models (profile order)                 */
+  int32_t n_replicas;            /* <= GS_ENGINE_MAX_REPLICAS              */
+  int32_t n_devices;             /* <= GS_ENGINE_MAX_DEVICES               */
+  int32_t n_gears;
+  int32_t max_stages;            /* L                                      */
+  int32_t batch_cap;             /* max over models of max_profiled_batch  */
+  const int32_t* replica_device; /* [R]                                    */
+  const int32_t* replica_model;  /* [R] model column                       */
+  const int32_t* replica_rank;   /* [R] rank of replica_id in string order */
+  const int32_t* model_max_batch;  /* [n_cols]                             */
+  const int64_t* model_runtime_us; /* [n_cols][batch_cap + 1]              */
+  const int32_t* gear_n_stages;  /* [G]                                    */
+  const int32_t* gear_model;     /* [G][L]                                 */
+  const double* gear_thr;        /* [G][L] (last stage unused)             */
+  const int32_t* gear_rep_off;   /* [G][L + 1] CSR offsets                 */
+  const int32_t* gear_rep;       /* replica index per CSR entry            */
+  const double* gear_cum;        /* np.cumsum of the load weights, per entry */
+  const int32_t* gear_min_qlen;  /* [G][R] Gear.min_queue_length (default 1) */
+  double qps_max;
+} gs_engine_plan;
+
+#define GS_ENGINE_MAX_REPLICAS 256
+#define GS_ENGINE_MAX_DEVICES 64
+
+typedef struct gs_engine_record { /* RequestRecord (src/engine.py:49-56)   */
+  int64_t completion_us;
+  int32_t request_id;            /* arrival index; arrival_us = arrivals[id] */
+  uint8_t stages_executed;
+  uint8_t correct;
+  uint16_t gear_index;
+} gs_engine_record;
+
+typedef struct gs_engine_window { /* WindowRecord (src/engine.py:59-73)    */
+  int64_t end_us;
+  double measured_qps;
+  int32_t first_stage_queue_len, gear_before, candidate_gear, gear_after;
+  int64_t completed;
+  int64_t p95_us;                /* -1: None                               */
+  double accuracy;               /* NaN: None                              */
+} gs_engine_window;
+
+typedef struct gs_engine_job {
+  const gs_engine_plan* plan;    /* device pointer                         */
+  const int64_t* arrivals;       /* device [n_arrivals], non-decreasing    */
+  int64_t n_arrivals;
+  int64_t horizon_us;            /* WorkloadTrace.duration_us              */
+  uint64_t rng_state_hi, rng_state_lo, rng_inc_hi, rng_inc_lo;
+  uint32_t rng_has_uint32, rng_uinteger;   /* PCG64 bit_generator.state    */
+  int32_t initial_gear;
+  int32_t enable_ticks;
+  int64_t measure_period_us;
+  double alpha;
+  int32_t* item_next;            /* scratch [n_arrivals]                   */
+  uint32_t* item_meta;           /* scratch [n_arrivals]                   */
+  int64_t* scratch;              /* scratch [n_arrivals] (window latencies) */
+  gs_engine_record* records;     /* out [n_arrivals], completion order     */
+  gs_engine_window* windows;     /* out [windows_cap]                      */
+  int64_t windows_cap;
+  int64_t* model_batches;        /* out [n_cols][batch_cap + 1]            */
+  int64_t* replica_counts;       /* out [R][2]: routed arrivals, queue length at horizon */
+  int64_t* result;               /* out [8]: arrivals, completed, in_flight,
+                                    windows, rng state hi, lo, has_uint32, uinteger */
+} gs_engine_job;
+
+/* jobs: device array of n_jobs descriptors; one warp per job. */
+int gs_engine_run(const gs_engine_job* jobs, int32_t n_jobs, void* stream);
+
 /* ------------------------------------------------------------------------
  * Threshold-grid quantiles on the device: np.quantile(column, qs) with
  * numpy's default "linear" method, bit-exact (cascades.build_threshold_grid,

@@ -328,3 +328,55 @@ def grid_values(cert_column, levels: int) -> tuple:
     qs = [k / levels for k in range(1, levels)]
     quants = np.quantile(np.asarray(cert_column, dtype=np.float64), qs)
     return tuple(sorted({0.0} | {float(q) for q in quants}))
+
+
+# ------------------------------------------------------------- PCG64 ---
+class Pcg64:
+    """numpy's default_rng bit generator (PCG64, XSL-RR output of the
+    advanced state) with its buffered 32-bit half, restated in Python: the
+    stream gs_engine.cu / the device sampler reproduce.  Test infrastructure."""
+
+    MULT = 0x2360ED051FC65DA44385DF649FCCF645
+    M128 = (1 << 128) - 1
+
+    def __init__(self, seed):
+        st = np.random.default_rng(seed).bit_generator.state
+        self.s, self.inc = int(st["state"]["state"]), int(st["state"]["inc"])
+        self.has32, self.u32 = int(st["has_uint32"]), int(st["uinteger"])
+
+    def state(self):
+        return (self.s, self.has32, self.u32)
+
+    def next64(self) -> int:
+        self.s = (self.s * self.MULT + self.inc) & self.M128
+        x = ((self.s >> 64) ^ self.s) & ((1 << 64) - 1)
+        r = self.s >> 122
+        return ((x >> r) | (x << ((64 - r) & 63))) & ((1 << 64) - 1)
+
+    def next32(self) -> int:
+        if self.has32:
+            self.has32 = 0
+            return self.u32
+        n = self.next64()
+        self.has32, self.u32 = 1, n >> 32
+        return n & 0xFFFFFFFF
+
+    def random(self) -> float:
+        return (self.next64() >> 11) * (1.0 / 9007199254740992.0)
+
+    def bounded(self, rng: int) -> int:
+        """numpy's Lemire sampler on [0, rng] (rng < 2^32)."""
+        if rng == 0:
+            return 0
+        excl = rng + 1
+        m = self.next32() * excl
+        if (m & 0xFFFFFFFF) < excl:
+            thr = (0xFFFFFFFF - rng) % excl
+            while (m & 0xFFFFFFFF) < thr:
+                m = self.next32() * excl
+        return m >> 32
+
+    def integers(self, lo: int, hi: int | None = None) -> int:
+        if hi is None:
+            lo, hi = 0, lo
+        return lo + self.bounded(hi - 1 - lo)

@@ -17,6 +17,11 @@ in-process to an unmodified `gearserve` import (no reference file edited):
       -> the gate on the device, one packed H2D / kernel / D2H per batch
          (gs_stage_gate_packed); completions, queue appends and the shared
          Generator's draws in the reference's order.
+  gearserve.engine.run (src/engine.py:452-520), with engine_run=True
+      -> the whole virtual-clock event loop on the device (replay.py,
+         gs_engine_run), which the planner's probes call too
+         (src/planner.py:306, :348); wall-clock pacing (it sleeps in real
+         time) and the batch log (record_batches) stay the reference's loop.
 
 Everything that is not on the hot path (planner SP2-SP4, the LP, the event
 loop, the threaded server, formats, CLI) stays the reference's own code.
@@ -36,6 +41,7 @@ from . import _lib
 from . import cascades as b200_cascades
 from . import kernels as b200_kernels
 from .stage import GateBatcher
+from . import replay
 
 CALLS: Counter = Counter()
 _INSTALLED: dict = {}
@@ -144,7 +150,35 @@ def _make_finish_batch(engine_mod):
     return finish_batch
 
 
-def install(package: str = "gearserve", engine_gate: bool = True) -> Counter:
+def _make_run(engine_mod, reference_run):
+    def run(plan, trace, validation, profiles, clock_mode="virtual", seed=None, config=None):
+        """engine.run with the virtual-clock loop on the device."""
+        if clock_mode not in ("virtual", "wall"):
+            raise ValueError(f"clock_mode must be 'virtual' or 'wall', got {clock_mode!r}")
+        if len(trace) == 0:
+            raise ValueError("trace is empty")
+        cfg = config or engine_mod.EngineConfig()
+        if clock_mode == "wall" or cfg.record_batches:
+            CALLS["run_reference_loop"] += 1
+            return reference_run(plan, trace, validation, profiles, clock_mode=clock_mode,
+                                 seed=seed, config=config)
+        if seed is not None:
+            cfg = engine_mod.replace(cfg, seed=seed)
+        engine_mod.CompiledPlan(plan, profiles, validation)  # the reference's validation
+        if not 0 <= cfg.initial_gear_index < len(plan.gears):
+            raise ValueError(f"initial gear {cfg.initial_gear_index} out of range")
+        CALLS["run"] += 1
+        dp = replay.DevicePlan(plan, profiles, validation)
+        job = replay.Job(dp, trace.arrivals, trace.duration_us, replay.EngineConfig(
+            seed=cfg.seed, measure_period_us=cfg.measure_period_us, alpha=cfg.alpha,
+            initial_gear_index=cfg.initial_gear_index, enable_ticks=cfg.enable_ticks))
+        return replay.run_many([job])[0].to_sim_metrics(engine_mod)
+
+    return run
+
+
+def install(package: str = "gearserve", engine_gate: bool = True,
+            engine_run: bool = False) -> Counter:
     """Route the reference package's hot path to the B200 library (no CPU
     fallback: the first routed call raises if the library or the GPU is
     missing).  Idempotent; returns the call counters."""
@@ -173,6 +207,9 @@ def install(package: str = "gearserve", engine_gate: bool = True) -> Counter:
     if engine_gate:
         saved.append((engine.EngineState, "finish_batch", engine.EngineState.finish_batch))
         engine.EngineState.finish_batch = _make_finish_batch(engine)
+    if engine_run:
+        saved.append((engine, "run", engine.run))
+        engine.run = _make_run(engine, engine.run)
     _INSTALLED[package] = saved
     return CALLS
 

@@ -166,3 +166,53 @@ def kernels_bench_problem(n_records: int = 4000, n_models: int = 6, n_cascades: 
     certainty = rng.random((n_records, n_models))
     correct = (rng.random((n_records, n_models)) < 0.7).astype(np.uint8)
     return certainty, correct, stage_model, thresholds, n_stages, cost1
+
+
+def bursty_counts(seconds: int, seed: int = 0, base: float = 100.0, sigma: float = 0.7):
+    """Per-second request counts of an Azure-like bursty series (lognormal
+    levels, default_rng(seed)); scale with replay.scale_trace."""
+    rng = np.random.default_rng(seed)
+    return np.rint(base * rng.lognormal(0.0, sigma, seconds)).astype(np.int64) + 1
+
+
+def trace_from_counts(counts):
+    """Arrivals at the start of each second, counts[s] of them (the input
+    scale_trace reads per-second counts from)."""
+    from .types import WorkloadTrace
+    counts = np.asarray(counts, dtype=np.int64)
+    return WorkloadTrace(np.repeat(np.arange(counts.size, dtype=np.int64) * 1_000_000, counts))
+
+
+def constant_rate_trace(qps: float, seconds: float):
+    """Evenly spaced arrivals (reference synth.constant_rate_trace :121-133)."""
+    from .types import WorkloadTrace
+    if qps <= 0 or seconds <= 0:
+        raise ValueError("qps and seconds must be positive")
+    n = int(round(qps * seconds))
+    if n == 0:
+        raise ValueError(f"qps {qps} over {seconds}s yields no arrivals")
+    arrivals = np.floor(np.arange(n, dtype=np.float64) * (1_000_000 / qps)).astype(np.int64)
+    duration = int(round(seconds * 1_000_000))
+    if int(arrivals[-1]) >= duration:
+        duration = (int(arrivals[-1]) // 1_000_000 + 1) * 1_000_000
+    return WorkloadTrace(arrivals, duration_us=duration)
+
+
+def step_trace(steps):
+    """Constant-rate segments [(qps, seconds), ...] back to back, qps 0 =
+    silence (reference synth.step_trace :135-154)."""
+    from .types import WorkloadTrace
+    if not steps:
+        raise ValueError("step trace needs at least one segment")
+    parts, offset = [], 0
+    for qps, seconds in steps:
+        if seconds <= 0:
+            raise ValueError(f"segment duration must be positive, got {seconds}")
+        if qps < 0:
+            raise ValueError(f"segment qps must be >= 0, got {qps}")
+        if qps > 0:
+            parts.append(constant_rate_trace(qps, seconds).arrivals + offset)
+        offset += int(round(seconds * 1_000_000))
+    if not parts:
+        raise ValueError("step trace has no arrivals")
+    return WorkloadTrace(np.concatenate(parts), duration_us=offset)

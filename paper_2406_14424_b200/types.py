@@ -246,3 +246,83 @@ class Cascade:
         parts = [f"{m}(>{self.thresholds[i]:g})" if i < len(self.thresholds) else m
                  for i, m in enumerate(self.stages)]
         return " -> ".join(parts)
+
+
+# ---------------------------------------------------------------- serving --
+# The plan / trace types the replay engine (replay.py, csrc/gs_engine.cu)
+# consumes: reference types.py:232-469 (Replica, Placement, Gear, GearPlan,
+# WorkloadTrace), reduced to the fields the event loop reads.  Reference
+# objects of these classes are accepted as well (same attribute names).
+
+@dataclass(frozen=True)
+class Replica:
+    replica_id: str
+    model_id: str
+    device_id: str
+
+
+class Placement:
+    """Model replicas on devices, in placement order (reference :247-306)."""
+
+    def __init__(self, replicas):
+        ids = [r.replica_id for r in replicas]
+        _require(len(set(ids)) == len(ids), "duplicate replica id")
+        pairs = [(r.model_id, r.device_id) for r in replicas]
+        _require(len(set(pairs)) == len(pairs), "a model is placed twice on one device")
+        self.replicas = tuple(replicas)
+
+    def replicas_of(self, model_id: str):
+        return tuple(r for r in self.replicas if r.model_id == model_id)
+
+    def __len__(self) -> int:
+        return len(self.replicas)
+
+
+@dataclass(frozen=True)
+class Gear:
+    """Cascade, per-replica minimum batch (queue length) and per-model load
+    split over replicas (reference :309-346)."""
+
+    cascade: Cascade
+    min_queue_length: dict
+    load_weights: dict
+
+
+@dataclass(frozen=True)
+class GearPlan:
+    """One gear per QPS range; range i covers [i, i+1) * qps_max / n_ranges,
+    clamped to the top range (reference :376-410)."""
+
+    placement: Placement
+    slo: object
+    qps_max: float
+    gears: tuple
+
+    @property
+    def n_ranges(self) -> int:
+        return len(self.gears)
+
+    def range_for_qps(self, qps: float) -> int:
+        _require(qps >= 0, f"qps must be >= 0, got {qps}")
+        return min(int(np.floor(qps * self.n_ranges / self.qps_max)), self.n_ranges - 1)
+
+
+class WorkloadTrace:
+    """Non-decreasing integer-µs arrival times; the horizon defaults to the
+    end of the last second holding an arrival (reference :433-469)."""
+
+    def __init__(self, arrivals, duration_us: int | None = None):
+        arrivals = np.asarray(arrivals, dtype=np.int64)
+        if arrivals.size:
+            _require(int(arrivals.min()) >= 0, "arrival times must be >= 0")
+            _require(bool(np.all(np.diff(arrivals) >= 0)), "arrival times must be non-decreasing")
+        if duration_us is None:
+            duration_us = 0 if arrivals.size == 0 else (int(arrivals[-1]) // US_PER_S + 1) * US_PER_S
+        else:
+            _require(arrivals.size == 0 or int(arrivals[-1]) < duration_us,
+                     "duration_us must exceed the last arrival")
+        self.arrivals = arrivals
+        self.duration_us = int(duration_us)
+
+    def __len__(self) -> int:
+        return int(self.arrivals.size)

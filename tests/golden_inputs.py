@@ -181,3 +181,78 @@ def engine_cases():
         cases.append(dict(mids=mids, n_rec=n_rec, cert=cert, corr=corr, replicas=replicas,
                           gears=gears, items=items, now=10_000, seed=int(rng.integers(0, 99))))
     return cases
+
+
+# ------------------------------------------------------------- replay ----
+def bursty_counts(seconds: int, seed: int, base: float = 100.0, sigma: float = 0.7):
+    """Per-second request counts of a bursty (Azure-like) series: lognormal
+    levels, default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    return np.rint(base * rng.lognormal(0.0, sigma, seconds)).astype(np.int64) + 1
+
+
+def trace_from_counts(counts):
+    """A trace with counts[s] arrivals at the start of second s (input to
+    scale_trace, which only reads the per-second counts)."""
+    return np.repeat(np.arange(len(counts), dtype=np.int64) * 1_000_000, counts)
+
+
+def replay_cases():
+    """Engine replay scenarios (plain data; tests build reference or mirror
+    objects from them).  Each exercises a different part of engine.run:
+    gear switching under bursts, zero-weight stages (rng.integers draws),
+    min queue lengths, multi-device dispatch order, probes without ticks,
+    a t=0 burst (burst-throughput probe), a C7-like step trace."""
+    def plan(models, replicas, gears, qps_max):
+        return {"models": models, "replicas": replicas, "gears": gears, "qps_max": qps_max}
+
+    m3 = {"n_models": 3, "cost_ratios": [1.0, 4.0, 16.0]}
+    m4 = {"n_models": 4, "cost_ratios": [1.0, 4.0, 16.0, 64.0]}
+    reps_a = [["m0@d0", "m0", "d0"], ["m1@d0", "m1", "d0"], ["m2@d1", "m2", "d1"],
+              ["m0@d1", "m0", "d1"]]
+    gears_a = [
+        {"stages": ["m0", "m1", "m2"], "thresholds": [0.5, 0.6], "min_q": {"m0@d0": 2},
+         "weights": {"m0": {"m0@d0": 3.0, "m0@d1": 1.0}, "m1": {"m1@d0": 1.0},
+                     "m2": {"m2@d1": 1.0}}},
+        {"stages": ["m0", "m2"], "thresholds": [0.7], "min_q": {},
+         "weights": {"m0": {"m0@d0": 0.0, "m0@d1": 0.0}, "m2": {"m2@d1": 2.0}}},
+    ]
+    reps_c = [["m0@d0", "m0", "d0"], ["m1@d0", "m1", "d0"], ["m0@d1", "m0", "d1"],
+              ["m2@d1", "m2", "d1"], ["m3@d2", "m3", "d2"], ["m1@d2", "m1", "d2"],
+              ["m2@d2", "m2", "d2"]]
+    gears_c = [
+        {"stages": ["m0", "m1", "m2", "m3"], "thresholds": [0.55, 0.62, 0.7],
+         "min_q": {"m3@d2": 2},
+         "weights": {"m0": {"m0@d0": 1.0, "m0@d1": 1.0}, "m1": {"m1@d0": 2.0, "m1@d2": 1.0},
+                     "m2": {"m2@d1": 1.0, "m2@d2": 0.5}, "m3": {"m3@d2": 1.0}}},
+        {"stages": ["m0", "m2", "m3"], "thresholds": [0.6, 0.75], "min_q": {"m0@d0": 3},
+         "weights": {"m0": {"m0@d0": 1.0, "m0@d1": 2.0}, "m2": {"m2@d1": 0.0, "m2@d2": 0.0},
+                     "m3": {"m3@d2": 1.0}}},
+        {"stages": ["m0", "m1"], "thresholds": [0.65], "min_q": {},
+         "weights": {"m0": {"m0@d0": 1.0, "m0@d1": 1.0}, "m1": {"m1@d0": 1.0, "m1@d2": 3.0}}},
+        {"stages": ["m0"], "thresholds": [], "min_q": {"m0@d0": 4, "m0@d1": 4},
+         "weights": {"m0": {"m0@d0": 1.0, "m0@d1": 1.0}}},
+    ]
+    return {
+        "bursty_two_gears": {"profiles": m3, "plan": plan(m3, reps_a, gears_a, 400.0),
+                             "val": [500, 0.8, 1], "trace": {"bursty": [12, 5, 300.0]},
+                             "seed": 7, "period": 100_000, "alpha": 8.0, "ticks": True,
+                             "initial_gear": 0},
+        "probe_no_ticks": {"profiles": m3, "plan": plan(m3, reps_a, gears_a[:1], 200.0),
+                           "val": [300, 0.7, 2], "trace": {"constant": [200.0, 5.0]},
+                           "seed": 11, "period": 100_000, "alpha": 8.0, "ticks": False,
+                           "initial_gear": 0},
+        "four_gears_overload": {"profiles": m4, "plan": plan(m4, reps_c, gears_c, 1000.0),
+                                "val": [800, 0.8, 3], "trace": {"bursty": [10, 9, 900.0]},
+                                "seed": 3, "period": 50_000, "alpha": 4.0, "ticks": True,
+                                "initial_gear": 1},
+        "burst_at_zero": {"profiles": m3, "plan": plan(m3, reps_a, gears_a[1:], 1.0),
+                          "val": [400, 0.8, 4], "trace": {"zeros": [2000, 30_000_000]},
+                          "seed": 5, "period": 100_000, "alpha": 8.0, "ticks": False,
+                          "initial_gear": 0},
+        "step_trace": {"profiles": m4, "plan": plan(m4, reps_c, gears_c, 160.0),
+                       "val": [400, 0.9, 0], "trace": {"step": [[30.0, 6.0], [150.0, 6.0],
+                                                                [30.0, 8.0]]},
+                       "seed": 3, "period": 100_000, "alpha": 8.0, "ticks": True,
+                       "initial_gear": 0},
+    }

@@ -25,7 +25,7 @@ REF = Path(os.environ.get("GEARSERVE_REF", ROOT / "baseline" / "_ref"))
 pytestmark = pytest.mark.gpu
 
 
-def _run(tmp_path, targets, engine_gate=True, timeout=1500):
+def _run(tmp_path, targets, engine_gate=True, timeout=1500, engine_run=False):
     if not (REF / "gearserve").is_dir() or not (REF / "tests").is_dir():
         pytest.skip(f"reference suite not installed at {REF} (tools/install_reference.sh)")
     calls = tmp_path / "calls.json"
@@ -33,6 +33,7 @@ def _run(tmp_path, targets, engine_gate=True, timeout=1500):
     env["PYTHONPATH"] = os.pathsep.join([str(REF), str(ROOT), str(ROOT / "tests")])
     env["GS_REFSUITE_CALLS"] = str(calls)
     env["GS_REFSUITE_ENGINE"] = "1" if engine_gate else "0"
+    env["GS_REFSUITE_RUN"] = "1" if engine_run else "0"
     env["PYTHONDONTWRITEBYTECODE"] = "1"
     env.setdefault("NUMBA_CACHE_DIR", str(tmp_path / "numba"))
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "refsuite_plugin",
@@ -72,3 +73,12 @@ def test_reference_engine_planner_serving(tmp_path):
                                "test_types.py", "test_lp.py", "test_formats.py", "test_cli.py"])
     assert calls.get("finish_batch", 0) > 0
     assert calls.get("evaluate_encoded", 0) > 0
+
+
+def test_reference_suite_with_device_replay(tmp_path):
+    """engine.run itself on the device (replay.py / gs_engine_run): the
+    engine worked examples, determinism, C3/C4/C7/C9 and the planner, whose
+    simulator probes (_probe_range, _burst_throughput) call engine.run."""
+    calls, _ = _run(tmp_path, ["test_engine.py", "test_acceptance.py", "test_planner.py",
+                               "test_serving.py", "test_cli.py"], engine_run=True)
+    assert calls.get("run", 0) > 0

@@ -1,0 +1,43 @@
+"""Host side of the device replay (no GPU): the traces it replays equal the
+reference's (scale_trace, constant/step traces, golden arrivals), and the
+device PCG64 stream it relies on is numpy's (restated in oracle.Pcg64)."""
+
+import numpy as np
+
+import golden_inputs as gi
+from conftest import golden
+from oracle import oracle
+
+
+def test_traces_match_the_reference_goldens():
+    from replay_cases import build
+    g = golden("replay.npz")
+    for name, case in gi.replay_cases().items():
+        _, _, trace, _, _ = build(case)
+        assert np.array_equal(trace.arrivals, g[f"{name}_arrivals"]), name
+        assert trace.duration_us == int(g[f"{name}_horizon"]), name
+
+
+def test_split_round_robin():
+    from paper_2406_14424_b200 import replay, synth
+    t = replay.scale_trace(synth.trace_from_counts(synth.bursty_counts(30, 1)), 500.0)
+    parts = replay.split_round_robin(t, 3)
+    assert sum(len(p) for p in parts) == len(t)
+    assert np.array_equal(np.sort(np.concatenate([p.arrivals for p in parts])), t.arrivals)
+
+
+def test_pcg64_restatement_matches_numpy():
+    """The draws gs_engine.cu reproduces: random(), integers(n) (Lemire, with
+    the bit generator's buffered 32-bit half), interleaved."""
+    for seed in range(4):
+        a = np.random.default_rng(seed)
+        b = oracle.Pcg64(seed)
+        for t in range(3000):
+            if t % 3 == 1:
+                n = 1 + t % 9
+                assert int(a.integers(n)) == b.integers(n)
+            else:
+                assert a.random() == b.random()
+        assert b.state() == (a.bit_generator.state["state"]["state"],
+                             a.bit_generator.state["has_uint32"],
+                             a.bit_generator.state["uinteger"])
