@@ -245,6 +245,36 @@ int gs_stage_gate_packed(const double* certainty, const uint8_t* correct,
                          void* stream);
 
 
+
+/* ------------------------------------------------------------------------
+ * SP1's cascade sampler (cascades.sample_cascades, src/cascades.py:166-193)
+ * on the device: numpy default_rng(seed)'s draws reproduced exactly, every
+ * singleton first, duplicates dropped in order.  One job per seed, one warp
+ * each.  order: device [n_models] model column of each cost rank (models
+ * sorted by (runtime_table[1], index)); grids: device, concatenated per model
+ * column, grid_off device [n_models + 1] (each grid < 65536 values).
+ * Outputs per job (capacity n_models + n_samples rows): stage_model /
+ * thresholds / n_stages in evaluate_encoded's encoding, grid_index (each
+ * non-final stage's threshold index into its grid, -1 pad).  table: zeroed
+ * scratch of 2 * table_cap u64, table_cap a power of two >= 2 * capacity.
+ * ---------------------------------------------------------------------- */
+typedef struct gs_sampler_job {
+  uint64_t rng_state_hi, rng_state_lo, rng_inc_hi, rng_inc_lo;
+  uint32_t rng_has_uint32, rng_uinteger;
+  int64_t n_samples;
+  int32_t* stage_model;          /* [cap, n_models]                        */
+  double* thresholds;            /* [cap, n_models]                        */
+  int32_t* n_stages;             /* [cap]                                  */
+  int32_t* grid_index;           /* [cap, n_models]                        */
+  uint64_t* table;               /* [2 * table_cap], zero on entry         */
+  int64_t table_cap;
+  int64_t* result;               /* [5]: count, rng state hi, lo, has_uint32, uinteger */
+} gs_sampler_job;
+
+int gs_sample_cascades(int32_t n_models, const int32_t* order, const double* grids,
+                       const int32_t* grid_off, const gs_sampler_job* jobs,
+                       int32_t n_jobs, void* stream);
+
 /* ------------------------------------------------------------------------
  * Replay engine: engine.run (src/engine.py:452-520) in virtual-clock mode on
  * the device, for many independent runs per launch (config-5 trace replays,

@@ -380,3 +380,34 @@ class Pcg64:
         if hi is None:
             lo, hi = 0, lo
         return lo + self.bounded(hi - 1 - lo)
+
+
+def sample_cascades_pcg(order_grid_len, n_samples: int, seed: int):
+    """sample_cascades (src/cascades.py:166-193) restated on Pcg64: returns
+    the list of (cost ranks, threshold grid indices) in output order --
+    the algorithm gs_sampler.cu runs.  order_grid_len[r] is the grid length
+    of the model at cost rank r.  Test infrastructure."""
+    M = len(order_grid_len)
+    g = Pcg64(seed)
+    out = [((r,), ()) for r in range(M)]
+    seen = set(out)
+    for _ in range(n_samples):
+        k = g.integers(1, M + 1)
+        taken, pick = set(), []
+        for j in range(M - k, M):
+            v = g.bounded(j)
+            if v not in taken:
+                taken.add(v)
+                pick.append(v)
+            else:
+                taken.add(j)
+                pick.append(j)
+        for i in range(k - 1, 0, -1):
+            jj = g.bounded(i)
+            pick[jj], pick[i] = pick[i], pick[jj]
+        ranks = tuple(sorted(pick))
+        gidx = tuple(g.bounded(order_grid_len[r] - 1) for r in ranks[:-1])
+        if (ranks, gidx) not in seen:
+            seen.add((ranks, gidx))
+            out.append((ranks, gidx))
+    return out, g.state()

@@ -345,3 +345,92 @@ def sweep_grid(validation, profiles: ProfileSet, grid: ThresholdGrid) -> GridFro
                          forward_fraction={m: float(frac[i, s]) for s, m in enumerate(c.stages)})
              for i, c in enumerate(cascs)]
     return GridFront(cascades=cascs, evals=evals, config_index=idx_h, n_configs=sweep.n_configs)
+
+
+# ------------------------------------------------------- device sampler --
+class gs_sampler_job(ctypes.Structure):
+    _fields_ = [("rng_state_hi", ctypes.c_uint64), ("rng_state_lo", ctypes.c_uint64),
+                ("rng_inc_hi", ctypes.c_uint64), ("rng_inc_lo", ctypes.c_uint64),
+                ("rng_has_uint32", ctypes.c_uint32), ("rng_uinteger", ctypes.c_uint32),
+                ("n_samples", ctypes.c_int64), ("stage_model", ctypes.c_void_p),
+                ("thresholds", ctypes.c_void_p), ("n_stages", ctypes.c_void_p),
+                ("grid_index", ctypes.c_void_p), ("table", ctypes.c_void_p),
+                ("table_cap", ctypes.c_int64), ("result", ctypes.c_void_p)]
+
+
+@dataclass
+class SampledCascades:
+    """Device-resident output of sample_cascades_device for one seed:
+    evaluate_encoded's encoding (model columns in profile order) plus each
+    non-final stage's threshold index into its grid."""
+
+    stage_model: torch.Tensor   # i32 [count, M], -1 padded
+    thresholds: torch.Tensor    # f64 [count, M], 0 padded
+    n_stages: torch.Tensor      # i32 [count]
+    grid_index: torch.Tensor    # i32 [count, M], -1 padded
+    count: int
+    rng_state: tuple            # (state, has_uint32, uinteger) after sampling
+
+    def cascades(self, model_ids) -> list[Cascade]:
+        sm, th, ns = (t.cpu().numpy() for t in (self.stage_model, self.thresholds,
+                                                 self.n_stages))
+        return [Cascade(stages=tuple(model_ids[int(m)] for m in sm[i, :ns[i]]),
+                        thresholds=tuple(float(x) for x in th[i, : ns[i] - 1]))
+                for i in range(self.count)]
+
+
+def sample_cascades_device(profiles: ProfileSet, grid: ThresholdGrid, n_samples: int,
+                           rng_seeds) -> list[SampledCascades]:
+    """sample_cascades (reference :166-193) on the device for one or many
+    seeds in one launch (gs_sample_cascades): per seed, the same cascades in
+    the same order as the host sampler, kept on the device in
+    evaluate_encoded's encoding."""
+    if n_samples < 1:
+        raise ValueError(f"n_samples must be >= 1, got {n_samples}")
+    seeds = [rng_seeds] if np.isscalar(rng_seeds) else list(rng_seeds)
+    dev = _lib.device()
+    ids = list(profiles.model_ids)
+    M = len(ids)
+    order = sorted(ids, key=lambda m: (profiles[m].runtime_table[1], profiles.index(m)))
+    order_cols = np.array([profiles.index(m) for m in order], dtype=np.int32)
+    vals, off = [], [0]
+    for m in ids:
+        g = grid.per_model[m]
+        if len(g) >= 65536:
+            raise ValueError("device sampler supports grids of < 65536 values")
+        vals.extend(float(x) for x in g)
+        off.append(len(vals))
+    d_order = _lib.to_device(order_cols, torch.int32)
+    d_grid = _lib.to_device(np.array(vals, dtype=np.float64), torch.float64)
+    d_off = _lib.to_device(np.array(off, dtype=np.int32), torch.int32)
+    cap = M + int(n_samples)
+    tcap = 1 << max(4, int(2 * cap - 1).bit_length())
+    outs, raw = [], b""
+    for seed in seeds:
+        st = np.random.default_rng(seed).bit_generator.state
+        s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+        o = {"sm": torch.empty((cap, M), dtype=torch.int32, device=dev),
+             "th": torch.empty((cap, M), dtype=torch.float64, device=dev),
+             "ns": torch.empty(cap, dtype=torch.int32, device=dev),
+             "gi": torch.empty((cap, M), dtype=torch.int32, device=dev),
+             "tab": torch.zeros(2 * tcap, dtype=torch.int64, device=dev),
+             "res": torch.zeros(5, dtype=torch.int64, device=dev)}
+        m64 = (1 << 64) - 1
+        job = gs_sampler_job(s >> 64, s & m64, inc >> 64, inc & m64, int(st["has_uint32"]),
+                             int(st["uinteger"]), int(n_samples), o["sm"].data_ptr(),
+                             o["th"].data_ptr(), o["ns"].data_ptr(), o["gi"].data_ptr(),
+                             o["tab"].data_ptr(), tcap, o["res"].data_ptr())
+        raw += bytes(job)
+        outs.append(o)
+    table = torch.from_numpy(np.frombuffer(raw, dtype=np.uint8).copy()).to(dev)
+    _lib.check(_lib.load().gs_sample_cascades(M, d_order.data_ptr(), d_grid.data_ptr(),
+                                              d_off.data_ptr(), table.data_ptr(), len(seeds),
+                                              _lib.stream_ptr()), "sample_cascades")
+    res = torch.stack([o["res"] for o in outs]).cpu().numpy()
+    out = []
+    for o, r in zip(outs, res):
+        n = int(r[0])
+        state = (int(np.uint64(r[1])) << 64) | int(np.uint64(r[2]))
+        out.append(SampledCascades(o["sm"][:n], o["th"][:n], o["ns"][:n], o["gi"][:n], n,
+                                   (state, int(r[3]), int(r[4]))))
+    return out

@@ -17,6 +17,14 @@ in-process to an unmodified `gearserve` import (no reference file edited):
       -> the gate on the device, one packed H2D / kernel / D2H per batch
          (gs_stage_gate_packed); completions, queue appends and the shared
          Generator's draws in the reference's order.
+  gearserve.cascades.sample_cascades      (src/cascades.py:166-193)
+      -> the device sampler (gs_sample_cascades, numpy's stream reproduced)
+         (also the name planner.py imports), with planner=True
+  gearserve.planner.sp1_search_cascades   (src/planner.py:365-390), with
+      planner=True -> the same steps, with every candidate's burst-throughput
+         probe (_burst_throughput :329-357, one engine.run each in the
+         reference) replayed in ONE device launch (replay.run_many) and put in
+         the planner's own probe cache before its loop reads them.
   gearserve.engine.run (src/engine.py:452-520), with engine_run=True
       -> the whole virtual-clock event loop on the device (replay.py,
          gs_engine_run), which the planner's probes call too
@@ -177,8 +185,93 @@ def _make_run(engine_mod, reference_run):
     return run
 
 
+def _make_sample_cascades(types_mod):
+    def sample_cascades(profiles, grid, n_samples, rng_seed):
+        """sample_cascades on the device, returned as reference Cascades."""
+        if n_samples < 1:
+            raise ValueError(f"n_samples must be >= 1, got {n_samples}")
+        CALLS["sample_cascades"] += 1
+        out = b200_cascades.sample_cascades_device(profiles, grid, n_samples, rng_seed)[0]
+        ids = list(profiles.model_ids)
+        sm, th, ns = (t.cpu().numpy() for t in (out.stage_model, out.thresholds, out.n_stages))
+        return [types_mod.Cascade(stages=tuple(ids[int(m)] for m in sm[i, :ns[i]]),
+                                  thresholds=tuple(float(x) for x in th[i, : ns[i] - 1]))
+                for i in range(out.count)]
+
+    return sample_cascades
+
+
+def _burst_probes(planner_mod, types_mod, state, cascades) -> None:
+    """Every uncached _burst_throughput probe (src/planner.py:329-357) of
+    `cascades` replayed in one launch; results go into state._burst_cache
+    under the planner's own key, computed as the reference computes them."""
+    P = planner_mod
+    placement = state.placement
+    keys, jobs = [], []
+    for c in cascades:
+        key = (placement.signature(), c)
+        if key in state._burst_cache or key in keys:
+            continue
+        if any(not placement.replicas_of(m) for m in c.stages):
+            continue  # the reference's own path caches 0.0
+        weights = {m: {r.replica_id: 1.0 for r in placement.replicas_of(m)} for m in c.stages}
+        gear = P._build_gear(state, 0, placement=placement, cascade=c, weights=weights, q=1)
+        plan = types_mod.GearPlan(placement=placement, slo=state.slo, qps_max=1.0, gears=(gear,))
+        n = state.config.burst_probe_samples
+        serial_us = sum(state.profiles[m].runtime_table[1] for m in c.stages)
+        duration = n * serial_us * 2 + 1_000_000
+        dp = replay.DevicePlan(plan, state.profiles, state.validation)
+        keys.append(key)
+        jobs.append(replay.Job(dp, np.zeros(n, dtype=np.int64), duration,
+                               replay.EngineConfig(seed=state.seed, enable_ticks=False)))
+    if not jobs:
+        return
+    CALLS["burst_probe_launches"] += 1
+    CALLS["burst_probes"] += len(jobs)
+    for key, res in zip(keys, replay.run_many(jobs)):
+        if res.completed == 0:
+            val = 0.0
+        else:
+            makespan = int(res.records["completion_us"].max())
+            val = res.completed / (makespan / 1_000_000) if makespan > 0 else 0.0
+        state._burst_cache[key] = val
+
+
+def _make_sp1(planner_mod, types_mod):
+    P = planner_mod
+
+    def sp1_search_cascades(err, state):
+        """SP1 (src/planner.py:365-390): sample, evaluate, Pareto, fallback
+        singletons, then the candidates' burst probes -- all on the device,
+        the probes in one batched replay launch."""
+        state.counters["sp1"] += 1
+        if not err.is_ok:
+            raise P.UserInfeasible(
+                "impossible to meet the SLO given the provided hardware resource: "
+                + (err.reason or "all cascade downgrades exhausted"))
+        sampled = P.sample_cascades(state.profiles, state.grid, state.config.n_samples,
+                                    rng_seed=state.seed + state.counters["sp1"] - 1)
+        evals = P.evaluate_cascades(sampled, state.validation, state.profiles)
+        by_cascade = dict(zip(sampled, evals))
+        keep = [c for c, _ in P.pareto_filter(list(by_cascade.items()))]
+        singles = [(c, by_cascade[c]) for c in map(P._singleton, state.profiles.model_ids)]
+        cheapest = min(singles, key=lambda p: (p[1].mean_cost, p[0].stages))[0]
+        most_accurate = max(singles, key=lambda p: (p[1].accuracy, -p[1].mean_cost))[0]
+        for c in [cheapest, most_accurate] + keep:
+            if c not in state.candidate_cascades:
+                state.candidate_cascades[c] = P.CandidateInfo(
+                    cascade=c, eval=by_cascade[c], throughput_qps=0.0,
+                    added_at_call=state.call_index)
+        _burst_probes(P, types_mod, state, [i.cascade for i in state.candidate_cascades.values()])
+        for info in state.candidate_cascades.values():
+            info.throughput_qps = P._burst_throughput(state, info.cascade, state.placement)
+        return P.PlannerError.ok(), state
+
+    return sp1_search_cascades
+
+
 def install(package: str = "gearserve", engine_gate: bool = True,
-            engine_run: bool = False) -> Counter:
+            engine_run: bool = False, planner: bool = False) -> Counter:
     """Route the reference package's hot path to the B200 library (no CPU
     fallback: the first routed call raises if the library or the GPU is
     missing).  Idempotent; returns the call counters."""
@@ -210,10 +303,27 @@ def install(package: str = "gearserve", engine_gate: bool = True,
     if engine_run:
         saved.append((engine, "run", engine.run))
         engine.run = _make_run(engine, engine.run)
+    if planner:
+        types_mod = importlib.import_module(f"{package}.types")
+        saved += [(cascades, "sample_cascades", cascades.sample_cascades),
+                  (planner, "sample_cascades", planner.sample_cascades),
+                  (planner, "sp1_search_cascades", planner.sp1_search_cascades)]
+        sampler = _make_sample_cascades(types_mod)
+        cascades.sample_cascades = sampler
+        planner.sample_cascades = sampler
+        sp1 = _make_sp1(planner, types_mod)
+        planner.sp1_search_cascades = sp1
+        # the coordinate-descent loop holds the function in its table (:757-762)
+        table = planner._SUBMODULES
+        saved.append((table, 0, table[0]))
+        table[0] = ("sp1", sp1)
     _INSTALLED[package] = saved
     return CALLS
 
 
 def uninstall(package: str = "gearserve") -> None:
     for obj, name, value in reversed(_INSTALLED.pop(package, [])):
-        setattr(obj, name, value)
+        if isinstance(obj, list):
+            obj[name] = value
+        else:
+            setattr(obj, name, value)

@@ -13,7 +13,8 @@ import os
 def pytest_configure(config):
     from paper_2406_14424_b200 import refbinding
     refbinding.install("gearserve", engine_gate=os.environ.get("GS_REFSUITE_ENGINE", "1") == "1",
-                       engine_run=os.environ.get("GS_REFSUITE_RUN", "0") == "1")
+                       engine_run=os.environ.get("GS_REFSUITE_RUN", "0") == "1",
+                       planner=os.environ.get("GS_REFSUITE_PLANNER", "0") == "1")
 
 
 def pytest_sessionfinish(session, exitstatus):

@@ -25,7 +25,7 @@ REF = Path(os.environ.get("GEARSERVE_REF", ROOT / "baseline" / "_ref"))
 pytestmark = pytest.mark.gpu
 
 
-def _run(tmp_path, targets, engine_gate=True, timeout=1500, engine_run=False):
+def _run(tmp_path, targets, engine_gate=True, timeout=1500, engine_run=False, planner=False):
     if not (REF / "gearserve").is_dir() or not (REF / "tests").is_dir():
         pytest.skip(f"reference suite not installed at {REF} (tools/install_reference.sh)")
     calls = tmp_path / "calls.json"
@@ -34,6 +34,7 @@ def _run(tmp_path, targets, engine_gate=True, timeout=1500, engine_run=False):
     env["GS_REFSUITE_CALLS"] = str(calls)
     env["GS_REFSUITE_ENGINE"] = "1" if engine_gate else "0"
     env["GS_REFSUITE_RUN"] = "1" if engine_run else "0"
+    env["GS_REFSUITE_PLANNER"] = "1" if planner else "0"
     env["PYTHONDONTWRITEBYTECODE"] = "1"
     env.setdefault("NUMBA_CACHE_DIR", str(tmp_path / "numba"))
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "refsuite_plugin",
@@ -78,7 +79,12 @@ def test_reference_engine_planner_serving(tmp_path):
 def test_reference_suite_with_device_replay(tmp_path):
     """engine.run itself on the device (replay.py / gs_engine_run): the
     engine worked examples, determinism, C3/C4/C7/C9 and the planner, whose
-    simulator probes (_probe_range, _burst_throughput) call engine.run."""
+    simulator probes (_probe_range, _burst_throughput) call engine.run; and
+    SP1 on the device: the sampler (gs_sample_cascades) and all of a call's
+    burst probes in one batched replay launch."""
     calls, _ = _run(tmp_path, ["test_engine.py", "test_acceptance.py", "test_planner.py",
-                               "test_serving.py", "test_cli.py"], engine_run=True)
+                               "test_serving.py", "test_cli.py", "test_cascades.py"],
+                    engine_run=True, planner=True)
     assert calls.get("run", 0) > 0
+    assert calls.get("sample_cascades", 0) > 0
+    assert calls.get("burst_probe_launches", 0) > 0

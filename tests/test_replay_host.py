@@ -41,3 +41,23 @@ def test_pcg64_restatement_matches_numpy():
         assert b.state() == (a.bit_generator.state["state"]["state"],
                              a.bit_generator.state["has_uint32"],
                              a.bit_generator.state["uinteger"])
+
+
+def test_sampler_restatement_matches_numpy_sampler():
+    """oracle.sample_cascades_pcg (the algorithm gs_sampler.cu runs) equals
+    the numpy sampler (the reference's stream), incl. 1- and 2-value grids
+    (no draw / one-bit draws) and M = 1..6."""
+    from paper_2406_14424_b200.cascades import ThresholdGrid, sample_cascades
+    from paper_2406_14424_b200 import synth
+    for M, lens, seed, n in ((3, (10, 10, 10), 0, 500), (1, (4,), 3, 20), (4, (1, 2, 7, 1), 5, 400),
+                             (6, (3, 100, 1, 2, 50, 9), 9, 300)):
+        prof = synth.make_profiles(n_models=M, cost_ratios=tuple(float(4 ** j) for j in range(M)))
+        ids = prof.model_ids
+        grid = ThresholdGrid({m: tuple(float(x) for x in np.arange(lens[j]) / 100.0)
+                              for j, m in enumerate(ids)})
+        want = sample_cascades(prof, grid, n, rng_seed=seed)
+        got, _ = oracle.sample_cascades_pcg(lens, n, seed)  # cost order == column order here
+        assert len(got) == len(want)
+        for (ranks, gidx), c in zip(got, want):
+            assert tuple(ids[r] for r in ranks) == c.stages
+            assert tuple(grid.per_model[ids[r]][i] for r, i in zip(ranks, gidx)) == c.thresholds
