@@ -416,6 +416,8 @@ def run_ours(args, world, rank, local):
             line["config3"] = c3 = _guarded(config3_bench, args, dev)
             if "entropy" in c3:  # the online stage step at the config-3 shape
                 line["stage_step"] = {k: c3[k]["stage_step"] for k in ("entropy", "margin")}
+        if not args.skip_config5:
+            line["config5"] = _guarded(config5_bench, args, dev)
         line["host"] = host_info()
         print(json.dumps(line), flush=True)
 
@@ -993,6 +995,153 @@ def config3_e2e(logits, corr, cost1, dev):
                     "host wall clock, best of 3"}
 
 
+def config5_bench(args, dev):
+    """BASELINE configs[4]: an Azure-like bursty trace (20 min of lognormal
+    per-second levels, default_rng(0), scaled to 7,600 max QPS with
+    formats.scale_trace semantics: 1.32M requests) replayed through the
+    serving engine -- batched routing, the certainty gate, gear switching
+    every 100 ms -- by 8 independent replica groups (synth.replica_group_plan,
+    request i -> group i % 8), each one engine.run (virtual clock) on the
+    device: replay.run_many, one launch, one warp per group.  The replay is a
+    sequential event loop per group, so a group runs on one warp; the GPU's
+    width goes to independent groups and probes (the `probes` sub-leg: 1,024
+    SP1 burst-throughput probes, src/planner.py:329-357, in one launch).
+    CPU: the reference engine loop (oracle.engine_run restatement, and the
+    shipped reference from baseline/_ref when present) on a bounded prefix of
+    group 0's trace, one core; parity: that prefix's records, device vs CPU."""
+    import torch
+
+    from oracle import oracle
+    from paper_2406_14424_b200 import replay, synth
+    from paper_2406_14424_b200.types import (Cascade, Gear, GearPlan, ValidationArrays,
+                                             WorkloadTrace)
+    groups = 8
+    trace = replay.scale_trace(synth.trace_from_counts(synth.bursty_counts(1200, 0)), 7600.0)
+    parts = replay.split_round_robin(trace, groups)
+    prof, plan = synth.replica_group_plan(qps_max=7600.0 / groups)
+    cert, corr = synth.validation_matrices(4, 100_000, 0.8, 5)
+    val = ValidationArrays(prof.model_ids, certainty=cert, correct=corr)
+    dp = replay.DevicePlan(plan, prof, val)
+    cfg = replay.EngineConfig(seed=0)
+    jobs = [replay.Job(dp, p.arrivals, p.duration_us, replay.EngineConfig(seed=g))
+            for g, p in enumerate(parts)]
+    replay.run_many(jobs[:1])  # warm
+    torch.cuda.synchronize()
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a_ev.record()
+    bufs = replay.launch(jobs)
+    b_ev.record()
+    torch.cuda.synchronize()
+    ms = a_ev.elapsed_time(b_ev)
+    res = [replay.collect(j, b) for j, b in zip(jobs, bufs)]
+    done = sum(r.completed for r in res)
+    routed = sum(int(r.records["stages_executed"].sum()) for r in res)
+    gear_hist = np.bincount(np.concatenate([r.windows["gear_after"] for r in res]), minlength=4)
+    t = time.perf_counter()
+    replay.run_many(jobs)
+    e2e_ms = (time.perf_counter() - t) * 1e3
+    out = {"workload": "cfg5: 20-min bursty trace scaled to 7,600 max QPS (1.32M requests), "
+                       "8 replica groups x (4-model cascade on 4 devices, 4 gears), "
+                       "engine.run virtual clock per group",
+           "requests": len(trace), "groups": groups, "ms": ms,
+           "requests_per_s": len(trace) / (ms * 1e-3),
+           "routed_samples_per_s": routed / (ms * 1e-3), "completed": done,
+           "gear_windows": gear_hist.tolist(),
+           "e2e": {"ms": e2e_ms, "value": routed / (e2e_ms * 1e-3), "unit": "routed samples/s",
+                   "path": "replay.run_many: plan tables + traces H2D, one launch, records / "
+                           "windows / counters D2H; host wall clock"},
+           "launches": 1, "bound": "latency: one sequential event loop per group (warp)"}
+    # CPU: the reference engine loop on a prefix of group 0, one core
+    n_cpu = 60_000
+    sub = WorkloadTrace(parts[0].arrivals[:n_cpu],
+                        duration_us=int(parts[0].arrivals[n_cpu - 1]) // 1_000_000 * 1_000_000 +
+                        1_000_000)
+    ids = list(prof.model_ids)
+    runtime = [[0] + [prof[m].runtime_us(b) for b in range(1, 9)] for m in ids]
+    t = time.perf_counter()
+    ref = oracle.engine_run(plan, sub, cert, corr, runtime, [8] * 4,
+                            {m: j for j, m in enumerate(ids)}, seed=0)
+    cpu_s = time.perf_counter() - t
+    dev_sub = replay.run_many([replay.Job(dp, sub.arrivals, sub.duration_us, cfg)])[0]
+    r = dev_sub.records
+    got = np.stack([r["request_id"], dev_sub.arrival_us[r["request_id"]], r["completion_us"],
+                    r["stages_executed"], r["correct"], r["gear_index"]], 1).astype(np.int64)
+    routed_cpu = int(ref["records"][:, 3].sum())
+    out["parity_prefix"] = bool(np.array_equal(got, ref["records"]))
+    out["cpu_baseline"] = {"value": routed_cpu / cpu_s, "unit": "routed samples/s", "cores": 1,
+                           "kind": "port", "requests_per_s": n_cpu / cpu_s,
+                           "sample": f"first {n_cpu} requests of group 0, oracle.engine_run "
+                                     "(engine.run's loop restated), one core"}
+    refmod = _ref_gearserve()
+    if refmod is not None:
+        try:
+            from gearserve import engine as reng
+            from gearserve import types as rt
+            rplan = rt.GearPlan(
+                placement=rt.Placement([rt.Replica(x.replica_id, x.model_id, x.device_id)
+                                        for x in plan.placement.replicas]),
+                slo=rt.Slo.latency(400_000), qps_max=plan.qps_max,
+                gears=tuple(rt.Gear(rt.Cascade(g.cascade.stages, g.cascade.thresholds),
+                                    dict(g.min_queue_length), dict(g.load_weights))
+                            for g in plan.gears))
+            from gearserve import synth as rsynth
+            rprof = rsynth.make_profiles(4, (1.0, 4.0, 16.0, 64.0), base_runtime_us=1_000)
+            rval = rsynth.make_validation(rprof, n_samples=2000, easy_fraction=0.8, seed=5)
+            rsub = rt.WorkloadTrace(sub.arrivals[:20_000])
+            t = time.perf_counter()
+            m = reng.run(rplan, rsub, rval, rprof, config=reng.EngineConfig(seed=0))
+            dt = time.perf_counter() - t
+            out["cpu_baseline"]["reference_engine_run"] = {
+                "routed_samples_per_s": sum(x.stages_executed for x in m.per_request) / dt,
+                "requests_per_s": len(rsub) / dt, "cores": 1, "kind": "reference",
+                "sample": "first 20k requests of group 0, baseline/_ref gearserve.engine.run"}
+        except Exception as e:  # noqa: BLE001
+            out["cpu_baseline"]["reference_engine_run"] = {"error": f"{type(e).__name__}: {e}"}
+    # probes: SP1 burst-throughput probes (_burst_throughput), 1,024 per launch
+    cands = []
+    rng = np.random.default_rng(0)
+    for _ in range(1024):
+        k = int(rng.integers(1, 5))
+        st = tuple(sorted(rng.choice(4, size=k, replace=False)))
+        stages = tuple(f"m{i}" for i in st)
+        thr = tuple(float(x) for x in np.round(rng.uniform(0.6, 0.9, k - 1), 3))
+        cands.append(Cascade(stages, thr))
+    pjobs = []
+    for c in cands:
+        w = {m: {r.replica_id: 1.0 for r in plan.placement.replicas_of(m)} for m in c.stages}
+        q = {r.replica_id: 1 for m in c.stages for r in plan.placement.replicas_of(m)}
+        pplan = GearPlan(placement=plan.placement, slo=None, qps_max=1.0, gears=(Gear(c, q, w),))
+        serial = sum(prof[m].runtime_table[1] for m in c.stages)
+        pjobs.append(replay.Job(replay.DevicePlan(pplan, prof, val), np.zeros(256, np.int64),
+                                256 * serial * 2 + 1_000_000,
+                                replay.EngineConfig(seed=0, enable_ticks=False)))
+    replay.run_many(pjobs[:4])
+    torch.cuda.synchronize()
+    a_ev.record()
+    pb = replay.launch(pjobs)
+    b_ev.record()
+    torch.cuda.synchronize()
+    pms = a_ev.elapsed_time(b_ev)
+    t = time.perf_counter()
+    for c in cands[:64]:
+        w = {m: {r.replica_id: 1.0 for r in plan.placement.replicas_of(m)} for m in c.stages}
+        q = {r.replica_id: 1 for m in c.stages for r in plan.placement.replicas_of(m)}
+        pplan = GearPlan(placement=plan.placement, slo=None, qps_max=1.0, gears=(Gear(c, q, w),))
+        serial = sum(prof[m].runtime_table[1] for m in c.stages)
+        oracle.engine_run(pplan, WorkloadTrace(np.zeros(256, np.int64),
+                                               duration_us=256 * serial * 2 + 1_000_000),
+                          cert, corr, runtime, [8] * 4, {m: j for j, m in enumerate(ids)},
+                          seed=0, enable_ticks=False)
+    probe_cpu = 64 / (time.perf_counter() - t)
+    out["probes"] = {"probes": len(pjobs), "ms": pms, "probes_per_s": len(pjobs) / (pms * 1e-3),
+                     "requests_per_probe": 256, "launches": 1,
+                     "cpu_baseline": {"value": probe_cpu, "unit": "probes/s", "cores": 1,
+                                      "kind": "port",
+                                      "sample": "64 of the probes, oracle.engine_run, one core"}}
+    del pb
+    return out
+
+
 def cpu_baseline(cert, corr, grids, cost1, args):
     """Oracle port of _evaluate_numba on a bounded config sample, all threads."""
     from oracle import oracle
@@ -1063,6 +1212,7 @@ def main():
     ap.add_argument("--skip-config1", action="store_true", help="skip the 3-model cfg1 leg")
     ap.add_argument("--skip-list", action="store_true", help="skip the list-path legs")
     ap.add_argument("--skip-config3", action="store_true", help="skip the cfg3 cascade leg")
+    ap.add_argument("--skip-config5", action="store_true", help="skip the cfg5 replay leg")
     ap.add_argument("--flush", choices=["write", "clean", "none"], default="write",
                     help="L2 eviction between timed steps (see flush_l2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,

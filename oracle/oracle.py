@@ -411,3 +411,148 @@ def sample_cascades_pcg(order_grid_len, n_samples: int, seed: int):
             seen.add((ranks, gidx))
             out.append((ranks, gidx))
     return out, g.state()
+
+
+# --------------------------------------------------------- engine.run ---
+def engine_run(plan, trace, cert, corr, runtime, max_batch, model_index, seed: int = 0,
+               period_us: int = 100_000, alpha: float = 8.0, initial_gear: int = 0,
+               enable_ticks: bool = True):
+    """engine.run (src/engine.py:452-520) in virtual-clock mode restated over
+    plain arrays: the event heap, submit (:299-319), scan_device /
+    choose_dispatch (:321-353, :248-253), finish_batch (:355-383), tick /
+    maybe_switch_gear (:389-410, :123-133), nearest-rank p95 (:111-120).
+    plan: objects with .placement.replicas (replica_id, model_id, device_id),
+    .gears (cascade.stages / thresholds, min_queue_length, load_weights) and
+    .qps_max; runtime[model][batch] µs; returns a dict of arrays.  Test
+    infrastructure (the checker of gs_engine.cu and the config-5 CPU
+    baseline); the reference is pure Python, so this loop is its cost model."""
+    import heapq
+    import math
+    from collections import deque
+    reps = list(plan.placement.replicas)
+    R = len(reps)
+    devices, dindex = [], {}
+    for r in reps:
+        if r.device_id not in dindex:
+            dindex[r.device_id] = len(devices)
+            devices.append(r.device_id)
+    device_of = [dindex[r.device_id] for r in reps]
+    model_of = [model_index[r.model_id] for r in reps]
+    rid_of = [r.replica_id for r in reps]
+    gears = []
+    for g in plan.gears:
+        st = g.cascade.stages
+        ridx = [[i for i, r in enumerate(reps) if r.model_id == m] for m in st]
+        cum = [np.cumsum([g.load_weights[m].get(reps[i].replica_id, 0.0) for i in idx])
+               for m, idx in zip(st, ridx)]
+        minq = [1] * R
+        for rid, q in g.min_queue_length.items():
+            minq[rid_of.index(rid)] = q
+        gears.append(([model_index[m] for m in st], list(g.cascade.thresholds) + [None],
+                      ridx, cum, minq))
+    rng = np.random.default_rng(seed)
+
+    def choose(cum):
+        total = cum[-1]
+        if total <= 0.0:
+            return int(rng.integers(len(cum)))
+        x = rng.random() * total
+        return int(np.searchsorted(cum, x, side="right").clip(0, len(cum) - 1))
+
+    queues = [deque() for _ in range(R)]
+    busy = [False] * len(devices)
+    item_stage, item_gear = {}, {}
+    arrivals_t = np.asarray(trace.arrivals, dtype=np.int64)
+    n_rec = cert.shape[0]
+    cur = initial_gear
+    rec, wins = [], []
+    batches = {}
+    st = {"arrivals": 0, "completed": 0, "in_flight": 0}
+    win = {"arr": 0, "lat": [], "ok": 0}
+    heap, seq = [], 0
+    horizon = trace.duration_us
+    if enable_ticks:
+        t = period_us
+        while t <= horizon:
+            heapq.heappush(heap, (t, 1, seq, "tick", None))
+            seq += 1
+            t += period_us
+    nxt = 0
+    if len(arrivals_t):
+        heapq.heappush(heap, (int(arrivals_t[0]), 2, seq, "arrival", 0))
+        seq += 1
+        nxt = 1
+    while heap:
+        t, _, _, kind, arg = heapq.heappop(heap)
+        if t > horizon:
+            break
+        if kind == "arrival":
+            rid = arg
+            g = gears[cur]
+            item_stage[rid], item_gear[rid] = 0, cur
+            ridx = int(g[2][0][choose(g[3][0])])
+            queues[ridx].append(rid)
+            st["arrivals"] += 1
+            win["arr"] += 1
+            touched = {device_of[ridx]}
+            if nxt < len(arrivals_t):
+                heapq.heappush(heap, (int(arrivals_t[nxt]), 2, seq, "arrival", nxt))
+                seq += 1
+                nxt += 1
+        elif kind == "complete":
+            d, items = arg
+            busy[d] = False
+            st["in_flight"] -= len(items)
+            touched = {d}
+            for rid in items:
+                g = gears[item_gear[rid]]
+                s = item_stage[rid]
+                m = g[0][s]
+                last = s == len(g[0]) - 1
+                row = rid % n_rec
+                if last or cert[row, m] >= g[1][s]:
+                    ok = bool(corr[row, m])
+                    rec.append((rid, int(arrivals_t[rid]), t, s + 1, int(ok), item_gear[rid]))
+                    st["completed"] += 1
+                    win["lat"].append(t - int(arrivals_t[rid]))
+                    win["ok"] += 1 if ok else 0
+                else:
+                    item_stage[rid] = s + 1
+                    ridx = int(g[2][s + 1][choose(g[3][s + 1])])
+                    queues[ridx].append(rid)
+                    touched.add(device_of[ridx])
+        else:
+            qps = win["arr"] / (period_us / 1_000_000)
+            q0 = sum(len(queues[r]) for r in gears[cur][2][0])
+            cand = min(int(math.floor(qps * len(gears) / plan.qps_max)), len(gears) - 1)
+            after = cur if (cand < cur and qps < alpha * q0) else cand
+            lat = win["lat"]
+            p95 = -1
+            if lat:
+                arr = np.sort(np.asarray(lat))
+                p95 = int(arr[max(1, math.ceil(95 / 100 * arr.size)) - 1])
+            wins.append((t, qps, q0, cur, cand, after, len(lat), p95,
+                         (win["ok"] / len(lat)) if lat else float("nan")))
+            cur = after
+            win = {"arr": 0, "lat": [], "ok": 0}
+            touched = set(range(len(devices)))
+        for d in sorted(touched):
+            if busy[d]:
+                continue
+            cands = [(item_stage[queues[r][0]], -len(queues[r]), rid_of[r], r) for r in range(R)
+                     if device_of[r] == d and queues[r] and len(queues[r]) >= gears[cur][4][r]]
+            if not cands:
+                continue
+            r = min(cands)[3]
+            m = model_of[r]
+            size = min(len(queues[r]), max_batch[m])
+            items = [queues[r].popleft() for _ in range(size)]
+            busy[d] = True
+            st["in_flight"] += size
+            batches[(m, size)] = batches.get((m, size), 0) + 1
+            heapq.heappush(heap, (t + int(runtime[m][size]), 0, seq, "complete", (d, items)))
+            seq += 1
+    return {"records": np.array(rec, dtype=np.int64).reshape(-1, 6),
+            "windows": wins, "arrivals": st["arrivals"], "completed": st["completed"],
+            "in_flight": st["in_flight"], "queue_len": [len(q) for q in queues],
+            "batches": batches, "rng_state": rng.bit_generator.state}

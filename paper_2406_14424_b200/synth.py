@@ -216,3 +216,29 @@ def step_trace(steps):
     if not parts:
         raise ValueError("step trace has no arrivals")
     return WorkloadTrace(np.concatenate(parts), duration_us=offset)
+
+
+def replica_group_plan(qps_max: float = 950.0, prefix: str = ""):
+    """Config 5's replica group (one per GPU): a Sentiment-140-shaped 4-model
+    cascade (make_profiles(4, cost ratios 1:4:16:64, 1 ms base)) on four
+    devices, and one gear per QPS quarter, from the full cascade at low load
+    to the cheapest model alone at the top range (the gear switching the
+    engine's tick applies).  Returns (profiles, plan)."""
+    from .types import Cascade, Gear, GearPlan, Placement, Replica
+    prof = make_profiles(n_models=4, cost_ratios=(1.0, 4.0, 16.0, 64.0), base_runtime_us=1_000)
+    d = [f"{prefix}d{i}" for i in range(4)]
+    reps = [Replica(f"m0@{d[0]}", "m0", d[0]), Replica(f"m0@{d[1]}", "m0", d[1]),
+            Replica(f"m1@{d[1]}", "m1", d[1]), Replica(f"m1@{d[2]}", "m1", d[2]),
+            Replica(f"m2@{d[2]}", "m2", d[2]), Replica(f"m3@{d[3]}", "m3", d[3])]
+    w0 = {f"m0@{d[0]}": 2.0, f"m0@{d[1]}": 1.0}
+    w1 = {f"m1@{d[1]}": 1.0, f"m1@{d[2]}": 1.0}
+    gears = (
+        Gear(Cascade(("m0", "m1", "m2", "m3"), (0.62, 0.7, 0.75)), {f"m0@{d[0]}": 2},
+             {"m0": w0, "m1": w1, "m2": {f"m2@{d[2]}": 1.0}, "m3": {f"m3@{d[3]}": 1.0}}),
+        Gear(Cascade(("m0", "m1", "m2"), (0.66, 0.72)), {f"m0@{d[0]}": 4},
+             {"m0": w0, "m1": w1, "m2": {f"m2@{d[2]}": 1.0}}),
+        Gear(Cascade(("m0", "m1"), (0.7,)), {f"m0@{d[0]}": 8, f"m0@{d[1]}": 4},
+             {"m0": w0, "m1": w1}),
+        Gear(Cascade(("m0",), ()), {f"m0@{d[0]}": 8, f"m0@{d[1]}": 8}, {"m0": w0}),
+    )
+    return prof, GearPlan(placement=Placement(reps), slo=None, qps_max=qps_max, gears=gears)

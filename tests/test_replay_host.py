@@ -61,3 +61,27 @@ def test_sampler_restatement_matches_numpy_sampler():
         for (ranks, gidx), c in zip(got, want):
             assert tuple(ids[r] for r in ranks) == c.stages
             assert tuple(grid.per_model[ids[r]][i] for r, i in zip(ranks, gidx)) == c.thresholds
+
+
+def test_oracle_engine_matches_reference_goldens():
+    """oracle.engine_run (the CPU checker of the device replay) equals the
+    reference engine.run goldens on every scenario."""
+    from replay_cases import build
+    g = golden("replay.npz")
+    for name, case in gi.replay_cases().items():
+        prof, val, trace, plan, cfg = build(case)
+        ids = list(prof.model_ids)
+        cap = max(prof[m].max_profiled_batch for m in ids)
+        runtime = [[0] + [prof[m].runtime_us(b) for b in range(1, cap + 1)] for m in ids]
+        out = oracle.engine_run(plan, trace, val.certainty, val.correct, runtime,
+                                [prof[m].max_profiled_batch for m in ids],
+                                {m: j for j, m in enumerate(ids)}, seed=cfg.seed,
+                                period_us=cfg.measure_period_us, alpha=cfg.alpha,
+                                initial_gear=cfg.initial_gear_index, enable_ticks=cfg.enable_ticks)
+        assert np.array_equal(out["records"], g[f"{name}_rec"]), name
+        w = np.array([[x[0], x[2], x[3], x[4], x[5], x[4], x[6], x[7]] for x in out["windows"]],
+                     dtype=np.int64).reshape(-1, 8)
+        assert np.array_equal(w, g[f"{name}_win"]), name
+        wf = np.array([[x[1], x[8]] for x in out["windows"]]).reshape(-1, 2)
+        assert np.array_equal(wf, g[f"{name}_winf"], equal_nan=True), name
+        assert out["queue_len"] == g[f"{name}_qlen"].tolist(), name
