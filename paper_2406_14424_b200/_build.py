@@ -38,15 +38,18 @@ def _headers() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
-def build(verbose: bool = False, force: bool = False, phase_timing: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, phase_timing: bool = False,
+          defines: tuple = (), tag: str = "") -> Path:
     """Compile every kernel source for sm_100a and link the shared library.
     phase_timing: a separate build (libgearserve_b200_phases.so, objects in
     _objs_phases/) whose kernels stamp %globaltimer at phase boundaries
     (GS_PHASE_TIMING; read back with gs_debug_phases) for tools/phase_probe.py."""
     nvcc = _nvcc()
-    build_dir = BUILD.with_name("_objs_phases") if phase_timing else BUILD
-    lib_path = LIB.with_name("libgearserve_b200_phases.so") if phase_timing else LIB
-    extra = ["-DGS_PHASE_TIMING"] if phase_timing else []
+    build_dir = BUILD.with_name("_objs_phases" + tag) if phase_timing else BUILD
+    lib_path = LIB.with_name(f"libgearserve_b200_phases{tag}.so") if phase_timing else LIB
+    extra = (["-DGS_PHASE_TIMING"] if phase_timing else []) + [f"-D{d}" for d in defines]
+    if defines and not phase_timing:
+        raise ValueError("experiment defines are for phase-timing builds only")
     build_dir.mkdir(exist_ok=True)
     hdr_mtime = max((p.stat().st_mtime for p in _headers()), default=0.0)
     objs = []

@@ -6,8 +6,8 @@ import ctypes, os, sys
 import numpy as np
 sys.path.insert(0, ".")
 from paper_2406_14424_b200 import _build
-lib_path = _build.build(phase_timing=True)
-os.environ["GS_LIB_PATH"] = str(lib_path)
+if not os.environ.get("GS_LIB_PATH"):
+    os.environ["GS_LIB_PATH"] = str(_build.build(phase_timing=True))
 import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2406_14424_b200 import _lib  # noqa: E402
