@@ -52,6 +52,7 @@
 #include "gs_common.cuh"
 #include "gs_grid4.cuh"
 #include "gs_grid_lut.cuh"
+#include "gs_sweep5.cuh"
 
 namespace gs {
 namespace {
@@ -75,6 +76,7 @@ struct Plan {
   size_t offH16 = 0, offHF = 0, offF = 0, offHP = 0, offP = 0, offFlag = 0, bytes = 0;
   bool g4 = false;    // M == 4 fast path (gs_grid4.cu)
   bool walk = false;  // M == 4: fused b_0 prefix + full-structure scoring
+  bool w5 = false;    // M == 5: slab-sorted build + b_0 walk (gs_sweep5.cu)
   size_t offFaces = 0;
 };
 
@@ -152,6 +154,14 @@ int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   p->g4 = grid4_supported(n_rec, M, p->glen);
   if (p->g4) {
     p->bytes = grid4_layout(p->glen, n_rec).bytes;
+    return GS_OK;
+  }
+  p->w5 = w5_supported(n_rec, M, p->glen);
+  if (p->w5) {
+    const W5Layout L = w5_layout(p->glen, n_rec);
+    p->bytes = L.bytes;
+    p->offFaces = L.offFaces;
+    p->offP = L.offP;
     return GS_OK;
   }
   p->walk = M == 4 && p->dims[0] <= 160 &&
@@ -1408,6 +1418,9 @@ extern "C" int gs_grid_plan(int64_t n_rec, int32_t n_models, const int32_t* grid
   if (p.g4) {
     info->build_launches = 2;  // g4_sort + g4_gather (one-shot) or g4_hist + g4_plane
     info->eval_launches = 1;   // g4_eval
+  } else if (p.w5) {
+    info->build_launches = 5;  // w5_bin, w5_scan, w5_scatter, w5_slab (two variants)
+    info->eval_launches = 2;   // w5_walk + the regular eval
   } else {
     // mirrors gs_grid_build / prefix_table / gs_grid_eval below
     int b = 1 + (n_rec >= 65536 ? 1 : 0);
@@ -1449,6 +1462,11 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
     return GS_OK;
   }
   if (passes != 3) return GS_EUNSUPPORTED;
+  if (p.w5) {
+    GS_CUDA_TRY(w5_build(certainty, correct, n_rec, grids, p.glen, ws,
+                         (flags & GS_GRID_WORKSPACE_DIRTY) != 0, st));
+    return GS_OK;
+  }
   float* F = reinterpret_cast<float*>(ws + p.offHF);
   uint32_t* P = reinterpret_cast<uint32_t*>(ws + p.offHP);
   auto* H16 = reinterpret_cast<unsigned long long*>(ws + p.offH16);
@@ -1620,7 +1638,16 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
     reg_end = std::min<int64_t>(reg_end, w.sb);
     if (reg_end <= config_begin) return GS_OK;
   }
-  if (p.M == 5 && p.glen[3] <= kFull5MaxRow && p.cellsP > 0) {
+  if (p.w5) {
+    // the b_0 walk scores the full cascade and leaves the face cells the
+    // regular eval reads (it runs even when the range holds no full-cascade
+    // config)
+    const int64_t sb = p.struct_begin[p.n_struct - 1];
+    GS_CUDA_TRY(w5_walk(n_rec, p.glen, sb, cost1, config_begin, config_count, accuracy, mean_cost,
+                        forward_frac, n_correct, ws, st));
+    reg_end = std::min<int64_t>(reg_end, sb);
+    if (reg_end <= config_begin) return GS_OK;
+  } else if (p.M == 5 && p.glen[3] <= kFull5MaxRow && p.cellsP > 0) {
     // the full cascade (the last structure): full5_eval_kernel
     Full5Args f{};
     f.g0 = p.glen[0];
@@ -1653,7 +1680,7 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
   a.cfg_count = reg_end - config_begin;
   a.row_lo = global_row(p, a.row_begin, config_begin);
   a.row_hi = global_row(p, a.row_begin, reg_end - 1) + 1;
-  a.F = reinterpret_cast<const uint4*>(ws + (p.walk ? p.offFaces : p.offF));
+  a.F = reinterpret_cast<const uint4*>(ws + ((p.walk || p.w5) ? p.offFaces : p.offF));
   a.P = reinterpret_cast<const uint4*>(ws + p.offP);
   a.cost1 = cost1;
   a.acc = accuracy;

@@ -499,3 +499,57 @@ def test_batched_sweep_rejects_bad_input():
         BatchedSweep(rng.random((2, 50, 4)), np.zeros((2, 50, 4), np.uint8), [g, g], cost1)
     res = BatchedSweep(cert, corr, [g, g], cost1).run()
     assert tuple(res.accuracy.shape) == (2, 3 + 2 * 2 + 3 + 2 * 3)
+
+
+@pytest.mark.parametrize("n_rec,glen,ties", [
+    (3000, (7, 5, 9, 11, 3), False), (5000, (12, 1, 6, 20, 4), True), (1, (1, 1, 1, 1, 1), False),
+    (80_000, (2, 3, 2, 4, 2), True)])
+def test_five_model_slab_walk_vs_oracle(n_rec, glen, ties):
+    """The five-model path (gs_sweep5.cu: slab-sorted build, b0 walk, faces
+    for the regular eval) over uneven grids, heavy ties, a b0 slab past 2^16
+    records (the 21-bit variant of the slab pass), every config vs the
+    oracle walk."""
+    rng = np.random.default_rng(n_rec + sum(glen))
+    cert = np.round(rng.random((n_rec, 5)), 1) if ties else rng.random((n_rec, 5))
+    corr = (rng.random((n_rec, 5)) < 0.6).astype(np.uint8)
+    grids = [np.concatenate([[0.0], np.sort(rng.choice(np.unique(cert[:, j]),
+                                                       size=min(g - 1, len(np.unique(cert[:, j]))),
+                                                       replace=False))])
+             if g > 1 else np.array([0.0]) for j, g in enumerate(glen)]
+    grids = [np.unique(g) for g in grids]
+    cost1 = rng.uniform(100, 5000, 5)
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, cost1)
+    assert sw.info.build_launches == 5, "the five-model slab path did not run"
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
+    assert np.array_equal(acc, want[0])
+    assert np.array_equal(cost, want[1])
+    assert np.array_equal(frac, want[2])
+    idx, _ = sw.pareto()
+    assert np.array_equal(idx.cpu().numpy(), np.flatnonzero(oracle.pareto_keep(want[0], want[1])))
+
+
+def test_config4b_shape_sampled_vs_oracle():
+    """Config 4b (5 models, 100-level grids, 100k records, C = 105,101,005):
+    the slab path, configs of every structure sampled against the oracle."""
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.cascades import grid_values
+    from paper_2406_14424_b200.gridsweep import GridSweep, structures
+    cert, corr = synth.validation_matrices(5, 100_000, 0.8, 5)
+    grids = [np.array(grid_values(cert[:, j], 100)) for j in range(5)]
+    cost1 = np.array([1.0, 4.0, 16.0, 64.0, 256.0])
+    sw = GridSweep(cert, corr, grids, cost1)
+    assert sw.n_configs == 105_101_005 and sw.info.build_launches == 5
+    res = sw.evaluate()
+    rng = np.random.default_rng(1)
+    pick = []
+    for _, b, n in structures(5, sw.grid_len):
+        pick.extend(sorted(set(rng.integers(b, b + n, size=min(n, 24)).tolist())))
+    pick = np.array(pick)
+    sm, thr, ns = (t.cpu().numpy() for t in sw.decode(pick))
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
+    import torch
+    ip = torch.from_numpy(pick).cuda()
+    assert np.array_equal(res.accuracy[ip].cpu().numpy(), want[0])
+    assert np.array_equal(res.mean_cost[ip].cpu().numpy(), want[1])
+    assert np.array_equal(res.forward_frac[ip].cpu().numpy(), want[2])
