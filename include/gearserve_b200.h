@@ -342,8 +342,8 @@ typedef struct gs_engine_job {
   int32_t enable_ticks;
   int64_t measure_period_us;
   double alpha;
-  int32_t* item_next;            /* scratch [n_arrivals]                   */
-  uint32_t* item_meta;           /* scratch [n_arrivals]                   */
+  uint64_t* rings;               /* scratch [n_replicas][ring_cap]: the queues */
+  int64_t ring_cap;              /* >= n_arrivals (a queue never holds more) */
   int64_t* scratch;              /* scratch [n_arrivals] (window latencies) */
   gs_engine_record* records;     /* out [n_arrivals], completion order     */
   gs_engine_window* windows;     /* out [windows_cap]                      */
@@ -354,7 +354,9 @@ typedef struct gs_engine_job {
                                     windows, rng state hi, lo, has_uint32, uinteger */
 } gs_engine_job;
 
-/* jobs: device array of n_jobs descriptors; one warp per job. */
+/* jobs: device array of n_jobs descriptors; one warp per job.  Replica ids
+ * are ranked in replica_rank; n_replicas <= 256 (the dispatch key holds the
+ * replica index in 8 bits) and arrival indices < 2^32. */
 int gs_engine_run(const gs_engine_job* jobs, int32_t n_jobs, void* stream);
 
 /* ------------------------------------------------------------------------

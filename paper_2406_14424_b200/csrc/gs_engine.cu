@@ -7,9 +7,13 @@
 // groups of a bursty trace replay (config 5: one engine state per replica
 // group), Monte-Carlo seeds, and the planner's simulator probes
 // (_probe_range / _burst_throughput, src/planner.py:293-356), which call
-// engine.run once per candidate.  One warp per run, lane 0 working: a run's
-// control flow is data-dependent, so packing runs into lanes would only
-// serialise them under divergence.
+// engine.run once per candidate.  One warp per run: the event loop's control
+// flow is uniform across the warp (every lane reads the same shared-memory
+// state and replays the same generator draws, so no lane waits for another),
+// and the data-parallel parts go across lanes -- a finished batch's items
+// (one lane each: queue entry, certainty, correct flag, record write), the
+// dispatch scan over a device's replicas (one lane per replica, a warp
+// min-reduction of (stage, -length, id rank)).
 //
 // Exactness.  Event order is the reference heap's (t, priority, seq) order:
 // complete (0) < tick (1) < arrival (2) at equal t, pushes numbered in the
@@ -21,10 +25,11 @@
 // when a stage's weights sum to zero.  The gate is the reference's f64
 // compare cert[row, m] >= thr.  Percentiles are nearest-rank (:111-120).
 //
-// State per run: each request lives in two scratch words indexed by its
-// arrival index (next pointer of the queue it sits in; stage | gear), queues
-// are singly linked lists (head, tail, length) in shared memory, so a
-// request moves between queues without copying.
+// State per run: every replica queue is a ring buffer in global memory
+// (rings[R][ring_cap]) whose entries carry the request whole -- arrival index,
+// stage, gear -- so a request moves between queues as one 8-byte store and a
+// batch pop is a head advance; heads, tails, device state and counters live
+// in shared memory.
 #include <math.h>
 
 #include "gs_common.cuh"
@@ -83,21 +88,23 @@ struct Pcg64 {
 
 constexpr int kMaxR = GS_ENGINE_MAX_REPLICAS;
 constexpr int kMaxD = GS_ENGINE_MAX_DEVICES;
-constexpr int32_t kNil = -1;
 
 struct RunSmem {
-  int32_t head[kMaxR], tail[kMaxR], qlen[kMaxR];
+  uint32_t head[kMaxR], tail[kMaxR];  // ring positions (mod ring_cap): len = tail - head
   int64_t routed[kMaxR];
   int64_t t_done[kMaxD], seq_done[kMaxD];
-  int32_t batch_head[kMaxD], batch_n[kMaxD];
+  uint32_t batch_head[kMaxD];
+  int32_t batch_r[kMaxD], batch_n[kMaxD];
   uint8_t busy[kMaxD];
 };
 
-__device__ __forceinline__ uint32_t meta(int stage, int gear) {
-  return (uint32_t)stage | ((uint32_t)gear << 8);
+// a queue entry: arrival index | stage << 32 | gear << 40
+__device__ __forceinline__ uint64_t entry(uint32_t rid, uint32_t stage, uint32_t gear) {
+  return (uint64_t)rid | ((uint64_t)stage << 32) | ((uint64_t)gear << 40);
 }
 
-// choose_weighted (src/engine.py:238-245) over one gear stage's CSR slice
+// choose_weighted (src/engine.py:238-245) over one gear stage's CSR slice;
+// every lane runs it alike (same generator state, same result)
 __device__ int32_t choose_replica(const gs_engine_plan& p, int gear, int stage, Pcg64& rng) {
   const int32_t* off = p.gear_rep_off + (int64_t)gear * (p.max_stages + 1);
   const int32_t b = off[stage], e = off[stage + 1];
@@ -146,26 +153,27 @@ __device__ int64_t select_kth(int64_t* a, int64_t n, int64_t k) {
 
 __global__ void __launch_bounds__(32) engine_kernel(const gs_engine_job* __restrict__ jobs, int n_jobs) {
   __shared__ RunSmem sm;
+  __shared__ int64_t s_p95;
   if (blockIdx.x >= (unsigned)n_jobs) return;
   const gs_engine_job job = jobs[blockIdx.x];
   const gs_engine_plan p = *job.plan;
   const int R = p.n_replicas, D = p.n_devices, L = p.max_stages;
-  for (int i = threadIdx.x; i < kMaxR; i += 32) {
-    sm.head[i] = kNil;
-    sm.tail[i] = kNil;
-    sm.qlen[i] = 0;
+  const int lane = threadIdx.x;
+  const uint32_t cap = (uint32_t)job.ring_cap;
+  for (int i = lane; i < kMaxR; i += 32) {
+    sm.head[i] = 0u;
+    sm.tail[i] = 0u;
     sm.routed[i] = 0;
   }
-  for (int i = threadIdx.x; i < kMaxD; i += 32) {
+  for (int i = lane; i < kMaxD; i += 32) {
     sm.busy[i] = 0;
     sm.batch_n[i] = 0;
   }
   const int64_t nb = (int64_t)p.n_cols * (p.batch_cap + 1);
-  for (int64_t i = threadIdx.x; i < nb; i += 32) job.model_batches[i] = 0;
+  for (int64_t i = lane; i < nb; i += 32) job.model_batches[i] = 0;
   __syncwarp();
-  if (threadIdx.x != 0) return;
 
-  Pcg64 rng;
+  Pcg64 rng;  // replicated in every lane
   rng.state = ((unsigned __int128)job.rng_state_hi << 64) | job.rng_state_lo;
   rng.inc = ((unsigned __int128)job.rng_inc_hi << 64) | job.rng_inc_lo;
   rng.has32 = job.rng_has_uint32;
@@ -186,7 +194,8 @@ __global__ void __launch_bounds__(32) engine_kernel(const gs_engine_job* __restr
   const double period_s = (double)period / 1000000.0;
 
   while (true) {
-    // ---- pop the minimum (t, prio, seq) event
+    __syncwarp();
+    // ---- pop the minimum (t, prio, seq) event (uniform: every lane alike)
     int kind = -1;  // 0 complete, 1 tick, 2 arrival
     int64_t bt = 0, bseq = 0;
     int bdev = -1;
@@ -215,14 +224,14 @@ __global__ void __launch_bounds__(32) engine_kernel(const gs_engine_job* __restr
 
     uint64_t touched = 0;
     if (kind == 2) {  // ---- EngineState.submit (:299-319)
-      const int32_t rid = (int32_t)arr_idx;
-      job.item_next[rid] = kNil;
-      job.item_meta[rid] = meta(0, gear_now);
       const int32_t ridx = choose_replica(p, gear_now, 0, rng);
-      if (sm.tail[ridx] == kNil) sm.head[ridx] = rid; else job.item_next[sm.tail[ridx]] = rid;
-      sm.tail[ridx] = rid;
-      sm.qlen[ridx] += 1;
-      sm.routed[ridx] += 1;
+      const uint32_t t = sm.tail[ridx];
+      if (lane == 0) job.rings[(int64_t)ridx * cap + (t % cap)] = entry((uint32_t)arr_idx, 0u, (uint32_t)gear_now);
+      __syncwarp();
+      if (lane == 0) {
+        sm.tail[ridx] = t + 1;
+        sm.routed[ridx] += 1;
+      }
       arrivals += 1;
       win_arrivals += 1;
       touched = 1ull << p.replica_device[ridx];
@@ -235,75 +244,101 @@ __global__ void __launch_bounds__(32) engine_kernel(const gs_engine_job* __restr
       }
     } else if (kind == 0) {  // ---- EngineState.finish_batch (:355-383)
       const int d = bdev;
-      sm.busy[d] = 0;
       const int n = sm.batch_n[d];
+      const int br = sm.batch_r[d];
+      const uint32_t bh = sm.batch_head[d];
+      __syncwarp();
+      if (lane == 0) sm.busy[d] = 0;
       in_flight -= n;
       touched = 1ull << d;
-      int32_t rid = sm.batch_head[d];
-      for (int k = 0; k < n; ++k) {
-        const int32_t nxt = job.item_next[rid];  // read before re-linking rid
-        const uint32_t mt = job.item_meta[rid];
-        const int stage = (int)(mt & 0xFF), gear = (int)(mt >> 8);
-        const int m = p.gear_model[(int64_t)gear * L + stage];
-        const bool last = stage == p.gear_n_stages[gear] - 1;
-        const int64_t row = (int64_t)rid % p.n_records;
-        const int64_t cell = row * p.n_cols + m;
-        if (last || p.cert[cell] >= p.gear_thr[(int64_t)gear * L + stage]) {
-          const uint8_t ok = p.corr[cell] ? 1 : 0;
+      for (int c0 = 0; c0 < n; c0 += 32) {  // 32 items at a time, a lane each
+        const int k = c0 + lane;
+        const bool live = k < n;
+        uint64_t e = 0;
+        bool stop = false;
+        uint8_t ok = 0;
+        if (live) {
+          e = job.rings[(int64_t)br * cap + ((bh + (uint32_t)k) % cap)];
+          const uint32_t rid = (uint32_t)e, stage = (uint32_t)(e >> 32) & 0xFFu,
+                         gear = (uint32_t)(e >> 40);
+          const int m = p.gear_model[(int64_t)gear * L + stage];
+          const bool last = (int)stage == p.gear_n_stages[gear] - 1;
+          const int64_t cell = ((int64_t)rid % p.n_records) * p.n_cols + m;
+          stop = last || p.cert[cell] >= p.gear_thr[(int64_t)gear * L + stage];
+          if (stop) ok = p.corr[cell] ? 1 : 0;
+        }
+        const uint32_t smask = __ballot_sync(0xffffffffu, stop);
+        const uint32_t cmask = __ballot_sync(0xffffffffu, stop && ok);
+        if (stop) {
           gs_engine_record rec;
           rec.completion_us = now;
-          rec.request_id = rid;
-          rec.stages_executed = (uint8_t)(stage + 1);
+          rec.request_id = (int32_t)(uint32_t)e;
+          rec.stages_executed = (uint8_t)(((e >> 32) & 0xFFu) + 1);
           rec.correct = ok;
-          rec.gear_index = (uint16_t)gear;
-          job.records[completed] = rec;
-          completed += 1;
-          win_correct += ok;
-        } else {
-          const int32_t ridx = choose_replica(p, gear, stage + 1, rng);
-          job.item_next[rid] = kNil;
-          job.item_meta[rid] = meta(stage + 1, gear);
-          if (sm.tail[ridx] == kNil) sm.head[ridx] = rid; else job.item_next[sm.tail[ridx]] = rid;
-          sm.tail[ridx] = rid;
-          sm.qlen[ridx] += 1;
+          rec.gear_index = (uint16_t)(e >> 40);
+          job.records[completed + __popc(smask & ((1u << lane) - 1u))] = rec;
+        }
+        completed += __popc(smask);
+        win_correct += __popc(cmask);
+        // forwarded items in batch order: one draw each, every lane alike
+        uint32_t fmask = __ballot_sync(0xffffffffu, live && !stop);
+        while (fmask) {
+          const int src = __ffs(fmask) - 1;
+          fmask &= fmask - 1;
+          const uint64_t fe = __shfl_sync(0xffffffffu, e, src);
+          const uint32_t stage = (uint32_t)(fe >> 32) & 0xFFu, gear = (uint32_t)(fe >> 40);
+          const int32_t ridx = choose_replica(p, (int)gear, (int)stage + 1, rng);
+          const uint32_t t = sm.tail[ridx];
+          if (lane == 0) {
+            job.rings[(int64_t)ridx * cap + (t % cap)] = entry((uint32_t)fe, stage + 1, gear);
+            sm.tail[ridx] = t + 1;
+          }
+          __syncwarp();
           touched |= 1ull << p.replica_device[ridx];
         }
-        rid = nxt;
       }
     } else {  // ---- tick (:389-410) and maybe_switch_gear (:123-133)
       tick_idx += 1;
       const double qps = (double)win_arrivals / period_s;
       const int32_t* off = p.gear_rep_off + (int64_t)gear_now * (L + 1);
       int64_t q0 = 0;
-      for (int e = off[0]; e < off[1]; ++e) q0 += sm.qlen[p.gear_rep[e]];
+      for (int e = off[0]; e < off[1]; ++e) {
+        const int r = p.gear_rep[e];
+        q0 += (int64_t)(sm.tail[r] - sm.head[r]);
+      }
       const int n_ranges = p.n_gears;
       int64_t cand = (int64_t)floor(qps * (double)n_ranges / p.qps_max);
       if (cand > n_ranges - 1) cand = n_ranges - 1;
       int after = (int)cand;
       if (cand < gear_now && qps < job.alpha * (double)q0) after = gear_now;
       const int64_t nlat = completed - win_start;
-      gs_engine_window w;
-      w.end_us = now;
-      w.measured_qps = qps;
-      w.first_stage_queue_len = (int32_t)q0;
-      w.gear_before = gear_now;
-      w.candidate_gear = (int32_t)cand;
-      w.gear_after = after;
-      w.completed = nlat;
       if (nlat > 0) {
-        for (int64_t i = 0; i < nlat; ++i) {
+        for (int64_t i = lane; i < nlat; i += 32) {  // latencies of the window, lane-parallel
           const gs_engine_record& r = job.records[win_start + i];
           job.scratch[i] = r.completion_us - job.arrivals[r.request_id];
         }
-        int64_t k = (int64_t)ceil(95.0 / 100.0 * (double)nlat);
-        if (k < 1) k = 1;
-        w.p95_us = select_kth(job.scratch, nlat, k - 1);
-        w.accuracy = (double)win_correct / (double)nlat;
-      } else {
-        w.p95_us = -1;
-        w.accuracy = __longlong_as_double(0x7ff8000000000000ll);
+        __syncwarp();
+        if (lane == 0) {
+          int64_t k = (int64_t)ceil(95.0 / 100.0 * (double)nlat);
+          if (k < 1) k = 1;
+          s_p95 = select_kth(job.scratch, nlat, k - 1);
+        }
+        __syncwarp();
       }
-      if (n_windows < job.windows_cap) job.windows[n_windows] = w;
+      if (lane == 0) {
+        gs_engine_window w;
+        w.end_us = now;
+        w.measured_qps = qps;
+        w.first_stage_queue_len = (int32_t)q0;
+        w.gear_before = gear_now;
+        w.candidate_gear = (int32_t)cand;
+        w.gear_after = after;
+        w.completed = nlat;
+        w.p95_us = nlat > 0 ? s_p95 : -1;
+        w.accuracy = nlat > 0 ? (double)win_correct / (double)nlat
+                              : __longlong_as_double(0x7ff8000000000000ll);
+        if (n_windows < job.windows_cap) job.windows[n_windows] = w;
+      }
       n_windows += 1;
       gear_now = after;
       win_arrivals = 0;
@@ -312,58 +347,68 @@ __global__ void __launch_bounds__(32) engine_kernel(const gs_engine_job* __restr
       touched = (D >= 64) ? ~0ull : ((1ull << D) - 1);
     }
 
+    __syncwarp();  // lane 0's shared-memory updates are seen by every lane
     // ---- scan_device for the touched devices in ascending order (:321-353)
     while (touched) {
       const int d = __ffsll((long long)touched) - 1;
       touched &= touched - 1;
       if (sm.busy[d]) continue;
-      int best = -1, bstage = 0, blen = 0, brank = 0;
+      // a lane per replica: candidate key (stage, -len, id rank), warp minimum
       const int32_t* minq = p.gear_min_qlen + (int64_t)gear_now * R;
-      for (int r = 0; r < R; ++r) {
+      uint64_t best = ~0ull;
+      for (int r = lane; r < R; r += 32) {
         if (p.replica_device[r] != d) continue;
-        const int len = sm.qlen[r];
-        if (len == 0 || len < minq[r]) continue;
-        const int st = (int)(job.item_meta[sm.head[r]] & 0xFF);
-        const int rk = p.replica_rank[r];
-        // choose_dispatch: earliest stage, then longest queue, then lowest id
-        if (best < 0 || st < bstage || (st == bstage && (len > blen || (len == blen && rk < brank)))) {
-          best = r;
-          bstage = st;
-          blen = len;
-          brank = rk;
-        }
+        const uint32_t len = sm.tail[r] - sm.head[r];
+        if (len == 0 || (int)len < minq[r]) continue;
+        const uint64_t e = job.rings[(int64_t)r * cap + (sm.head[r] % cap)];
+        const uint64_t st = (e >> 32) & 0xFFu;
+        const uint64_t key = (st << 56) | ((uint64_t)(0xFFFFFFFFu - len) << 16) |
+                             ((uint64_t)p.replica_rank[r] << 8) | (uint64_t)r;
+        best = key < best ? key : best;
       }
-      if (best < 0) continue;
-      const int m = p.replica_model[best];
-      const int size = min(sm.qlen[best], p.model_max_batch[m]);
-      const int32_t first = sm.head[best];
-      int32_t h = first;
-      for (int k = 0; k < size; ++k) h = job.item_next[h];
-      sm.head[best] = h;
-      if (h == kNil) sm.tail[best] = kNil;
-      sm.qlen[best] -= size;
-      sm.busy[d] = 1;
-      sm.batch_head[d] = first;
-      sm.batch_n[d] = size;
-      sm.t_done[d] = now + p.model_runtime_us[(int64_t)m * (p.batch_cap + 1) + size];
-      sm.seq_done[d] = seq++;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y < best ? y : best;
+      }
+      if (best == ~0ull) continue;
+      const int r = (int)(best & 0xFFu);
+      const int m = p.replica_model[r];
+      const uint32_t len = sm.tail[r] - sm.head[r];
+      const int size = min((int)len, p.model_max_batch[m]);
+      const uint32_t h = sm.head[r];
+      __syncwarp();
+      if (lane == 0) {
+        sm.head[r] = h + (uint32_t)size;
+        sm.busy[d] = 1;
+        sm.batch_head[d] = h;
+        sm.batch_r[d] = r;
+        sm.batch_n[d] = size;
+        sm.t_done[d] = now + p.model_runtime_us[(int64_t)m * (p.batch_cap + 1) + size];
+        sm.seq_done[d] = seq;
+        job.model_batches[(int64_t)m * (p.batch_cap + 1) + size] += 1;
+      }
+      __syncwarp();
+      seq++;
       in_flight += size;
-      job.model_batches[(int64_t)m * (p.batch_cap + 1) + size] += 1;
     }
   }
 
-  for (int r = 0; r < R; ++r) {
+  __syncwarp();
+  for (int r = lane; r < R; r += 32) {
     job.replica_counts[2 * r] = sm.routed[r];
-    job.replica_counts[2 * r + 1] = sm.qlen[r];
+    job.replica_counts[2 * r + 1] = (int64_t)(sm.tail[r] - sm.head[r]);
   }
-  job.result[0] = arrivals;
-  job.result[1] = completed;
-  job.result[2] = in_flight;
-  job.result[3] = n_windows;
-  job.result[4] = (int64_t)(uint64_t)(rng.state >> 64);
-  job.result[5] = (int64_t)(uint64_t)rng.state;
-  job.result[6] = rng.has32;
-  job.result[7] = rng.u32;
+  if (lane == 0) {
+    job.result[0] = arrivals;
+    job.result[1] = completed;
+    job.result[2] = in_flight;
+    job.result[3] = n_windows;
+    job.result[4] = (int64_t)(uint64_t)(rng.state >> 64);
+    job.result[5] = (int64_t)(uint64_t)rng.state;
+    job.result[6] = rng.has32;
+    job.result[7] = rng.u32;
+  }
 }
 
 }  // namespace

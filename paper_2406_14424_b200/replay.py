@@ -54,7 +54,7 @@ class gs_engine_job(ctypes.Structure):
                 ("rng_has_uint32", ctypes.c_uint32), ("rng_uinteger", ctypes.c_uint32),
                 ("initial_gear", ctypes.c_int32), ("enable_ticks", ctypes.c_int32),
                 ("measure_period_us", ctypes.c_int64), ("alpha", ctypes.c_double),
-                ("item_next", ctypes.c_void_p), ("item_meta", ctypes.c_void_p),
+                ("rings", ctypes.c_void_p), ("ring_cap", ctypes.c_int64),
                 ("scratch", ctypes.c_void_p), ("records", ctypes.c_void_p),
                 ("windows", ctypes.c_void_p), ("windows_cap", ctypes.c_int64),
                 ("model_batches", ctypes.c_void_p), ("replica_counts", ctypes.c_void_p),
@@ -321,8 +321,8 @@ class _JobBuffers:
         i32 = dict(dtype=torch.int32, device=dev)
         i64 = dict(dtype=torch.int64, device=dev)
         m = max(n, 1)
-        self.item_next = torch.empty(m, **i32)
-        self.item_meta = torch.empty(m, **i32)
+        # a ring per replica queue, each able to hold every request
+        self.rings = torch.empty(R * m, **i64)
         self.scratch = torch.empty(m, **i64)
         self.records = torch.empty(m * 2, **i64)           # 16-byte records
         self.windows = torch.empty(max(self.n_windows_cap, 1) * 7, **i64)  # 56-byte windows
@@ -334,25 +334,42 @@ class _JobBuffers:
             p.struct.data_ptr(), self.arr.data_ptr() if n else None, n, int(job.horizon_us),
             w[0], w[1], w[2], w[3], w[4], w[5], int(cfg.initial_gear_index),
             1 if cfg.enable_ticks else 0, int(cfg.measure_period_us), float(cfg.alpha),
-            self.item_next.data_ptr(), self.item_meta.data_ptr(), self.scratch.data_ptr(),
+            self.rings.data_ptr(), m, self.scratch.data_ptr(),
             self.records.data_ptr(), self.windows.data_ptr(), int(self.n_windows_cap),
             self.batches.data_ptr(), self.counts.data_ptr(), self.result.data_ptr())
+
+
+class Prepared:
+    """Device buffers and the descriptor table of a batch of jobs: the host
+    work (allocation, trace and plan uploads) done once, so run() is one
+    kernel launch and can be repeated (every launch rewrites the outputs)."""
+
+    def __init__(self, jobs: list[Job]):
+        dev = _lib.device()
+        self.jobs = list(jobs)
+        self.bufs = [_JobBuffers(j, dev) for j in self.jobs]
+        raw = b"".join(bytes(b.struct) for b in self.bufs)
+        self.table = torch.from_numpy(np.frombuffer(raw, dtype=np.uint8).copy()).to(dev) \
+            if raw else None
+
+    def run(self) -> "Prepared":
+        """One gs_engine_run launch over every job, on the current stream."""
+        if self.bufs:
+            _lib.check(_lib.load().gs_engine_run(self.table.data_ptr(), len(self.bufs),
+                                                 _lib.stream_ptr()), "engine replay")
+        return self
+
+    def results(self) -> list["ReplayResult"]:
+        return [collect(j, b) for j, b in zip(self.jobs, self.bufs)]
 
 
 def launch(jobs: list[Job]) -> list[_JobBuffers]:
     """Enqueue every job's replay in ONE gs_engine_run launch on the current
     stream; returns the per-job device buffers (read them with collect())."""
-    dev = _lib.device()
-    bufs = [_JobBuffers(j, dev) for j in jobs]
-    if not bufs:
-        return bufs
-    raw = b"".join(bytes(b.struct) for b in bufs)
-    table = torch.from_numpy(np.frombuffer(raw, dtype=np.uint8).copy()).to(dev)
-    _lib.check(_lib.load().gs_engine_run(table.data_ptr(), len(bufs), _lib.stream_ptr()),
-               "engine replay")
-    for b in bufs:
-        b.table = table  # keep the descriptor table alive with the buffers
-    return bufs
+    prep = Prepared(jobs).run()
+    for b in prep.bufs:
+        b.table = prep.table  # keep the descriptor table alive with the buffers
+    return prep.bufs
 
 
 def collect(job: Job, b: _JobBuffers) -> ReplayResult:
