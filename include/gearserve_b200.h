@@ -246,6 +246,59 @@ int gs_stage_gate_packed(const double* certainty, const uint8_t* correct,
 
 
 
+
+/* ------------------------------------------------------------------------
+ * Config 4a: the exact Pareto front (cascades.pareto_filter semantics, exact
+ * ties kept, src/cascades.py:116-129) of the full five-model cascade
+ * m0 -> m1 -> m2 -> m3 -> m4 over every threshold tuple (k0, k1, k2, k3) of
+ * grids of up to 1023 values (~1e12 configs at 1000 levels), each config
+ * scored like _evaluate_numba (src/kernels.py:39-62) but never written out.
+ * certainty [n, 5] f64, correct [n, 5] u8 on the device, n < 2^21; grids:
+ * device, models 0..3 concatenated; grid_len HOST [5].  Config index =
+ * ((k0 g1 + k1) g2 + k2) g3 + k3.
+ *   prepare: bins, records sorted by (b2, b0), side tables; resets the
+ *            per-accuracy minimum costs (mincost, int64 order-preserving
+ *            cost bits at workspace + mincost_offset, n + 1 entries).
+ *   pass1:   k0 in [k0_begin, k0_end): lowers mincost.  Sharded runs reduce
+ *            mincost with MIN across ranks before select.
+ *   select:  the front's accuracies and cost keys; *n_front (device) = how
+ *            many distinct accuracies it has.
+ *   pass2:   k0 in [k0_begin, k0_end): every config on the front, in no
+ *            order: out_index [cap] config index, out_cost [cap] mean cost,
+ *            out_counts [cap][6] {correct, n, reach after stages 0..3};
+ *            *out_n (device, zero it first) the count (may exceed cap);
+ *            out_cap = 0: no list, only the per-accuracy summary (ties,
+ *            min_index) -- routing-equivalent threshold tuples tie, and a
+ *            1000-level front can hold 1e9 configs.
+ * ---------------------------------------------------------------------- */
+typedef struct gs_front5_info {
+  int64_t n_configs;        /* g0 g1 g2 g3                                */
+  size_t workspace_bytes;
+  size_t mincost_offset;    /* byte offset of mincost in the workspace    */
+  size_t front_offset;      /* after select: int64 [n + 1] the front point's
+                               cost key per accuracy, or 0x7f7f7f7f7f7f7f7f */
+  size_t ties_offset;       /* after pass2: u64 [n + 1] front configs per
+                               accuracy (tied configs all counted)          */
+  size_t min_index_offset;  /* after pass2: u64 [n + 1] their smallest index */
+  int32_t k0_count;         /* g0: the k0 values to shard                 */
+  int32_t bucket_shift;
+} gs_front5_info;
+
+int gs_front5_plan(int64_t n_rec, const int32_t* grid_len, gs_front5_info* info);
+int gs_front5_prepare(const double* certainty, const uint8_t* correct, int64_t n_rec,
+                      const double* grids, const int32_t* grid_len, void* workspace,
+                      size_t workspace_bytes, void* stream);
+int gs_front5_pass1(int64_t n_rec, const int32_t* grid_len, const double* cost1,
+                    int32_t k0_begin, int32_t k0_end, void* workspace,
+                    size_t workspace_bytes, void* stream);
+int gs_front5_select(int64_t n_rec, const int32_t* grid_len, void* workspace,
+                     size_t workspace_bytes, unsigned long long* n_front, void* stream);
+int gs_front5_pass2(int64_t n_rec, const int32_t* grid_len, const double* cost1,
+                    int32_t k0_begin, int32_t k0_end, void* workspace,
+                    size_t workspace_bytes, unsigned long long* out_index,
+                    double* out_cost, uint32_t* out_counts, unsigned long long* out_n,
+                    int64_t out_cap, void* stream);
+
 /* ------------------------------------------------------------------------
  * SP1's cascade sampler (cascades.sample_cascades, src/cascades.py:166-193)
  * on the device: numpy default_rng(seed)'s draws reproduced exactly, every

@@ -100,6 +100,14 @@ _SIGNATURES = {
                       c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_double,
                       c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "gs_engine_run": [c_void_p, c_int32, c_void_p],
+    "gs_front5_plan": [c_int64, POINTER(c_int32), c_void_p],
+    "gs_front5_prepare": [c_void_p, c_void_p, c_int64, c_void_p, POINTER(c_int32), c_void_p,
+                          c_size_t, c_void_p],
+    "gs_front5_pass1": [c_int64, POINTER(c_int32), c_void_p, c_int32, c_int32, c_void_p, c_size_t,
+                        c_void_p],
+    "gs_front5_select": [c_int64, POINTER(c_int32), c_void_p, c_size_t, c_void_p, c_void_p],
+    "gs_front5_pass2": [c_int64, POINTER(c_int32), c_void_p, c_int32, c_int32, c_void_p, c_size_t,
+                        c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     "gs_sample_cascades": [c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p],
     "gs_stage_gate_packed_bytes": [c_int64, POINTER(c_size_t), POINTER(c_size_t),
                                    POINTER(c_size_t)],
