@@ -1087,11 +1087,8 @@ def config4a_bench(args, dev, world, rank):
     acc_cnt, cost, ties, mi = f5.points()
     # spot check: the cheapest and the most accurate front points' smallest
     # configs against the oracle walk
-    from paper_2406_14424_b200.gridsweep import GridSweep
-    sw = GridSweep(cert, corr, grids, cost1, build=False)
-    sb = sw.n_configs - f5.n_configs
     chk = np.unique(np.concatenate([mi[:3], mi[-3:]]).astype(np.int64))
-    sm, thr, ns = (x.cpu().numpy() for x in sw.decode(sb + chk))
+    sm, thr, ns = f5.decode(chk)
     want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=os.cpu_count() or 1)
     pos = {int(m): k for k, m in enumerate(mi)}
     ok = all(want[0][q] == acc_cnt[pos[int(c)]] / n and want[1][q] == cost[pos[int(c)]]
@@ -1099,7 +1096,7 @@ def config4a_bench(args, dev, world, rank):
     threads = os.cpu_count() or 1
     rng = np.random.default_rng(4)
     pick = np.sort(rng.choice(f5.n_configs, size=4096, replace=False))
-    csm, cthr, cns = (x.cpu().numpy() for x in sw.decode(sb + pick))
+    csm, cthr, cns = f5.decode(pick)
     t = time.perf_counter()
     oracle.evaluate_encoded(cert, corr, csm, cthr, cns, cost1, n_threads=threads)
     cpu_rate = len(pick) / (time.perf_counter() - t)

@@ -63,6 +63,7 @@ class Front5:
                 raise ValueError(f"grid {j} must be a non-empty strictly increasing 1-D array")
             host.append(g)
         self.n_rec = int(self.cert.shape[0])
+        self.grids_host = host
         self.grid_len = [int(g.size) for g in host]
         self._glen = _lib.int32_array(self.grid_len)
         self.grids = _lib.to_device(np.concatenate(host[:4]), torch.float64)
@@ -135,6 +136,24 @@ class Front5:
             if k <= cap:
                 return idx[:k], cost[:k], cnt[:k]
             cap = k  # rare: more tied front configs than room; redo with room
+
+    def decode(self, index) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """Config indices -> evaluate_encoded's encoding (stage_model [n, 5]
+        = 0..4, thresholds [n, 5], n_stages [n] = 5)."""
+        idx = np.asarray(index, dtype=np.int64).reshape(-1)
+        g = self.grid_len
+        k = np.empty((idx.size, 4), dtype=np.int64)
+        rest = idx.copy()
+        for j in (3, 2, 1, 0):
+            k[:, j] = rest % g[j]
+            rest //= g[j]
+        if np.any(rest != 0) or np.any(idx < 0):
+            raise IndexError("config index outside the full cascade's block")
+        thr = np.zeros((idx.size, 5))
+        for j in range(4):
+            thr[:, j] = self.grids_host[j][k[:, j]]
+        sm = np.tile(np.arange(5, dtype=np.int32), (idx.size, 1))
+        return sm, thr, np.full(idx.size, 5, dtype=np.int32)
 
     def _ws_view(self, off: int) -> torch.Tensor:
         return self.ws[off: off + 8 * (self.n_rec + 1)].view(torch.int64)

@@ -57,11 +57,14 @@ def test_front_equals_materialised_sweep(n_rec, levels, ties):
         assert int(t) == len(pts[(int(nc), float(cc))]) and int(m) == min(pts[(int(nc), float(cc))])
     assert np.array_equal(f.mean_cost, want[2])
     assert np.array_equal(f.forward_frac, want[3])
-    # and the oracle walk on the front configs themselves
+    # and the oracle walk on the front configs themselves (front5's decode =
+    # gridsweep's decode of the full cascade's block)
     from paper_2406_14424_b200.gridsweep import GridSweep
     sw = GridSweep(cert, corr, grids, cost1, build=False)
     sb = sw.n_configs - int(np.prod([len(g) for g in grids[:4]]))
     sm, thr, ns = (t.cpu().numpy() for t in sw.decode(sb + f.index.astype(np.int64)))
+    dsm, dthr, dns = f5.decode(f.index)
+    assert np.array_equal(dsm, sm) and np.array_equal(dthr, thr) and np.array_equal(dns, ns)
     w = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=8)
     assert np.array_equal(w[0], f.accuracy) and np.array_equal(w[1], f.mean_cost)
 
