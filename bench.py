@@ -123,8 +123,16 @@ def init_dist():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # GS_ONE_DEVICE=1 + GS_DIST_BACKEND=gloo: every rank on cuda:0, for
+        # exercising the sharded paths on a one-GPU box (not a measurement)
+        dev_index = 0 if os.environ.get("GS_ONE_DEVICE") == "1" else local
+        torch.cuda.set_device(dev_index)
+        backend = os.environ.get("GS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
+        local = dev_index
     else:
         torch.cuda.set_device(0)
     return world, rank, local
