@@ -1125,6 +1125,58 @@ def config4a_bench(args, dev, world, rank):
                                                        "x 100k records, oracle/oracle_eval.c"}}
 
 
+def online_router_bench(plan, prof, cert, corr):
+    """The live-serving shape of the stage step: StageRouter.finish_batch
+    (EngineState.finish_batch, src/engine.py:355-383) on batches of 4 / 8 /
+    64 / 1024 items -- one packed H2D, the device gate, one packed D2H, the
+    host's replica draws and queue appends per call -- against the
+    reference's loop restated (oracle.finish_batch) on the same batches,
+    one core.  At 4-8 items a call is latency-bound (one round trip)."""
+    from oracle import oracle
+    from paper_2406_14424_b200.engine import GearTables, Item, StageRouter
+    reps = list(plan.placement.replicas)
+    ids = list(prof.model_ids)
+    devs = []
+    for r in reps:
+        if r.device_id not in devs:
+            devs.append(r.device_id)
+    tables = GearTables.from_gears(plan.gears, [(r.replica_id, r.model_id) for r in reps],
+                                   {m: j for j, m in enumerate(ids)})
+    gears_o = [{"stage_model": tables.stage_models[g], "thresholds": tables.thresholds[g],
+                "replica_idx": tables.replicas[g], "cum_weights": tables.cum_weights[g]}
+               for g in range(len(plan.gears))]
+    rng = np.random.default_rng(0)
+    out = {}
+    for bsz in (4, 8, 64, 1024):
+        n_calls = max(20, 40_000 // bsz)
+        batches = []
+        for c in range(n_calls):
+            g = rng.integers(0, len(plan.gears), bsz)
+            st = np.array([int(rng.integers(0, len(tables.stage_models[x]))) for x in g])
+            rows = rng.integers(0, cert.shape[0], bsz)
+            batches.append([(int(c * bsz + k), int(rows[k]), int(st[k]), int(g[k])) for k in range(bsz)])
+        router = StageRouter(tables, cert, corr, [devs.index(r.device_id) for r in reps], seed=0)
+        for b in batches[:3]:
+            router.finish_batch(0, [Item(i, r, s_, g_, 0) for i, r, s_, g_ in b], 10)
+        t = time.perf_counter()
+        for b in batches:
+            router.finish_batch(0, [Item(i, r, s_, g_, 0) for i, r, s_, g_ in b], 10)
+        dev_rate = n_calls * bsz / (time.perf_counter() - t)
+        orng = np.random.default_rng(0)
+        t = time.perf_counter()
+        for b in batches:
+            oracle.finish_batch([{"request_id": i, "row": r, "stage": s_, "gear": g_, "arrival_us": 0}
+                                 for i, r, s_, g_ in b], gears_o, cert, corr, orng, 10)
+        cpu_rate = n_calls * bsz / (time.perf_counter() - t)
+        out[f"batch_{bsz}"] = {"samples_per_s": dev_rate, "calls": n_calls,
+                               "cpu_baseline_samples_per_s": cpu_rate}
+    out["path"] = ("StageRouter.finish_batch: Item objects in, packed pinned H2D, gs_stage_gate "
+                   "(one tile), packed pinned D2H, numpy replica draws, deque appends; host "
+                   "wall clock. cpu_baseline: oracle.finish_batch (the reference loop restated), "
+                   "1 core")
+    return out
+
+
 def config5_bench(args, dev):
     """BASELINE configs[4]: an Azure-like bursty trace (20 min of lognormal
     per-second levels, default_rng(0), scaled to 7,600 max QPS with
@@ -1267,6 +1319,7 @@ def config5_bench(args, dev):
                           cert, corr, runtime, [8] * 4, {m: j for j, m in enumerate(ids)},
                           seed=0, enable_ticks=False)
     probe_cpu = 64 / (time.perf_counter() - t)
+    out["online_router"] = _guarded(online_router_bench, plan, prof, cert, corr)
     out["probes"] = {"probes": len(pjobs), "ms": pms, "probes_per_s": len(pjobs) / (pms * 1e-3),
                      "requests_per_probe": 256, "launches": 1,
                      "first_throughputs_qps": thr_probe,

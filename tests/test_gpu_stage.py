@@ -143,3 +143,39 @@ def test_gate_batcher_matches_stage_gate():
         assert np.array_equal(near, ref.near_idx.cpu().numpy())
         want = (cert[rows, model] >= thr) | last
         assert np.array_equal(stop, want)
+
+
+@pytest.mark.parametrize("kind", ["margin", "entropy"])
+def test_stage_step_at_config3_scale(kind):
+    """The stage step at config 3's shape (1M rows x 1000-class f32 logits,
+    the bench's data) with the threshold at the 35th certainty percentile
+    (350k rows defer, so compaction runs over every tile): margin certainty,
+    stop mask and deferred order bit-exact against the f64 oracle; entropy
+    within 5e-7, every decision that differs from the oracle's inside the
+    kernel's near-threshold list."""
+    import torch
+
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.stage import stage_step
+    logits, _, _ = synth.imagenet_logits(1_000_000, 1000, 1, seed=0)
+    x = logits[0]
+    host = x.cpu().numpy()
+    cref = np.empty(x.shape[0])
+    fn = oracle.margin_rows if kind == "margin" else oracle.entropy_rows
+    for lo in range(0, x.shape[0], 100_000):
+        cref[lo:lo + 100_000] = fn(host[lo:lo + 100_000])
+    thr = float(np.quantile(cref, 0.35))
+    out = stage_step(x, torch.full((x.shape[0],), thr, dtype=torch.float64, device=x.device),
+                     kind=kind)
+    cert = out.cert.cpu().numpy()
+    stop = out.stop.cpu().numpy().astype(bool)
+    deferred = out.deferred_idx.cpu().numpy()
+    assert np.array_equal(np.flatnonzero(~stop), deferred)  # stable compaction, batch order
+    if kind == "margin":
+        assert np.array_equal(cert, cref)
+        assert np.array_equal(stop, cref >= thr)
+    else:
+        assert np.max(np.abs(cert - cref)) <= 5e-7
+        differ = np.flatnonzero(stop != (cref >= thr))
+        assert np.all(np.isin(differ, out.near_idx.cpu().numpy()))
+    assert 0.3 < deferred.size / x.shape[0] < 0.4
