@@ -41,6 +41,10 @@ extern "C" {
 #define GS_BF16 2
 
 int gs_version(void);
+/* Benchmark support: write `bytes` (> L2) to evict the L2 between timed
+ * steps; max_carveout != 0 runs it with the largest shared-memory carveout
+ * (the sweep kernels' configuration, so no L1/smem switch at the boundary). */
+int gs_flush_l2(void* buffer, size_t bytes, int32_t max_carveout, void* stream);
 const char* gs_strerror(int code);
 /* last CUDA error string seen by this thread (for GS_ECUDA) */
 const char* gs_last_cuda_error(void);

@@ -62,6 +62,7 @@ class gs_jsonl_info(ctypes.Structure):
 # symbol -> argtypes (all return c_int unless listed in _RESTYPES)
 _SIGNATURES = {
     "gs_version": [],
+    "gs_flush_l2": [c_void_p, c_size_t, c_int32, c_void_p],
     "gs_strerror": [c_int32],
     "gs_last_cuda_error": [],
     "gs_eval_encoded_workspace": [c_int64, c_int32, c_int64, c_int32, POINTER(c_size_t)],
