@@ -28,7 +28,7 @@ extern "C" {
 #define GS_EUNSUPPORTED (-4) /* shape outside the kernel's supported range   */
 
 #define GS_MAX_MODELS 8      /* grid path: models per validation set        */
-#define GS_MAX_STAGES 16     /* list path: stages per encoded cascade        */
+#define GS_MAX_STAGES 64     /* list path: stages per encoded cascade        */
 
 /* certainty kinds for gs_certainty / gs_stage_step */
 #define GS_CERT_MARGIN 0      /* Eq. 5: top1 - top2 (singleton: the score)   */

@@ -281,8 +281,12 @@ extern "C" int gs_eval_encoded(const double* certainty, const uint8_t* correct, 
     e = launch_eval<4>(a, grid, smem, st);
   else if (max_len <= 8)
     e = launch_eval<8>(a, grid, smem, st);
-  else
+  else if (max_len <= 16)
     e = launch_eval<16>(a, grid, smem, st);
+  else if (max_len <= 32)
+    e = launch_eval<32>(a, grid, smem, st);  // 17+ stage cascades: rare, per-thread arrays spill
+  else
+    e = launch_eval<64>(a, grid, smem, st);
   GS_CUDA_TRY(e);
 
   const int threads = 256;

@@ -477,7 +477,7 @@ bool w5_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
   if (M != 5 || n_rec < 1 || n_rec >= (1ll << 21)) return false;
   for (int j = 0; j < 4; ++j)
     if (glen[j] < 1 || glen[j] > 254) return false;
-  const int64_t d2 = glen[2] + 1, d3 = glen[3] + 1;
+  const int64_t d3 = glen[3] + 1;
   return d3 <= 32 * kW5Seg && d3 <= 32 * kW5U &&
          (int64_t)(glen[0] + 1) * (glen[1] + 1) <= 26 * 1024;  // side table scanned in smem
 }

@@ -98,3 +98,26 @@ def test_bad_model_index_raises():
     with pytest.raises(IndexError):
         kernels.evaluate_encoded(np.zeros((2, 2)), np.zeros((2, 2)), np.array([[0, 2]]),
                                  np.zeros((1, 2)), np.array([2]), np.ones(2))
+
+
+def test_long_cascades_vs_oracle():
+    """Encoded cascades of 17..40 stages (40 models): the 32- and 64-stage
+    instances of the list kernel."""
+    from paper_2406_14424_b200 import kernels
+    rng = np.random.default_rng(3)
+    n_models, n_rec = 40, 3000
+    cert = rng.random((n_rec, n_models))
+    corr = (rng.random((n_rec, n_models)) < 0.6).astype(np.uint8)
+    for L in (20, 40):
+        n_casc = 50
+        sm = np.full((n_casc, L), -1, dtype=np.int32)
+        thr = np.zeros((n_casc, L))
+        ns = rng.integers(1, L + 1, n_casc).astype(np.int32)
+        for c in range(n_casc):
+            sm[c, :ns[c]] = rng.choice(n_models, ns[c], replace=False)
+            thr[c, :ns[c] - 1] = rng.random(ns[c] - 1) * 0.3 + 0.7
+        cost1 = rng.uniform(1, 100, n_models)
+        got = kernels.evaluate_encoded(cert, corr, sm, thr, ns, cost1)
+        want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
