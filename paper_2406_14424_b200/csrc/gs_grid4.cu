@@ -249,12 +249,14 @@ constexpr int kZeroBytes = 16384;  // zero source of the bulk stores that re-zer
 
 struct G4PlaneArgs {
   float* H;                  // [d1][d0][hp] float4, re-zeroed here
-  unsigned long long* S;     // [d0][d1][d2p] packed {cnt, c3, c2}
+  unsigned long long* S;     // [d0][nbk][d1][W] packed {cnt, c3, c2}, columns < d2 - 1
+  unsigned long long* G;     // [d0][d1p] the same at column d2 - 1 (b2 = any)
   uint32_t* R1;              // [d0][d1p]
   uint32_t* G0;              // [d0] raw c0, re-zeroed here
   uint32_t* P0;              // [d0] inclusive prefix of G0
   int32_t d0, d1, d2, d2p, d1p;
   int32_t hp;                // histogram row pitch in cells (odd: conflict-free row walk)
+  int32_t W, nbk;            // S column blocks (the eval's units)
   int32_t half;              // b0 rows of the cluster's first CTA
   int32_t ns2, seg2;         // b2 segments of the row walk
   int32_t ns0, seg0;         // b0 segments of the column walk
@@ -272,6 +274,21 @@ __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, u
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem),
                "r"(smem_u32(src_smem)), "r"(bytes)
                : "memory");
+}
+
+// Where column c of row b1 lives in the prefix tables, and the step
+// between consecutive b0: columns < d2 - 1 in the eval's column blocks
+// S[b0][c / W][b1][c % W], the last (b2 = any) in G[b0][b1].
+__device__ __forceinline__ unsigned long long* table_column(unsigned long long* S, unsigned long long* G,
+                                                            int W, int nbk, int d1, int d1p, int d2,
+                                                            int b1, int c, int64_t& step) {
+  if (c < d2 - 1) {
+    const int blk = c / W;
+    step = (int64_t)nbk * d1 * W;
+    return S + ((int64_t)blk * d1 + b1) * W + (c - blk * W);
+  }
+  step = d1p;
+  return G + b1;
 }
 
 // The (b0, b2) plane of one b1 is contiguous in H ([b1][b0][hp]).  A
@@ -298,7 +315,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
   float4* s_zero = s_carry + d2;            // kZeroBytes of zeros
   const uint32_t tile_bytes = (uint32_t)(nr * hp * sizeof(float4));
   float4* H = reinterpret_cast<float4*>(a.H) + ((int64_t)b1 * d0 + r_beg) * hp;
-  const int64_t plane = (int64_t)a.d1 * a.d2p;  // S cells per b0 slab
   phase(1, 0);
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -384,13 +400,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPlaneThreads, 2)
   if (live) {
     float4 P = h ? s_carry[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int q = 0; q < s; ++q) P = add4f(P, s_seg[q * d2 + c]);
-    unsigned long long* S = a.S + (int64_t)b1 * a.d2p + c;
+    int64_t step;
+    unsigned long long* S = table_column(a.S, a.G, a.W, a.nbk, a.d1, a.d1p, d2, b1, c, step);
     for (int r = r_lo; r < r_hi; ++r) {
       P = add4f(P, s_tile[(size_t)r * hp + c]);
       const int64_t b0 = r_beg + r;
-      S[b0 * plane] = (unsigned long long)f2u_exact(P.x) |
-                      ((unsigned long long)f2u_exact(P.y) << 21) |
-                      ((unsigned long long)f2u_exact(P.z) << 42);
+      S[b0 * step] = (unsigned long long)f2u_exact(P.x) |
+                     ((unsigned long long)f2u_exact(P.y) << 21) |
+                     ((unsigned long long)f2u_exact(P.z) << 42);
       if (c == d2 - 1) a.R1[b0 * a.d1p + b1] = f2u_exact(P.w);
     }
   }
@@ -609,12 +626,14 @@ struct G4GatherArgs {
   const uint32_t* keys;
   const uint32_t* off;        // [parts][nb + 1]
   int32_t n_parts, nb;
-  unsigned long long* S;      // [d0][d1][d2p] packed {cnt, c3, c2}
+  unsigned long long* S;      // [d0][nbk][d1][W] packed {cnt, c3, c2}, columns < d2 - 1
+  unsigned long long* G;      // [d0][d1p] the same at column d2 - 1 (b2 = any)
   uint32_t* R1;               // [d0][d1p]
   uint32_t* G0;               // [d0] raw c0, re-zeroed here
   uint32_t* P0;               // [d0] inclusive prefix of G0
   int32_t d0, d1, d2, d2p, d1p;
   int32_t hp;                 // plane row pitch in cells (odd: conflict-free row walk)
+  int32_t W, nbk;             // S column blocks (the eval's units)
   int32_t ns2, seg2;          // b2 segments of the row walk
   int32_t ns0, seg0;          // b0 segments of the column walk
 };
@@ -644,6 +663,9 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
     s_c2[i] = 0u;
   }
   for (int i = tid; i < d0; i += kGatherThreads) s_c1[i] = 0u;
+  // the eval's CTAs (one per SM, pinned by their register file) take the
+  // SMs this kernel leaves idle and wait there in griddepcontrol.wait
+  pdl_release();
   pdl_wait();  // keys, offsets and G0 are complete
   if (b1 == 0 && warp == nwarps - 1) {  // c0: inclusive prefix over b0, re-zero
     uint32_t carry = 0;
@@ -805,37 +827,37 @@ __global__ void __launch_bounds__(kGatherThreads, 1) g4_gather_kernel(const __gr
   if (live) {
     unsigned long long P = 0;
     for (int p = 0; p < s; ++p) P += s_seg[p * d2 + c];
-    const int64_t plane = (int64_t)a.d1 * a.d2p;
-    unsigned long long* dst = a.S + (int64_t)b1 * a.d2p + c + (int64_t)r_lo * plane;
+    int64_t step;
+    unsigned long long* dst = table_column(a.S, a.G, a.W, a.nbk, a.d1, a.d1p, d2, b1, c, step);
+    dst += r_lo * step;
     const unsigned long long* src = s_pl + (size_t)r_lo * hp + c;
     for (int r = r_lo; r < r_hi; ++r) {  // pointers stepped, no per-row index math
       P += *src;
       *dst = P;
       src += hp;
-      dst += plane;
+      dst += step;
     }
   }
-  // the eval is released only once every plane is written: launched
-  // earlier, its clusters would be placed around this kernel's CTAs and the
-  // last ones could miss the first wave
-  pdl_release();
   phase(1, 5);
 }
 
 // ------------------------------------------------------------------ eval --
-constexpr int kEval4Threads = 512;
+constexpr int kEvalThreads = 256;
 
 struct G4EvalArgs {
-  int32_t d0, d1, d2, d2p, d1p;
-  int32_t rows, nseg, seg_len;          // b1 rows per CTA of the cluster, row segments
+  int32_t d0, d1, d2, d1p, d0p;
+  int32_t W, Wp, nbk, nseg, seg_len;    // columns per unit, walker row pitch, column blocks per slab, row segments
+  int32_t n_units;                      // d0 * nbk
   int64_t sb[16];                       // first config of the structure with model mask m
   int64_t cfg_begin, cfg_count;
   int64_t n_rec;
   double rcp_n;
   const double* cost1;
-  const unsigned long long* S;  // prefixed along b0 and b2, packed {cnt, c3, c2}
+  const unsigned long long* S;  // [d0][nbk][d1][W] prefixed along b0 and b2, packed {cnt, c3, c2}
+  const unsigned long long* G;  // [d0][d1p] the same at b2 = any (row totals)
   const uint32_t* R1;           // [d0][d1p] C1 over b0 <= k0, b1, any b2
-  const uint32_t* P0;           // [d0] C0(k0)
+  const uint32_t* P0;           // [d0p] C0(k0)
+  int32_t group_smem;           // bytes of shared memory per group
   double* acc;
   double* cost;
   double* frac;
@@ -896,181 +918,123 @@ __device__ __forceinline__ void put4(const G4EvalArgs& a, int64_t cfg, const uin
   store4<false>(a, i, fr[0], fr[1], fr[2], fr[3], mean, correct, n, rcp);
 }
 
-// A cluster of CL CTAs owns slab k0, split along b1 (rows): each
-// bulk-copies its rows, sums its columns over them and hands the column
-// sums to every CTA of the cluster through distributed shared memory (a
-// rank's b1 carry is the sum over the ranks before it; the slab total over
-// all of them).  Then each walks its own rows.  Four CTAs of 256 threads
-// per slab (B200: up to 148 four-CTA clusters resident, 101 needed for
-// 100-level grids, so the grid is one wave even when launched around the
-// previous kernel's last CTAs) and a walk of a quarter slab per CTA.
-template <bool ALL, int THREADS, int CL>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THREADS)
-    g4_eval_kernel(const __grid_constant__ G4EvalArgs a) {
-  extern __shared__ __align__(16) unsigned long long s_slab[];  // [rows][d2p], then tables
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t s_c0[2];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int h = (int)cluster.block_rank();
-  const int d0 = a.d0, d1 = a.d1, d2 = a.d2, d2p = a.d2p;
+// Scoring.  Units are (b0 slab k0, block of W columns k2); the gather left
+// S prefixed along b0 and b2 in blocks [k0][block][b1][W] (plus the row
+// totals G = the b2 = "any" column, and R1), so the b1 prefix of a column
+// needs only that column: no exchange between CTAs (the previous design
+// split a slab by rows over a four-CTA cluster and exchanged the b1 carry
+// through distributed shared memory).  A unit is staged by three bulk
+// copies and scored by a group of 256 threads:
+//   1. walker (column c, row segment s) sums its segment; warps 0 / 1
+//      prefix the row totals and C1 along b1;
+//   2. row-shared terms of every row (the stage-2 fraction, the partial
+//      mean cost and correct count of the longest structure); the edge
+//      configs at k2 = any of this block's share of the rows;
+//   3. the walk: carry = the segments before, then each row's prefix P
+//      scores config (k0, k1, c); the last row (k1 = any) is the column
+//      total and scores the structure that skips model 1 at (k0, c).
+constexpr int kEvalGroups = 4;
+
+// Named barrier of one 256-thread group (ids 1..kEvalGroups; 0 is __syncthreads).
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "n"(kEvalThreads) : "memory");
+}
+
+template <bool ALL>
+__device__ __forceinline__ void eval_unit(const G4EvalArgs& a, int u, const unsigned long long* s_col,
+                                          unsigned long long* s_g, uint32_t* s_c1,
+                                          const uint32_t* s_p0, unsigned long long* s_seg,
+                                          double* s_rowf, double* s_rowm, uint32_t* s_rowc,
+                                          int tid, int grp) {
+  const int d0 = a.d0, d1 = a.d1, d2 = a.d2, W = a.W, nbk = a.nbk;
   const int g0 = d0 - 1, g1 = d1 - 1, g2 = d2 - 1;
-  const int k0 = blockIdx.x / CL;
-  const int rb = h * a.rows, re = min(d1, rb + a.rows), nr = re - rb;
-  const bool last = re == d1;  // owns row g1
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool any0 = k0 == g0;  // the "any" slab: structures without model 0
-  unsigned long long* s_colg = s_slab + (size_t)a.rows * d2p;  // [rows] row totals, prefixed
-  double* s_rowf = reinterpret_cast<double*>(s_colg + a.rows);   // [rows] row-shared fraction
-  double* s_rowm = s_rowf + a.rows;                              // [rows] partial mean cost
-  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(s_rowm + a.rows);  // [nseg][d2]
-  unsigned long long* s_sums = s_seg + (size_t)a.nseg * d2;      // [CL][d2] column sums per rank
-  unsigned long long* s_carry = s_sums + (size_t)CL * d2;        // [d2] over the ranks before
-  unsigned long long* s_tot = s_carry + d2;                      // [d2] over the slab
-  uint32_t* s_c1 = reinterpret_cast<uint32_t*>(s_tot + d2);      // [d1] C1 prefix along b1
-  uint32_t* s_rowc = s_c1 + d1;                                  // [rows]
-  // skip a slab none of whose configs is in the requested range (all CTAs
-  // of the cluster decide alike): a slab k0 < g0 scores structures (0,1) ..
-  // (0,1,2,3), the first starting at sb[3] + k0 and the last ending at
-  // sb[15] + (k0 + 1) g1 g2; the any slab scores the singletons (from
-  // config 0) through (1,2,3)
+  const int k0 = u / nbk, blk = u - k0 * nbk;
+  const int c_lo = blk * W, nc = min(g2, c_lo + W) - c_lo;
+  const int lane = tid & 31, warp = tid >> 5;
+  const bool any0 = k0 == g0;
+  // skip a slab none of whose configs is in the requested range: a slab
+  // k0 < g0 scores structures (0,1) .. (0,1,2,3), the first starting at
+  // sb[3] + k0 and the last ending at sb[15] + (k0 + 1) g1 g2; the any slab
+  // scores the singletons (from config 0) through (1,2,3)
   const int64_t lo = any0 ? 0 : a.sb[3] + k0;
   const int64_t hi = any0 ? a.sb[14] + (int64_t)g1 * g2 : a.sb[15] + (int64_t)(k0 + 1) * g1 * g2;
   if (hi <= a.cfg_begin || lo >= a.cfg_begin + a.cfg_count) return;
   const bool full = lo >= a.cfg_begin && hi <= a.cfg_begin + a.cfg_count;
-  phase(2, 0);
-  // every CTA of the cluster must be running before its shared memory is
-  // written by the others: arrive now, wait before the first remote write
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  const uint32_t bytes = (uint32_t)((int64_t)max(nr, 0) * d2p * 8);
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_wait();  // the prefix tables are complete
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bar, bytes);
-    const unsigned long long* src = a.S + ((int64_t)k0 * d1 + rb) * d2p;
-    constexpr uint32_t kChunk = 32768;
-    for (uint32_t off = 0; off < bytes; off += kChunk)
-      bulk_g2s(reinterpret_cast<uint8_t*>(s_slab) + off, reinterpret_cast<const uint8_t*>(src) + off,
-               min(kChunk, bytes - off), &bar);
-  }
-  // while the slab is in flight: C1(k0, b1) prefix along b1 (warp 1), C0 (warp 2)
-  if (warp == 1) {
-    const uint32_t* row = a.R1 + (int64_t)k0 * a.d1p;
-    uint32_t carry = 0;
-    for (int b = 0; b < d1; b += 32) {
-      const int b1 = b + lane;
-      uint32_t x = b1 < d1 ? row[b1] : 0u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      x += carry;
-      if (b1 < d1) s_c1[b1] = x;
-      carry = __shfl_sync(0xffffffffu, x, 31);
-    }
-  } else if (warp == 2 && lane == 0) {
-    s_c0[0] = a.P0[k0];
-    s_c0[1] = a.P0[g0];
-  }
-  mbar_wait(&bar, 0);
-  phase(2, 1);
-  // column sums over this CTA's rows: thread (column col, row segment seg)
-  const int col = tid % d2, seg = tid / d2;
-  const bool live = seg < a.nseg;
-  const int r_lo = seg * a.seg_len, r_hi = min(nr, r_lo + a.seg_len);
-  unsigned long long ssum = 0;
-  if (live)
-    for (int r = r_lo; r < r_hi; ++r) ssum += s_slab[(size_t)r * d2p + col];
-  if (live) s_seg[seg * d2 + col] = ssum;
-  __syncthreads();
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-  if (live && seg == 0) {
+  // 1. segment sums; prefixes of the row totals and of C1 along b1
+  const int wc = tid % a.Wp, ws = tid / a.Wp;
+  const bool walker = ws < a.nseg && wc < nc;
+  const int r_lo = ws * a.seg_len, r_hi = min(d1, r_lo + a.seg_len);
+  if (walker) {
     unsigned long long t = 0;
-    for (int q = 0; q < a.nseg; ++q) t += s_seg[q * d2 + col];
-#pragma unroll
-    for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(s_sums + h * d2 + col, r) = t;
+    for (int r = r_lo; r < r_hi; ++r) t += s_col[r * W + wc];
+    s_seg[ws * W + wc] = t;
   }
-  cluster.sync();
-  if (tid < d2) {
-    unsigned long long c = 0, t = 0;
-#pragma unroll
-    for (int r = 0; r < CL; ++r) {
-      const unsigned long long v = s_sums[r * d2 + tid];
-      if (r < h) c += v;
-      t += v;
-    }
-    s_carry[tid] = c;
-    s_tot[tid] = t;
-  }
-  __syncthreads();
-  if (nr <= 0) return;  // a rank past the slab's last row (small d1) only adds zeros
-  phase(2, 2);
-  // column g2 (row totals) prefix along b1 over own rows, after the carry
   if (warp == 0) {
-    unsigned long long carry = s_carry[g2];
-    for (int b = 0; b < nr; b += 32) {
+    unsigned long long carry = 0;
+    for (int b = 0; b < d1; b += 32) {
       const int r = b + lane;
-      unsigned long long x = r < nr ? s_slab[(size_t)r * d2p + g2] : 0ull;
+      unsigned long long x = r < d1 ? s_g[r] : 0ull;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
       x += carry;
-      if (r < nr) s_colg[r] = x;
+      if (r < d1) s_g[r] = x;
+      carry = __shfl_sync(0xffffffffu, x, 31);
+    }
+  } else if (warp == 1) {
+    uint32_t carry = 0;
+    for (int b = 0; b < d1; b += 32) {
+      const int r = b + lane;
+      uint32_t x = r < d1 ? s_c1[r] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      x += carry;
+      if (r < d1) s_c1[r] = x;
       carry = __shfl_sync(0xffffffffu, x, 31);
     }
   }
-  __syncthreads();
-
+  group_sync(grp);
   const double n = (double)a.n_rec, rcp = a.rcp_n;
   const double one = div_count(n, n, rcp);
   const double c0c = __ldg(a.cost1 + 0), c1c = __ldg(a.cost1 + 1), c2c = __ldg(a.cost1 + 2),
                c3c = __ldg(a.cost1 + 3);
-  const Cell3 tot = unpack3(s_tot[g2]);  // slab total: (k0, g1, g2)
+  const Cell3 tot = unpack3(s_g[g1]);  // slab total: (k0, g1, g2)
   const uint32_t C1g = s_c1[g1];
-  const uint32_t base0 = s_c0[1] - s_c0[0];  // slab k0: model 0 completes b0 > k0
-  const double f1 = div_count((double)tot.cnt, n, rcp);  // slab k0: after stage 0
+  const uint32_t base0 = s_p0[g0] - s_p0[k0];  // slab k0: model 0 completes b0 > k0
+  const double f1 = div_count((double)tot.cnt, n, rcp);
   const double m1 = dadd(dadd(0.0, dmul(one, c0c)), dmul(f1, c1c));
-  // row-shared terms of the longest structure of this slab:
+  // 2. row-shared terms of the longest structure:
   //   slab k0: (0,1,2,3) -> frac[2] = cnt(k0,k1,g)/n, mean through stage 2,
   //            correct through stage 1 plus C2(k0,k1,g)
   //   any:     (1,2,3)   -> frac[1] = cnt(g,k1,g)/n, mean through stage 1,
   //            correct of stage 0 (model 1) plus C2(g,k1,g)
-  for (int r = tid; r < nr; r += THREADS) {
-    const int k1 = rb + r;
-    const Cell3 rg = unpack3(s_colg[r]);
+  for (int r = tid; r < g1; r += kEvalThreads) {
+    const Cell3 rg = unpack3(s_g[r]);
     const double fr = div_count((double)rg.cnt, n, rcp);
     s_rowf[r] = fr;
     if (!any0) {
       s_rowm[r] = dadd(m1, dmul(fr, c2c));
-      s_rowc[r] = base0 + (C1g - s_c1[k1]) + rg.c2;
+      s_rowc[r] = base0 + (C1g - s_c1[r]) + rg.c2;
     } else {
       s_rowm[r] = dadd(dadd(0.0, dmul(one, c1c)), dmul(fr, c2c));
-      s_rowc[r] = (C1g - s_c1[k1]) + rg.c2;
+      s_rowc[r] = (C1g - s_c1[r]) + rg.c2;
     }
   }
-  __syncthreads();
-
-  phase(2, 3);
-  // Threads [0, nwalk) walk the interior (column w % g2, row segment
-  // w / g2); the spare threads score the edge cells meanwhile (their
-  // prefixes are already known): last column (k2 = g2) from the row totals
-  // s_colg; last row (k1 = g1, last rank) from the slab's column totals;
-  // the corner from the slab total.
-  const int nwalk = a.nseg * g2;
-  if (tid >= nwalk) {
-    const int n_row = min(nr, g1 - rb);          // own rows k1 < g1
-    const int n_col = last ? g2 : 0;             // last-row cells
-    const int n_items = n_row + n_col + (last ? 1 : 0);
-    for (int e = tid - nwalk; e < n_items; e += THREADS - nwalk) {
-      if (e < n_row) {
-        const int k1 = rb + e;
-        const Cell3 p = unpack3(s_colg[e]);
+  // edge configs at k2 = any for this block's share of the rows, and (block
+  // 0) the slab's corner structures
+  {
+    const int per = (g1 + nbk - 1) / nbk;
+    const int e_lo = min(g1, blk * per), e_hi = min(g1, e_lo + per);
+    const int n_items = (e_hi - e_lo) + (blk == 0 ? 1 : 0);
+    for (int e = tid; e < n_items; e += kEvalThreads) {
+      if (e < e_hi - e_lo) {
+        const int k1 = e_lo + e;
+        const Cell3 p = unpack3(s_g[k1]);
         if (!any0) {  // (0,1,2) and (0,1,3) at (k0, k1)
           const uint32_t reach[2] = {tot.cnt, p.cnt};
           const uint32_t c01 = base0 + (C1g - s_c1[k1]);
@@ -1084,19 +1048,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THR
           put4<2>(a, a.sb[6] + k1, reach, cA, c1 + p.c2, n, rcp, one);
           put4<2>(a, a.sb[10] + k1, reach, cB, c1 + p.c3, n, rcp, one);
         }
-      } else if (e < n_row + n_col) {  // last row: P = (k0, g1, k2)
-        const int k2 = e - n_row;
-        const Cell3 p = unpack3(s_tot[k2]);
-        if (!any0) {  // (0,2,3) at (k0, k2)
-          const uint32_t reach[2] = {tot.cnt, p.cnt};
-          const double cst[3] = {c0c, c2c, c3c};
-          put4<3>(a, a.sb[13] + (int64_t)k0 * g2 + k2, reach, cst, base0 + (tot.c2 - p.c2) + p.c3,
-                  n, rcp, one);
-        } else {  // (2,3) at k2
-          const uint32_t reach[1] = {p.cnt};
-          const double cst[2] = {c2c, c3c};
-          put4<2>(a, a.sb[12] + k2, reach, cst, (tot.c2 - p.c2) + p.c3, n, rcp, one);
-        }
       } else if (!any0) {  // (0,1), (0,2), (0,3) at k0
         const uint32_t reach[1] = {tot.cnt};
         const double cA[2] = {c0c, c1c}, cB[2] = {c0c, c2c}, cC[2] = {c0c, c3c};
@@ -1106,34 +1057,30 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THR
       } else {  // singletons
         const uint32_t* none = nullptr;
         const double cA[1] = {c0c}, cB[1] = {c1c}, cC[1] = {c2c}, cD[1] = {c3c};
-        put4<1>(a, a.sb[1], none, cA, s_c0[1], n, rcp, one);
+        put4<1>(a, a.sb[1], none, cA, s_p0[g0], n, rcp, one);
         put4<1>(a, a.sb[2], none, cB, C1g, n, rcp, one);
         put4<1>(a, a.sb[4], none, cC, tot.c2, n, rcp, one);
         put4<1>(a, a.sb[8], none, cD, tot.c3, n, rcp, one);
       }
     }
-    return;
   }
-  phase(2, 4);
-
-  // interior: the longest structure, one config per position (k1, k2),
-  // k1 < g1, k2 < g2; its index is row_base + k1 * g2
-  const int wc = tid % g2, ws = tid / g2;
-  const int w_lo = ws * a.seg_len, w_hi = min(nr, w_lo + a.seg_len);
-  unsigned long long P = s_carry[wc];
-  for (int q = 0; q < ws; ++q) P += s_seg[q * d2 + wc];
-  const int64_t row_base =
-      (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + wc - a.cfg_begin;
-  const int r_end = min(w_hi, g1 - rb);
+  group_sync(grp);
+  if (!walker) return;
+  // 3. the walk
+  const int col = c_lo + wc;
+  unsigned long long P = 0;
+  for (int q = 0; q < ws; ++q) P += s_seg[q * W + wc];
+  const int64_t row_base = (any0 ? a.sb[14] : a.sb[15] + (int64_t)k0 * g1 * g2) + col - a.cfg_begin;
+  const int r_end = min(r_hi, g1);
   if (ALL && full && !a.n_correct) {
     // the usual sweep: every output of the slab requested, the configs of
     // consecutive rows g2 apart -- walk three output pointers
-    const int64_t i0 = row_base + (int64_t)(rb + w_lo) * g2;
+    const int64_t i0 = row_base + (int64_t)r_lo * g2;
     double* pf = a.frac + i0 * 4;
     double* pc = a.cost + i0;
     double* pa = a.acc + i0;
-    for (int r = w_lo; r < r_end; ++r) {
-      P += s_slab[(size_t)r * d2p + wc];
+    for (int r = r_lo; r < r_end; ++r) {
+      P += s_col[r * W + wc];
       const Cell3 p = unpack3(P);
       const double f3 = div_count((double)p.cnt, n, rcp);
       const double rf = s_rowf[r];
@@ -1149,22 +1096,88 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THR
       pc += g2;
       pa += g2;
     }
-    phase(2, 5);
-    return;
+  } else {
+    for (int r = r_lo; r < r_end; ++r) {
+      P += s_col[r * W + wc];
+      const int64_t i = row_base + (int64_t)r * g2;
+      if (!full && (i < 0 || i >= a.cfg_count)) continue;
+      const Cell3 p = unpack3(P);
+      const double f3 = div_count((double)p.cnt, n, rcp);
+      const double rf = s_rowf[r];
+      const double mean = dadd(s_rowm[r], dmul(f3, c3c));
+      const uint32_t correct = s_rowc[r] - p.c2 + p.c3;
+      if (!any0)
+        store4<ALL>(a, i, one, f1, rf, f3, mean, correct, n, rcp);
+      else
+        store4<ALL>(a, i, one, rf, f3, 0.0, mean, correct, n, rcp);
+    }
   }
-  for (int r = w_lo; r < r_end; ++r) {
-    P += s_slab[(size_t)r * d2p + wc];
-    const int64_t i = row_base + (int64_t)(rb + r) * g2;
-    if (!full && (i < 0 || i >= a.cfg_count)) continue;
+  if (r_hi == d1) {  // the last segment: P is the column total (k0, g1, col)
+    P += s_col[g1 * W + wc];
     const Cell3 p = unpack3(P);
-    const double f3 = div_count((double)p.cnt, n, rcp);
-    const double rf = s_rowf[r];
-    const double mean = dadd(s_rowm[r], dmul(f3, c3c));
-    const uint32_t correct = s_rowc[r] - p.c2 + p.c3;
-    if (!any0)
-      store4<ALL>(a, i, one, f1, rf, f3, mean, correct, n, rcp);
-    else
-      store4<ALL>(a, i, one, rf, f3, 0.0, mean, correct, n, rcp);
+    if (!any0) {  // (0,2,3) at (k0, col)
+      const uint32_t reach[2] = {tot.cnt, p.cnt};
+      const double cst[3] = {c0c, c2c, c3c};
+      put4<3>(a, a.sb[13] + (int64_t)k0 * g2 + col, reach, cst, base0 + (tot.c2 - p.c2) + p.c3, n,
+              rcp, one);
+    } else {  // (2,3) at col
+      const uint32_t reach[1] = {p.cnt};
+      const double cst[2] = {c2c, c3c};
+      put4<2>(a, a.sb[12] + col, reach, cst, (tot.c2 - p.c2) + p.c3, n, rcp, one);
+    }
+  }
+}
+
+// One CTA of kEvalGroups x 256 threads per SM (its 64-register threads
+// fill the register file, so the CTAs cannot pile onto the SMs the gather
+// frees first, which the launch-early programmatic dependency would do with
+// small CTAs: 118 SMs hosting four and 17 none).  Group g of CTA c scores
+// units u = c + (g + kEvalGroups * k) * gridDim.x: every SM gets
+// n_units / #SMs units, within one.  A group syncs on its own named barrier
+// and stages each unit with three bulk copies on its own mbarrier.
+template <bool ALL>
+__global__ void __launch_bounds__(kEvalGroups * kEvalThreads, 1) g4_eval_kernel(const __grid_constant__ G4EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char s_raw[];  // per group: unit buffer, P0, tables
+  __shared__ __align__(8) uint64_t bar[kEvalGroups];
+  const int d1 = a.d1, W = a.W, nbk = a.nbk;
+  const int grp = threadIdx.x / kEvalThreads, tid = threadIdx.x % kEvalThreads;
+  const uint32_t col_bytes = (uint32_t)d1 * W * 8, g_bytes = (uint32_t)a.d1p * 8,
+                 r_bytes = (uint32_t)a.d1p * 4, p0_bytes = (uint32_t)a.d0p * 4;
+  const uint32_t buf_bytes = col_bytes + g_bytes + r_bytes;
+  unsigned char* buf = s_raw + (size_t)grp * a.group_smem;
+  uint32_t* s_p0 = reinterpret_cast<uint32_t*>(buf + buf_bytes);
+  unsigned long long* s_seg = reinterpret_cast<unsigned long long*>(s_p0 + a.d0p);  // [nseg][W]
+  double* s_rowf = reinterpret_cast<double*>(s_seg + (size_t)a.nseg * W);             // [d1]
+  double* s_rowm = s_rowf + d1;                                                        // [d1]
+  uint32_t* s_rowc = reinterpret_cast<uint32_t*>(s_rowm + d1);                         // [d1]
+  phase(2, 0);
+  if (tid == 0) {
+    mbar_init(&bar[grp], 1);
+    fence_mbar_init();
+  }
+  group_sync(grp);
+  pdl_wait();  // the prefix tables are complete
+  uint32_t parity = 0;
+  bool first = true;
+  for (int u = blockIdx.x + grp * gridDim.x; u < a.n_units; u += kEvalGroups * gridDim.x) {
+    if (tid == 0) {
+      const int k0 = u / nbk, blk = u - k0 * nbk;
+      fence_proxy_async();  // the generic reads of the buffer (previous unit) come first
+      mbar_arrive_expect_tx(&bar[grp], buf_bytes + (first ? p0_bytes : 0u));
+      bulk_g2s(buf, a.S + ((int64_t)k0 * nbk + blk) * d1 * W, col_bytes, &bar[grp]);
+      bulk_g2s(buf + col_bytes, a.G + (int64_t)k0 * a.d1p, g_bytes, &bar[grp]);
+      bulk_g2s(buf + col_bytes + g_bytes, a.R1 + (int64_t)k0 * a.d1p, r_bytes, &bar[grp]);
+      if (first) bulk_g2s(s_p0, a.P0, p0_bytes, &bar[grp]);
+    }
+    first = false;
+    mbar_wait(&bar[grp], parity);
+    parity ^= 1u;
+    phase(2, 1);
+    eval_unit<ALL>(a, u, reinterpret_cast<const unsigned long long*>(buf),
+                   reinterpret_cast<unsigned long long*>(buf + col_bytes),
+                   reinterpret_cast<uint32_t*>(buf + col_bytes + g_bytes), s_p0, s_seg, s_rowf, s_rowm,
+                   s_rowc, tid, grp);
+    group_sync(grp);  // the buffer is free again
   }
   phase(2, 5);
 }
@@ -1172,18 +1185,48 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(THREADS, 1024 / THR
 }  // namespace
 
 // ------------------------------------------------------------ host side --
+#ifndef GS_G4_EVAL_W
+#define GS_G4_EVAL_W 20  // columns per eval unit (config 2: five blocks of 20 per slab)
+#endif
+
+// Eval unit shape: W columns (even: the unit's block is a 16-byte multiple
+// for the bulk copy), row segments for 256 threads, and the shared memory
+// of two unit buffers plus the tables.
+#ifndef GS_G4_EVAL_WARP_ROWS
+#define GS_G4_EVAL_WARP_ROWS 1  // walkers of a row segment padded to whole warps
+#endif
+
+struct EvalShape {
+  int W, Wp, nbk, nseg, seg_len;
+  size_t smem;
+};
+
+EvalShape eval_shape(int64_t d0, int64_t d1, int64_t d2) {
+  const int64_t d1p = (d1 + 3) & ~3ll, d0p = (d0 + 3) & ~3ll, g2 = d2 - 1;
+  EvalShape e{};
+  for (e.W = (int)std::min<int64_t>(GS_G4_EVAL_W, (g2 + 1) & ~1ll); e.W >= 2; e.W -= 2) {
+    e.Wp = GS_G4_EVAL_WARP_ROWS && e.W <= 32 ? 32 : e.W;
+    e.nseg = (int)std::max<int64_t>(1, std::min<int64_t>(kEvalThreads / e.Wp, d1));
+    e.seg_len = (int)((d1 + e.nseg - 1) / e.nseg);
+    e.nseg = (int)((d1 + e.seg_len - 1) / e.seg_len);
+    e.smem = round_up((size_t)(d1 * e.W * 8 + d1p * 12) + (size_t)d0p * 4 + (size_t)e.nseg * e.W * 8 +
+                          (size_t)d1 * 20, 128);  // per group
+    if (e.smem * kEvalGroups <= kGrid4SlabMax) break;
+  }
+  e.nbk = e.W >= 2 ? (int)((g2 + e.W - 1) / e.W) : 0;
+  return e;
+}
+
 bool grid4_supported(int64_t n_rec, int32_t M, const int32_t* glen) {
   if (M != 4 || n_rec < 1 || n_rec >= kGrid4MaxRec) return false;
   const int64_t d0 = glen[0] + 1, d1 = glen[1] + 1, d2 = glen[2] + 1;
-  const int64_t d2p = (d2 + 1) & ~1ll;
   const int64_t grid_bytes = (int64_t)(glen[0] + glen[1] + glen[2]) * 8 + 3 * kLutBuckets * kLutEntryBytes;
   if (glen[0] + glen[1] + glen[2] > 5 * kHist4Threads) return false;
-  // plane tile [d0][d2p] x 16 B plus segment sums; eval slab [d1][d2p] x 8 B
+  // plane tile [d0][d2p] x 16 B plus segment sums
   const int64_t plane_smem = ((d0 + 1) / 2 * (d2 | 1) + kPlaneThreads + d2) * 16 + kZeroBytes;
   return d0 <= kMaxDim4 && d2 <= kMaxDim4 && d1 <= 4096 && grid_bytes <= 96 * 1024 &&
-         d2 <= kPlaneThreads && plane_smem <= (int64_t)kGrid4SlabMax &&
-         d2 <= kEval4Threads && d1 >= 2 &&
-         (d1 + 1) / 2 * (d2p * 8 + 28) + (kEval4Threads + 4 * d2) * 8 + d1 * 4 <= (int64_t)kGrid4SlabMax;
+         d2 <= kPlaneThreads && plane_smem <= (int64_t)kGrid4SlabMax && d1 >= 2 &&
+         eval_shape(d0, d1, d2).W >= 2;
 }
 
 // Shared memory of the sorted build's two kernels (0 when it does not apply).
@@ -1223,14 +1266,19 @@ Grid4Layout grid4_layout(const int32_t* glen, int64_t n_rec) {
   L.hp = L.d2 | 1;
   L.nb = L.d1;
   L.max_parts = sm_count();
+  const EvalShape es = eval_shape(L.d0, L.d1, L.d2);
+  L.W = es.W;
+  L.nbk = es.nbk;
   const size_t bH = round_up((size_t)L.d0 * L.d1 * L.hp * 16, 256);
-  const size_t bS = round_up((size_t)L.d0 * L.d1 * L.d2p * 8, 256);
+  const size_t bS = round_up((size_t)L.d0 * L.nbk * L.d1 * L.W * 8, 256);
+  const size_t bGt = round_up((size_t)L.d0 * L.d1p * 8, 256);
   const size_t bR1 = round_up((size_t)L.d0 * L.d1p * 4, 256);
   const size_t bG = round_up((size_t)L.d0 * 4, 256);
   L.offH = 0;
   L.offG0 = bH;
   L.offS = bH + bG;
-  L.offR1 = L.offS + bS;
+  L.offGt = L.offS + bS;
+  L.offR1 = L.offGt + bGt;
   L.offP0 = L.offR1 + bR1;
   L.offCnt = L.offP0 + bG;
   L.offKeys = L.offCnt + 256;
@@ -1285,6 +1333,9 @@ cudaError_t grid4_finish(const int32_t* glen, uint8_t* ws, cudaStream_t st) {
   G4PlaneArgs p{};
   p.H = H;
   p.S = reinterpret_cast<unsigned long long*>(ws + L.offS);
+  p.G = reinterpret_cast<unsigned long long*>(ws + L.offGt);
+  p.W = L.W;
+  p.nbk = L.nbk;
   p.R1 = reinterpret_cast<uint32_t*>(ws + L.offR1);
   p.G0 = G0;
   p.P0 = reinterpret_cast<uint32_t*>(ws + L.offP0);
@@ -1365,6 +1416,9 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   g.n_parts = sp.parts;
   g.nb = L.nb;
   g.S = reinterpret_cast<unsigned long long*>(ws + L.offS);
+  g.G = reinterpret_cast<unsigned long long*>(ws + L.offGt);
+  g.W = L.W;
+  g.nbk = L.nbk;
   g.R1 = reinterpret_cast<uint32_t*>(ws + L.offR1);
   g.G0 = G0;
   g.P0 = reinterpret_cast<uint32_t*>(ws + L.offP0);
@@ -1384,33 +1438,14 @@ cudaError_t grid4_build(const double* cert, const uint8_t* corr, int64_t n_rec, 
   return launch_pdl(g4_gather_kernel, (unsigned)L.d1, kGatherThreads, sp.gather_smem, st, g);
 }
 
-// Row split of a slab over the CL CTAs of a cluster: rows per CTA, and row
-// segments that serve both the column sums (d2 columns) and the interior
-// walk (g2 columns), leaving >= 32 threads for the edge cells.
-template <int THREADS, int CL>
-void eval_split(G4EvalArgs& a, const Grid4Layout& L) {
-  a.rows = (L.d1 + CL - 1) / CL;
-  const int g2w = std::max(1, L.d2 - 1);
-  a.nseg = std::max(1, std::min(std::min((THREADS - 32) / g2w, THREADS / L.d2), a.rows));
-  a.seg_len = (a.rows + a.nseg - 1) / a.nseg;
-  a.nseg = (a.rows + a.seg_len - 1) / a.seg_len;
-}
-
-template <int THREADS, int CL>
-size_t eval_smem(G4EvalArgs a, const Grid4Layout& L) {
-  eval_split<THREADS, CL>(a, L);
-  return (size_t)a.rows * L.d2p * 8 + (size_t)a.rows * (8 + 8 + 8 + 4) +
-         ((size_t)a.nseg + CL + 2) * L.d2 * 8 + (size_t)L.d1 * 4;
-}
-
-template <bool ALL, int THREADS, int CL>
-cudaError_t launch_eval(G4EvalArgs a, const Grid4Layout& L, cudaStream_t st) {
-  eval_split<THREADS, CL>(a, L);
-  const size_t smem = eval_smem<THREADS, CL>(a, L);
+template <bool ALL>
+cudaError_t launch_eval(const G4EvalArgs& a, cudaStream_t st) {
   static SmemAttr done;
-  cudaError_t e = ensure_smem(g4_eval_kernel<ALL, THREADS, CL>, done, (size_t)kGrid4SlabMax);
+  const size_t smem = (size_t)kEvalGroups * a.group_smem;
+  cudaError_t e = ensure_smem(g4_eval_kernel<ALL>, done, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(g4_eval_kernel<ALL, THREADS, CL>, (unsigned)(CL * L.d0), THREADS, smem, st, a);
+  const int grid = std::max(1, std::min(a.n_units, sm_count()));
+  return launch_pdl(g4_eval_kernel<ALL>, (unsigned)grid, kEvalGroups * kEvalThreads, smem, st, a);
 }
 
 cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct_begin,
@@ -1419,11 +1454,18 @@ cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct
                        double* frac, uint32_t* n_correct, const uint8_t* ws, cudaStream_t st) {
   const Grid4Layout L = grid4_layout(glen, n_rec);
   G4EvalArgs a{};
+  const EvalShape es = eval_shape(L.d0, L.d1, L.d2);
   a.d0 = L.d0;
   a.d1 = L.d1;
   a.d2 = L.d2;
-  a.d2p = L.d2p;
   a.d1p = L.d1p;
+  a.d0p = (L.d0 + 3) & ~3;
+  a.W = es.W;
+  a.Wp = es.Wp;
+  a.nbk = es.nbk;
+  a.nseg = es.nseg;
+  a.seg_len = es.seg_len;
+  a.n_units = L.d0 * es.nbk;
   for (int s = 0; s < n_struct; ++s) a.sb[struct_mask[s] & 15u] = struct_begin[s];
   a.cfg_begin = cfg_begin;
   a.cfg_count = cfg_count;
@@ -1431,20 +1473,16 @@ cudaError_t grid4_eval(int64_t n_rec, const int32_t* glen, const int64_t* struct
   a.rcp_n = 1.0 / (double)n_rec;
   a.cost1 = cost1;
   a.S = reinterpret_cast<const unsigned long long*>(ws + L.offS);
+  a.G = reinterpret_cast<const unsigned long long*>(ws + L.offGt);
   a.R1 = reinterpret_cast<const uint32_t*>(ws + L.offR1);
   a.P0 = reinterpret_cast<const uint32_t*>(ws + L.offP0);
+  a.group_smem = (int32_t)es.smem;
   a.acc = acc;
   a.cost = cost;
   a.frac = frac;
   a.n_correct = n_correct;
   const bool all = acc && cost && frac && (reinterpret_cast<uintptr_t>(frac) & 31u) == 0;
-  // four CTAs of 256 threads per slab when the slab is tall enough, else
-  // two of 512
-  const bool four = L.d1 >= 16 && L.d2 <= 224 && eval_smem<256, 4>(a, L) <= kGrid4SlabMax;
-  if (four)
-    return all ? launch_eval<true, 256, 4>(a, L, st) : launch_eval<false, 256, 4>(a, L, st);
-  return all ? launch_eval<true, kEval4Threads, 2>(a, L, st)
-             : launch_eval<false, kEval4Threads, 2>(a, L, st);
+  return all ? launch_eval<true>(a, st) : launch_eval<false>(a, st);
 }
 
 }  // namespace gs

@@ -12,9 +12,10 @@ constexpr size_t kGrid4SlabMax = 200 * 1024;      // one (b1, b2) slab in shared
 struct Grid4Layout {
   int32_t d0, d1, d2, d2p, d1p;  // table dims (grid length + 1), padded pitches
   int32_t hp;                    // histogram row pitch (odd)
-  int32_t nb, max_parts;         // sorted build: buckets (2 per b1), record ranges
+  int32_t nb, max_parts;         // sorted build: buckets (one per b1), record ranges
+  int32_t W, nbk;                // eval units: column blocks of W columns, nbk per b0 slab
   bool sorted;                   // one-shot builds take the bucket-sort kernels
-  size_t offH, offG0, offS, offR1, offP0, offCnt, offKeys, offOff, bytes;
+  size_t offH, offG0, offS, offGt, offR1, offP0, offCnt, offKeys, offOff, bytes;
 };
 
 bool grid4_supported(int64_t n_rec, int32_t n_models, const int32_t* grid_len);

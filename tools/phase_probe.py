@@ -17,7 +17,7 @@ K, CTAS, SLOTS = 3, 1024, 8
 names = ["g4_sort", "g4_gather", "g4_eval"]
 labels = [["start", "grid in", "tables", "loop done", "scanned", "end"],
           ["start", "segments", "plane built", "row walk", "cluster", "end"],
-          ["start", "slab in", "cluster", "tables", "edges", "end"]]
+          ["start", "staged", "unit 1", "unit 2", "unit 3", "end"]]
 _, cert, corr, grids, cost1 = bench.workload(0)
 sw = GridSweep(cert, corr, grids, cost1, build=False)
 out = None
