@@ -1,6 +1,8 @@
 """Grid path (gs_grid_build/eval/decode + gs_pareto_counts) vs the reference
 golden (config 1) and the oracle walk over the enumerated configs."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -553,3 +555,44 @@ def test_config4b_shape_sampled_vs_oracle():
     assert np.array_equal(res.accuracy[ip].cpu().numpy(), want[0])
     assert np.array_equal(res.mean_cost[ip].cpu().numpy(), want[1])
     assert np.array_equal(res.forward_frac[ip].cpu().numpy(), want[2])
+
+
+def _sweep_general(cert, corr, grids, cost1):
+    """The same sweep through the general path (GS_GRID_GENERAL=1 at plan time)."""
+    os.environ["GS_GRID_GENERAL"] = "1"
+    try:
+        from paper_2406_14424_b200.gridsweep import GridSweep
+        sw = GridSweep(cert, corr, grids, cost1)
+        assert sw.info.fast_path == 0 and sw.info.build_launches != 5
+        return sw, sw.evaluate()
+    finally:
+        del os.environ["GS_GRID_GENERAL"]
+
+
+def test_config4b_full_product_vs_general_path():
+    """Config 4b over its whole enumeration (105,101,005 configs): the
+    five-model slab path (narrow and wide T slabs, faces, regular eval) equals
+    the general path (dense histogram, in-place prefixes, general eval) bit
+    for bit on every output; every 50,000th config also against the oracle."""
+    import torch
+    from paper_2406_14424_b200 import synth
+    from paper_2406_14424_b200.cascades import grid_values
+    from paper_2406_14424_b200.gridsweep import GridSweep
+    cert, corr = synth.validation_matrices(5, 100_000, 0.8, 5)
+    grids = [np.array(grid_values(cert[:, j], 100)) for j in range(5)]
+    cost1 = np.array([1.0, 4.0, 16.0, 64.0, 256.0])
+    sw = GridSweep(cert, corr, grids, cost1)
+    assert sw.n_configs == 105_101_005 and sw.info.build_launches == 5
+    fast = sw.evaluate()
+    gen_sw, gen = _sweep_general(cert, corr, grids, cost1)
+    assert gen_sw.n_configs == sw.n_configs
+    for a, b in ((fast.accuracy, gen.accuracy), (fast.mean_cost, gen.mean_cost),
+                 (fast.forward_frac, gen.forward_frac)):
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+    pick = np.arange(0, sw.n_configs, 50_000)
+    sm, thr, ns = (t.cpu().numpy() for t in sw.decode(pick))
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=os.cpu_count() or 8)
+    ip = torch.from_numpy(pick).cuda()
+    assert np.array_equal(fast.accuracy[ip].cpu().numpy(), want[0])
+    assert np.array_equal(fast.mean_cost[ip].cpu().numpy(), want[1])
+    assert np.array_equal(fast.forward_frac[ip].cpu().numpy(), want[2])
