@@ -247,7 +247,8 @@ class ThresholdGrid:
 
 def quantiles(column, qs) -> np.ndarray:
     """np.quantile(column, qs) (numpy "linear", bit-exact) computed on the
-    device (gs_quantiles: device sort + numpy's interpolation arithmetic).
+    device (gs_quantiles: a radix select of the needed order statistics +
+    numpy's interpolation arithmetic).
     column: a 1-D numpy array or CUDA tensor (any stride)."""
     qs = np.ascontiguousarray(np.asarray(qs, dtype=np.float64).reshape(-1))
     col = column if isinstance(column, torch.Tensor) else torch.from_numpy(
