@@ -85,7 +85,7 @@ int gs_eval_encoded(const double* certainty, const uint8_t* correct,
  *             increasing (grid_len[j] values for model j)
  *   grid_len  HOST array [n_models]
  * gs_grid_info reports the config count and the workspace the tables need
- * (n_rec < 2^24).  gs_grid_build fills the prefix tables; it must run
+ * (n_rec < 2^30).  gs_grid_build fills the prefix tables; it must run
  * before gs_grid_eval on the same workspace.  The workspace's histogram
  * region must be zero when gs_grid_build starts and is left zero when it
  * returns; pass GS_GRID_WORKSPACE_DIRTY on the first build of a fresh (or

@@ -60,7 +60,16 @@ namespace gs {
 namespace {
 
 constexpr int kMaxM = GS_MAX_MODELS;
-constexpr int64_t kMaxExactF32 = 1ll << 24;
+constexpr int64_t kMaxExactF32 = 1ll << 24;  // f32 fallback histogram exact below
+constexpr int64_t kMaxRec = 1ll << 30;        // 32-bit record indices (with grid-stride headroom) and counts
+constexpr int64_t kMaxRcp = 1ll << 26;        // div_count's range (gs_common.cuh)
+
+// count / n, correctly rounded: div_count's three FP64 ops below 2^26
+// records (the host passes rcp = 1/n), IEEE division above (rcp = 0)
+__device__ __forceinline__ double div_n(double x, double n, double rcp) {
+  return rcp != 0.0 ? div_count(x, n, rcp) : __ddiv_rn(x, n);
+}
+inline double rcp_of(int64_t n) { return n < kMaxRcp ? 1.0 / (double)n : 0.0; }
 constexpr int kHistThreads = 512;
 constexpr size_t kSidePrivMax = 16 * 1024;
 constexpr size_t kSlabSmemMax = 200 * 1024;
@@ -84,7 +93,7 @@ struct Plan {
 
 int make_plan(int64_t n_rec, int32_t M, const int32_t* grid_len, Plan* p) {
   if (M < 1 || !grid_len || n_rec < 1) return GS_EINVAL;
-  if (M > kMaxM || n_rec >= kMaxExactF32) return GS_EUNSUPPORTED;
+  if (M > kMaxM || n_rec >= kMaxRec) return GS_EUNSUPPORTED;
   p->M = M;
   p->D = M - 1;
   p->DP = M >= 4 ? M - 3 : 0;
@@ -207,6 +216,7 @@ struct HistArgs {
   uint32_t* P;             // side histogram (u32 counts)
   unsigned long long* H16; // packed main histogram: 4 x 16-bit counts per cell
   uint32_t* flag;          // set when a cell count reaches 2^16 (fallback needed)
+  int32_t f_u32;           // fallback histogram in u32 words (n_rec >= 2^24: f32 would round)
 };
 
 // MODE 0: main table as ONE 64-bit atomic add per record (fields {cnt,
@@ -214,7 +224,8 @@ struct HistArgs {
 // count, so no field can carry unless some cell's count passes 0xFFFF, and the
 // thread that moves a count from 0xFFFF sees it in the returned old value and
 // raises the flag).  MODE 1: exits at once unless the flag is up; then redoes
-// the main table with f32 vector reductions (exact below 2^24).
+// the main table with f32 vector reductions (exact below 2^24), or with u32
+// atomics for larger record sets (f_u32).
 // Bin lookup: gs_grid_lut.cuh.
 template <int M, typename Cell, int MODE>
 __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_constant__ HistArgs a) {
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     }
   }
 
-  // n_rec < 2^24 and M <= 8, so record offsets fit 32 bits
+  // n_rec < 2^30: record indices fit 32 bits (offsets are taken in 64)
   const int n_rec = (int)a.n_rec;
   const int step = gridDim.x * blockDim.x;
   // the overflow test on each atomic's old value is made one iteration late,
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rec; r += step) {
     double x[M];
     uint32_t k[M];
-    const double* row = a.cert + r * M;
+    const double* row = a.cert + (int64_t)r * M;
     if (M % 2 == 0 && a.vec_ok) {
 #pragma unroll
       for (int j = 0; j < (M / 2) * 2; j += 2) {
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
       for (int j = 0; j < M; ++j) k[j] = ((w >> (8 * j)) & 0xffu) != 0;
     } else {
 #pragma unroll
-      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + r * M + j) != 0;
+      for (int j = 0; j < M; ++j) k[j] = __ldg(a.corr + (int64_t)r * M + j) != 0;
     }
     Cell cellF = 0, cellP = 0;
 #pragma unroll
@@ -321,7 +332,14 @@ __global__ void __launch_bounds__(kHistThreads) grid_hist_kernel(const __grid_co
     for (int i = 0; i < 3; ++i)
       if (M - 1 - i >= 0) v[1 + i] = k[M - 1 - i];
     if (MODE == 1) {
-      red_add_v4(a.F + cellF * 4, 1.f, (float)v[1], (float)v[2], (float)v[3]);
+      if (a.f_u32) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(a.F) + cellF * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (v[i]) atomicAdd(w + i, v[i]);
+      } else {
+        red_add_v4(a.F + cellF * 4, 1.f, (float)v[1], (float)v[2], (float)v[3]);
+      }
       continue;
     }
     const unsigned long long inc = 1ull | ((unsigned long long)v[1] << 16) |
@@ -424,7 +442,7 @@ __global__ void __launch_bounds__(256) rowscan_kernel(uint4* src, uint4* T, int6
 // up, re-zeroes what it read, and writes the u32 prefix.
 __global__ void __launch_bounds__(256) rowscan_first_kernel(unsigned long long* H16, uint4* HF,
                                                             const uint32_t* flag, uint4* T,
-                                                            int64_t n_rows, int len) {
+                                                            int64_t n_rows, int len, int hf_u32) {
   const int lane = (int)lane_id();
   const bool fb = *flag != 0u;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -442,7 +460,7 @@ __global__ void __launch_bounds__(256) rowscan_first_kernel(unsigned long long* 
         if (c < len) {
           if (fb) {
             uint4 f = inF[c];
-            e[u] = to_u4(*reinterpret_cast<float4*>(&f));
+            e[u] = hf_u32 ? f : to_u4(*reinterpret_cast<float4*>(&f));
           } else {
             const unsigned long long w = in16[c];
             e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
@@ -491,7 +509,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
                                                           const uint32_t* flag, uint4* T,
                                                           int64_t n_slabs, int rows, int cols,
                                                           uint4* sideH, uint4* sideT, int side_len,
-                                                          int parts, int zero) {
+                                                          int parts, int zero, int hf_u32) {
   // a slab may be split into `parts` column ranges, one CTA each: every CTA
   // reads whole rows (for the row prefix) but keeps, scans and stores only
   // its own columns, so twice the CTAs share the work
@@ -583,7 +601,7 @@ __global__ void __launch_bounds__(1024) slab_first_kernel(unsigned long long* H1
           if (c < cols) {
             if (fb) {
               uint4 f = inF[c];
-              e[u] = to_u4(*reinterpret_cast<float4*>(&f));
+              e[u] = hf_u32 ? f : to_u4(*reinterpret_cast<float4*>(&f));
             } else {
               const unsigned long long w = in16[c];
               e[u] = make_uint4((uint32_t)(w & 0xffff), (uint32_t)((w >> 16) & 0xffff),
@@ -805,7 +823,7 @@ __device__ __forceinline__ void store_config(const EvalGridArgs& a, int64_t i, c
     }
   }
   if (a.cost) a.cost[i] = mean;
-  if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+  if (a.acc) a.acc[i] = div_n((double)correct, n, rcp);
   if (a.n_correct) a.n_correct[i] = correct;
 }
 
@@ -817,7 +835,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
   const int lane = (int)lane_id();
   const double n = (double)a.n_rec;
   const double rcp = a.rcp_n;
-  const double one = div_count(n, n, rcp);  // first-stage fraction: n / n
+  const double one = div_n(n, n, rcp);  // first-stage fraction: n / n
   const uint4 totF = __ldg(a.F + a.cellsF - 1);
   uint4 totP[NVPX];
 #pragma unroll
@@ -904,7 +922,7 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
           for (int v = 0; v < NVPX; ++v) vP[v] = __ldg(a.P + cP * NVP + v);
         }
         cp += A - chan<M>(vF, vP, m);
-        fr[t + 1] = div_count((double)vF.x, n, rcp);
+        fr[t + 1] = div_n((double)vF.x, n, rcp);
         mp = dadd(mp, dmul(fr[t + 1], __ldg(a.cost1 + ((mdl >> (4 * (t + 1))) & 15u))));
       }
     }
@@ -937,11 +955,11 @@ __global__ void __launch_bounds__(256) grid_eval_kernel(const __grid_constant__ 
         const bool ok = kl < gL && i >= 0 && i < a.cfg_count;
         const uint32_t correct =
             cp + a_last - chan<M>(wF[u], wP[u], mL) + chan<M>(wF[u], wP[u], mK);
-        const double frK = div_count((double)wF[u].x, n, rcp);
+        const double frK = div_n((double)wF[u].x, n, rcp);
         const double mean = dadd(mp, dmul(frK, costK));
         if (ok) {
           if (a.cost) a.cost[i] = mean;
-          if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+          if (a.acc) a.acc[i] = div_n((double)correct, n, rcp);
           if (a.n_correct) a.n_correct[i] = correct;
         }
         // forward_frac: the warp's 32 consecutive [M]-rows go through a
@@ -1007,7 +1025,7 @@ __global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_
   const bool full = cta_first >= a.cfg_begin && cta_end <= a.cfg_begin + a.cfg_count;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double n = (double)a.n_rec, rcp = a.rcp_n;
-  const double one = div_count(n, n, rcp);
+  const double one = div_n(n, n, rcp);
   const double c0 = __ldg(a.cost1), c1 = __ldg(a.cost1 + 1), c2 = __ldg(a.cost1 + 2),
                c3 = __ldg(a.cost1 + 3), c4 = __ldg(a.cost1 + 4);
   const uint4 Fk0 = __ldg(a.F + k0 * a.sF0 + (int64_t)g1 * a.sF1 + (int64_t)g2 * a.sF2 + g3);
@@ -1015,8 +1033,8 @@ __global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_
   const uint4 Pgg = __ldg(a.P + (int64_t)a.g0 * a.d1 + g1);
   const uint4 Pk0 = __ldg(a.P + (int64_t)k0 * a.d1 + g1);
   const uint4 Pk01 = __ldg(a.P + (int64_t)k0 * a.d1 + k1);
-  const double fr1 = div_count((double)Fk0.x, n, rcp);
-  const double fr2 = div_count((double)Fk01.x, n, rcp);
+  const double fr1 = div_n((double)Fk0.x, n, rcp);
+  const double fr2 = div_n((double)Fk01.x, n, rcp);
   const double m2 = dadd(dadd(dadd(0.0, dmul(one, c0)), dmul(fr1, c1)), dmul(fr2, c2));
   // models 0, 1 complete between their positions; model 2's count before k2
   const uint32_t base = (Pgg.x - Pk0.x) + (Pk0.y - Pk01.y) + Fk01.w;
@@ -1039,7 +1057,7 @@ __global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_
                                  __shfl_sync(0xffffffffu, cell[u].w, g3 & 31));
       if (u == (g3 >> 5)) rc = t;
     }
-    const double fr3 = div_count((double)rc.x, n, rcp);
+    const double fr3 = div_n((double)rc.x, n, rcp);
     const double m3 = dadd(m2, dmul(fr3, c3));
     const uint32_t cr = base - rc.w + rc.z;  // through model 2, plus model 3's count before k3
     const int64_t i0 = cta_first + (int64_t)k2 * g3 - a.cfg_begin;  // config of k3 = 0
@@ -1048,13 +1066,13 @@ __global__ void __launch_bounds__(kFull5Threads) full5_eval_kernel(const __grid_
       const int k3 = lane + 32 * u;
       if (k3 < g3) {
         const uint4 c = cell[u];
-        const double fr4 = div_count((double)c.x, n, rcp);
+        const double fr4 = div_n((double)c.x, n, rcp);
         const double mean = dadd(m3, dmul(fr4, c4));
         const uint32_t correct = cr - c.z + c.y;
         const int64_t i = i0 + k3;
         if (full || (i >= 0 && i < a.cfg_count)) {
           if (a.cost) a.cost[i] = mean;
-          if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+          if (a.acc) a.acc[i] = div_n((double)correct, n, rcp);
           if (a.n_correct) a.n_correct[i] = correct;
         }
         double* f = buf + k3 * 5;
@@ -1188,7 +1206,7 @@ __global__ void __launch_bounds__(512) walk_eval_kernel(const __grid_constant__ 
   const int k1 = cell / d2, k2 = cell - k1 * d2;
   const int xcol = k1 == ra ? 0 : 1;
   const double n = (double)a.n_rec, rcp = a.rcp_n;
-  const double one = div_count(n, n, rcp);
+  const double one = div_n(n, n, rcp);
   const double cA = __ldg(a.cost1 + 0), cB = __ldg(a.cost1 + 1), cC = __ldg(a.cost1 + 2),
                cD = __ldg(a.cost1 + 3);
   const double m0 = dadd(0.0, dmul(one, cA));
@@ -1205,9 +1223,9 @@ __global__ void __launch_bounds__(512) walk_eval_kernel(const __grid_constant__ 
     const uint4 X1 = s_ext[xcol][k0];  // (k0, k1, g2): after stage 1
     // channels {cnt, c3, c2, c1}; c0 from the side table
     const uint32_t correct = (side_tot - s_side[k0]) + (X0.w - X1.w) + (X1.z - P.z) + P.y;
-    const double f1 = div_count((double)X0.x, n, rcp);
-    const double f2 = div_count((double)X1.x, n, rcp);
-    const double f3 = div_count((double)P.x, n, rcp);
+    const double f1 = div_n((double)X0.x, n, rcp);
+    const double f2 = div_n((double)X1.x, n, rcp);
+    const double f3 = div_n((double)P.x, n, rcp);
     const double mean = dadd(dadd(dadd(m0, dmul(f1, cB)), dmul(f2, cC)), dmul(f3, cD));
     if (a.frac) {
       double2* row = reinterpret_cast<double2*>(a.frac + i * 4);
@@ -1215,7 +1233,7 @@ __global__ void __launch_bounds__(512) walk_eval_kernel(const __grid_constant__ 
       row[1] = make_double2(f2, f3);
     }
     if (a.cost) a.cost[i] = mean;
-    if (a.acc) a.acc[i] = div_count((double)correct, n, rcp);
+    if (a.acc) a.acc[i] = div_n((double)correct, n, rcp);
     if (a.n_correct) a.n_correct[i] = correct;
   }
 }
@@ -1331,7 +1349,8 @@ cudaError_t launch_grid_eval(const EvalGridArgs& a, cudaStream_t st) {
 cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int64_t cells, int vec,
                          cudaStream_t st, unsigned long long* H16 = nullptr,
                          const uint32_t* flag = nullptr, bool h_f32 = true, int skip_leading = 0,
-                         uint4* sideH = nullptr, uint4* sideT = nullptr, int side_len = 0) {
+                         uint4* sideH = nullptr, uint4* sideT = nullptr, int side_len = 0,
+                         bool hf_u32 = false) {
   int fused = 0;  // trailing dims already scanned by the first pass
   if (H16 && ndim >= 2 &&
       (size_t)dims[ndim - 1] * dims[ndim - 2] * sizeof(uint4) <= kSlabSmemMax) {
@@ -1349,7 +1368,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     // after the pass instead
     slab_first_kernel<<<(unsigned)blocks, 1024, smem, st>>>(H16, H, flag, T, n_slabs, rows, cols,
                                                             sideH, sideT, side_len, parts,
-                                                            parts == 1 ? 1 : 0);
+                                                            parts == 1 ? 1 : 0, hf_u32 ? 1 : 0);
     e = cudaGetLastError();
     if (e == cudaSuccess && parts > 1) {
       e = cudaMemsetAsync(H16, 0, (size_t)cells * 8, st);
@@ -1366,7 +1385,7 @@ cudaError_t prefix_table(uint4* H, uint4* T, int ndim, const int64_t* dims, int6
     const int64_t rows = cells / len;
     int64_t blocks = (rows * 32 + 255) / 256;
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 16));
-    rowscan_first_kernel<<<(unsigned)blocks, 256, 0, st>>>(H16, H, flag, T, rows, (int)len);
+    rowscan_first_kernel<<<(unsigned)blocks, 256, 0, st>>>(H16, H, flag, T, rows, (int)len, hf_u32 ? 1 : 0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || ndim <= 1) return e;
     fused = 1;
@@ -1506,6 +1525,7 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
   h.P = P;
   h.H16 = H16;
   h.flag = flag;
+  h.f_u32 = n_rec >= kMaxExactF32 ? 1 : 0;
   const size_t smem = (size_t)h.grid_doubles * sizeof(double) + (size_t)p.D * kLutBuckets * 4 +
                       (h.priv ? side_bytes : 0) + 16;
   if (smem > 200 * 1024) return GS_EUNSUPPORTED;
@@ -1531,7 +1551,7 @@ extern "C" int gs_grid_build(const double* certainty, const uint8_t* correct, in
                            p.dims, p.cellsF, 1, st, H16, flag, true, p.walk ? 1 : 0,
                            fold_side ? reinterpret_cast<uint4*>(P) : nullptr,
                            fold_side ? reinterpret_cast<uint4*>(ws + p.offP) : nullptr,
-                           fold_side ? (int)p.cellsP : 0));
+                           fold_side ? (int)p.cellsP : 0, n_rec >= kMaxExactF32));
   if (p.DP > 0 && !fold_side)
     GS_CUDA_TRY(prefix_table(reinterpret_cast<uint4*>(P), reinterpret_cast<uint4*>(ws + p.offP), p.DP,
                              p.dims, p.cellsP, p.NVP, st, nullptr, nullptr, false));
@@ -1598,7 +1618,7 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
   for (int j = 0; j < p.D; ++j) a.strideF[j] = p.strideF[j];
   for (int j = 0; j < p.DP; ++j) a.strideP[j] = p.strideP[j];
   a.n_rec = n_rec;
-  a.rcp_n = 1.0 / (double)n_rec;
+  a.rcp_n = rcp_of(n_rec);
   a.cellsF = p.cellsF;
   a.cellsP = p.cellsP;
   a.cfg_begin = config_begin;
@@ -1624,7 +1644,7 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
     w.cfg_begin = config_begin;
     w.cfg_count = config_count;
     w.n_rec = n_rec;
-    w.rcp_n = 1.0 / (double)n_rec;
+    w.rcp_n = rcp_of(n_rec);
     w.cost1 = cost1;
     w.S = reinterpret_cast<const uint4*>(ws + p.offF);
     w.faces = reinterpret_cast<uint4*>(const_cast<uint8_t*>(ws) + p.offFaces);
@@ -1668,7 +1688,7 @@ extern "C" int gs_grid_eval(int64_t n_rec, int32_t n_models, const int32_t* grid
     f.cfg_begin = config_begin;
     f.cfg_count = config_count;
     f.n_rec = n_rec;
-    f.rcp_n = 1.0 / (double)n_rec;
+    f.rcp_n = rcp_of(n_rec);
     f.cost1 = cost1;
     f.F = reinterpret_cast<const uint4*>(ws + p.offF);
     f.P = reinterpret_cast<const uint4*>(ws + p.offP);

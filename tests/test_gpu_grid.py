@@ -596,3 +596,23 @@ def test_config4b_full_product_vs_general_path():
     assert np.array_equal(fast.accuracy[ip].cpu().numpy(), want[0])
     assert np.array_equal(fast.mean_cost[ip].cpu().numpy(), want[1])
     assert np.array_equal(fast.forward_frac[ip].cpu().numpy(), want[2])
+
+
+@pytest.mark.parametrize("n_rec,M,glen", [(2**24 + 1001, 3, (4, 3, 2)), (2**26 + 3, 2, (3, 2))])
+def test_general_path_past_f32_and_rcp_ranges(n_rec, M, glen):
+    """Record sets past 2^24 (the f32 fallback histogram would round: the
+    16-bit packed table overflows and the fallback counts in u32) and past
+    2^26 (the three-op division's range: IEEE division instead), every config
+    vs the oracle."""
+    rng = np.random.default_rng(n_rec)
+    cert = rng.random((n_rec, M))
+    corr = (rng.random((n_rec, M)) < 0.7).astype(np.uint8)
+    grids = [np.sort(rng.random(g)) for g in glen]
+    cost1 = np.arange(1.0, M + 1.0) * 3.0
+    sw, (acc, cost, frac, nc) = _sweep(cert, corr, grids, cost1)
+    assert sw.info.fast_path == 0
+    sm, thr, ns = oracle.grid_configs(grids)
+    want = oracle.evaluate_encoded(cert, corr, sm, thr, ns, cost1, n_threads=os.cpu_count() or 8)
+    assert np.array_equal(acc, want[0])
+    assert np.array_equal(cost, want[1])
+    assert np.array_equal(frac, want[2])
