@@ -74,5 +74,41 @@ def build(verbose: bool = False, force: bool = False, phase_timing: bool = False
     return lib_path
 
 
+TORCH_OPS_SRC = CSRC / "gs_torch_ops.cpp"
+TORCH_OPS_LIB = PKG / "libgearserve_b200_torch.so"
+
+
+def build_torch_ops(verbose: bool = False, force: bool = False) -> Path:
+    """The torch operator library (TORCH_LIBRARY gearserve_b200): a thin
+    host-only C++ shim over libgearserve_b200.so, compiled with g++ against
+    torch's headers and linked to the kernel library by an $ORIGIN rpath."""
+    import torch
+    from torch.utils import cpp_extension as ce
+
+    lib = build(verbose=verbose, force=force)
+    newest = max(TORCH_OPS_SRC.stat().st_mtime, lib.stat().st_mtime,
+                 max(p.stat().st_mtime for p in INCLUDE.glob("*.h")))
+    if not force and TORCH_OPS_LIB.exists() and TORCH_OPS_LIB.stat().st_mtime >= newest:
+        return TORCH_OPS_LIB
+    cuda_home = Path(_nvcc()).resolve().parent.parent
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-fPIC", "-shared",
+           f"-D_GLIBCXX_USE_CXX11_ABI={abi}", "-DTORCH_API_INCLUDE_EXTENSION_H",
+           str(TORCH_OPS_SRC), "-I", str(INCLUDE), "-I", str(cuda_home / "include")]
+    for inc in ce.include_paths():
+        cmd += ["-I", inc]
+    for d in ce.library_paths():
+        cmd += ["-L", d, f"-Wl,-rpath,{d}"]
+    cmd += ["-L", str(PKG), "-lgearserve_b200", "-Wl,-rpath,$ORIGIN",
+            "-lc10", "-lc10_cuda", "-ltorch", "-ltorch_cpu", "-ltorch_cuda",
+            "-o", str(TORCH_OPS_LIB.with_suffix(".so.tmp"))]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(TORCH_OPS_LIB.with_suffix(".so.tmp"), TORCH_OPS_LIB)
+    return TORCH_OPS_LIB
+
+
 if __name__ == "__main__":
     print(build(verbose=True))
+    print(build_torch_ops(verbose=True))
