@@ -423,6 +423,23 @@ int gs_engine_run(const gs_engine_job* jobs, int32_t n_jobs, void* stream);
  * elements apart (a column of a row-major [n, M] matrix: stride = M);
  * qs: HOST array of n_q values in [0, 1]; out: device f64 [n_q].
  * ---------------------------------------------------------------------- */
+/* ------------------------------------------------------------------------
+ * A cascade stage's classifier head on the tensor cores, fused with the
+ * stage step's certainty (north_star's tensor-core use; the reference runs a
+ * model and then cascades.certainty on its scores, src/serving.py:79-97,
+ * src/cascades.py:20-28): logits = features @ weight^T (+ bias) by
+ * tcgen05.mma (bf16 in, f32 in TMEM), each row's certainty over the n_cls
+ * logits in the epilogue; the logits never reach HBM unless logits_out.
+ *   features  [n_rows, n_feat] bf16 row-major, 16-byte aligned
+ *   weight    [n_cls, n_feat] bf16 row-major (nn.Linear layout), aligned
+ *   bias      [n_cls] f32 or NULL;  n_feat % 64 == 0
+ *   kind      GS_CERT_MARGIN / GS_CERT_MAX_SOFTMAX / GS_CERT_ENTROPY
+ *   cert_out  [n_rows] f64;  logits_out [n_rows, n_cls] f32 or NULL
+ * ---------------------------------------------------------------------- */
+int gs_head_certainty(const void* features, const void* weight, const float* bias,
+                      int64_t n_rows, int32_t n_cls, int32_t n_feat, int32_t kind,
+                      double* cert_out, float* logits_out, void* stream);
+
 int gs_quantiles_workspace(int64_t n, int32_t n_q, size_t* bytes);
 int gs_quantiles(const double* column, int64_t n, int64_t stride,
                  const double* qs, int32_t n_q, double* out, void* workspace,

@@ -114,6 +114,8 @@ _SIGNATURES = {
                                    POINTER(c_size_t)],
     "gs_stage_gate_packed": [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_double,
                              c_void_p, c_void_p, c_size_t, c_int32, c_void_p],
+    "gs_head_certainty": [c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p,
+                          c_void_p, c_void_p],
 }
 _RESTYPES = {"gs_strerror": ctypes.c_char_p, "gs_last_cuda_error": ctypes.c_char_p,
              "gs_jsonl_close": None}
