@@ -51,7 +51,10 @@ def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+        out = {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+        if d.get("bf16_tflops"):
+            out["bf16_tflops"] = float(d["bf16_tflops"])
+        return out
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
@@ -461,6 +464,8 @@ def run_ours(args, world, rank, local):
                 line["stage_step"] = {k: c3[k]["stage_step"] for k in ("entropy", "margin")}
         if not args.skip_config5:
             line["config5"] = _guarded(config5_bench, args, dev)
+        if not args.skip_head:
+            line["head"] = _guarded(head_bench, args, dev)
         line["host"] = host_info()
         print(json.dumps(line), flush=True)
 
@@ -1125,6 +1130,60 @@ def config4a_bench(args, dev, world, rank):
                                                        "x 100k records, oracle/oracle_eval.c"}}
 
 
+def head_bench(args, dev, B=262_144, N=1000, K=2048):
+    """A cascade stage's classifier head on the tensor cores fused with its
+    certainty (gs_head_certainty): ResNet-50-shaped head (2048 features ->
+    1000 classes), bf16 features and weight, f32 accumulation in TMEM, entropy
+    certainty per row.  CUDA events around back-to-back calls (the 1 GB of
+    features exceeds L2); beside it the unfused path (cuBLAS bf16 GEMM ->
+    logits -> gs_certainty).  Parity: the first 4096 rows vs a float64 torch
+    reference of the same op."""
+    import math
+    import torch
+
+    from paper_2406_14424_b200.cascades import certainty_rows
+    from paper_2406_14424_b200.head import head_certainty
+
+    g = torch.Generator(device=dev).manual_seed(7)
+    f = torch.randn(B, K, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=dev, generator=g) / math.sqrt(K) * 3).to(torch.bfloat16)
+    bias = torch.randn(N, device=dev, generator=g) * 0.1
+
+    def timed(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    ms = timed(lambda: head_certainty(f, w, bias, kind="entropy"))
+    ms_unfused = timed(lambda: certainty_rows(f @ w.T + bias, kind="entropy"))
+    cert = head_certainty(f[:4096], w, bias, kind="entropy")
+    x = f[:4096].double() @ w.double().T + bias.double()
+    p = torch.softmax(x, dim=1)
+    ref = 1.0 - (-(p * torch.log_softmax(x, dim=1)).sum(dim=1)) / math.log(N)
+    err = float((cert - ref).abs().max())
+    flops = 2.0 * B * N * K
+    tf = flops / (ms * 1e-3) / 1e12
+    pk = peaks()
+    peak = pk.get("bf16_tflops") or 2250.0
+    return {"workload": f"classifier head + entropy certainty: features [{B}, {K}] bf16 x weight [{N}, {K}] "
+                        "bf16 (+ f32 bias) -> f64 certainty per row; logits never stored",
+            "ms": ms, "rows_per_s": B / (ms * 1e-3), "tflops": tf,
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                         "frac": tf / peak,
+                         "peak_source": "measured" if pk.get("bf16_tflops") else "nominal"},
+            "unfused": {"ms": ms_unfused, "tflops": flops / (ms_unfused * 1e-3) / 1e12,
+                        "path": "torch bf16 matmul (cuBLAS) + bias -> bf16 logits -> certainty_rows"},
+            "max_abs_err_vs_f64": err, "parity_ok": err < 2e-5,
+            "timing": "CUDA events around 10 back-to-back calls after 3 warm-up calls"}
+
+
 def online_router_bench(plan, prof, cert, corr):
     """The live-serving shape of the stage step: StageRouter.finish_batch
     (EngineState.finish_batch, src/engine.py:355-383) on batches of 4 / 8 /
@@ -1402,6 +1461,7 @@ def main():
     ap.add_argument("--skip-config3", action="store_true", help="skip the cfg3 cascade leg")
     ap.add_argument("--skip-config5", action="store_true", help="skip the cfg5 replay leg")
     ap.add_argument("--skip-config4a", action="store_true", help="skip the cfg4a front leg")
+    ap.add_argument("--skip-head", action="store_true", help="skip the tensor-core head leg")
     ap.add_argument("--flush", choices=["write", "clean", "none"], default="write",
                     help="L2 eviction between timed steps (see flush_l2)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
