@@ -15,6 +15,7 @@
 //   pareto_counts     cascades.pareto_filter on integer counts (src/cascades.py:116-129)
 //   certainty         cascades.certainty per row (src/cascades.py:20-28)
 //   quantiles         np.quantile(column, qs) for build_threshold_grid (src/cascades.py:150-163)
+//   head_certainty    a stage's classifier head + certainty on the tensor cores (gs_head.cu)
 #include <ATen/ATen.h>
 #include <ATen/cuda/CUDAContext.h>
 #include <c10/cuda/CUDAGuard.h>
@@ -180,6 +181,28 @@ at::Tensor quantiles(const at::Tensor& column, at::ArrayRef<double> qs) {
   return out.narrow(0, 0, (int64_t)q.size());
 }
 
+at::Tensor head_certainty(const at::Tensor& features, const at::Tensor& weight, const c10::optional<at::Tensor>& bias,
+                          int64_t kind) {
+  TORCH_CHECK_VALUE(features.dim() == 2 && weight.dim() == 2 && features.size(1) == weight.size(1),
+                    "features [B, K] and weight [N, K] must share K");
+  const at::Device dev = features.device();
+  TORCH_CHECK_VALUE(dev.is_cuda(), "features must be a CUDA tensor");
+  const c10::cuda::CUDAGuard guard(dev);
+  const auto f = dev_contig(features, at::kBFloat16, dev, "features");
+  const auto w = dev_contig(weight, at::kBFloat16, dev, "weight");
+  at::Tensor b;
+  if (bias.has_value()) {
+    b = dev_contig(*bias, at::kFloat, dev, "bias");
+    TORCH_CHECK_VALUE(b.numel() == w.size(0), "bias must hold one value per class");
+  }
+  auto cert = at::empty({f.size(0)}, f.options().dtype(at::kDouble));
+  check_rc(gs_head_certainty(f.data_ptr(), w.data_ptr(), b.defined() ? b.data_ptr<float>() : nullptr, f.size(0),
+                             (int32_t)w.size(0), (int32_t)f.size(1), (int32_t)kind, cert.data_ptr<double>(), nullptr,
+                             cur_stream()),
+           "head_certainty");
+  return cert;
+}
+
 }  // namespace
 
 TORCH_LIBRARY(gearserve_b200, m) {
@@ -190,6 +213,7 @@ TORCH_LIBRARY(gearserve_b200, m) {
   m.def("pareto_counts(Tensor n_correct, Tensor mean_cost, int n_rec) -> Tensor");
   m.def("certainty(Tensor scores, int kind=0) -> Tensor");
   m.def("quantiles(Tensor column, float[] qs) -> Tensor");
+  m.def("head_certainty(Tensor features, Tensor weight, Tensor? bias=None, int kind=2) -> Tensor");
 }
 
 TORCH_LIBRARY_IMPL(gearserve_b200, CUDA, m) {
@@ -198,4 +222,5 @@ TORCH_LIBRARY_IMPL(gearserve_b200, CUDA, m) {
   m.impl("pareto_counts", &pareto_counts);
   m.impl("certainty", &certainty);
   m.impl("quantiles", &quantiles);
+  m.impl("head_certainty", &head_certainty);
 }

@@ -12,6 +12,7 @@ kernel: a CPU tensor raises (no fallback).
     front = ops.pareto_counts(n_correct, cost, n_rec)
     cert = ops.certainty(logits, 2)       # GS_CERT_* kind
     q = ops.quantiles(column, [0.1, 0.5])
+    cert = ops.head_certainty(features_bf16, weight_bf16, bias_f32, 2)
 """
 
 from __future__ import annotations
@@ -23,7 +24,7 @@ import torch
 from . import _lib
 
 LIB = Path(__file__).resolve().parent / "libgearserve_b200_torch.so"
-OPS = ("evaluate_encoded", "grid_sweep", "pareto_counts", "certainty", "quantiles")
+OPS = ("evaluate_encoded", "grid_sweep", "pareto_counts", "certainty", "quantiles", "head_certainty")
 _loaded = False
 
 

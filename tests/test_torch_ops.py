@@ -53,3 +53,9 @@ def test_ops_match_the_library_and_the_oracle():
     assert np.array_equal(ops.quantiles(col, [0.1, 0.5, 0.9]).cpu().numpy(), quantiles(col, [0.1, 0.5, 0.9]))
     with pytest.raises(ValueError):
         ops.evaluate_encoded(d(cert), d(corr[:10]), d(sm), d(thr), d(ns), d(cost1))
+    # the tensor-core head
+    from paper_2406_14424_b200.head import head_certainty
+    f = torch.randn(300, 128, device="cuda").to(torch.bfloat16)
+    w = torch.randn(50, 128, device="cuda").to(torch.bfloat16)
+    b = torch.randn(50, device="cuda")
+    assert torch.equal(ops.head_certainty(f, w, b, 2), head_certainty(f, w, b, kind="entropy"))
