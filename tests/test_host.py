@@ -75,7 +75,8 @@ def test_grid_plan_rejects_bad_input():
     assert lib.gs_grid_plan(0, 2, _lib.int32_array([3, 3]), ctypes.byref(info)) == -1
     assert lib.gs_grid_plan(10, 2, _lib.int32_array([0, 3]), ctypes.byref(info)) == -1
     assert lib.gs_grid_plan(10, 9, _lib.int32_array([2] * 9), ctypes.byref(info)) == -4
-    assert lib.gs_grid_plan(1 << 24, 2, _lib.int32_array([3, 3]), ctypes.byref(info)) == -4
+    assert lib.gs_grid_plan(1 << 24, 2, _lib.int32_array([3, 3]), ctypes.byref(info)) == 0  # u32 fallback
+    assert lib.gs_grid_plan(1 << 30, 2, _lib.int32_array([3, 3]), ctypes.byref(info)) == -4
 
 
 def test_structures_order_matches_oracle_enumeration():

@@ -73,5 +73,24 @@ if which in ("all", "stage"):
     gb.gate(np.arange(7), np.zeros(7, np.int32), np.full(7, 0.5), np.zeros(7, bool))
     print("stage ok", flush=True)
 
+if which in ("all", "quantile"):
+    from paper_2406_14424_b200.cascades import quantiles
+    x = np.round(rng.random(20_000), 2)  # ties: long lists in the final select
+    qs = [k / 50 for k in range(1, 50)]
+    assert np.array_equal(quantiles(x, qs), np.quantile(x, qs))
+    y = rng.random(30_000)
+    assert np.array_equal(quantiles(y, qs), np.quantile(y, qs))
+    print("quantile ok", flush=True)
+
+if which in ("all", "head"):
+    from paper_2406_14424_b200.head import head_certainty
+    f = torch.randn(700, 256, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(300, 256, device="cuda") / 16).to(torch.bfloat16)
+    cert, lg = head_certainty(f, w, kind="entropy", logits=True)
+    ref = f.double() @ w.double().T
+    assert torch.allclose(lg.double(), ref, rtol=1e-5, atol=1e-5)
+    head_certainty(f, w, kind="margin")
+    print("head ok", flush=True)
+
 torch.cuda.synchronize()
 print("sanitize run ok")
