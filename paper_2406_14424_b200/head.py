@@ -42,3 +42,23 @@ def head_certainty(features: torch.Tensor, weight: torch.Tensor, bias: torch.Ten
                                        None if out is None else out.data_ptr(), _lib.stream_ptr())
     _lib.check(rc, "head_certainty")
     return (cert, out) if logits else cert
+
+
+def head_stage_step(features: torch.Tensor, weight: torch.Tensor, thr, bias: torch.Tensor | None = None,
+                    is_last=None, *, kind: str = "entropy", forward_features: bool = True,
+                    near_eps: float = 1e-5):
+    """One online cascade stage on the tensor cores: the head's certainty per
+    row (head_certainty), then the stage gate on it — stop when
+    cert >= thr (or the stage is the last), deferred rows compacted in batch
+    order and, with forward_features, their feature rows gathered into the
+    next stage's contiguous batch (stage.stage_step on the [n, 1] certainty
+    column: a one-class row's margin is its value).  near_eps lists the rows
+    whose certainty lies within it of the threshold (the head's f32
+    accumulation and ex2 put its certainty within ~5e-6 of a float64
+    recomputation, so the default band is wider than the score path's)."""
+    from .stage import stage_step
+    f = _lib.to_device(features, torch.bfloat16)
+    cert = head_certainty(f, weight, bias, kind=kind)
+    res = stage_step(cert.view(-1, 1), thr, is_last, kind="margin", payload=f if forward_features else None,
+                     near_eps=near_eps)
+    return res

@@ -53,3 +53,26 @@ def test_head_certainty_rejects_bad_shapes():
     with pytest.raises(ValueError):
         head_certainty(torch.zeros(10, 64, dtype=torch.bfloat16, device="cuda"),
                        torch.zeros(5, 128, dtype=torch.bfloat16, device="cuda"))  # K mismatch
+
+
+def test_head_stage_step_gates_and_forwards():
+    """head -> gate -> compaction: the deferred rows are exactly the rows whose
+    head certainty is below the threshold, in batch order, with their feature
+    rows gathered; decisions differ from a float64 recomputation only inside
+    the listed near-threshold band."""
+    from paper_2406_14424_b200.head import head_certainty, head_stage_step
+    g = torch.Generator(device="cuda").manual_seed(3)
+    B, N, K = 5000, 1000, 512
+    f = torch.randn(B, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K) * 4).to(torch.bfloat16)
+    cert = head_certainty(f, w, kind="entropy")
+    thr = float(torch.quantile(cert, 0.35))
+    res = head_stage_step(f, w, thr, kind="entropy")
+    want = torch.nonzero(cert < thr).flatten()
+    got = res.deferred_idx
+    assert torch.equal(got, want)
+    assert torch.equal(res.next_payload[: got.numel()], f[got])
+    ref = _cert64(f.double() @ w.double().T, "entropy")
+    differ = torch.nonzero((ref < thr) != (cert < thr)).flatten()
+    near = set(res.near_idx.tolist())
+    assert all(int(i) in near for i in differ)
