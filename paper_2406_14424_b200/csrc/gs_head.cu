@@ -39,7 +39,8 @@ constexpr int kHStages = 4;
 constexpr int kHEpiWarps = 8;   // two per TMEM lane quadrant, each half of a chunk's columns
 constexpr int kHThreads = 64 + 32 * kHEpiWarps;  // warp 0 TMA, warp 1 MMA (+ TMEM owner), then the epilogue
 constexpr uint32_t kHABytes = kHM * kHK * 2, kHBBytes = kHN * kHK * 2;
-constexpr size_t kHSmem = 1024 + (size_t)kHStages * (kHABytes + kHBBytes);  // + 1 KB alignment slack
+constexpr int kHBiasSmem = 4096;  // bias staged in shared memory up to this many classes
+constexpr size_t kHSmem = 1024 + (size_t)kHStages * (kHABytes + kHBBytes) + kHBiasSmem * 4;  // + 1 KB alignment slack
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -149,6 +150,10 @@ __global__ void __launch_bounds__(kHThreads, 1) head_certainty_kernel(const __gr
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* s_a = base;                                // [stages][128 x 64] bf16, swizzled
   uint8_t* s_b = base + (size_t)kHStages * kHABytes;  // [stages][256 x 64] bf16, swizzled
+  float* s_bias = reinterpret_cast<float*>(s_b + (size_t)kHStages * kHBBytes);  // [N] when N <= kHBiasSmem
+  const bool bias_smem = a.bias && a.N <= kHBiasSmem;
+  if (bias_smem)
+    for (int i = threadIdx.x; i < a.N; i += blockDim.x) s_bias[i] = a.bias[i];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = (a.B + kHM - 1) / kHM;  // persistent: tiles blockIdx.x, += gridDim.x
   const int n_chunks = (a.N + kHN - 1) / kHN, n_k = a.K / kHK;
@@ -237,14 +242,33 @@ __global__ void __launch_bounds__(kHThreads, 1) head_certainty_kernel(const __gr
         if (col0 >= a.N) break;  // warp-uniform
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kHN + g * 32), v);
-        float lmax = -INFINITY;
+        const bool full = col0 + 32 <= a.N;  // warp-uniform: only the last group is ragged
+        if (a.bias) {
+          if (bias_smem) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int col = col0 + i;
-          if (col < a.N) {
-            if (a.bias) v[i] += __ldg(a.bias + col);
-            lmax = fmaxf(lmax, v[i]);
+            for (int i = 0; i < 32; i += 4) {
+              if (full || col0 + i + 3 < a.N) {
+                const float4 b4 = *reinterpret_cast<const float4*>(s_bias + col0 + i);
+                v[i] += b4.x;
+                v[i + 1] += b4.y;
+                v[i + 2] += b4.z;
+                v[i + 3] += b4.w;
+              } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (col0 + i + j < a.N) v[i + j] += s_bias[col0 + i + j];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < a.N) v[i] += __ldg(a.bias + col0 + i);
           }
+        }
+        if (!full) {  // padding classes never count
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i >= a.N) v[i] = -INFINITY;
         }
         if (a.logits && r < a.B) {
           float* out = a.logits + r * (int64_t)a.N + col0;
@@ -254,19 +278,22 @@ __global__ void __launch_bounds__(kHThreads, 1) head_certainty_kernel(const __gr
         }
         if (a.kind == GS_CERT_MARGIN) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (col0 + i < a.N) {
-              const float x = v[i];
-              if (x > st.top1) {
-                st.top2 = st.top1;
-                st.top1 = x;
-              } else if (x > st.top2) {
-                st.top2 = x;
-              }
-            }
+          for (int i = 0; i < 32; ++i) {
+            const float x = v[i];
+            const float lo = fminf(x, st.top1);
+            st.top1 = fmaxf(x, st.top1);
+            st.top2 = fmaxf(st.top2, lo);
+          }
           continue;
         }
-        const float ly = lmax * kLog2e;
+        // max by a tree, then four independent (s, t) chains: the FADD / FFMA
+        // latencies of one row's 32 terms overlap instead of queueing
+        float mx[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mx[j] = fmaxf(fmaxf(v[j], v[j + 8]), fmaxf(v[j + 16], v[j + 24]));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mx[j] = fmaxf(mx[j], mx[j + 4]);
+        const float ly = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * kLog2e;
         if (ly > st.m) {  // rescale the running sums to the new max
           if (st.s > 0.f) {
             const float d = st.m - ly, e = ex2(d);
@@ -275,13 +302,15 @@ __global__ void __launch_bounds__(kHThreads, 1) head_certainty_kernel(const __gr
           }
           st.m = ly;
         }
+        float ps[4] = {0.f, 0.f, 0.f, 0.f}, pt[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (col0 + i < a.N) {
-            const float d = fmaf(v[i], kLog2e, -st.m), e = ex2(d);
-            st.s += e;
-            st.t = fmaf(d, e, st.t);
-          }
+        for (int i = 0; i < 32; ++i) {
+          const float d = fmaf(v[i], kLog2e, -st.m), e = ex2(d);  // -inf padding: e = 0
+          ps[i & 3] += e;
+          pt[i & 3] = fmaf(e > 0.f ? d : 0.f, e, pt[i & 3]);
+        }
+        st.s += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        st.t += (pt[0] + pt[1]) + (pt[2] + pt[3]);
       }
       tc_fence_before();
       __syncwarp();
