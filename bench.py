@@ -389,7 +389,9 @@ def run_ours(args, world, rank, local):
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_gbs = (b_in + b_out) / (step_ms * 1e-3) / 1e9
     traffic = None
-    tfile = ROOT / "profiles" / "r1_traffic.json"
+    tfile = ROOT / "profiles" / "r2" / "traffic.json"
+    if not tfile.exists():
+        tfile = ROOT / "profiles" / "r1_traffic.json"
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(dom)
 

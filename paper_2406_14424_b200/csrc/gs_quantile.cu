@@ -39,7 +39,8 @@ namespace {
 constexpr int kQBits = 12;
 constexpr int kQBins = 1 << kQBits;
 constexpr int kQFinalBits = 10;        // 24 + 4 x 10 = 64
-constexpr int kQMaxTargets = 2 * 255 + 1;
+constexpr int kQChunk = 255;  // quantiles per select round (more: several rounds over the same keys)
+constexpr int kQMaxTargets = 2 * kQChunk + 1;
 constexpr int kQHash = 1024;           // >= 2 x targets, power of two
 constexpr uint64_t kQEmpty = ~0ull;    // never a prefix (its low 40 bits are zero)
 constexpr int kQPassThreads = 512;
@@ -432,7 +433,7 @@ struct QLayout {
   size_t keys, list, qs, tgt0, tgt1, rows, hist0, hist1, bytes;
 };
 QLayout q_layout(int64_t n, int32_t n_q) {
-  const int n_t = 2 * n_q + 1;
+  const int n_t = 2 * std::min(n_q, kQChunk) + 1;
   QLayout L{};
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -459,7 +460,7 @@ using namespace gs;
 
 extern "C" int gs_quantiles_workspace(int64_t n, int32_t n_q, size_t* bytes) {
   GS_REQUIRE(bytes && n > 0 && n_q >= 0);
-  if (n >= (int64_t)1 << 40 || 2 * n_q + 1 > kQMaxTargets) return GS_EUNSUPPORTED;
+  if (n >= (int64_t)1 << 40) return GS_EUNSUPPORTED;
   *bytes = q_layout(n, n_q).bytes;
   return GS_OK;
 }
@@ -486,33 +487,36 @@ extern "C" int gs_quantiles(const double* column, int64_t n, int64_t stride, con
   RowInfo* rows = reinterpret_cast<RowInfo*>(ws + L.rows);
   uint32_t* hist0 = reinterpret_cast<uint32_t*>(ws + L.hist0);
   uint32_t* hist1 = reinterpret_cast<uint32_t*>(ws + L.hist1);
-  const int n_t = 2 * n_q + 1;
   const int64_t blocks =
       std::max<int64_t>(1, std::min<int64_t>((n + kQPassThreads - 1) / kQPassThreads, (int64_t)sm_count() * 4));
   GS_CUDA_TRY(cudaMemcpyAsync(dq, qs, (size_t)n_q * 8, cudaMemcpyHostToDevice, st));
   GS_CUDA_TRY(cudaMemsetAsync(hist0, 0, (size_t)kQBins * 4, st));
-  init_targets_kernel<<<(n_q + 1 + 127) / 128, 128, 0, st>>>(dq, n_q, n, t0);
-  GS_LAUNCH_CHECK();
+  // the keys and their top-12-bit histogram serve every round of targets
   gather_pass0_kernel<<<(unsigned)blocks, kQPassThreads, 0, st>>>(column, n, stride, keys, hist0);
-  GS_LAUNCH_CHECK();
-  // every target starts at prefix 0 (row 0 of the one-row pass-0 histogram);
-  // this resolve also zeroes pass 1's rows
-  resolve_kernel<<<(unsigned)n_t, kQResolveThreads, 0, st>>>(t0, t1, n_t, 0, hist0, hist1);
   GS_LAUNCH_CHECK();
   static SmemAttr pass1_attr;
   const size_t pass1_smem = (size_t)kQPrivRows * kQBins * 4;
   GS_CUDA_TRY(ensure_smem(pass1_kernel, pass1_attr, pass1_smem));
-  pass1_kernel<<<(unsigned)blocks, kQPassThreads, pass1_smem, st>>>(keys, n, t1, n_t, hist1);
-  GS_LAUNCH_CHECK();
-  resolve_kernel<<<(unsigned)n_t, kQResolveThreads, 0, st>>>(t1, t0, n_t, kQBits, hist1, nullptr);
-  GS_LAUNCH_CHECK();
-  plan_rows_kernel<<<1, 1024, 0, st>>>(t0, n_t, rows);
-  GS_LAUNCH_CHECK();
-  collect_kernel<<<(unsigned)blocks, kQPassThreads, 0, st>>>(keys, n, t0, n_t, rows, list);
-  GS_LAUNCH_CHECK();
-  final_select_kernel<<<(unsigned)n_t, kQResolveThreads, 0, st>>>(t0, rows, list);
-  GS_LAUNCH_CHECK();
-  lerp_kernel<<<(n_q + 127) / 128, 128, 0, st>>>(t0, n, dq, n_q, out);
-  GS_LAUNCH_CHECK();
+  for (int q0 = 0; q0 < n_q; q0 += kQChunk) {  // up to kQChunk quantiles (2 kQChunk + 1 targets) a round
+    const int nq = std::min(kQChunk, n_q - q0), n_t = 2 * nq + 1;
+    init_targets_kernel<<<(nq + 1 + 127) / 128, 128, 0, st>>>(dq + q0, nq, n, t0);
+    GS_LAUNCH_CHECK();
+    // every target starts at prefix 0 (row 0 of the one-row pass-0 histogram);
+    // this resolve also zeroes pass 1's rows
+    resolve_kernel<<<(unsigned)n_t, kQResolveThreads, 0, st>>>(t0, t1, n_t, 0, hist0, hist1);
+    GS_LAUNCH_CHECK();
+    pass1_kernel<<<(unsigned)blocks, kQPassThreads, pass1_smem, st>>>(keys, n, t1, n_t, hist1);
+    GS_LAUNCH_CHECK();
+    resolve_kernel<<<(unsigned)n_t, kQResolveThreads, 0, st>>>(t1, t0, n_t, kQBits, hist1, nullptr);
+    GS_LAUNCH_CHECK();
+    plan_rows_kernel<<<1, 1024, 0, st>>>(t0, n_t, rows);
+    GS_LAUNCH_CHECK();
+    collect_kernel<<<(unsigned)blocks, kQPassThreads, 0, st>>>(keys, n, t0, n_t, rows, list);
+    GS_LAUNCH_CHECK();
+    final_select_kernel<<<(unsigned)n_t, kQResolveThreads, 0, st>>>(t0, rows, list);
+    GS_LAUNCH_CHECK();
+    lerp_kernel<<<(nq + 127) / 128, 128, 0, st>>>(t0, n, dq + q0, nq, out + q0);
+    GS_LAUNCH_CHECK();
+  }
   return GS_OK;
 }

@@ -59,3 +59,16 @@ def test_threshold_grid_equals_reference_golden_on_synth():
     grid = gc.build_threshold_grid(va, p3, levels=10)
     for m in p3.model_ids:
         assert np.array_equal(np.array(grid.per_model[m]), g[f"synth_grid_{m}"])
+
+
+@pytest.mark.parametrize("kind", ["rand", "ties"])
+def test_many_quantiles_in_rounds(kind):
+    """1000-level grids (config 4a) need 999 quantiles: the select runs them in
+    rounds of 255 over the same keys."""
+    from paper_2406_14424_b200.cascades import grid_values, quantiles
+    rng = np.random.default_rng(11)
+    x = rng.random(200_000) if kind == "rand" else np.round(rng.random(200_000), 3)
+    qs = _q(1000)
+    assert np.array_equal(quantiles(x, qs), np.quantile(x, qs))
+    g = grid_values(x, 1000)
+    assert g == tuple(sorted({0.0} | {float(v) for v in np.quantile(x, qs)}))

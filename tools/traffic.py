@@ -7,7 +7,8 @@ out, reps = sys.argv[1], sys.argv[2:]
 names = {"g4_sort_kernel": "g4_sort", "g4_gather_kernel": "g4_gather", "g4_eval_kernel": "g4_eval",
          "g4_hist_kernel": "g4_hist", "g4_plane_kernel": "g4_plane", "bucket_min": "bucket_min",
          "stage_step_kernel<float, 0": "stage_step_kernel<float, 0",
-         "stage_step_kernel<float, 2": "stage_step_kernel<float, 2"}
+         "stage_step_kernel<float, 2": "stage_step_kernel<float, 2",
+         "head_certainty_kernel": "head_certainty"}
 res = {}
 for rep in reps:
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
