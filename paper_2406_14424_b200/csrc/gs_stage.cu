@@ -201,10 +201,29 @@ __device__ __forceinline__ RowPair warp_row_pair(const T* row, int n, bool vec_o
       return {(double)m1, (double)m2};
     }
     C m = neg_inf<C>();
-    each([&](T x) {
-      const C v = (C)to_float(x);
-      m = v > m ? v : m;
-    });
+    if constexpr (sizeof(C) == 4) {  // a max per 16-byte vector, then two chains over them
+      C ma = neg_inf<C>(), mb = neg_inf<C>();
+#pragma unroll
+      for (int u = 0; u < RV; ++u) {
+        if (lane + 32 * u < nv) {
+          const T* tv = reinterpret_cast<const T*>(&buf[u]);
+          C vm = (C)to_float(tv[0]);
+#pragma unroll
+          for (int q = 1; q < V; ++q) vm = fmaxf(vm, (C)to_float(tv[q]));
+          if (u & 1)
+            mb = fmaxf(mb, vm);
+          else
+            ma = fmaxf(ma, vm);
+        }
+      }
+      m = fmaxf(ma, mb);
+      if (has_tail) m = fmaxf(m, (C)to_float(tx));
+    } else {
+      each([&](T x) {
+        const C v = (C)to_float(x);
+        m = v > m ? v : m;
+      });
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const C y = __shfl_xor_sync(0xffffffffu, m, o);
@@ -223,6 +242,7 @@ __device__ __forceinline__ RowPair warp_row_pair(const T* row, int n, bool vec_o
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d * kLog2e));
         e = y;
       };
+      double s_odd = 0.0, t_odd = 0.0;  // two f64 chains over the vectors
 #pragma unroll
       for (int u = 0; u < RV; ++u) {
         if (lane + 32 * u < nv) {
@@ -235,10 +255,17 @@ __device__ __forceinline__ RowPair warp_row_pair(const T* row, int n, bool vec_o
             s4 += e;
             t4 = fmaf(e, d, t4);
           }
-          s += (double)s4;
-          if (KIND == GS_CERT_ENTROPY) t += (double)t4;
+          if (u & 1) {
+            s_odd += (double)s4;
+            if (KIND == GS_CERT_ENTROPY) t_odd += (double)t4;
+          } else {
+            s += (double)s4;
+            if (KIND == GS_CERT_ENTROPY) t += (double)t4;
+          }
         }
       }
+      s += s_odd;
+      t += t_odd;
       if (has_tail) {
         float e, d;
         term((float)to_float(tx), e, d);
@@ -334,13 +361,35 @@ template <typename T, int KIND, bool WIDE>
 __global__ void __launch_bounds__(256) certainty_kernel(const T* scores, int64_t n_rows, int n_cls,
                                                         int64_t stride, const int32_t* row_len,
                                                         bool vec_ok, double* out) {
-  if (WIDE) {
+  if (WIDE && KIND == GS_CERT_MARGIN) {  // nothing to finish: a row per warp trip
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t r = warp; r < n_rows; r += nw) {
       const int n = row_len ? row_len[r] : n_cls;
       const double c = warp_row_cert<T, KIND>(scores + r * stride, n, vec_ok && n == n_cls);
       if (lane_id() == 0) out[r] = c;
+    }
+  } else if (WIDE) {
+    // a warp takes 32 consecutive rows: lane k keeps row k's (sum, entropy)
+    // pair and every lane finishes its own row at the end (the logs and
+    // divisions leave the per-row chain; one coalesced store of 32 results)
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = (int)lane_id();
+    for (int64_t r0 = warp * 32; r0 < n_rows; r0 += nw * 32) {
+      RowPair mine{0.0, 0.0};
+      int my_n = n_cls;
+      const int nr = (int)min((int64_t)32, n_rows - r0);
+      for (int k = 0; k < nr; ++k) {
+        const int64_t r = r0 + k;
+        const int n = row_len ? row_len[r] : n_cls;
+        const RowPair pr = warp_row_pair<T, KIND>(scores + r * stride, n, vec_ok && n == n_cls);
+        if (lane == k) {
+          mine = pr;
+          my_n = n;
+        }
+      }
+      if (lane < nr) out[r0 + lane] = finish_cert<KIND>(mine, my_n, 0.0);
     }
   } else {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
@@ -532,7 +581,8 @@ cudaError_t launch_certainty(const void* scores, int64_t n_rows, int n_cls, int6
   const T* s = static_cast<const T*>(scores);
   const bool vec_ok = aligned16(scores) && ((stride * (int64_t)sizeof(T)) % 16 == 0);
   if (n_cls >= 32) {
-    int64_t blocks = (n_rows * 32 + 255) / 256;
+    // margin: a row per warp; else 32 rows a warp (8 warps a block)
+    int64_t blocks = KIND == GS_CERT_MARGIN ? (n_rows * 32 + 255) / 256 : (n_rows + 255) / 256;
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count() * 32));
     certainty_kernel<T, KIND, true><<<(unsigned)blocks, 256, 0, st>>>(s, n_rows, n_cls, stride, row_len,
                                                                       vec_ok, out);
