@@ -125,6 +125,7 @@ struct PrefixHash {
   uint64_t key[kQHash];
   int row[kQHash];
   int cid[kQHash];  // the row's index among the distinct rows, by row order
+  int slot_of[kQMaxTargets];  // compact id -> hash slot
   int n_rows;
 };
 __device__ __forceinline__ void build_hash(PrefixHash& h, const Target* t, int n_t) {
@@ -165,7 +166,10 @@ __device__ __forceinline__ void build_hash(PrefixHash& h, const Target* t, int n
   __syncthreads();
   int before = incl - head;
   for (int w = 0; w < warp; ++w) before += s_wsum[w];
-  if (head) h.cid[x] = before;
+  if (head) {
+    h.cid[x] = before;
+    h.slot_of[before] = x;
+  }
   if (j == (int)blockDim.x - 1) h.n_rows = before + head;
   __syncthreads();
 }
@@ -218,10 +222,9 @@ __global__ void __launch_bounds__(kQPassThreads) pass1_kernel(const uint64_t* __
       if (x >= 0) atomicAdd(s_hist + h.cid[x] * kQBins + ((uint32_t)(k >> shift) & (kQBins - 1)), 1u);
     }
     __syncthreads();
-    for (int x = 0; x < kQHash; ++x) {  // uniform loop: each distinct row merged once
-      if (h.key[x] == kQEmpty) continue;
-      const uint32_t* src = s_hist + h.cid[x] * kQBins;
-      uint32_t* dst = hist + (size_t)h.row[x] * kQBins;
+    for (int c = 0; c < h.n_rows; ++c) {  // each distinct row merged once
+      const uint32_t* src = s_hist + c * kQBins;
+      uint32_t* dst = hist + (size_t)h.row[h.slot_of[c]] * kQBins;
       for (int i = threadIdx.x; i < kQBins; i += blockDim.x)
         if (src[i]) atomicAdd(dst + i, src[i]);
     }
@@ -487,8 +490,9 @@ extern "C" int gs_quantiles(const double* column, int64_t n, int64_t stride, con
   RowInfo* rows = reinterpret_cast<RowInfo*>(ws + L.rows);
   uint32_t* hist0 = reinterpret_cast<uint32_t*>(ws + L.hist0);
   uint32_t* hist1 = reinterpret_cast<uint32_t*>(ws + L.hist1);
+  // the key passes: a few CTAs per SM (each builds the prefix hash once)
   const int64_t blocks =
-      std::max<int64_t>(1, std::min<int64_t>((n + kQPassThreads - 1) / kQPassThreads, (int64_t)sm_count() * 4));
+      std::max<int64_t>(1, std::min<int64_t>((n + kQPassThreads - 1) / kQPassThreads, (int64_t)sm_count() * 2));
   GS_CUDA_TRY(cudaMemcpyAsync(dq, qs, (size_t)n_q * 8, cudaMemcpyHostToDevice, st));
   GS_CUDA_TRY(cudaMemsetAsync(hist0, 0, (size_t)kQBins * 4, st));
   // the keys and their top-12-bit histogram serve every round of targets
