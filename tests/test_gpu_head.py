@@ -28,7 +28,8 @@ def _cert64(logits: torch.Tensor, kind: str) -> torch.Tensor:
 
 
 @pytest.mark.parametrize("B,N,K,bias", [(1000, 1000, 512, True), (300, 10, 64, False), (4097, 1000, 2048, True),
-                                        (129, 257, 128, False), (64, 1, 64, True), (8192, 100, 256, False)])
+                                        (129, 257, 128, False), (64, 1, 64, True), (8192, 100, 256, False),
+                                        (256, 5000, 64, True)])
 @pytest.mark.parametrize("kind", ["entropy", "max_softmax", "margin"])
 def test_head_certainty_vs_torch_f64(B, N, K, bias, kind):
     from paper_2406_14424_b200.head import head_certainty
