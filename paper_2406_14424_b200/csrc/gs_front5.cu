@@ -221,11 +221,19 @@ struct F5PassArgs {
   unsigned long long* min_index;  // [n_rec + 1] smallest front config index per accuracy
 };
 
-// the suffix minimum of gbest (smin[j] = min over buckets >= j), by one warp
-__device__ void refresh_bound(const F5PassArgs& a, unsigned long long* smin, int lane) {
+// the suffix minimum of gbest (smin[j] = min over buckets >= j): every
+// thread of the CTA fetches part of gbest into smin (all loads in flight at
+// once), then one warp turns it into suffix minima in place.  Called by the
+// whole CTA (it synchronises).
+__device__ void refresh_bound(const F5PassArgs& a, unsigned long long* smin) {
+  for (int j = threadIdx.x; j < kF5Bins; j += blockDim.x)
+    smin[j] = *reinterpret_cast<volatile const unsigned long long*>(a.gbest + j);
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   unsigned long long carry = kF5Inf;
   for (int j0 = kF5Bins - 32; j0 >= 0; j0 -= 32) {
-    unsigned long long x = *reinterpret_cast<volatile const unsigned long long*>(a.gbest + j0 + lane);
+    unsigned long long x = smin[j0 + lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long y = __shfl_down_sync(0xffffffffu, x, o);
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   const bool wlive = k1 < a.g1;
   unsigned long long* hist = s_hist + (size_t)warp * kF5Bins;
   for (int b = lane; b < kF5Bins; b += 32) hist[b] = 0ull;
-  if (warp == 0) refresh_bound(a, s_smin, lane);
+  refresh_bound(a, s_smin);
   if (threadIdx.x == 0) s_smin[kF5Bins] = kF5Inf;
   __syncthreads();
   const double n = (double)a.n_rec, rcp = a.rcp_n;
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   for (int k2 = 0; k2 < a.g2; ++k2) {
     if ((k2 & 15) == 15) {  // pull in the bound the rest of the grid has found
       __syncthreads();
-      if (warp == 0) refresh_bound(a, s_smin, lane);
+      refresh_bound(a, s_smin);
       __syncthreads();
     }
     // stream bucket b2 = k2, records with b0 <= k0 (a prefix of the bucket)
@@ -347,7 +355,11 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       if (k3 >= g3) break;
       const uint32_t reach5 = (uint32_t)(acc & kF5M21);
       const uint32_t correct = crow + (uint32_t)((acc >> 21) & kF5M21) - (uint32_t)(acc >> 42);
-      const bool stair = correct >= run_max;
+      // pass 1 keeps only a row's first config of each new correct count:
+      // later ones with the same count cost no less (cost is non-decreasing
+      // in k3), so they cannot lower mincost; pass 2 also needs their exact
+      // ties
+      const bool stair = a.pass == 1 ? (correct > run_max || k3 == 0) : correct >= run_max;
       run_max = max(run_max, correct);
       if (!stair) continue;
       const double fr4 = div_count((double)reach5, n, rcp);
