@@ -6,14 +6,17 @@
 // feeds the device sweep in a fraction of a second instead of a Python loop.
 //
 // Semantics follow the reference reader: blank lines are skipped; unknown
-// keys are ignored; sample_id goes through int() (truncation); correct
-// through bool(); every score through float() (correctly rounded strtod,
-// "NaN"/"Infinity" accepted like Python's json); a line that is not such an
+// keys are ignored; sample_id goes through int() (integer tokens exactly,
+// float tokens truncated, NaN / inf rejected, decimal strings and bools as
+// int() takes them); correct through bool(); every score through float()
+// (correctly rounded strtod); number tokens follow json.loads: the JSON
+// grammar plus NaN / Infinity / -Infinity, nothing else; a line that is not such an
 // object fails with its 1-based line number.  Cross-record checks (unique
 // non-negative ids, one model set, non-empty scores) are reported per line
 // too.  Model order is the first record's key order.
 #include <cctype>
 #include <cerrno>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -96,25 +99,103 @@ struct Parser {
     ++p;
     return true;
   }
-  bool number(double* v) {
+  // A number token as json.loads reads it: the JSON grammar
+  // -?(0|[1-9][0-9]*)(.[0-9]+)?([eE][+-]?[0-9]+)? or the literals NaN,
+  // Infinity, -Infinity (json.loads accepts them); is_int: no fraction or
+  // exponent (json.loads returns an int).  Nothing else (hex, "inf", "nan",
+  // a leading '+') is accepted.
+  bool number_token(std::string* tok, bool* is_int) {
     ws();
-    if (p >= end) return fail("expected a number");
-    char buf[64];
-    size_t n = 0;
-    while (p + n < end && n < sizeof(buf) - 1) {
-      const char c = p[n];
-      if (std::isalnum((unsigned char)c) || c == '-' || c == '+' || c == '.') ++n;
-      else break;
+    const char* q = p;
+    auto lit = [&](const char* w) {
+      const size_t n = std::strlen(w);
+      return (size_t)(end - q) >= n && !std::strncmp(q, w, n) ? n : (size_t)0;
+    };
+    size_t n = lit("NaN");
+    if (!n) n = lit("Infinity");
+    if (!n) n = lit("-Infinity");
+    *is_int = false;
+    if (!n) {
+      const char* r = q;
+      if (r < end && *r == '-') ++r;
+      if (r >= end || !std::isdigit((unsigned char)*r)) return fail("expected a number");
+      if (*r == '0') ++r;
+      else
+        while (r < end && std::isdigit((unsigned char)*r)) ++r;
+      *is_int = true;
+      if (r < end && *r == '.') {
+        ++r;
+        if (r >= end || !std::isdigit((unsigned char)*r)) return fail("bad number");
+        while (r < end && std::isdigit((unsigned char)*r)) ++r;
+        *is_int = false;
+      }
+      if (r < end && (*r == 'e' || *r == 'E')) {
+        ++r;
+        if (r < end && (*r == '+' || *r == '-')) ++r;
+        if (r >= end || !std::isdigit((unsigned char)*r)) return fail("bad number");
+        while (r < end && std::isdigit((unsigned char)*r)) ++r;
+        *is_int = false;
+      }
+      n = (size_t)(r - q);
     }
-    if (n == 0) return fail("expected a number");
-    std::memcpy(buf, p, n);
-    buf[n] = 0;
-    char* e = nullptr;
-    errno = 0;
-    const double x = std::strtod(buf, &e);
-    if (e != buf + n) return fail("bad number");
-    *v = x;
+    tok->assign(q, n);
     p += n;
+    return true;
+  }
+  bool number(double* v) {
+    std::string tok;
+    bool is_int;
+    if (!number_token(&tok, &is_int)) return false;
+    if (tok == "NaN") *v = NAN;
+    else if (tok == "Infinity") *v = INFINITY;
+    else if (tok == "-Infinity") *v = -INFINITY;
+    else *v = std::strtod(tok.c_str(), nullptr);  // the C locale's '.': correctly rounded
+    return true;
+  }
+  // int(value) of a JSON value, as the reference's int(rec["sample_id"]):
+  // an integer token exactly, a float token truncated (NaN / inf raise), a
+  // string through int(str) (optional sign and surrounding whitespace), a
+  // bool as 0 / 1
+  bool integer(int64_t* v) {
+    ws();
+    if (end - p >= 4 && !std::strncmp(p, "true", 4)) { p += 4; *v = 1; return true; }
+    if (end - p >= 5 && !std::strncmp(p, "false", 5)) { p += 5; *v = 0; return true; }
+    std::string tok;
+    bool is_int = false;
+    if (p < end && *p == '"') {
+      if (!string(&tok)) return false;
+      size_t a = 0, b = tok.size();
+      while (a < b && std::isspace((unsigned char)tok[a])) ++a;
+      while (b > a && std::isspace((unsigned char)tok[b - 1])) --b;
+      tok = tok.substr(a, b - a);
+      size_t i = (!tok.empty() && (tok[0] == '-' || tok[0] == '+')) ? 1 : 0;
+      if (i >= tok.size()) return fail("invalid literal for int()");
+      for (; i < tok.size(); ++i)
+        if (!std::isdigit((unsigned char)tok[i])) return fail("invalid literal for int()");
+      is_int = true;
+    } else if (!number_token(&tok, &is_int)) {
+      return false;
+    }
+    errno = 0;
+    if (is_int) {
+      char* e = nullptr;
+      const long long x = std::strtoll(tok.c_str(), &e, 10);
+      if (errno == ERANGE) return fail("integer out of range");
+      *v = (int64_t)x;
+      return true;
+    }
+    double d;
+    if (!number_token_value(tok, &d)) return false;
+    if (!std::isfinite(d)) return fail("cannot convert float NaN or infinity to integer");
+    if (!(d > -9.3e18 && d < 9.3e18)) return fail("integer out of range");
+    *v = (int64_t)d;  // int(float): truncation toward zero
+    return true;
+  }
+  bool number_token_value(const std::string& tok, double* d) {
+    if (tok == "NaN") *d = NAN;
+    else if (tok == "Infinity") *d = INFINITY;
+    else if (tok == "-Infinity") *d = -INFINITY;
+    else *d = std::strtod(tok.c_str(), nullptr);
     return true;
   }
   // any JSON value (for ignored keys)
@@ -167,9 +248,7 @@ bool parse_line(Parser& ps, std::vector<std::string>& ids, bool discover, Line* 
       std::string key;
       if (!ps.string(&key) || !ps.eat(':')) return ps.fail("bad key");
       if (key == "sample_id") {
-        double d;
-        if (!ps.number(&d)) return false;
-        ln->sample_id = (int64_t)d;  // int(): truncation
+        if (!ps.integer(&ln->sample_id)) return false;  // int(value)
         have_id = true;
       } else if (key == "models") {
         if (!ps.eat('{')) return ps.fail("models must be an object");

@@ -115,3 +115,25 @@ def test_columnar_rejects_foreign_files(tmp_path):
     p.write_bytes(b"not a container at all")
     with pytest.raises(ValueError):
         formats.load_validation_columnar(p)
+
+
+def test_number_tokens_and_int_sample_ids(tmp_path):
+    """json.loads's number grammar (no hex, no bare inf / nan, no leading '+';
+    NaN / Infinity literals accepted) and int() of the sample id: integer
+    tokens exactly (past 2^53), floats truncated, decimal strings, bools."""
+    def rec(sid, score="0.5"):
+        return f'{{"sample_id": {sid}, "models": {{"a": {{"scores": [{score}], "correct": true}}}}}}'
+
+    ok = tmp_path / "ok.jsonl"
+    ok.write_text("\n".join([rec(9007199254740993), rec("3.9"), rec('" 12 "'), rec("true"),
+                             rec(7, "NaN"), rec(8, "-Infinity"), rec(9, "1e-3")]) + "\n")
+    vs = formats.load_validation(ok)
+    assert [r.sample_id for r in vs.records] == [9007199254740993, 3, 12, 1, 7, 8, 9]
+    assert math.isnan(vs.records[4].outputs["a"].scores[0])
+    assert vs.records[5].outputs["a"].scores[0] == -math.inf
+    for bad in (rec(1, "0x1p3"), rec(1, "inf"), rec(1, "nan"), rec(1, "+1.0"), rec("NaN"), rec('"1.5"'),
+                rec(1, "1."), rec(1, ".5")):
+        path = tmp_path / "bad.jsonl"
+        path.write_text(bad + "\n")
+        with pytest.raises(ValueError):
+            formats.load_validation(path)
