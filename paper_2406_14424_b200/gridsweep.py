@@ -382,29 +382,31 @@ def pareto_counts(n_correct: torch.Tensor, mean_cost: torch.Tensor, n_rec: int,
 
 
 class BatchedSweep:
-    """Full grid sweeps of many three-model validation sets, one launch per
-    run() (gs_grid_sweep_batched): certainty [R, n, 3] f64, correct
-    [R, n, 3] u8, grids [R][3] per-set grids (each strictly increasing; the
-    three lengths shared by every set), cost1 [3].  run() fills [R, C]
-    accuracy / mean_cost and [R, C, 3] forward_frac, each row equal to that
-    set's GridSweep(...).evaluate() (config 1 stacked: the reference's CPU
-    default is launch-bound as one sweep).  The constructor does the host
-    work (validation, grid upload), so run() is one C call."""
+    """Full grid sweeps of many validation sets of M models: certainty
+    [R, n, M] f64, correct [R, n, M] u8, grids [R][M] per-set grids (each
+    strictly increasing; the M lengths shared by every set), cost1 [M].
+    run() fills [R, C] accuracy / mean_cost and [R, C, M] forward_frac, each
+    row equal to that set's GridSweep(...).evaluate().  Three models (config
+    1 stacked: the reference's CPU default is launch-bound as one sweep) take
+    one launch per run() (gs_grid_sweep_batched); other M run the sets'
+    sweeps back to back on the stream (one workspace per set, built here).
+    The constructor does the host work (validation, grid upload)."""
 
     def __init__(self, certainty, correct, grids, cost1):
         self.cert = _lib.to_device(certainty, torch.float64)
         self.corr = _lib.to_device(correct, torch.uint8)
-        if (self.cert.ndim != 3 or self.cert.shape[2] != 3
-                or tuple(self.corr.shape) != tuple(self.cert.shape)):
-            raise ValueError("certainty and correct must both be [n_sets, n_records, 3]")
+        if (self.cert.ndim != 3 or tuple(self.corr.shape) != tuple(self.cert.shape)
+                or self.cert.shape[2] < 1):
+            raise ValueError("certainty and correct must both be [n_sets, n_records, n_models]")
         self.n_sets, self.n_rec = int(self.cert.shape[0]), int(self.cert.shape[1])
+        M = self.n_models = int(self.cert.shape[2])
         if len(grids) != self.n_sets:
-            raise ValueError(f"need {self.n_sets} grid triples, got {len(grids)}")
+            raise ValueError(f"need {self.n_sets} grid sets, got {len(grids)}")
         glen = None
         flat = []
         for s_idx, triple in enumerate(grids):
-            if len(triple) != 3:
-                raise ValueError(f"set {s_idx}: need 3 grids")
+            if len(triple) != M:
+                raise ValueError(f"set {s_idx}: need {M} grids")
             lens = []
             for j, g in enumerate(triple):
                 g = np.asarray(g.cpu() if isinstance(g, torch.Tensor) else g, dtype=np.float64)
@@ -421,20 +423,41 @@ class BatchedSweep:
         self._glen = _lib.int32_array(glen)
         self.grids = _lib.to_device(np.concatenate(flat), torch.float64)
         self.cost1 = _lib.to_device(np.asarray(cost1, dtype=np.float64), torch.float64)
-        if self.cost1.numel() != 3:
-            raise ValueError("cost1 must have 3 entries")
-        g0, g1, _ = glen
-        self.n_configs = 3 + 2 * g0 + g1 + g0 * g1
+        if self.cost1.numel() != M:
+            raise ValueError(f"cost1 must have {M} entries")
+        self._sweeps = None
+        self._bufs = None
+        if M == 3:
+            g0, g1, _ = glen
+            self.n_configs = 3 + 2 * g0 + g1 + g0 * g1
+        else:  # one GridSweep per set (its own workspace), run back to back
+            c1 = np.asarray(cost1, dtype=np.float64)
+            self._sweeps = [GridSweep(self.cert[s], self.corr[s], list(grids[s]), c1, build=False)
+                            for s in range(self.n_sets)]
+            self.n_configs = self._sweeps[0].n_configs if self._sweeps else 0
         dev = self.cert.device
         self.out = SweepResult(
             accuracy=torch.empty((self.n_sets, self.n_configs), dtype=torch.float64, device=dev),
             mean_cost=torch.empty((self.n_sets, self.n_configs), dtype=torch.float64, device=dev),
-            forward_frac=torch.empty((self.n_sets, self.n_configs, 3), dtype=torch.float64,
+            forward_frac=torch.empty((self.n_sets, self.n_configs, M), dtype=torch.float64,
                                      device=dev),
             n_correct=None, config_begin=0)
 
     def run(self) -> SweepResult:
         o = self.out
+        if self._sweeps is not None:
+            # each set scores into its sweep's own (aligned) buffers, then its
+            # row of the stacked result (rows of an odd C are not 16-byte
+            # aligned, which the vector stores need)
+            if self._bufs is None:
+                self._bufs = [None] * self.n_sets
+            for s, sw in enumerate(self._sweeps):
+                sw.build()
+                self._bufs[s] = sw.evaluate(out=self._bufs[s])
+                o.accuracy[s].copy_(self._bufs[s].accuracy)
+                o.mean_cost[s].copy_(self._bufs[s].mean_cost)
+                o.forward_frac[s].copy_(self._bufs[s].forward_frac)
+            return o
         rc = _lib.load().gs_grid_sweep_batched(
             self.cert.data_ptr(), self.corr.data_ptr(), self.n_sets, self.n_rec, 3,
             self.grids.data_ptr(), self._glen, self.cost1.data_ptr(), o.accuracy.data_ptr(),

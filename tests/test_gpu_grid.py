@@ -497,7 +497,7 @@ def test_batched_sweep_rejects_bad_input():
         BatchedSweep(cert, corr, [g, [g[0], g[1][:2], g[2]]], cost1)
     with pytest.raises(ValueError):  # not increasing
         BatchedSweep(cert, corr, [g, [g[0][::-1], g[1], g[2]]], cost1)
-    with pytest.raises(ValueError):  # four models
+    with pytest.raises(ValueError):  # a grid per model
         BatchedSweep(rng.random((2, 50, 4)), np.zeros((2, 50, 4), np.uint8), [g, g], cost1)
     res = BatchedSweep(cert, corr, [g, g], cost1).run()
     assert tuple(res.accuracy.shape) == (2, 3 + 2 * 2 + 3 + 2 * 3)
@@ -616,3 +616,24 @@ def test_general_path_past_f32_and_rcp_ranges(n_rec, M, glen):
     assert np.array_equal(acc, want[0])
     assert np.array_equal(cost, want[1])
     assert np.array_equal(frac, want[2])
+
+
+@pytest.mark.parametrize("M", [2, 4, 5])
+def test_batched_sweep_other_model_counts(M):
+    """Sets of 2, 4 or 5 models: the batched API runs each set's sweep (no
+    single-launch kernel for them) and every row equals that set's GridSweep."""
+    from paper_2406_14424_b200.gridsweep import BatchedSweep, GridSweep
+    rng = np.random.default_rng(M)
+    R, n = 3, 2000
+    cert = rng.random((R, n, M))
+    corr = (rng.random((R, n, M)) < 0.6).astype(np.uint8)
+    lens = [5, 4, 6, 3, 2][:M]
+    grids = [[np.sort(rng.choice(cert[s, :, j], size=lens[j], replace=False)) for j in range(M)]
+             for s in range(R)]
+    cost1 = np.arange(1.0, M + 1.0) * 2.0
+    res = BatchedSweep(cert, corr, grids, cost1).run()
+    for s in range(R):
+        one = GridSweep(cert[s], corr[s], grids[s], cost1).evaluate()
+        assert np.array_equal(res.accuracy[s].cpu().numpy(), one.accuracy.cpu().numpy())
+        assert np.array_equal(res.mean_cost[s].cpu().numpy(), one.mean_cost.cpu().numpy())
+        assert np.array_equal(res.forward_frac[s].cpu().numpy(), one.forward_frac.cpu().numpy())
