@@ -1231,8 +1231,8 @@ def online_router_bench(plan, prof, cert, corr):
         cpu_rate = n_calls * bsz / (time.perf_counter() - t)
         out[f"batch_{bsz}"] = {"samples_per_s": dev_rate, "calls": n_calls,
                                "cpu_baseline_samples_per_s": cpu_rate}
-    out["path"] = ("StageRouter.finish_batch: Item objects in, packed pinned H2D, gs_stage_gate "
-                   "(one tile), packed pinned D2H, numpy replica draws, deque appends; host "
+    out["path"] = ("StageRouter.finish_batch: Item objects in, packed pinned H2D, gs_stage_gate_packed "
+                   "(one tile), packed pinned D2H, replica draws (Python lists up to 256 items, numpy above), deque appends; host "
                    "wall clock. cpu_baseline: oracle.finish_batch (the reference loop restated), "
                    "1 core")
     return out

@@ -21,6 +21,7 @@ forwarded items are drawn at once.
 
 from __future__ import annotations
 
+from bisect import bisect_right
 from collections import deque
 from dataclasses import dataclass
 
@@ -170,6 +171,58 @@ class StageRouter:
         # near_keep of them (bounded for long-running routers), and a count
         self.near_threshold: deque[int] = deque(maxlen=near_keep)
         self.n_near_threshold = 0
+        # Python-list copies of the tables for small batches (numpy's per-call
+        # overhead exceeds the work at the reference's 4-8 items)
+        G = len(tables.stage_models)
+        self._model_l = [[int(tables._model[g, s]) for s in range(tables.max_stages)] for g in range(G)]
+        self._thr_l = [[float(tables._thr[g, s]) for s in range(tables.max_stages)] for g in range(G)]
+        self._nst_l = [int(tables._n_stages[g]) for g in range(G)]
+        self._cum_l = [[[float(x) for x in c] for c in tables.cum_weights[g]] for g in range(G)]
+        self._rep_l = [[[int(x) for x in r] for r in tables.replicas[g]] for g in range(G)]
+        self._dev_l = [int(d) for d in self.replica_device]
+
+    SMALL = 256  # batches up to this size take the list path
+
+    def _finish_small(self, device_idx: int, items: list[Item], now: int) -> set[int]:
+        """finish_batch for a small batch: the same gate call and the same
+        draws (one rng.random() per forwarded item in batch order, or
+        rng.integers for a zero-weight stage: route's stream), over lists."""
+        touched = {device_idx}
+        ml, tl, nst = self._model_l, self._thr_l, self._nst_l
+        rows, model, thr, last = [], [], [], []
+        for it in items:
+            g, st = it.gear_idx, it.stage
+            rows.append(it.row)
+            model.append(ml[g][st])
+            thr.append(tl[g][st])
+            last.append(st == nst[g] - 1)
+        stop, correct, near = self.gate.gate_small(rows, model, thr, last)
+        if near:
+            self.n_near_threshold += len(near)
+            self.near_threshold.extend(items[i].request_id for i in near)
+        rng, cl, rl, dl = self.rng, self._cum_l, self._rep_l, self._dev_l
+        for i, it in enumerate(items):
+            if stop[i]:
+                ok = bool(correct[i])
+                self.completed.append(Completion(it.request_id, it.arrival_us, now, it.stage + 1, ok,
+                                                 it.gear_idx))
+                self.n_completed += 1
+                self.window_latencies.append(now - it.arrival_us)
+                self.window_correct += 1 if ok else 0
+        for i, it in enumerate(items):  # forwards in batch order
+            if stop[i]:
+                continue
+            g, st = it.gear_idx, it.stage + 1
+            cum = cl[g][st]
+            if cum[-1] <= 0.0:
+                pos = int(rng.integers(len(cum)))
+            else:
+                pos = min(bisect_right(cum, rng.random() * cum[-1]), len(cum) - 1)
+            r = rl[g][st][pos]
+            it.stage = st
+            self.queues[r].append(it)
+            touched.add(dl[r])
+        return touched
 
     def finish_batch(self, device_idx: int, items: list[Item], now: int) -> set[int]:
         """Complete certain items, forward the rest (batch order kept);
@@ -178,6 +231,8 @@ class StageRouter:
         touched = {device_idx}
         if not items:
             return touched
+        if len(items) <= self.SMALL:
+            return self._finish_small(device_idx, items, now)
         t = self.tables
         gear = np.fromiter((it.gear_idx for it in items), dtype=np.int64, count=len(items))
         stage = np.fromiter((it.stage for it in items), dtype=np.int64, count=len(items))

@@ -19,6 +19,7 @@ matrices (CompiledPlan.cert/corr, src/engine.py:217), per item
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -171,6 +172,8 @@ class GateBatcher:
         self.n_rec, self.n_models = int(self.cert.shape[0]), int(self.cert.shape[1])
         self.near_eps = float(near_eps)
         self.cap = 0
+        self._args = None
+        self._args_cap = 0
         self._grow(max(1, int(capacity)))
 
     def _grow(self, n: int) -> None:
@@ -184,6 +187,30 @@ class GateBatcher:
         self._in = self.h_in.numpy()
         self._out = self.h_out.numpy()
         self.cap = n
+
+    def gate_small(self, rows: list, model: list, thr: list, is_last: list):
+        """gate() for a handful of items given as Python lists (the online
+        batch of finish_batch): struct packing into the pinned buffer, the
+        same single C call, the outcome as Python lists (stop, correct,
+        near positions)."""
+        n = len(rows)
+        if n > self.cap:
+            self._grow(max(n, 2 * self.cap))
+        if self._args is None or self._args_cap != self.cap:
+            self._lib = _lib.load()
+            self._mv_in = memoryview(self._in)
+            self._mv_out = memoryview(self._out)
+            self._args = (self.cert.data_ptr(), self.corr.data_ptr(), self.n_rec, self.n_models,
+                          self.h_in.data_ptr())
+            self._args2 = (self.near_eps, self.h_out.data_ptr(), self.d_buf.data_ptr(), self.d_buf.numel(), 1)
+            self._args_cap = self.cap
+        struct.pack_into(f"<{n}q{n}d{n}i{n}?", self._mv_in, 0, *rows, *thr, *model, *is_last)
+        rc = self._lib.gs_stage_gate_packed(*self._args, n, *self._args2, _lib.stream_ptr())
+        _lib.check(rc, "gate batch")
+        n_near = struct.unpack_from("<q", self._mv_out, 8)[0]
+        flags = struct.unpack_from(f"<{2 * n}B", self._mv_out, 16)
+        near = struct.unpack_from(f"<{n_near}q", self._mv_out, (16 + 2 * n + 7) // 8 * 8) if n_near else ()
+        return flags[:n], flags[n:], near
 
     def gate(self, rows, model, thr, is_last):
         """(stop bool[n], correct u8[n], near positions i64) for one batch;
