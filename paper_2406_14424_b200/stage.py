@@ -174,6 +174,7 @@ class GateBatcher:
         self.cap = 0
         self._args = None
         self._args_cap = 0
+        self._graphs: dict = {}  # n -> captured packed-gate graph (gate_small)
         self._grow(max(1, int(capacity)))
 
     def _grow(self, n: int) -> None:
@@ -204,13 +205,38 @@ class GateBatcher:
                           self.h_in.data_ptr())
             self._args2 = (self.near_eps, self.h_out.data_ptr(), self.d_buf.data_ptr(), self.d_buf.numel(), 1)
             self._args_cap = self.cap
+            self._graphs = {}
         struct.pack_into(f"<{n}q{n}d{n}i{n}?", self._mv_in, 0, *rows, *thr, *model, *is_last)
-        rc = self._lib.gs_stage_gate_packed(*self._args, n, *self._args2, _lib.stream_ptr())
-        _lib.check(rc, "gate batch")
+        graph = self._graphs.get(n)
+        if graph is None and len(self._graphs) < 64:
+            graph = self._capture(n)
+        if graph is not None:  # H2D, gate, D2H as one graph launch
+            graph.replay()
+            torch.cuda.current_stream().synchronize()
+        else:
+            rc = self._lib.gs_stage_gate_packed(*self._args, n, *self._args2, _lib.stream_ptr())
+            _lib.check(rc, "gate batch")
         n_near = struct.unpack_from("<q", self._mv_out, 8)[0]
         flags = struct.unpack_from(f"<{2 * n}B", self._mv_out, 16)
         near = struct.unpack_from(f"<{n_near}q", self._mv_out, (16 + 2 * n + 7) // 8 * 8) if n_near else ()
         return flags[:n], flags[n:], near
+
+    def _capture(self, n: int):
+        """The packed gate call for n items as a CUDA graph (its buffers are
+        fixed), or None when capture is not possible here."""
+        try:
+            rc = self._lib.gs_stage_gate_packed(*self._args, n, *self._args2, _lib.stream_ptr())  # warm
+            _lib.check(rc, "gate batch")
+            g = torch.cuda.CUDAGraph()
+            a2 = self._args2[:-1] + (0,)  # no synchronize inside the graph
+            with torch.cuda.graph(g):
+                rc = self._lib.gs_stage_gate_packed(*self._args, n, *a2, _lib.stream_ptr())
+            _lib.check(rc, "gate batch")
+        except RuntimeError:
+            self._graphs[n] = None
+            return None
+        self._graphs[n] = g
+        return g
 
     def gate(self, rows, model, thr, is_last):
         """(stop bool[n], correct u8[n], near positions i64) for one batch;
