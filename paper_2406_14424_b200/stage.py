@@ -207,9 +207,10 @@ class GateBatcher:
             self._args_cap = self.cap
             self._graphs = {}
         struct.pack_into(f"<{n}q{n}d{n}i{n}?", self._mv_in, 0, *rows, *thr, *model, *is_last)
-        graph = self._graphs.get(n)
-        if graph is None and len(self._graphs) < 64:
-            graph = self._capture(n)
+        if n in self._graphs:
+            graph = self._graphs[n]  # None: capture failed here once, use the plain call
+        else:
+            graph = self._capture(n) if len(self._graphs) < 64 else None
         if graph is not None:  # H2D, gate, D2H as one graph launch
             graph.replay()
             torch.cuda.current_stream().synchronize()
