@@ -348,8 +348,19 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     if (lane == 0) run_max = 0;
     uint64_t acc = excl;
     uint32_t cur_a = 0xffffffffu, run_n = 0, first_k3 = 0xffffffffu;  // pass 2: run of one front point
+    // the whole lane at once: its cheapest config is its first (cost is
+    // non-decreasing in k3) and every config's accuracy bucket is at most
+    // amax's, whose bound is the loosest (a suffix minimum); if that bound
+    // already beats the cheapest cost, the in-loop test below would drop
+    // every config of the lane
+    bool lane_live = 32 * lane < g3;
+    if (lane_live) {
+      const uint32_t r5 = (uint32_t)((excl + hist[lane]) & kF5M21);
+      const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)r5, n, rcp), c4)));
+      lane_live = s_smin[(int)(amax >> a.bucket_shift) + 1] > key0;
+    }
 #pragma unroll 4
-    for (int t = 0; t < 32; ++t) {
+    for (int t = 0; t < (lane_live ? 32 : 0); ++t) {
       acc += hist[t * 32 + lane];
       const int k3 = 32 * lane + t;
       if (k3 >= g3) break;
