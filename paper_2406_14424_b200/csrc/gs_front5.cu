@@ -198,6 +198,7 @@ struct F5PassArgs {
   int32_t g0, g1, g2, g3, d0, d1;
   int32_t pass;                 // 1: min costs, 2: emit the front
   int32_t k0_begin, k0_end;
+  int32_t k0_stride;            // CTA group i takes k0 = k0_begin + i * k0_stride (< k0_end)
   int32_t n_groups;             // k1 groups of kF5Warps
   int32_t bucket_shift;         // accuracy bucket = correct >> shift (kF5Bins buckets)
   int64_t n_rec;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   __shared__ unsigned long long s_smin[kF5Bins + 1];             // suffix min of gbest
   __shared__ uint32_t s_rec[kF5Tile];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k0 = a.k0_begin + blockIdx.x / a.n_groups;
+  const int k0 = a.k0_begin + (int)(blockIdx.x / a.n_groups) * a.k0_stride;
   const int k1 = (blockIdx.x % a.n_groups) * kF5Warps + warp;
   const bool wlive = k1 < a.g1;
   unsigned long long* hist = s_hist + (size_t)warp * kF5Bins;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   // correct through stage 1: C0 of b0 > k0, C1 of (b0 <= k0, b1 > k1)
   const uint32_t base01 = (__ldg(a.c0pre + g0) - __ldg(a.c0pre + k0)) + (s0g.y - s01.y);
   const uint32_t c2_r3 = s01.z;  // C2 over R3
-  uint32_t c2_r4 = 0, reach4 = 0, c3_r4 = 0;
+  uint32_t c2_r4 = 0, reach4 = 0, c3_r4 = 0, c4_r4 = 0;
   const int64_t k01 = ((int64_t)k0 * g1 + k1) * a.g2;
   for (int k2 = 0; k2 < a.g2; ++k2) {
     if ((k2 & 15) == 15) {  // pull in the bound the rest of the grid has found
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
         reach4 += __popc(m);
         c2_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 20) & 1u)));
         c3_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 21) & 1u)));
+        c4_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 22) & 1u)));
         while (m) {  // one lane applies the adds (few records per row)
           const int src = __ffs(m) - 1;
           m &= m - 1;
@@ -315,6 +317,15 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     const double fr3 = div_count((double)reach4, n, rcp);
     const double m3 = dadd(m2, dmul(fr3, c3));
     const uint32_t crow = base01 + (c2_r3 - c2_r4) + c3_r4;  // + C4(k3) - C3(k3) per config
+    {  // the whole row at once: no config of it is more accurate than
+       // crow + C4(R4), none cheaper than k3 = 0 (reach5 = bin 0); if the
+       // bound of that accuracy already beats that cost, every config of the
+       // row would be dropped below
+      const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)(uint32_t)(hist[0] & kF5M21), n, rcp), c4)));
+      // crow + C4(R4) counts C3(R4) and C4(R4) both, so it can pass n: clamp
+      const uint32_t ub = min(crow + c4_r4, (uint32_t)a.n_rec);
+      if (s_smin[(int)(ub >> a.bucket_shift) + 1] <= key0) continue;
+    }
     // lane totals, their exclusive scan (the prefix before this lane's bins),
     // each lane's highest correct count, and the running maximum over the
     // lanes before it (configs with smaller k3 cost no more)
@@ -589,6 +600,7 @@ static F5PassArgs pass_args(const F5Layout& L, const int32_t* glen, int64_t n_re
   a.pass = pass;
   a.k0_begin = k0_begin;
   a.k0_end = k0_end;
+  a.k0_stride = 1;
   a.n_groups = (glen[1] + kF5Warps - 1) / kF5Warps;
   a.bucket_shift = L.bucket_shift;
   a.n_rec = n_rec;
@@ -613,9 +625,21 @@ cudaError_t f5_pass1(const int32_t* glen, int64_t n_rec, const double* cost1, ui
   cudaError_t e = ensure_smem(f5_pass_kernel, attr, smem);
   if (e != cudaSuccess) return e;
   // k0 slices of ~one wave each: every slice starts from the bound the
-  // slices before it found
+  // slices before it found.  First one wave of k0 values spread over the
+  // range, so every later slice starts from a bound that already spans the
+  // whole front (the pruning only drops configs a recorded one dominates,
+  // so the order does not change the front; the spread k0 are scored again
+  // in their slices, a few percent of the work)
   const int groups = (glen[1] + kF5Warps - 1) / kF5Warps;
   const int per = std::max(1, sm_count() / std::max(1, groups));
+  const int span = k0_end - k0_begin;
+  const int spread = std::min(4 * per, span / 8);  // k0 values in the first pass
+  if (spread >= 2) {
+    F5PassArgs a = pass_args(L, glen, n_rec, cost1, ws, 1, k0_begin, k0_end);
+    a.k0_stride = span / spread;
+    f5_pass_kernel<<<(unsigned)(spread * groups), kF5Warps * 32, smem, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   for (int k = k0_begin; k < k0_end; k += per) {
     F5PassArgs a = pass_args(L, glen, n_rec, cost1, ws, 1, k, std::min(k0_end, k + per));
     f5_pass_kernel<<<(unsigned)((a.k0_end - a.k0_begin) * groups), kF5Warps * 32, smem, st>>>(a);
