@@ -329,9 +329,17 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // lane totals, their exclusive scan (the prefix before this lane's bins),
     // each lane's highest correct count, and the running maximum over the
     // lanes before it (configs with smaller k3 cost no more)
+    // one pass over the lane's bins: its total and the largest C4 - C3 of
+    // its local prefixes (the fields add without carries, so a config's
+    // correct count is crow + (C4 - C3)(prefix before the lane) + that local
+    // difference)
     uint64_t tot = 0;
+    int dmax = -(1 << 22);
 #pragma unroll 8
-    for (int t = 0; t < 32; ++t) tot += hist[t * 32 + lane];
+    for (int t = 0; t < 32; ++t) {
+      tot += hist[t * 32 + lane];
+      if (32 * lane + t < g3) dmax = max(dmax, (int)((tot >> 21) & kF5M21) - (int)(tot >> 42));
+    }
     uint64_t excl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -339,16 +347,8 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       if (lane >= o) excl += y;
     }
     excl -= tot;
-    uint32_t amax = 0;
-    {
-      uint64_t acc = excl;
-#pragma unroll 8
-      for (int t = 0; t < 32; ++t) {
-        acc += hist[t * 32 + lane];
-        const uint32_t ct = crow + (uint32_t)((acc >> 21) & kF5M21) - (uint32_t)(acc >> 42);
-        if (32 * lane + t < g3) amax = max(amax, ct);
-      }
-    }
+    const uint32_t amax =
+        32 * lane < g3 ? (uint32_t)((int)crow + (int)((excl >> 21) & kF5M21) - (int)(excl >> 42) + dmax) : 0u;
     uint32_t pmax = amax;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
