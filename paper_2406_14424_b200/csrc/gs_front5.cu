@@ -640,8 +640,12 @@ cudaError_t f5_pass1(const int32_t* glen, int64_t n_rec, const double* cost1, ui
     f5_pass_kernel<<<(unsigned)(spread * groups), kF5Warps * 32, smem, st>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  for (int k = k0_begin; k < k0_end; k += per) {
-    F5PassArgs a = pass_args(L, glen, n_rec, cost1, ws, 1, k, std::min(k0_end, k + per));
+#ifndef GS_F5_SLICE_WAVES
+#define GS_F5_SLICE_WAVES 0  // 0: the whole range in one launch (the CTAs refresh the bound every 16 rows)
+#endif
+  const int slice = GS_F5_SLICE_WAVES > 0 ? per * GS_F5_SLICE_WAVES : span;
+  for (int k = k0_begin; k < k0_end; k += slice) {
+    F5PassArgs a = pass_args(L, glen, n_rec, cost1, ws, 1, k, std::min(k0_end, k + slice));
     f5_pass_kernel<<<(unsigned)((a.k0_end - a.k0_begin) * groups), kF5Warps * 32, smem, st>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
