@@ -295,19 +295,19 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
         const uint32_t t = t0 + lane;
         const uint32_t k = t < nk ? s_rec[t] : 0xffffffffu;
         const bool in = t < nk && (k & 1023u) <= (uint32_t)k1;
-        uint32_t m = __ballot_sync(0xffffffffu, in);
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        const uint32_t m3 = __ballot_sync(0xffffffffu, in && ((k >> 21) & 1u));
+        const uint32_t m4 = __ballot_sync(0xffffffffu, in && ((k >> 22) & 1u));
         reach4 += __popc(m);
         c2_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 20) & 1u)));
-        c3_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 21) & 1u)));
-        c4_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 22) & 1u)));
-        while (m) {  // one lane applies the adds (few records per row)
-          const int src = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t kk = __shfl_sync(0xffffffffu, k, src);
-          if (lane == 0) {
-            const int b3 = (int)((kk >> 10) & 1023u);
-            hist[bin_pos(b3)] += 1ull | ((uint64_t)((kk >> 22) & 1u) << 21) | ((uint64_t)((kk >> 21) & 1u) << 42);
-          }
+        c3_r4 += __popc(m3);
+        c4_r4 += __popc(m4);
+        if (in) {  // the lanes of one b3 bin add as one: its lowest lane applies their sum
+          const uint32_t b3 = (k >> 10) & 1023u;
+          const uint32_t peers = __match_any_sync(m, b3);
+          if (lane == __ffs(peers) - 1)
+            hist[bin_pos((int)b3)] += (uint64_t)__popc(peers) | ((uint64_t)__popc(peers & m4) << 21) |
+                                      ((uint64_t)__popc(peers & m3) << 42);
         }
         __syncwarp();
       }
@@ -365,10 +365,12 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // already beats the cheapest cost, the in-loop test below would drop
     // every config of the lane
     bool lane_live = 32 * lane < g3;
+    uint64_t lane_bound = kF5Inf;
     if (lane_live) {
       const uint32_t r5 = (uint32_t)((excl + hist[lane]) & kF5M21);
       const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)r5, n, rcp), c4)));
-      lane_live = s_smin[(int)(amax >> a.bucket_shift) + 1] > key0;
+      lane_bound = s_smin[(int)(amax >> a.bucket_shift) + 1];
+      lane_live = lane_bound > key0;
     }
 #pragma unroll 4
     for (int t = 0; t < (lane_live ? 32 : 0); ++t) {
@@ -387,6 +389,9 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       const double fr4 = div_count((double)reach5, n, rcp);
       const double mean = dadd(m3, dmul(fr4, c4));
       const uint64_t key = cost_key(mean);
+      // the same test for the rest of the lane: its later configs cost no
+      // less and reach at most amax's bucket, whose bound is the loosest
+      if (key >= lane_bound) break;
       const int bk = (int)(correct >> a.bucket_shift);
       if (s_smin[bk + 1] <= key) continue;  // a strictly more accurate config costs no more
       if (a.pass == 1) {
