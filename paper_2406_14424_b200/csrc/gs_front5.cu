@@ -212,6 +212,10 @@ struct F5PassArgs {
   unsigned long long* mincost;  // [n_rec + 1] order-preserving cost keys
   unsigned long long* gbest;    // [kF5Bins] min cost key per accuracy bucket
   const unsigned long long* front_key;  // pass 2: [n_rec + 1] the front pair's cost key or kF5Inf
+  uint32_t* row_flag;           // [g0][g1][n_words] bit k2: pass 1 saw a config of row (k0, k1, k2)
+                                // at or below mincost[correct] as it stood then
+  const uint8_t* k0_done;       // [g0] pass 1 has flagged this k0's rows
+  int32_t n_words;
   // pass 2 outputs
   unsigned long long* out_idx;  // config index within the full cascade
   double* out_cost;
@@ -254,11 +258,31 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   const int k0 = a.k0_begin + (int)(blockIdx.x / a.n_groups) * a.k0_stride;
   const int k1 = (blockIdx.x % a.n_groups) * kF5Warps + warp;
   const bool wlive = k1 < a.g1;
+  __shared__ int s_k2end;
   unsigned long long* hist = s_hist + (size_t)warp * kF5Bins;
   for (int b = lane; b < kF5Bins; b += 32) hist[b] = 0ull;
+  if (threadIdx.x == 0) s_k2end = a.pass == 1 ? a.g2 - 1 : -1;
   refresh_bound(a, s_smin);
   if (threadIdx.x == 0) s_smin[kF5Bins] = kF5Inf;
+  // pass 2 scores only the rows pass 1 flagged (every row on the front is
+  // one: see f5_pass2), and walks k2 only as far as the last of them; lane
+  // j holds the warp's flag word j (k2 = 32 j ..)
+  uint32_t fword = 0xffffffffu;
+  int wlast = a.g2 - 1;
+  if (a.pass == 2) {
+    if (!wlive) {
+      fword = 0u;
+    } else if (__ldg(a.k0_done + k0)) {
+      fword = lane < a.n_words ? __ldg(a.row_flag + ((int64_t)k0 * a.g1 + k1) * a.n_words + lane) : 0u;
+    }
+    const uint32_t nz = __ballot_sync(0xffffffffu, fword != 0u);
+    const int hl = nz ? 31 - __clz(nz) : -1;
+    wlast = hl < 0 ? -1 : 32 * hl + 31 - __clz(__shfl_sync(0xffffffffu, fword, hl));
+    wlast = min(wlast, a.g2 - 1);
+    if (lane == 0 && wlast >= 0) atomicMax(&s_k2end, wlast);
+  }
   __syncthreads();
+  const int k2_end = s_k2end;
   const double n = (double)a.n_rec, rcp = a.rcp_n;
   const double one = div_count(n, n, rcp);
   const double c0 = __ldg(a.cost1), c1 = __ldg(a.cost1 + 1), c2 = __ldg(a.cost1 + 2),
@@ -277,7 +301,8 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   const uint32_t c2_r3 = s01.z;  // C2 over R3
   uint32_t c2_r4 = 0, reach4 = 0, c3_r4 = 0, c4_r4 = 0;
   const int64_t k01 = ((int64_t)k0 * g1 + k1) * a.g2;
-  for (int k2 = 0; k2 < a.g2; ++k2) {
+  bool rflag = false;  // pass 1: this row has a config at or below mincost
+  for (int k2 = 0; k2 <= k2_end; ++k2) {
     if ((k2 & 15) == 15) {  // pull in the bound the rest of the grid has found
       __syncthreads();
       refresh_bound(a, s_smin);
@@ -290,7 +315,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       __syncthreads();
       for (uint32_t t = threadIdx.x; t < nk; t += blockDim.x) s_rec[t] = __ldg(a.keys + beg + c0r + t);
       __syncthreads();
-      if (!wlive) continue;
+      if (!wlive || k2 > wlast) continue;
       for (uint32_t t0 = 0; t0 < nk; t0 += 32) {
         const uint32_t t = t0 + lane;
         const uint32_t k = t < nk ? s_rec[t] : 0xffffffffu;
@@ -312,7 +337,8 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
         __syncwarp();
       }
     }
-    if (!wlive) continue;
+    const bool flagged = (__shfl_sync(0xffffffffu, fword, k2 >> 5) >> (k2 & 31)) & 1u;
+    if (!wlive || !flagged) continue;
     // score row (k0, k1, k2): lane l owns k3 = 32 l .. 32 l + 31
     const double fr3 = div_count((double)reach4, n, rcp);
     const double m3 = dadd(m2, dmul(fr3, c3));
@@ -397,7 +423,9 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       if (a.pass == 1) {
         // most surviving configs tie the recorded minimum (routing-equivalent
         // threshold tuples): a read skips their atomic
-        if (__ldcg(a.mincost + correct) <= key) continue;
+        const unsigned long long cur = __ldcg(a.mincost + correct);
+        rflag |= cur >= key;
+        if (cur <= key) continue;
         const unsigned long long old = atomicMin(a.mincost + correct, (unsigned long long)key);
         if (key < old) atomicMin(a.gbest + bk, (unsigned long long)key);
       } else if (__ldg(a.front_key + correct) == key) {
@@ -425,6 +453,11 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
           o[5] = reach5;
         }
       }
+    }
+    if (a.pass == 1) {
+      if (__any_sync(0xffffffffu, rflag) && lane == 0)
+        atomicOr(a.row_flag + ((int64_t)k0 * a.g1 + k1) * a.n_words + (k2 >> 5), 1u << (k2 & 31));
+      rflag = false;
     }
     if (a.pass == 2) {  // the lanes' last runs: one atomic per distinct point in the warp
       const uint32_t live = __ballot_sync(0xffffffffu, run_n > 0);
@@ -537,6 +570,9 @@ F5Layout f5_layout(const int32_t* glen, int64_t n_rec) {
   L.offTies = take((size_t)(n_rec + 1) * 8);
   L.offMinIdx = take((size_t)(n_rec + 1) * 8);
   L.offNFront = take(256);
+  L.n_words = (glen[2] + 31) / 32;
+  L.offRowFlag = take((size_t)glen[0] * glen[1] * L.n_words * 4);
+  L.offK0Done = take((size_t)glen[0]);
   L.bytes = o;
   return L;
 }
@@ -590,6 +626,8 @@ cudaError_t f5_prepare(const double* cert, const uint8_t* corr, int64_t n_rec, c
   // min-cost keys and bucket bounds start empty
   if ((e = cudaMemsetAsync(ws + L.offMin, 0x7f, (size_t)(n_rec + 1) * 8, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(ws + L.offGbest, 0x7f, (size_t)kF5Bins * 8, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(ws + L.offRowFlag, 0, (size_t)L.offK0Done - L.offRowFlag + L.d0 - 1, st)) != cudaSuccess)
+    return e;
   return cudaSuccess;
 }
 
@@ -619,6 +657,9 @@ static F5PassArgs pass_args(const F5Layout& L, const int32_t* glen, int64_t n_re
   a.mincost = reinterpret_cast<unsigned long long*>(ws + L.offMin);
   a.gbest = reinterpret_cast<unsigned long long*>(ws + L.offGbest);
   a.front_key = reinterpret_cast<const unsigned long long*>(ws + L.offFront);
+  a.row_flag = reinterpret_cast<uint32_t*>(ws + L.offRowFlag);
+  a.k0_done = ws + L.offK0Done;
+  a.n_words = L.n_words;
   return a;
 }
 
@@ -654,6 +695,10 @@ cudaError_t f5_pass1(const int32_t* glen, int64_t n_rec, const double* cost1, ui
     f5_pass_kernel<<<(unsigned)((a.k0_end - a.k0_begin) * groups), kF5Warps * 32, smem, st>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
+  // these k0's row flags are complete (stream-ordered after the passes)
+  if (k0_end > k0_begin &&
+      (e = cudaMemsetAsync(ws + L.offK0Done + k0_begin, 1, (size_t)(k0_end - k0_begin), st)) != cudaSuccess)
+    return e;
   return cudaSuccess;
 }
 
@@ -670,6 +715,14 @@ cudaError_t f5_select(const int32_t* glen, int64_t n_rec, uint8_t* ws, unsigned 
   return cudaGetLastError();
 }
 
+// Pass 2 scores only the rows pass 1 flagged, for the k0 that pass 1 has
+// walked (others: every row).  Every row holding a front config is flagged:
+// pass 1 drops a config only for one that strictly dominates it (not a
+// front config) or, by the strict staircase, for an earlier config of the
+// row with the same correct count and no higher cost -- which then ties the
+// front point and is visited instead; a visited front config has cost ==
+// the final mincost <= mincost when pass 1 read it, which flags the row.
+// So the ties and smallest indices are those of the full walk.
 cudaError_t f5_pass2(const int32_t* glen, int64_t n_rec, const double* cost1, uint8_t* ws, int k0_begin,
                      int k0_end, unsigned long long* out_idx, double* out_cost, uint32_t* out_rec,
                      unsigned long long* out_count, int64_t out_cap, cudaStream_t st) {

@@ -11,7 +11,8 @@ namespace gs {
 struct F5Layout {
   int32_t d0, d1, d2, d3, bucket_shift;
   size_t offTmp, offKeys, offPre02, offCur, offBstart, offS01, offC0, offMin, offFront, offGbest,
-      offNFront, offTies, offMinIdx, bytes;
+      offNFront, offTies, offMinIdx, offRowFlag, offK0Done, bytes;
+  int32_t n_words;  // row-flag words per (k0, k1): ceil(g2 / 32)
 };
 
 bool f5_supported(int64_t n_rec, const int32_t* grid_len);
