@@ -5,7 +5,7 @@ set -u
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in racecheck synccheck memcheck; do
-  for part in ${PARTS:-grid4 general list stage quantile head}; do
+  for part in ${PARTS:-grid4 general list stage quantile head front5}; do
     extra=""
     [ "$tool" = racecheck ] && extra="--racecheck-report all"
     timeout 900 $CS --tool $tool $extra --print-limit 50 python tools/sanitize_run.py $part \

@@ -92,5 +92,22 @@ if which in ("all", "head"):
     head_certainty(f, w, kind="margin")
     print("head ok", flush=True)
 
+if which in ("all", "front5"):
+    # config 4a's path (prepare, both passes with the row flags, select)
+    # against the materialised five-model sweep + exact front (config 4b's path)
+    from paper_2406_14424_b200.front5 import Front5
+    from paper_2406_14424_b200.gridsweep import pareto_counts
+    c5, k5 = synth.validation_matrices(5, 3000, 0.8, 2)
+    grids5 = [np.array(grid_values(c5[:, j], 10)) for j in range(5)]
+    cost5 = np.array([1.0, 4.0, 16.0, 64.0, 256.0])
+    f = Front5(c5, k5, grids5, cost5).front()
+    sw5 = GridSweep(c5, k5, grids5, cost5)
+    sb = sw5.n_configs - int(np.prod([len(g) for g in grids5[:4]]))
+    res5 = sw5.evaluate(sb, sw5.n_configs - sb, n_correct=True)
+    idx = pareto_counts(res5.n_correct, res5.mean_cost, sw5.n_rec).cpu().numpy()
+    assert np.array_equal(f.index.astype(np.int64), idx)
+    assert np.array_equal(f.mean_cost, res5.mean_cost.cpu().numpy()[idx])
+    print("front5 ok", flush=True)
+
 torch.cuda.synchronize()
 print("sanitize run ok")
