@@ -1069,8 +1069,7 @@ def config4a_bench(args, dev, world, rank):
     grids = [np.array(grid_values(cert[:, j], 1000)) for j in range(5)]
     cost1 = np.array([1.0, 4.0, 16.0, 64.0, 256.0])
     f5 = Front5(cert, corr, grids, cost1)
-    g0 = f5.grid_len[0]
-    cuts = np.linspace(0, g0, world + 1).astype(int)
+    cuts = f5.k0_cuts(world)  # about equal work per rank (a k0's cost grows with #(b0 <= k0))
     b, e = int(cuts[rank]), int(cuts[rank + 1])
 
     def step():

@@ -44,6 +44,26 @@ class Front:
     n_configs: int
 
 
+def k0_cuts(cert0, grid0, world: int) -> np.ndarray:
+    """Cut points [world + 1] of k0 = 0..g0 for sharding the passes over the
+    ranks with about equal work each.  A k0's rows stream the records with
+    b0 <= k0, so its cost grows with R(k0) = #(b0 <= k0); measured on one
+    B200 (config 4a) a k0 near R = 0.6 n costs about twice one near R = 0,
+    modelled as 1 + 2 R(k0) / n.  Equal-count cuts would leave the last rank
+    about 1.4x the mean at 8 ranks."""
+    g = np.asarray(grid0, dtype=np.float64)
+    x = np.asarray(cert0, dtype=np.float64)
+    n = max(1, x.size)
+    g0 = int(g.size)
+    b0 = np.searchsorted(g, x, side="right")  # #(g <= x), the kernel's bin
+    r = np.cumsum(np.bincount(b0, minlength=g0 + 1))[:g0]  # R(k0) for k0 = 0..g0-1
+    w = 1.0 + 2.0 * r / n
+    cw = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = np.searchsorted(cw, cw[-1] * np.arange(world + 1) / world, side="left")
+    cuts[0], cuts[-1] = 0, g0
+    return np.maximum.accumulate(np.clip(cuts, 0, g0)).astype(np.int64)
+
+
 class Front5:
     """Prepared records (bins, sorted keys, side tables) of one validation
     set and its grids; pass1 / select / pass2 compute the front."""
@@ -64,6 +84,7 @@ class Front5:
             host.append(g)
         self.n_rec = int(self.cert.shape[0])
         self.grids_host = host
+        self._cert0 = self.cert[:, 0].cpu().numpy()  # k0_cuts' record bins
         self.grid_len = [int(g.size) for g in host]
         self._glen = _lib.int32_array(self.grid_len)
         self.grids = _lib.to_device(np.concatenate(host[:4]), torch.float64)
@@ -77,6 +98,10 @@ class Front5:
         self.n_configs = int(info.n_configs)
         self.ws = torch.empty(int(info.workspace_bytes), dtype=torch.uint8, device=_lib.device())
         self.prepare()
+
+    def k0_cuts(self, world: int) -> np.ndarray:
+        """k0 ranges of about equal work for `world` ranks (k0_cuts)."""
+        return k0_cuts(self._cert0, self.grids_host[0], world)
 
     def prepare(self) -> None:
         """Bin and sort the records, build the side tables, reset mincost."""
