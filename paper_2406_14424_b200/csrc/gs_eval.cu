@@ -138,18 +138,76 @@ __global__ void __launch_bounds__(kEvalThreads) eval_list_kernel(EvalArgs a) {
       __syncthreads();
     }
     if (active && ns > 0) {
-      for (int r = 0; r < rows; ++r) {
-        const double* crow = tc + r * M;
-        const uint8_t* krow = tk + r * M;
+      if (MAXL <= 4) {
+        // branch-free: every stage's certainty is loaded at once (the loads
+        // do not wait on the stop decisions) and the first stopping stage
+        // found by predicates; stages s >= ns - 1 compare against NaN (never
+        // true: the last stage always stops), the stop stage's model comes
+        // out of a byte-packed copy of sm, and the records stopping at each
+        // stage are counted in 16-bit fields of one word (flushed to the
+        // reach counts per tile, <= 256 records) -- reach[s] is their suffix
+        double tq[MAXL];
+        uint32_t smp = 0;
 #pragma unroll
         for (int s = 0; s < MAXL; ++s) {
-          if (s >= ns) break;
-          const int m = sm[s];
-          if (s == ns - 1 || crow[m] >= th[s]) {
-            correct += krow[m];
-            break;
+          tq[s] = s < ns - 1 ? th[s] : __longlong_as_double(0x7ff8000000000000ll);
+          smp |= (uint32_t)sm[s] << (8 * s);
+        }
+        uint64_t stops = 0;
+#pragma unroll 2
+        for (int r = 0; r < rows; ++r) {
+          const double* crow = tc + r * M;
+          const uint8_t* krow = tk + r * M;
+          double v[MAXL];
+#pragma unroll
+          for (int s = 0; s < MAXL - 1; ++s) v[s] = crow[sm[s]];  // sm[s] = 0 past ns: a valid read
+          int stop = ns - 1;
+#pragma unroll
+          for (int s = MAXL - 2; s >= 0; --s)
+            if (v[s] >= tq[s]) stop = s;
+          stops += 1ull << (16 * stop);
+          correct += krow[(smp >> (8 * stop)) & 0xffu];
+        }
+        uint32_t above = 0;
+#pragma unroll
+        for (int s = MAXL - 1; s >= 1; --s) {
+          above += (uint32_t)(stops >> (16 * s)) & 0xffffu;
+          reach[s] += above;
+        }
+      } else if (MAXL <= 8) {
+        // as above with per-stage counters (eight stages do not fit one word)
+#pragma unroll 2
+        for (int r = 0; r < rows; ++r) {
+          const double* crow = tc + r * M;
+          const uint8_t* krow = tk + r * M;
+          double v[MAXL];
+#pragma unroll
+          for (int s = 0; s < MAXL; ++s) v[s] = crow[sm[s]];  // sm[s] = 0 past ns: a valid read
+          int stop = ns - 1, m = sm[0];
+#pragma unroll
+          for (int s = MAXL - 2; s >= 0; --s)
+            if (s < ns - 1 && v[s] >= th[s]) stop = s;
+#pragma unroll
+          for (int s = 1; s < MAXL; ++s) {
+            reach[s] += s <= stop ? 1u : 0u;
+            m = s == stop ? sm[s] : m;
           }
-          if (s + 1 < MAXL) reach[s + 1] += 1;
+          correct += krow[m];
+        }
+      } else {
+        for (int r = 0; r < rows; ++r) {
+          const double* crow = tc + r * M;
+          const uint8_t* krow = tk + r * M;
+#pragma unroll
+          for (int s = 0; s < MAXL; ++s) {
+            if (s >= ns) break;
+            const int m = sm[s];
+            if (s == ns - 1 || crow[m] >= th[s]) {
+              correct += krow[m];
+              break;
+            }
+            if (s + 1 < MAXL) reach[s + 1] += 1;
+          }
         }
       }
     }
