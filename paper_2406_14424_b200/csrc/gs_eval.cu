@@ -141,19 +141,27 @@ __global__ void __launch_bounds__(kEvalThreads) eval_list_kernel(EvalArgs a) {
       if (MAXL <= 4) {
         // branch-free: every stage's certainty is loaded at once (the loads
         // do not wait on the stop decisions) and the first stopping stage
-        // found by predicates; stages s >= ns - 1 compare against NaN (never
-        // true: the last stage always stops), the stop stage's model comes
-        // out of a byte-packed copy of sm, and the records stopping at each
-        // stage are counted in 16-bit fields of one word (flushed to the
-        // reach counts per tile, <= 256 records) -- reach[s] is their suffix
+        // picked by predicated selects; stages s >= ns - 1 compare against
+        // NaN (never true: the last stage always stops).  The select picks
+        // the stop stage's model and its count increment: the records
+        // stopping at stage t >= 1 are counted in 10-bit field t - 1 of one
+        // word (flushed to the reach counts per tile, <= 256 records) --
+        // reach[s] is the suffix sum of those fields
         double tq[MAXL];
-        uint32_t smp = 0;
+        uint32_t inc_s[MAXL];
 #pragma unroll
         for (int s = 0; s < MAXL; ++s) {
           tq[s] = s < ns - 1 ? th[s] : __longlong_as_double(0x7ff8000000000000ll);
-          smp |= (uint32_t)sm[s] << (8 * s);
+          inc_s[s] = s == 0 ? 0u : 1u << (10 * (s - 1));
         }
-        uint64_t stops = 0;
+        uint32_t inc_last = inc_s[0], m_last = (uint32_t)sm[0];
+#pragma unroll
+        for (int s = 1; s < MAXL; ++s)
+          if (s == ns - 1) {
+            inc_last = inc_s[s];
+            m_last = (uint32_t)sm[s];
+          }
+        uint32_t stops = 0;
 #pragma unroll 2
         for (int r = 0; r < rows; ++r) {
           const double* crow = tc + r * M;
@@ -161,17 +169,20 @@ __global__ void __launch_bounds__(kEvalThreads) eval_list_kernel(EvalArgs a) {
           double v[MAXL];
 #pragma unroll
           for (int s = 0; s < MAXL - 1; ++s) v[s] = crow[sm[s]];  // sm[s] = 0 past ns: a valid read
-          int stop = ns - 1;
+          uint32_t inc = inc_last, m = m_last;
 #pragma unroll
           for (int s = MAXL - 2; s >= 0; --s)
-            if (v[s] >= tq[s]) stop = s;
-          stops += 1ull << (16 * stop);
-          correct += krow[(smp >> (8 * stop)) & 0xffu];
+            if (v[s] >= tq[s]) {
+              inc = inc_s[s];
+              m = (uint32_t)sm[s];
+            }
+          stops += inc;
+          correct += krow[m];
         }
         uint32_t above = 0;
 #pragma unroll
         for (int s = MAXL - 1; s >= 1; --s) {
-          above += (uint32_t)(stops >> (16 * s)) & 0xffffu;
+          above += (stops >> (10 * (s - 1))) & 1023u;
           reach[s] += above;
         }
       } else if (MAXL <= 8) {
