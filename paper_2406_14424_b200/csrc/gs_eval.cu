@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kEvalThreads) eval_list_kernel(EvalArgs a) {
             m_last = (uint32_t)sm[s];
           }
         uint32_t stops = 0;
-#pragma unroll 2
+#pragma unroll 4
         for (int r = 0; r < rows; ++r) {
           const double* crow = tc + r * M;
           const uint8_t* krow = tk + r * M;
