@@ -397,11 +397,16 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)r5, n, rcp), c4)));
       lane_bound = s_smin[(int)(amax >> a.bucket_shift) + 1];
       lane_live = lane_bound > key0;
+      // pass 1 scores only configs above the row's running maximum: none
+      // of this lane's is when an earlier lane already reached its amax
+      if (a.pass == 1 && lane > 0 && amax <= run_max) lane_live = false;
     }
 #pragma unroll 4
     for (int t = 0; t < (lane_live ? 32 : 0); ++t) {
-      acc += hist[t * 32 + lane];
       const int k3 = 32 * lane + t;
+      // ... and none of the rest of the lane once it has reached amax itself
+      if (a.pass == 1 && k3 > 0 && run_max >= amax) break;
+      acc += hist[t * 32 + lane];
       if (k3 >= g3) break;
       const uint32_t reach5 = (uint32_t)(acc & kF5M21);
       const uint32_t correct = crow + (uint32_t)((acc >> 21) & kF5M21) - (uint32_t)(acc >> 42);
