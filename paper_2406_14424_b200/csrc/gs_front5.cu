@@ -14,7 +14,10 @@
 //   values (a warp each).  It walks k2 = 0 .. g2-1: the records of bucket
 //   b2 = k2 with b0 <= k0 are a prefix of that bucket (pre02), streamed
 //   through shared memory; each warp adds those with b1 <= k1 to its b3
-//   histogram {cnt, c4, c3} (R4 = the records reaching stage 4), then scores
+//   histogram (R4 = the records reaching stage 4; a bin is one u64: the
+//   count in the low word, C4 - C3 two's-complement in the high word -- the
+//   low word never carries, n < 2^21 -- so a prefix sum gives reach5 and
+//   the correct count's change without unpacking), then scores
 //   the row (k0, k1, k2, k3 = 0 .. g3-1) from the histogram's prefix:
 //     reach5(k3) = #(R4, b3 <= k3), correct = C0 + C1 + C2 (row terms)
 //                + C3(R4) - C3(R4, b3 <= k3) + C4(R4, b3 <= k3)
@@ -39,7 +42,6 @@ namespace {
 constexpr int kF5Warps = 24;              // k1 values per CTA (a warp each)
 constexpr int kF5Bins = 1024;             // histogram bins (d3 <= 1024)
 constexpr int kF5Tile = 1024;             // records staged per round
-constexpr uint64_t kF5M21 = (1ull << 21) - 1;
 constexpr uint64_t kF5Inf = 0x7f7f7f7f7f7f7f7full;  // empty min-cost key (a memset 0x7f fill);
                                                     // above every cost key (costs < 1e300)
 
@@ -331,8 +333,9 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
           const uint32_t b3 = (k >> 10) & 1023u;
           const uint32_t peers = __match_any_sync(m, b3);
           if (lane == __ffs(peers) - 1)
-            hist[bin_pos((int)b3)] += (uint64_t)__popc(peers) | ((uint64_t)__popc(peers & m4) << 21) |
-                                      ((uint64_t)__popc(peers & m3) << 42);
+            hist[bin_pos((int)b3)] +=
+                (uint64_t)__popc(peers) +
+                ((uint64_t)(int64_t)(__popc(peers & m4) - __popc(peers & m3)) << 32);
         }
         __syncwarp();
       }
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
        // crow + C4(R4), none cheaper than k3 = 0 (reach5 = bin 0); if the
        // bound of that accuracy already beats that cost, every config of the
        // row would be dropped below
-      const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)(uint32_t)(hist[0] & kF5M21), n, rcp), c4)));
+      const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)(uint32_t)hist[0], n, rcp), c4)));
       // crow + C4(R4) counts C3(R4) and C4(R4) both, so it can pass n: clamp
       const uint32_t ub = min(crow + c4_r4, (uint32_t)a.n_rec);
       if (s_smin[(int)(ub >> a.bucket_shift) + 1] <= key0) continue;
@@ -356,15 +359,14 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // each lane's highest correct count, and the running maximum over the
     // lanes before it (configs with smaller k3 cost no more)
     // one pass over the lane's bins: its total and the largest C4 - C3 of
-    // its local prefixes (the fields add without carries, so a config's
-    // correct count is crow + (C4 - C3)(prefix before the lane) + that local
-    // difference)
+    // its local prefixes (a config's correct count is crow + (C4 - C3)(prefix
+    // before the lane) + that local difference)
     uint64_t tot = 0;
     int dmax = -(1 << 22);
 #pragma unroll 8
     for (int t = 0; t < 32; ++t) {
       tot += hist[t * 32 + lane];
-      if (32 * lane + t < g3) dmax = max(dmax, (int)((tot >> 21) & kF5M21) - (int)(tot >> 42));
+      if (32 * lane + t < g3) dmax = max(dmax, (int)(tot >> 32));
     }
     uint64_t excl = tot;
 #pragma unroll
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     }
     excl -= tot;
     const uint32_t amax =
-        32 * lane < g3 ? (uint32_t)((int)crow + (int)((excl >> 21) & kF5M21) - (int)(excl >> 42) + dmax) : 0u;
+        32 * lane < g3 ? (uint32_t)((int)crow + (int)(excl >> 32) + dmax) : 0u;
     uint32_t pmax = amax;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     bool lane_live = 32 * lane < g3;
     uint64_t lane_bound = kF5Inf;
     if (lane_live) {
-      const uint32_t r5 = (uint32_t)((excl + hist[lane]) & kF5M21);
+      const uint32_t r5 = (uint32_t)(excl + hist[lane]);
       const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)r5, n, rcp), c4)));
       lane_bound = s_smin[(int)(amax >> a.bucket_shift) + 1];
       lane_live = lane_bound > key0;
@@ -408,8 +410,8 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       if (a.pass == 1 && k3 > 0 && run_max >= amax) break;
       acc += hist[t * 32 + lane];
       if (k3 >= g3) break;
-      const uint32_t reach5 = (uint32_t)(acc & kF5M21);
-      const uint32_t correct = crow + (uint32_t)((acc >> 21) & kF5M21) - (uint32_t)(acc >> 42);
+      const uint32_t reach5 = (uint32_t)acc;
+      const uint32_t correct = crow + (uint32_t)(acc >> 32);
       // pass 1 keeps only a row's first config of each new correct count:
       // later ones with the same count cost no less (cost is non-decreasing
       // in k3), so they cannot lower mincost; pass 2 also needs their exact
