@@ -41,7 +41,6 @@ namespace {
 
 constexpr int kF5Warps = 24;              // k1 values per CTA (a warp each)
 constexpr int kF5Bins = 1024;             // histogram bins (d3 <= 1024)
-constexpr int kF5Tile = 1024;             // records staged per round
 constexpr uint64_t kF5Inf = 0x7f7f7f7f7f7f7f7full;  // empty min-cost key (a memset 0x7f fill);
                                                     // above every cost key (costs < 1e300)
 
@@ -252,10 +251,30 @@ __device__ void refresh_bound(const F5PassArgs& a, unsigned long long* smin) {
   }
 }
 
+// The same, by one warp and without barriers, while the other warps keep
+// reading: each entry is only ever lowered to a suffix minimum of a newer
+// gbest, and any value an entry holds is the cost of a recorded config in a
+// bucket at or above it -- a valid bound at every moment.
+__device__ void refresh_bound_warp(const F5PassArgs& a, unsigned long long* smin) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long carry = kF5Inf;
+#pragma unroll 4
+  for (int j0 = kF5Bins - 32; j0 >= 0; j0 -= 32) {
+    unsigned long long x = __ldcg(a.gbest + j0 + lane);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_down_sync(0xffffffffu, x, o);
+      if (lane + o < 32 && y < x) x = y;
+    }
+    x = x < carry ? x : carry;
+    if (x < smin[j0 + lane]) smin[j0 + lane] = x;
+    carry = __shfl_sync(0xffffffffu, x, 0);
+  }
+}
+
 __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_constant__ F5PassArgs a) {
   extern __shared__ __align__(16) unsigned long long s_hist[];  // [kF5Warps][kF5Bins]
   __shared__ unsigned long long s_smin[kF5Bins + 1];             // suffix min of gbest
-  __shared__ uint32_t s_rec[kF5Tile];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k0 = a.k0_begin + (int)(blockIdx.x / a.n_groups) * a.k0_stride;
   const int k1 = (blockIdx.x % a.n_groups) * kF5Warps + warp;
@@ -304,24 +323,20 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   uint32_t c2_r4 = 0, reach4 = 0, c3_r4 = 0, c4_r4 = 0;
   const int64_t k01 = ((int64_t)k0 * g1 + k1) * a.g2;
   bool rflag = false;  // pass 1: this row has a config at or below mincost
+  // the warps walk their rows independently (no barriers): each streams the
+  // records itself (the CTA's warps read the same lines, L1 hits after the
+  // first), and in pass 1 one warp in turn pulls in the bound the rest of the
+  // grid has found every 16 rows
   for (int k2 = 0; k2 <= k2_end; ++k2) {
-    if ((k2 & 15) == 15) {  // pull in the bound the rest of the grid has found
-      __syncthreads();
-      refresh_bound(a, s_smin);
-      __syncthreads();
-    }
+    if (a.pass == 1 && (k2 & 15) == 15 && ((k2 >> 4) % kF5Warps) == warp) refresh_bound_warp(a, s_smin);
+    if (!wlive || k2 > wlast) continue;
     // stream bucket b2 = k2, records with b0 <= k0 (a prefix of the bucket)
     const uint32_t beg = __ldg(a.bstart + k2), cnt = __ldg(a.pre02 + (int64_t)k2 * a.d0 + k0);
-    for (uint32_t c0r = 0; c0r < cnt; c0r += kF5Tile) {
-      const uint32_t nk = min((uint32_t)kF5Tile, cnt - c0r);
-      __syncthreads();
-      for (uint32_t t = threadIdx.x; t < nk; t += blockDim.x) s_rec[t] = __ldg(a.keys + beg + c0r + t);
-      __syncthreads();
-      if (!wlive || k2 > wlast) continue;
-      for (uint32_t t0 = 0; t0 < nk; t0 += 32) {
+    {
+      for (uint32_t t0 = 0; t0 < cnt; t0 += 32) {
         const uint32_t t = t0 + lane;
-        const uint32_t k = t < nk ? s_rec[t] : 0xffffffffu;
-        const bool in = t < nk && (k & 1023u) <= (uint32_t)k1;
+        const uint32_t k = t < cnt ? __ldg(a.keys + beg + t) : 0xffffffffu;
+        const bool in = t < cnt && (k & 1023u) <= (uint32_t)k1;
         const uint32_t m = __ballot_sync(0xffffffffu, in);
         const uint32_t m3 = __ballot_sync(0xffffffffu, in && ((k >> 21) & 1u));
         const uint32_t m4 = __ballot_sync(0xffffffffu, in && ((k >> 22) & 1u));
@@ -341,7 +356,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       }
     }
     const bool flagged = (__shfl_sync(0xffffffffu, fword, k2 >> 5) >> (k2 & 31)) & 1u;
-    if (!wlive || !flagged) continue;
+    if (!flagged) continue;
     // score row (k0, k1, k2): lane l owns k3 = 32 l .. 32 l + 31
     const double fr3 = div_count((double)reach4, n, rcp);
     const double m3 = dadd(m2, dmul(fr3, c3));
