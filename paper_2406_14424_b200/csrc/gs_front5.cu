@@ -267,7 +267,7 @@ __device__ void refresh_bound_warp(const F5PassArgs& a, unsigned long long* smin
       if (lane + o < 32 && y < x) x = y;
     }
     x = x < carry ? x : carry;
-    if (x < smin[j0 + lane]) smin[j0 + lane] = x;
+    atomicMin(smin + j0 + lane, x);  // an atomic: the readers race with it by design
     carry = __shfl_sync(0xffffffffu, x, 0);
   }
 }

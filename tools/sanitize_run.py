@@ -98,7 +98,7 @@ if which in ("all", "front5"):
     from paper_2406_14424_b200.front5 import Front5
     from paper_2406_14424_b200.gridsweep import pareto_counts
     c5, k5 = synth.validation_matrices(5, 3000, 0.8, 2)
-    grids5 = [np.array(grid_values(c5[:, j], 10)) for j in range(5)]
+    grids5 = [np.array(grid_values(c5[:, j], 40)) for j in range(5)]  # g2 > 16: the in-place bound refresh runs
     cost5 = np.array([1.0, 4.0, 16.0, 64.0, 256.0])
     f = Front5(c5, k5, grids5, cost5).front()
     sw5 = GridSweep(c5, k5, grids5, cost5)
