@@ -263,11 +263,16 @@ int gs_stage_gate_packed(const double* certainty, const uint8_t* correct,
  *   prepare: bins, records sorted by (b2, b0), side tables; resets the
  *            per-accuracy minimum costs (mincost, int64 order-preserving
  *            cost bits at workspace + mincost_offset, n + 1 entries).
- *   pass1:   k0 in [k0_begin, k0_end): lowers mincost.  Sharded runs reduce
- *            mincost with MIN across ranks before select.
+ *   pass1:   k0 in [k0_begin, k0_end): lowers mincost, and flags (a bit per
+ *            row (k0, k1, k2) in the workspace, g0 g1 ceil(g2/32) words)
+ *            the rows holding a config at or below mincost as it stood.
+ *            Sharded runs reduce mincost with MIN across ranks before
+ *            select.
  *   select:  the front's accuracies and cost keys; *n_front (device) = how
  *            many distinct accuracies it has.
- *   pass2:   k0 in [k0_begin, k0_end): every config on the front, in no
+ *   pass2:   k0 in [k0_begin, k0_end) (only the rows pass 1 flagged, for
+ *            the k0 pass 1 walked: every front config's row is one; other
+ *            k0 in full): every config on the front, in no
  *            order: out_index [cap] config index, out_cost [cap] mean cost,
  *            out_counts [cap][6] {correct, n, reach after stages 0..3};
  *            *out_n (device, zero it first) the count (may exceed cap);
