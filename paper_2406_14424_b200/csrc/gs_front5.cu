@@ -378,10 +378,14 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // before the lane) + that local difference)
     uint64_t tot = 0;
     int dmax = -(1 << 22);
+    // (bins past g3 only exist in the lane holding k3 = g3 - 1, whose amax
+    // then bounds rather than equals its largest count: only that lane's
+    // own tests use it, and those only need a bound -- every later lane is
+    // past g3 and idle)
 #pragma unroll 8
     for (int t = 0; t < 32; ++t) {
       tot += hist[t * 32 + lane];
-      if (32 * lane + t < g3) dmax = max(dmax, (int)(tot >> 32));
+      dmax = max(dmax, (int)(tot >> 32));
     }
     uint64_t excl = tot;
 #pragma unroll
