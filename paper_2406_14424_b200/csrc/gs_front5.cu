@@ -376,17 +376,24 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // one pass over the lane's bins: its total and the largest C4 - C3 of
     // its local prefixes (a config's correct count is crow + (C4 - C3)(prefix
     // before the lane) + that local difference)
-    uint64_t tot = 0;
-    int dmax = -(1 << 22);
+    uint64_t tot = 0, mid = 0;  // mid: the prefix of the lane's first 16 bins
+    int dlo = -(1 << 22), dhi = -(1 << 22);  // over its first / last 16 configs
     // (bins past g3 only exist in the lane holding k3 = g3 - 1, whose amax
     // then bounds rather than equals its largest count: only that lane's
     // own tests use it, and those only need a bound -- every later lane is
     // past g3 and idle)
 #pragma unroll 8
-    for (int t = 0; t < 32; ++t) {
+    for (int t = 0; t < 16; ++t) {
       tot += hist[t * 32 + lane];
-      dmax = max(dmax, (int)(tot >> 32));
+      dlo = max(dlo, (int)(tot >> 32));
     }
+    mid = tot;
+#pragma unroll 8
+    for (int t = 16; t < 32; ++t) {
+      tot += hist[t * 32 + lane];
+      dhi = max(dhi, (int)(tot >> 32));
+    }
+    const int dmax = max(dlo, dhi);
     uint64_t excl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -411,8 +418,16 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // amax's, whose bound is the loosest (a suffix minimum); if that bound
     // already beats the cheapest cost, the in-loop test below would drop
     // every config of the lane
+    // The same per half lane (configs 0..15, 16..31, each with its own
+    // largest count and cheapest config): a half whose bound beats its
+    // cheapest config holds only dominated configs and is skipped.  (A
+    // skipped first half leaves run_max lower in the second: more configs
+    // pass the staircase test there, each still a real config's cost.)
     bool lane_live = 32 * lane < g3;
-    uint64_t lane_bound = kF5Inf;
+    uint64_t lane_bound = kF5Inf, hi_bound = kF5Inf;
+    const uint32_t amax_lo = (uint32_t)((int)crow + (int)(excl >> 32) + dlo);
+    const uint32_t amax_hi = (uint32_t)((int)crow + (int)(excl >> 32) + dhi);
+    int t_begin = 0, t_end = 32;
     if (lane_live) {
       const uint32_t r5 = (uint32_t)(excl + hist[lane]);
       const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)r5, n, rcp), c4)));
@@ -421,12 +436,30 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       // pass 1 scores only configs above the row's running maximum: none
       // of this lane's is when an earlier lane already reached its amax
       if (a.pass == 1 && lane > 0 && amax <= run_max) lane_live = false;
+      if (lane_live) {
+        bool lo_live = s_smin[(int)(amax_lo >> a.bucket_shift) + 1] > key0 &&
+                       !(a.pass == 1 && lane > 0 && amax_lo <= run_max);
+        bool hi_live = 32 * lane + 16 < g3;
+        if (hi_live) {
+          const uint32_t r5h = (uint32_t)(excl + mid + hist[16 * 32 + lane]);
+          const uint64_t key0h = cost_key(dadd(m3, dmul(div_count((double)r5h, n, rcp), c4)));
+          hi_bound = s_smin[(int)(amax_hi >> a.bucket_shift) + 1];
+          hi_live = hi_bound > key0h && !(a.pass == 1 && amax_hi <= run_max && lane > 0);
+        }
+        if (!lo_live) {
+          t_begin = 16;
+          acc = excl + mid;
+        }
+        if (!hi_live) t_end = 16;
+        lane_live = t_begin < t_end;
+      }
     }
 #pragma unroll 4
-    for (int t = 0; t < (lane_live ? 32 : 0); ++t) {
+    for (int t = t_begin; t < (lane_live ? t_end : 0); ++t) {
       const int k3 = 32 * lane + t;
       // ... and none of the rest of the lane once it has reached amax itself
-      if (a.pass == 1 && k3 > 0 && run_max >= amax) break;
+      // (amax_hi once only the second half is left)
+      if (a.pass == 1 && k3 > 0 && run_max >= (t < 16 ? amax : amax_hi)) break;
       acc += hist[t * 32 + lane];
       if (k3 >= g3) break;
       const uint32_t reach5 = (uint32_t)acc;
@@ -443,7 +476,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       const uint64_t key = cost_key(mean);
       // the same test for the rest of the lane: its later configs cost no
       // less and reach at most amax's bucket, whose bound is the loosest
-      if (key >= lane_bound) break;
+      if (key >= (t < 16 ? lane_bound : hi_bound)) break;
       const int bk = (int)(correct >> a.bucket_shift);
       if (s_smin[bk + 1] <= key) continue;  // a strictly more accurate config costs no more
       if (a.pass == 1) {
