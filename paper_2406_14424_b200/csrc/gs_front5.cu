@@ -376,24 +376,27 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // one pass over the lane's bins: its total and the largest C4 - C3 of
     // its local prefixes (a config's correct count is crow + (C4 - C3)(prefix
     // before the lane) + that local difference)
-    uint64_t tot = 0, mid = 0;  // mid: the prefix of the lane's first 16 bins
-    int dlo = -(1 << 22), dhi = -(1 << 22);  // over its first / last 16 configs
-    // (bins past g3 only exist in the lane holding k3 = g3 - 1, whose amax
-    // then bounds rather than equals its largest count: only that lane's
-    // own tests use it, and those only need a bound -- every later lane is
-    // past g3 and idle)
-#pragma unroll 8
-    for (int t = 0; t < 16; ++t) {
-      tot += hist[t * 32 + lane];
-      dlo = max(dlo, (int)(tot >> 32));
+#ifndef GS_F5_SUB
+#define GS_F5_SUB 2  // halves: 4 and 8 blocks measured slower (1.18, 1.43 s against 1.16)
+#endif
+    constexpr int kSub = GS_F5_SUB, kLen = 32 / GS_F5_SUB;  // blocks of configs per lane
+    uint64_t tot = 0;
+    uint64_t pre[kSub];  // the prefix of the lane's bins before block q
+    int dq[kSub];        // the largest local C4 - C3 over block q's configs
+#pragma unroll
+    for (int q = 0; q < kSub; ++q) {
+      pre[q] = tot;
+      int d = -(1 << 22);
+#pragma unroll
+      for (int u = 0; u < kLen; ++u) {
+        tot += hist[(q * kLen + u) * 32 + lane];
+        d = max(d, (int)(tot >> 32));
+      }
+      dq[q] = d;
     }
-    mid = tot;
-#pragma unroll 8
-    for (int t = 16; t < 32; ++t) {
-      tot += hist[t * 32 + lane];
-      dhi = max(dhi, (int)(tot >> 32));
-    }
-    const int dmax = max(dlo, dhi);
+    int dmax = dq[0];
+#pragma unroll
+    for (int q = 1; q < kSub; ++q) dmax = max(dmax, dq[q]);
     uint64_t excl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -418,16 +421,16 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     // amax's, whose bound is the loosest (a suffix minimum); if that bound
     // already beats the cheapest cost, the in-loop test below would drop
     // every config of the lane
-    // The same per half lane (configs 0..15, 16..31, each with its own
-    // largest count and cheapest config): a half whose bound beats its
-    // cheapest config holds only dominated configs and is skipped.  (A
-    // skipped first half leaves run_max lower in the second: more configs
-    // pass the staircase test there, each still a real config's cost.)
+    // The same per block of kLen configs (each block's own largest count
+    // and cheapest config): a block whose bound beats its cheapest config
+    // holds only dominated configs and is skipped.  (A skipped block leaves
+    // run_max lower after it: more configs pass the staircase test there,
+    // each still a real config's cost.)
     bool lane_live = 32 * lane < g3;
-    uint64_t lane_bound = kF5Inf, hi_bound = kF5Inf;
-    const uint32_t amax_lo = (uint32_t)((int)crow + (int)(excl >> 32) + dlo);
-    const uint32_t amax_hi = (uint32_t)((int)crow + (int)(excl >> 32) + dhi);
-    int t_begin = 0, t_end = 32;
+    uint64_t lane_bound = kF5Inf;
+    uint64_t qbound[kSub];
+    uint32_t qsuf[kSub];  // the largest count over blocks q.. (pass 1's exit)
+    uint32_t live_mask = 0;
     if (lane_live) {
       const uint32_t r5 = (uint32_t)(excl + hist[lane]);
       const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)r5, n, rcp), c4)));
@@ -437,31 +440,49 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       // of this lane's is when an earlier lane already reached its amax
       if (a.pass == 1 && lane > 0 && amax <= run_max) lane_live = false;
       if (lane_live) {
-        bool lo_live = s_smin[(int)(amax_lo >> a.bucket_shift) + 1] > key0 &&
-                       !(a.pass == 1 && lane > 0 && amax_lo <= run_max);
-        bool hi_live = 32 * lane + 16 < g3;
-        if (hi_live) {
-          const uint32_t r5h = (uint32_t)(excl + mid + hist[16 * 32 + lane]);
-          const uint64_t key0h = cost_key(dadd(m3, dmul(div_count((double)r5h, n, rcp), c4)));
-          hi_bound = s_smin[(int)(amax_hi >> a.bucket_shift) + 1];
-          hi_live = hi_bound > key0h && !(a.pass == 1 && amax_hi <= run_max && lane > 0);
+        uint32_t suf = 0;
+#pragma unroll
+        for (int q = kSub - 1; q >= 0; --q) {
+          const uint32_t am = (uint32_t)((int)crow + (int)(excl >> 32) + dq[q]);
+          suf = max(suf, am);
+          qsuf[q] = suf;
+          qbound[q] = kF5Inf;
+          bool lv = 32 * lane + q * kLen < g3;
+          if (lv) {
+            const uint64_t k0q =
+                q == 0 ? key0
+                       : cost_key(dadd(m3, dmul(div_count((double)(uint32_t)(excl + pre[q] +
+                                                                              hist[q * kLen * 32 + lane]),
+                                                          n, rcp),
+                                               c4)));
+            qbound[q] = s_smin[(int)(am >> a.bucket_shift) + 1];
+            lv = qbound[q] > k0q && !(a.pass == 1 && lane > 0 && am <= run_max);
+          }
+          live_mask |= lv ? 1u << q : 0u;
         }
-        if (!lo_live) {
-          t_begin = 16;
-          acc = excl + mid;
-        }
-        if (!hi_live) t_end = 16;
-        lane_live = t_begin < t_end;
       }
     }
+    if (!lane_live) live_mask = 0;
+    bool stop = false;
+#pragma unroll 1
+    for (int q = 0; q < kSub && !stop; ++q) {
+      if (!((live_mask >> q) & 1u)) continue;
+      acc = excl + pre[q];
 #pragma unroll 4
-    for (int t = t_begin; t < (lane_live ? t_end : 0); ++t) {
+    for (int u = 0; u < kLen; ++u) {
+      const int t = q * kLen + u;
       const int k3 = 32 * lane + t;
-      // ... and none of the rest of the lane once it has reached amax itself
-      // (amax_hi once only the second half is left)
-      if (a.pass == 1 && k3 > 0 && run_max >= (t < 16 ? amax : amax_hi)) break;
+      // ... and none of the rest of the lane once it has reached the largest
+      // count of the blocks left
+      if (a.pass == 1 && k3 > 0 && run_max >= qsuf[q]) {
+        stop = true;
+        break;
+      }
       acc += hist[t * 32 + lane];
-      if (k3 >= g3) break;
+      if (k3 >= g3) {
+        stop = true;
+        break;
+      }
       const uint32_t reach5 = (uint32_t)acc;
       const uint32_t correct = crow + (uint32_t)(acc >> 32);
       // pass 1 keeps only a row's first config of each new correct count:
@@ -476,7 +497,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
       const uint64_t key = cost_key(mean);
       // the same test for the rest of the lane: its later configs cost no
       // less and reach at most amax's bucket, whose bound is the loosest
-      if (key >= (t < 16 ? lane_bound : hi_bound)) break;
+      if (key >= qbound[q]) break;  // the rest of this block
       const int bk = (int)(correct >> a.bucket_shift);
       if (s_smin[bk + 1] <= key) continue;  // a strictly more accurate config costs no more
       if (a.pass == 1) {
@@ -512,6 +533,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
           o[5] = reach5;
         }
       }
+    }
     }
     if (a.pass == 1) {
       if (__any_sync(0xffffffffu, rflag) && lane == 0)
