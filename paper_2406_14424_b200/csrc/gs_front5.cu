@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
   // correct through stage 1: C0 of b0 > k0, C1 of (b0 <= k0, b1 > k1)
   const uint32_t base01 = (__ldg(a.c0pre + g0) - __ldg(a.c0pre + k0)) + (s0g.y - s01.y);
   const uint32_t c2_r3 = s01.z;  // C2 over R3
-  uint32_t c2_r4 = 0, reach4 = 0, c3_r4 = 0, c4_r4 = 0;
+  uint32_t c2_r4 = 0, reach4 = 0, c3_r4 = 0, p4_r4 = 0;
   const int64_t k01 = ((int64_t)k0 * g1 + k1) * a.g2;
   bool rflag = false;  // pass 1: this row has a config at or below mincost
   // the warps walk their rows independently (no barriers): each streams the
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
         reach4 += __popc(m);
         c2_r4 += __popc(__ballot_sync(0xffffffffu, in && ((k >> 20) & 1u)));
         c3_r4 += __popc(m3);
-        c4_r4 += __popc(m4);
+        p4_r4 += __popc(m4 & ~m3);  // R4 records whose stage-4 answer adds a correct one
         if (in) {  // the lanes of one b3 bin add as one: its lowest lane applies their sum
           const uint32_t b3 = (k >> 10) & 1023u;
           const uint32_t peers = __match_any_sync(m, b3);
@@ -362,12 +362,12 @@ __global__ void __launch_bounds__(kF5Warps * 32, 1) f5_pass_kernel(const __grid_
     const double m3 = dadd(m2, dmul(fr3, c3));
     const uint32_t crow = base01 + (c2_r3 - c2_r4) + c3_r4;  // + C4(k3) - C3(k3) per config
     {  // the whole row at once: no config of it is more accurate than
-       // crow + C4(R4), none cheaper than k3 = 0 (reach5 = bin 0); if the
-       // bound of that accuracy already beats that cost, every config of the
-       // row would be dropped below
+       // crow + #(R4 records with C4 and not C3) -- a config's count is crow
+       // plus its prefix of C4 - C3, at most the +1 records -- and none is
+       // cheaper than k3 = 0 (reach5 = bin 0); if the bound of that accuracy
+       // already beats that cost, every config of the row would be dropped
       const uint64_t key0 = cost_key(dadd(m3, dmul(div_count((double)(uint32_t)hist[0], n, rcp), c4)));
-      // crow + C4(R4) counts C3(R4) and C4(R4) both, so it can pass n: clamp
-      const uint32_t ub = min(crow + c4_r4, (uint32_t)a.n_rec);
+      const uint32_t ub = min(crow + p4_r4, (uint32_t)a.n_rec);
       if (s_smin[(int)(ub >> a.bucket_shift) + 1] <= key0) continue;
     }
     // lane totals, their exclusive scan (the prefix before this lane's bins),
