@@ -23,9 +23,9 @@
 // {1, k3, k2, k1} per record into H[b1][b0][b2]) and g4_plane (the same
 // plane prefix from H, re-zeroing it).  Both leave the same S / R1 / P0.
 //
-//   g4_eval    a cluster of CTAs per b0 slab k0, split along b1: each
-//              bulk-copies its rows of S[k0], exchanges column sums through
-//              distributed shared memory (the b1 carry), then a column walk
+//   g4_eval    one CTA per SM (four 256-thread groups); a unit is a block
+//              of W columns (b2) of one b0 slab k0, stored contiguously in
+//              S's blocked layout and staged by bulk copies; a column walk
 //              along b1 finishes the prefix and scores each position
 //              (k1, k2) as the full cascade's config (k0, k1, k2), with
 //              row-shared terms (the stage-2 fraction, the partial mean cost,
