@@ -1,7 +1,7 @@
 """One small invocation of each kernel family, for compute-sanitizer
 (racecheck / synccheck / memcheck).  Shapes are reduced so the tools finish
 in minutes; every kernel path of the headline is taken: the four-model
-sorted build (g4_sort, g4_gather) and the four-CTA-cluster eval (g4_eval),
+sorted build (g4_sort, g4_gather) and the column-block eval (g4_eval),
 the general sweep, the list path, the stage step and gate, Pareto,
 quantiles.  Each result is checked against the oracle so a race that
 changes a value also fails loudly."""
