@@ -1,6 +1,7 @@
 """H2D of the config-2 certainty matrix [1M, 4] f64 from pinned host memory:
 the whole matrix (32 MB) vs only the three columns the grid path reads
-(cudaMemcpy2DAsync, 24 of every 32 bytes), CUDA events."""
+(cudaMemcpy2DAsync, 24 of every 32 bytes), and the whole matrix as two
+halves on two streams at once (both copy engines), CUDA events."""
 import torch
 from cuda.bindings import runtime as rt
 
@@ -21,7 +22,23 @@ def cols3():
     assert err == rt.cudaError_t.cudaSuccess, err
 
 
-for name, fn, nbytes in (("full 32 MB", full, 32e6), ("3 of 4 columns (2D)", cols3, 24e6)):
+s2 = torch.cuda.Stream()
+
+
+def halves():
+    e = torch.cuda.Event()
+    e.record(s)
+    s2.wait_event(e)
+    d[: N // 2].copy_(h[: N // 2], non_blocking=True)
+    with torch.cuda.stream(s2):
+        d[N // 2:].copy_(h[N // 2:], non_blocking=True)
+    e2 = torch.cuda.Event()
+    e2.record(s2)
+    s.wait_event(e2)
+
+
+for name, fn, nbytes in (("full 32 MB", full, 32e6), ("3 of 4 columns (2D)", cols3, 24e6),
+                         ("two halves, two streams", halves, 32e6)):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
